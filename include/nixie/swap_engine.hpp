@@ -1,0 +1,179 @@
+// nixie-b200 — the CUDA swap engine: the reference's modeled "memcpy loop"
+// (proj/src/transfer.cpp:173-186, occupancy kBlockBytes/bw) replaced by real
+// byte movement on one B200, behind the same registry / planner / lane
+// semantics.
+//
+//   tier 0 Gpu        device arena (cudaMalloc of the capped budget), 2 MiB frames
+//   tier 1 PinnedHost staging ring: cudaHostAlloc(mapped|portable) of exactly the
+//                     pinned budget, 2 MiB slots recycled FIFO; the budget is the
+//                     tier capacity, so MemState's back-pressure enforces it
+//   tier 2 PagedHost  pageable host memory, 2 MiB units mapped on first use
+//   tier 3 Disk       not backed by this engine (no configuration reaches it)
+//
+// PCIe lanes (pinned<->GPU) run the sm_100a swap kernel (K1, checksum fused)
+// or the copy engines (K2, cudaMemcpyAsync, with the K3 checksum kernel
+// around it), many legs in flight per direction, one CUDA stream per
+// direction. Host lanes (pinned<->paged) run on a NUMA-local thread pool.
+// Every arrival on the GPU is checked against the checksum recorded when the
+// block left it; a mismatch fails the switch (InvariantViolation).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "nixie/mem_model.hpp"
+#include "nixie/mlfq.hpp"
+#include "nixie/planner.hpp"
+#include "nixie/transfer.hpp"
+
+typedef struct CUstream_st* cudaStream_t;
+typedef struct CUevent_st* cudaEvent_t;
+
+namespace nixie::b200 {
+
+enum class CopyPath : int { Auto = 0, SmKernel = 1, CopyEngine = 2 };
+
+struct EngineConfig {
+  int device = 0;
+  Bytes gpu_capacity = 32 * kGiB;     // capped device budget (consumer-GPU emulation)
+  Bytes pinned_capacity = 16 * kGiB;  // enforced pinned budget
+  Bytes paged_capacity = 96 * kGiB;
+  CopyPath path = CopyPath::SmKernel;
+  int pcie_legs_in_flight = 256;      // per direction (x 2 MiB)
+  int legs_per_launch = 64;           // max legs per K1 launch / CE batch
+  int host_threads = 8;               // pinned<->paged copy workers
+  int host_legs_in_flight = 64;       // per host lane
+  int max_ctas = 0;                   // K1 grid cap; 0 = 2 x SM count
+  bool fused_launch = false;          // both directions in one launch stream (warp-group split)
+  bool verify = true;                 // checksum every restore
+  bool numa_bind = true;              // pinned ring + workers on the GPU's NUMA node
+};
+
+struct SwitchStats {
+  Bytes bytes_in = 0, bytes_out = 0;        // plan totals
+  Bytes pcie_h2d_bytes = 0, pcie_d2h_bytes = 0, host_bytes = 0;
+  double wall_s = 0;                        // host wall time of execute()
+  double plan_s = 0;                        // plan_switch time when run via switch_to()
+  double device_span_s = 0;                 // first PCIe launch start -> last end (CUDA events)
+  double kernel_s[2] = {0, 0};              // summed launch durations: [0] H2D stream, [1] D2H stream
+  int launches[2] = {0, 0};                 // K1/K3 kernel launches per stream
+  int ce_batches[2] = {0, 0};               // copy-engine batches per stream
+  int host_legs = 0;
+  std::uint64_t verified = 0, unverified = 0, mismatches = 0;
+};
+
+// Opens a launch gate on the device once the incoming app's last fetch has
+// been submitted: `value` is written to `device_word` on the H2D stream
+// (cuStreamWriteValue64), or `event` is recorded there if no word is given.
+struct GateRelease {
+  std::uint64_t* device_word = nullptr;
+  std::uint64_t value = 0;
+  cudaEvent_t event = nullptr;
+};
+
+struct LegTrace {
+  BlockId block;
+  TierId src, dst;
+};
+
+struct PcieProbe {
+  // GB/s (1e9 B/s). [0] CE (cudaMemcpyAsync), [1] SM kernel.
+  double h2d[2] = {0, 0};
+  double d2h[2] = {0, 0};
+  double bidir_h2d[2] = {0, 0};  // H2D rate while D2H runs concurrently
+  double bidir_d2h[2] = {0, 0};
+  double bidir_total[2] = {0, 0};
+  Bytes bytes_per_direction = 0;
+  Bytes chunk_bytes = 0;
+  int link_gen = 0, link_width = 0, link_gen_max = 0, link_width_max = 0;
+  int numa_node = -1;
+};
+
+class SwapEngine {
+ public:
+  explicit SwapEngine(const EngineConfig& cfg);
+  ~SwapEngine();
+  SwapEngine(const SwapEngine&) = delete;
+  SwapEngine& operator=(const SwapEngine&) = delete;
+
+  const EngineConfig& config() const;
+  MemState& mem();
+  const MemState& mem() const;
+  HardwareConfig hardware() const;  // capacities = budgets; link numbers from the last probe
+
+  // Registry entry points (interposer stand-ins) with physical placement.
+  std::vector<ChunkId> allocate(AppId app, Bytes size, TierId tier);
+  Bytes free_chunk(AppId app, ChunkId chunk);
+
+  // K4: synthetic working set. fill writes every block of `app` wherever it
+  // lives and records its checksum; verify returns the number of 16-byte
+  // vectors that differ from the pattern (0 = byte-exact).
+  void fill_pattern(AppId app, std::uint64_t seed);
+  std::uint64_t verify_pattern(AppId app, std::uint64_t seed);
+
+  // Executes a plan with real copies (same contract as nixie::execute).
+  // `drain`: the incumbent's stream; evictions start only after its queued
+  // kernels finish (device-side eviction gate).
+  ExecResult execute(const MigrationPlan& plan, const PlannerConfig& cfg, cudaStream_t drain = nullptr,
+                     const GateRelease* release = nullptr);
+  // plan_switch + execute.
+  ExecResult switch_to(AppId incoming, const PlannerConfig& cfg, cudaStream_t drain = nullptr);
+
+  const SwitchStats& last_stats() const;
+  const std::array<std::vector<LegTrace>, 6>& lane_trace() const;  // per lane, start order, last execute
+  std::uint64_t total_launches() const;  // kernels this engine has launched (all kinds)
+
+  // Device pointer of the frame holding a GPU-resident block; device table
+  // of frame pointers indexed by BlockId (0 when not on the GPU), refreshed
+  // on the H2D stream at the end of every execute.
+  void* frame_of(BlockId block) const;
+  const std::uint64_t* device_frame_table() const;
+  std::uint64_t block_checksum(BlockId block) const;  // last recorded departure checksum
+  // Test access to a resident block's bytes wherever it lives.
+  void read_block(BlockId block, void* host_dst);
+  void poke_block(BlockId block, std::uint64_t offset, std::uint8_t value);
+
+  cudaStream_t stream(int lane) const;  // 0 = H2D lane stream, 1 = D2H lane stream
+
+  // Measures the host link: CE and SM, H2D / D2H alone and both at once.
+  PcieProbe probe_pcie(Bytes bytes_per_direction, Bytes chunk_bytes);
+  // Per-batch-size choice for CopyPath::Auto: index k covers launches of
+  // 2^k legs; true = SM kernel, false = copy engines.
+  void set_auto_table(const std::vector<bool>& sm_faster);
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
+
+// Kernel-launch gate (§3 steps 1-2 and 6, §4): an app's kernels run
+// only while it holds the grant and its working set is GPU-resident.
+//   * before_launch(app, stream): a granted, resident app passes. Otherwise
+//     the app's request is enqueued with the scheduler and its stream gets a
+//     device-side wait (cuStreamWaitValue64 on the app's gate word) for its
+//     next grant epoch, so the kernel it is about to launch stays queued on
+//     the GPU until the swap-in lands. No host thread blocks.
+//   * context_switch(to, now): pauses the incumbent (its later launches are
+//     gated; its queued kernels drain before any eviction starts, on the
+//     device), plans with the scheduler's victim hint, executes with real
+//     copies, grants `to`, and writes its gate word on the H2D stream after
+//     the last fetch.
+class LaunchGate {
+ public:
+  LaunchGate(SwapEngine& engine, MlfqScheduler& sched, PlannerConfig cfg);
+  ~LaunchGate();
+
+  void attach(AppId app, cudaStream_t stream);
+  bool before_launch(AppId app, Seconds now);  // true = passed immediately
+  ExecResult context_switch(AppId to, Seconds now);
+  bool stream_mem_ops() const;  // device-side gating available
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
+
+}  // namespace nixie::b200

@@ -1,0 +1,202 @@
+/*
+ * nixie-b200 C ABI — the drop-in boundary of the B200 swap path.
+ *
+ * The reference (arxiv 2601.11743 "Nixie", /root/reference/proj) exposes a
+ * C++20 API in namespace nixie (proj/include/nixie/ headers) and no FFI. This
+ * header is the thin C layer beneath the same C++ API in this repo
+ * (include/nixie/ headers): plain pointers and sizes, status codes instead of
+ * exceptions, opaque handles. Each entry point names the reference interface
+ * it replaces or the paper mechanism it implements.
+ *
+ * Status codes: NX_OK, or 1 + nixie::Err (errors.hpp:8-21) for a SimError,
+ * NX_E_INVARIANT for an InvariantViolation (a bug: overcommit, deadlock, a
+ * restore whose checksum differs), NX_E_CUDA for a CUDA failure,
+ * NX_E_ARG for a bad argument. nx_last_error() returns the message of the
+ * calling thread's last failure.
+ */
+#ifndef NIXIE_B200_H_
+#define NIXIE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NX_OK 0
+#define NX_E_INVARIANT 100
+#define NX_E_CUDA 200
+#define NX_E_ARG 300
+
+/* Tier ids: reference TierId (proj/include/nixie/mem_model.hpp:14). */
+#define NX_TIER_GPU 0
+#define NX_TIER_PINNED 1
+#define NX_TIER_PAGED 2
+#define NX_TIER_DISK 3
+
+/* Copy paths for the PCIe lanes. */
+#define NX_PATH_AUTO 0   /* per-batch-size choice from nx_set_auto_table */
+#define NX_PATH_SM 1     /* K1: sm_100a swap kernel, checksum fused */
+#define NX_PATH_CE 2     /* K2: cudaMemcpyAsync copy engines + K3 checksum kernel */
+
+typedef struct nx_engine nx_engine;
+typedef struct nx_gate nx_gate;
+
+/* Engine configuration. Replaces HardwareConfig's tier capacities
+ * (proj/include/nixie/transfer.hpp:24-37): the GPU capacity becomes the
+ * capped device arena, the pinned capacity the enforced pinned budget. */
+typedef struct nx_engine_config {
+  int device;
+  uint64_t gpu_capacity;
+  uint64_t pinned_capacity;
+  uint64_t paged_capacity;
+  int path;
+  int pcie_legs_in_flight;
+  int legs_per_launch;
+  int host_threads;
+  int host_legs_in_flight;
+  int max_ctas;
+  int fused_launch;
+  int verify;
+  int numa_bind;
+} nx_engine_config;
+
+/* PlannerConfig (proj/include/nixie/planner.hpp:39-43). victim_order may be
+ * NULL (n_victims = 0). */
+typedef struct nx_planner_config {
+  uint64_t streaming_window;
+  uint64_t pinned_budget; /* UINT64_MAX = unbounded */
+  const uint32_t* victim_order;
+  size_t n_victims;
+} nx_planner_config;
+
+typedef struct nx_switch_stats {
+  uint64_t bytes_in, bytes_out;
+  uint64_t pcie_h2d_bytes, pcie_d2h_bytes, host_bytes;
+  double wall_s, plan_s, device_span_s;
+  double kernel_s_h2d, kernel_s_d2h;
+  int launches_h2d, launches_d2h, ce_batches_h2d, ce_batches_d2h, host_legs;
+  uint64_t verified, unverified, mismatches;
+  /* aggregate_throughput (proj/src/transfer.cpp:7-28) over the switch's
+   * GPU<->pinned records, device-timed, in bytes/s */
+  double tp_to_gpu, tp_from_gpu, tp_bidir;
+} nx_switch_stats;
+
+typedef struct nx_pcie_probe {
+  double h2d[2], d2h[2], bidir_h2d[2], bidir_d2h[2], bidir_total[2]; /* GB/s; [0] CE, [1] SM */
+  uint64_t bytes_per_direction, chunk_bytes;
+  int numa_node;
+} nx_pcie_probe;
+
+typedef struct nx_mlfq_config {
+  int levels;
+  double base_allotment, base_preemption, idle_threshold, tick;
+} nx_mlfq_config;
+
+/* ---- errors / library ---------------------------------------------------- */
+const char* nx_last_error(void);
+const char* nx_version(void);
+int nx_cuda_device_count(int* count);
+
+/* ---- engine lifecycle ---------------------------------------------------- */
+void nx_engine_config_default(nx_engine_config* cfg);
+void nx_planner_config_default(nx_planner_config* cfg);
+/* Creates one per-GPU Nixie instance: device arena, pinned staging ring,
+ * paged store, host copy pool, streams. */
+int nx_engine_create(const nx_engine_config* cfg, nx_engine** out);
+void nx_engine_destroy(nx_engine* e);
+
+/* ---- registry (interposer stand-ins) ------------------------------------ */
+/* MemState::allocate (proj/src/mem_model.cpp:48-86) plus physical
+ * placement; writes up to cap chunk ids, *n = number created. */
+int nx_alloc(nx_engine* e, uint32_t app, uint64_t size, int tier, uint64_t* chunks, size_t cap, size_t* n);
+/* MemState::free_chunk (proj/src/mem_model.cpp:88-116). */
+int nx_free_chunk(nx_engine* e, uint32_t app, uint64_t chunk, uint64_t* released);
+/* MemState::audit (proj/src/mem_model.cpp:274-325). */
+int nx_audit(nx_engine* e);
+/* MemState::app_bytes_resident for the four tiers. */
+int nx_app_resident(nx_engine* e, uint32_t app, uint64_t out[4]);
+/* MemState::pinned_physical / pinned_physical_peak (mem_model.cpp:244-247, 270-272). */
+int nx_pinned_physical(nx_engine* e, uint64_t* now, uint64_t* peak);
+
+/* ---- K4 synthetic working set ------------------------------------------- */
+int nx_fill_pattern(nx_engine* e, uint32_t app, uint64_t seed);
+/* Number of 16-byte vectors of app that differ from the pattern (0 = exact). */
+int nx_verify_pattern(nx_engine* e, uint32_t app, uint64_t seed, uint64_t* bad_vectors);
+/* Device pointer of a GPU-resident block's frame (NULL otherwise). */
+int nx_block_frame(nx_engine* e, uint64_t block, void** frame);
+int nx_block_checksum(nx_engine* e, uint64_t block, uint64_t* checksum);
+int nx_app_blocks(nx_engine* e, uint32_t app, uint64_t* blocks, size_t cap, size_t* n);
+/* Copies the 2 MiB of a resident block, wherever it lives, into host memory. */
+int nx_block_read(nx_engine* e, uint64_t block, void* host_dst);
+/* Overwrites one byte of a resident block in place (fault injection for the
+ * restore-verification tests). */
+int nx_block_poke(nx_engine* e, uint64_t block, uint64_t offset, uint8_t value);
+
+/* ---- swap-engine interface ----------------------------------------------- */
+/* plan_switch (proj/src/planner.cpp:111-216): the plan's dump()
+ * (`block src dst distance kind` lines) is written to dump (NUL-terminated,
+ * truncated to cap); *len = full length. */
+int nx_plan(nx_engine* e, uint32_t incoming, const nx_planner_config* cfg, char* dump, size_t cap, size_t* len,
+            uint64_t* bytes_in, uint64_t* bytes_out);
+/* plan_switch + execute (proj/src/transfer.cpp:250-271) with real copies:
+ * the modeled leg occupancy (transfer.cpp:173-186) becomes K1/K2 launches
+ * and host memcpy legs. drain_stream (cudaStream_t, may be NULL) is the
+ * incumbent's stream; evictions wait for its queued kernels on the device. */
+int nx_switch(nx_engine* e, uint32_t incoming, const nx_planner_config* cfg, void* drain_stream, nx_switch_stats* out);
+/* Per-lane leg sequence of the last switch (lane = 2*link + (up ? 0 : 1),
+ * transfer.cpp:39-45), in start order. */
+int nx_lane_trace(nx_engine* e, int lane, uint64_t* blocks, uint8_t* src, uint8_t* dst, size_t cap, size_t* n);
+uint64_t nx_total_launches(nx_engine* e);
+/* cudaStream_t of a PCIe lane: 0 = H2D, 1 = D2H. */
+void* nx_lane_stream(nx_engine* e, int lane);
+
+/* ---- host link ------------------------------------------------------------ */
+/* CE and SM bandwidth, H2D / D2H alone and simultaneously. */
+int nx_probe_pcie(nx_engine* e, uint64_t bytes_per_direction, uint64_t chunk_bytes, nx_pcie_probe* out);
+/* CopyPath::Auto table: sm_faster[k] for launches of 2^k legs. */
+int nx_set_auto_table(nx_engine* e, const int* sm_faster, size_t n);
+
+/* ---- scheduler + launch gate (§3, §6) ---------------------------- */
+/* MlfqConfig defaults (proj/include/nixie/mlfq.hpp:13-23). */
+void nx_mlfq_config_default(nx_mlfq_config* cfg);
+int nx_gate_create(nx_engine* e, const nx_mlfq_config* mcfg, const nx_planner_config* pcfg, nx_gate** out);
+void nx_gate_destroy(nx_gate* g);
+/* MlfqScheduler::register_app (mlfq.cpp:51-57) + the app's CUDA stream. */
+int nx_gate_attach(nx_gate* g, uint32_t app, void* stream, double now);
+/* Interposed kernel launch: *passed = 1 if the app may launch now; else its
+ * request is enqueued (mlfq.cpp:132-138) and its stream is gated on-device. */
+int nx_gate_before_launch(nx_gate* g, uint32_t app, double now, int* passed);
+/* MlfqScheduler::select_next (mlfq.cpp:144-162); *app = UINT32_MAX if none. */
+int nx_gate_select_next(nx_gate* g, double now, uint32_t* app);
+/* Pause incumbent, drain, plan, execute, grant `to`, release its gate. */
+int nx_gate_switch(nx_gate* g, uint32_t to, double now, nx_switch_stats* out);
+int nx_gate_granted(nx_gate* g, uint32_t* app);
+/* Test app kernel: sums the checksums of `app`'s blocks, reading them through
+ * the device frame table on `stream`; result (device-side) copied to *out
+ * after the stream reaches it. */
+int nx_gate_app_checksum_async(nx_gate* g, uint32_t app, void* stream, uint64_t* out_pinned);
+int nx_stream_sync(void* stream);
+int nx_pinned_alloc(size_t bytes, void** out);
+void nx_pinned_free(void* p);
+
+/* ---- workload driver / parity traces -------------------------------------- */
+/* Runs a scenario (include/nixie/scenario.hpp grammar) on the virtual clock
+ * with reference-identical link timing; no GPU needed. *trace is malloc'ed,
+ * free with nx_free. */
+int nx_scenario_model(const char* spec, char** trace, size_t* len);
+/* Same, with up to legs_per_lane legs in flight per lane (the concurrency the
+ * CUDA engine uses); per-lane sequences and placements must not change. */
+int nx_scenario_model_lanes(const char* spec, int legs_per_lane, char** trace, size_t* len);
+/* Same scenario through the CUDA engine (real copies). Every app is filled
+ * with the pattern (seed) up front; after each switch the incoming app is
+ * verified byte-exact (`V k app bad` lines) and at the end every app is. */
+int nx_scenario_real(const char* spec, const nx_engine_config* cfg, uint64_t seed, char** trace, size_t* len);
+void nx_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NIXIE_B200_H_ */

@@ -1,0 +1,76 @@
+// Launch interface of the sm_100a kernels (implemented in swap_kernels.cu),
+// callable from host C++ compiled by g++.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace nixie::b200 {
+
+// One 2 MiB leg. src/dst are device-visible addresses: HBM frames or mapped
+// pinned-host slots (UVA). For checksum-only legs dst is null; for fill /
+// compare legs `tag` carries the app id.
+struct NxLeg {
+  const void* src;
+  void* dst;
+  std::uint32_t block;
+  std::uint32_t tag;
+};
+
+inline constexpr int kMaxLegsPerLaunch = 256;  // d2h + h2d legs in one launch (kernel-parameter resident)
+inline constexpr int kMaxPartsLog2 = 4;        // a leg splits into at most 16 parts
+
+// Device-resident counters, read back once per switch.
+struct NxDevStatus {
+  unsigned long long mismatches;   // restores whose checksum differed from the departure checksum
+  unsigned long long verified;     // restores checked
+  unsigned long long unverified;   // restores of blocks with no recorded checksum
+  unsigned int n_bad;
+  unsigned int bad_blocks[64];
+};
+
+// Per-block checksum state (device arrays indexed by BlockId) plus the
+// per-stream scratch used to combine parts of a split leg.
+struct NxCkTables {
+  unsigned long long* ck_ref;   // checksum recorded when the block last left the GPU (or was filled)
+  unsigned long long* ck_seen;  // checksum observed at the last arrival on the GPU
+  unsigned int* ck_valid;       // 1 if ck_ref is meaningful
+  NxDevStatus* status;
+};
+
+struct NxScratch {
+  unsigned long long* part_sums;  // [kMaxLegsPerLaunch << kMaxPartsLog2]
+  unsigned int* part_count;       // [kMaxLegsPerLaunch], self-resetting
+};
+
+enum NxSwapFlags : std::uint32_t {
+  kNxVerify = 1u,      // compare arrival checksums with ck_ref
+  kNxNoChecksum = 2u,  // raw copy (probe only)
+};
+
+// K1: bidirectional swap. Legs [0, n_d2h) leave the GPU (their checksum is
+// recorded), legs [n_d2h, n_d2h + n_h2d) arrive (their checksum is checked).
+// With both lists non-empty every CTA runs one D2H warp group and one H2D
+// warp group; with one list, both groups serve it. Legs with dst == nullptr
+// are checksum-only (K3). Returns the launch error.
+cudaError_t launch_swap(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t flags, const NxCkTables& ck,
+                        const NxScratch& scratch, int max_ctas, cudaStream_t stream);
+
+// K4: pattern fill (records checksums, marks them valid) and compare (adds
+// the number of mismatching 16-byte vectors per leg into mismatches[i]).
+cudaError_t launch_fill(const NxLeg* legs, int n, std::uint64_t seed, const NxCkTables& ck, cudaStream_t stream);
+cudaError_t launch_compare(const NxLeg* legs, int n, std::uint64_t seed, unsigned long long* mismatches,
+                           cudaStream_t stream);
+
+// Number of SMs and the resident-CTA count used to size grids.
+int device_sm_count(int device);
+
+}  // namespace nixie::b200
+
+namespace nixie::b200 {
+// Launch-gate test kernel: out[0] += sum of block checksums read through the
+// frame table, out[1] += number of blocks with no frame.
+cudaError_t launch_table_checksum(const std::uint64_t* table, const unsigned* blocks, int n, unsigned long long* out,
+                                  cudaStream_t stream);
+}  // namespace nixie::b200

@@ -1,0 +1,901 @@
+// CUDA swap engine: the shared lane state machine (csrc/host/lanes.hpp)
+// driven by real copies. See include/nixie/swap_engine.hpp for the tier
+// backing; this file is the per-switch control loop.
+//
+// Control loop of execute():
+//   LaneSet::begin() starts the FIFO heads of every lane (up to the in-flight
+//   limit), each start = MemState::begin_move + a physical unit for the
+//   destination. Started PCIe legs are batched into K1 launches (or CE
+//   batches) on the lane's stream; started host legs go straight to the copy
+//   pool. The loop then polls batch-end events and pool completions, commits
+//   finished legs in per-lane FIFO order (LaneSet::finish_hop: commit_move,
+//   next hop, window, pump), and launches whatever the commits unblocked.
+//   A fetch into a full GPU therefore starts the moment the eviction that
+//   frees its frame has landed, with several launches queued per stream so
+//   the link never waits on the host.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <thread>
+
+#include "gate_ops.hpp"
+#include "lanes.hpp"
+#include "nixie/swap_engine.hpp"
+#include "nx_kernels.h"
+#include "phys.hpp"
+
+namespace nixie::b200 {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double secs_since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+constexpr int kH2D = 0;  // stream / PCIe lane index (lane 0 = pinned -> GPU)
+constexpr int kD2H = 1;  // (lane 1 = GPU -> pinned)
+constexpr std::uint32_t kBounceUnits = 64;  // 128 MiB pinned bounce for paged fills / compares
+
+int log2_bucket(int n) {
+  int k = 0;
+  while ((1 << (k + 1)) <= n) ++k;
+  return k;
+}
+
+}  // namespace
+
+struct ExecOptions {
+  cudaStream_t drain = nullptr;
+  CUdeviceptr gate_word = 0;  // written with gate_value on the H2D stream after the last fetch
+  std::uint64_t gate_value = 0;
+  cudaEvent_t gate_event = nullptr;  // recorded instead when stream memory ops are unavailable
+};
+
+struct SwapEngine::Impl final : detail::LaneSink {
+  EngineConfig cfg;
+  MemState mem;
+  HardwareConfig hw;
+  NumaInfo numa;
+  DeviceArena arena;
+  PinnedRing pinned;
+  PagedStore paged;
+  HostCopyPool pool;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaStream_t aux = nullptr;
+  int sm_count = 0;
+  int max_ctas = 0;
+
+  // Per-block state, indexed by BlockId.
+  std::vector<std::uint32_t> unit;  // frame / slot / paged unit of the block's current (source) tier
+  NxCkTables ck{};
+  std::size_t ck_cap = 0;
+  std::uint64_t* d_frames = nullptr;  // device frame table
+  std::uint64_t* h_frames = nullptr;  // pinned mirror
+  std::uint64_t* h_frames_stage = nullptr;
+  NxScratch scratch[2]{};
+  std::uint8_t* bounce = nullptr;  // pinned, kBounceUnits slots (outside the budget)
+  NxDevStatus status_seen{};
+  std::vector<bool> auto_sm;
+  std::uint64_t launches_total = 0;
+
+  // Per-execute state.
+  struct Leg {
+    std::size_t mi;
+    BlockId block;
+    TierId from, to;
+    std::uint32_t src_u, dst_u;
+    int lane;
+    bool done;
+    double t_start;
+    std::size_t rec;
+  };
+  struct Batch {
+    std::vector<std::uint32_t> legs;
+    cudaEvent_t ev_start, ev_end;
+    int stream;
+    bool ce;
+  };
+  detail::LaneSet* lanes = nullptr;
+  bool finished = false;
+  std::vector<Leg> legs;
+  std::array<std::vector<std::uint32_t>, detail::kLaneCount> pending;
+  std::array<std::deque<std::uint32_t>, detail::kLaneCount> host_fifo;
+  std::array<std::deque<Batch>, 2> inflight;
+  std::vector<Batch> landed;
+  std::vector<cudaEvent_t> events;
+  std::size_t events_used = 0;
+  cudaEvent_t ev0 = nullptr;
+  Clock::time_point t0;
+  SwitchStats stats;
+  std::array<std::vector<LegTrace>, detail::kLaneCount> trace;
+  std::vector<TransferRecord>* records = nullptr;
+  const ExecOptions* opts = nullptr;
+  std::size_t fetches_total = 0, fetches_submitted = 0;
+  AppId incoming = kNoApp;
+  bool gate_done = false;
+
+  explicit Impl(const EngineConfig& c) : cfg(c) {
+    if (cfg.gpu_capacity % kBlockBytes || cfg.pinned_capacity % kBlockBytes ||
+        (cfg.paged_capacity != kUnbounded && cfg.paged_capacity % kBlockBytes))
+      throw SimError(Err::ValidationError, "tier budgets must be multiples of 2 MiB");
+    if (cfg.legs_per_launch < 1 || cfg.legs_per_launch > kMaxLegsPerLaunch)
+      throw SimError(Err::ValidationError, "legs_per_launch must be in [1, 256]");
+    NX_CUDA(cudaSetDevice(cfg.device));
+    sm_count = device_sm_count(cfg.device);
+    max_ctas = cfg.max_ctas > 0 ? cfg.max_ctas : 2 * std::max(sm_count, 1);
+    if (cfg.numa_bind) numa = numa_for_device(cfg.device);
+
+    hw.tier_capacity[0] = cfg.gpu_capacity;
+    hw.tier_capacity[1] = cfg.pinned_capacity;
+    hw.tier_capacity[2] = cfg.paged_capacity;
+    hw.tier_capacity[3] = 0;
+    hw.apply_to(mem);
+
+    arena.init(cfg.gpu_capacity);
+    pinned.init(cfg.pinned_capacity, numa.node);
+    paged.init(cfg.paged_capacity);
+    pool.start(cfg.host_threads, numa.cpus);
+    for (auto& s : st) NX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    NX_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    NX_CUDA(cudaMalloc(&ck.status, sizeof(NxDevStatus)));
+    NX_CUDA(cudaMemset(ck.status, 0, sizeof(NxDevStatus)));
+    for (auto& s : scratch) {
+      NX_CUDA(cudaMalloc(&s.part_sums, sizeof(unsigned long long) * (kMaxLegsPerLaunch << kMaxPartsLog2)));
+      NX_CUDA(cudaMalloc(&s.part_count, sizeof(unsigned int) * kMaxLegsPerLaunch));
+      NX_CUDA(cudaMemset(s.part_count, 0, sizeof(unsigned int) * kMaxLegsPerLaunch));
+    }
+    void* b = nullptr;
+    NX_CUDA(cudaHostAlloc(&b, static_cast<std::size_t>(kBounceUnits) * kBlockBytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    bounce = static_cast<std::uint8_t*>(b);
+    NX_CUDA(cudaEventCreate(&ev0));
+    grow_tables(65536);
+  }
+
+  ~Impl() override {
+    cudaDeviceSynchronize();
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    if (ev0) cudaEventDestroy(ev0);
+    cudaFree(ck.ck_ref);
+    cudaFree(ck.ck_seen);
+    cudaFree(ck.ck_valid);
+    cudaFree(ck.status);
+    cudaFree(d_frames);
+    if (h_frames) cudaFreeHost(h_frames);
+    if (h_frames_stage) cudaFreeHost(h_frames_stage);
+    for (auto& s : scratch) {
+      cudaFree(s.part_sums);
+      cudaFree(s.part_count);
+    }
+    if (bounce) cudaFreeHost(bounce);
+    for (auto& s : st) cudaStreamDestroy(s);
+    cudaStreamDestroy(aux);
+  }
+
+  // ---- per-block tables -------------------------------------------------
+  template <typename T>
+  void grow_dev(T*& p, std::size_t old_n, std::size_t new_n) {
+    T* q = nullptr;
+    NX_CUDA(cudaMalloc(&q, sizeof(T) * new_n));
+    NX_CUDA(cudaMemset(q, 0, sizeof(T) * new_n));
+    if (p) {
+      NX_CUDA(cudaMemcpy(q, p, sizeof(T) * old_n, cudaMemcpyDeviceToDevice));
+      cudaFree(p);
+    }
+    p = q;
+  }
+
+  void grow_tables(std::size_t need) {
+    if (need <= ck_cap) return;
+    const std::size_t cap = std::max(need, 2 * ck_cap);
+    NX_CUDA(cudaDeviceSynchronize());
+    grow_dev(ck.ck_ref, ck_cap, cap);
+    grow_dev(ck.ck_seen, ck_cap, cap);
+    grow_dev(ck.ck_valid, ck_cap, cap);
+    grow_dev(d_frames, ck_cap, cap);
+    for (std::uint64_t** h : {&h_frames, &h_frames_stage}) {
+      void* q = nullptr;
+      NX_CUDA(cudaHostAlloc(&q, sizeof(std::uint64_t) * cap, cudaHostAllocPortable));
+      std::memset(q, 0, sizeof(std::uint64_t) * cap);
+      if (*h) {
+        std::memcpy(q, *h, sizeof(std::uint64_t) * ck_cap);
+        cudaFreeHost(*h);
+      }
+      *h = static_cast<std::uint64_t*>(q);
+    }
+    ck_cap = cap;
+  }
+
+  UnitRing& ring_of(TierId t) {
+    switch (t) {
+      case TierId::Gpu: return arena.ring;
+      case TierId::PinnedHost: return pinned.ring;
+      case TierId::PagedHost: return paged.ring;
+      default: throw SimError(Err::InvalidState, "the disk tier is not backed by the CUDA swap engine");
+    }
+  }
+
+  // Device-visible address of a unit (GPU frame or mapped pinned slot).
+  void* dev_addr(TierId t, std::uint32_t u) {
+    if (t == TierId::Gpu) return arena.frame(u);
+    if (t == TierId::PinnedHost) return pinned.dev(u);
+    throw InvariantViolation("PCIe leg touches a non-PCIe tier");
+  }
+  std::uint8_t* host_addr(TierId t, std::uint32_t u) {
+    if (t == TierId::PinnedHost) return pinned.host(u);
+    if (t == TierId::PagedHost) return paged.unit(u);
+    throw InvariantViolation("host leg touches a non-host tier");
+  }
+
+  // ---- registry entry points ---------------------------------------------
+  std::vector<ChunkId> allocate(AppId app, Bytes size, TierId tier) {
+    if (tier == TierId::Disk) throw SimError(Err::InvalidState, "the disk tier is not backed by the CUDA swap engine");
+    const std::size_t first = mem.block_count();
+    std::vector<ChunkId> out = mem.allocate(app, size, tier);
+    const std::size_t last = mem.block_count();
+    grow_tables(last);
+    unit.resize(last);
+    UnitRing& ring = ring_of(tier);
+    for (std::size_t b = first; b < last; ++b) {
+      unit[b] = ring.acquire(tier_name(tier));
+      h_frames[b] = tier == TierId::Gpu ? reinterpret_cast<std::uint64_t>(arena.frame(unit[b])) : 0;
+    }
+    if (tier == TierId::PagedHost)  // touch now, not inside a timed switch
+      for (std::size_t b = first; b < last; ++b) std::memset(paged.unit(unit[b]), 0, 4096);
+    push_frame_table(aux);
+    NX_CUDA(cudaStreamSynchronize(aux));
+    return out;
+  }
+
+  Bytes free_chunk(AppId app, ChunkId c) {
+    std::vector<std::pair<BlockId, TierId>> where;
+    if (mem.has_chunk(c))
+      for (BlockId b : mem.chunk(c).blocks) where.emplace_back(b, mem.block(b).loc.tier);
+    const Bytes released = mem.free_chunk(app, c);  // throws before any physical change
+    for (auto [b, t] : where) {
+      ring_of(t).release(unit[b]);
+      h_frames[b] = 0;
+    }
+    return released;
+  }
+
+  void push_frame_table(cudaStream_t s) {
+    const std::size_t n = mem.block_count();
+    if (n == 0) return;
+    NX_CUDA(cudaMemcpyAsync(d_frames, h_frames, sizeof(std::uint64_t) * n, cudaMemcpyHostToDevice, s));
+  }
+
+  // ---- K4 pattern fill / compare ----------------------------------------
+  std::vector<BlockId> blocks_of(AppId app) {
+    std::vector<BlockId> out;
+    for (ChunkId c : mem.chunks_of(app))
+      for (BlockId b : mem.chunk(c).blocks) {
+        if (!mem.block(b).loc.is_resident()) throw SimError(Err::InvalidState, "block in flight");
+        out.push_back(b);
+      }
+    return out;
+  }
+
+  void fill_pattern(AppId app, std::uint64_t seed) {
+    std::vector<NxLeg> direct;
+    std::vector<BlockId> paged_blocks;
+    for (BlockId b : blocks_of(app)) {
+      const TierId t = mem.block(b).loc.tier;
+      if (t == TierId::PagedHost)
+        paged_blocks.push_back(b);
+      else
+        direct.push_back(NxLeg{nullptr, dev_addr(t, unit[b]), static_cast<std::uint32_t>(b), app});
+    }
+    NX_CUDA(launch_fill(direct.data(), static_cast<int>(direct.size()), seed, ck, aux));
+    launches_total += (direct.size() + kMaxLegsPerLaunch - 1) / kMaxLegsPerLaunch;
+    for (std::size_t i = 0; i < paged_blocks.size(); i += kBounceUnits) {
+      const std::size_t n = std::min<std::size_t>(kBounceUnits, paged_blocks.size() - i);
+      std::vector<NxLeg> legs;
+      std::vector<std::pair<void*, const void*>> copies;
+      for (std::size_t k = 0; k < n; ++k) {
+        const BlockId b = paged_blocks[i + k];
+        std::uint8_t* slot = bounce + k * kBlockBytes;
+        legs.push_back(NxLeg{nullptr, slot, static_cast<std::uint32_t>(b), app});
+        copies.emplace_back(paged.unit(unit[b]), slot);
+      }
+      NX_CUDA(launch_fill(legs.data(), static_cast<int>(n), seed, ck, aux));
+      ++launches_total;
+      NX_CUDA(cudaStreamSynchronize(aux));
+      pool.copy_all(copies, kBlockBytes);
+    }
+    NX_CUDA(cudaStreamSynchronize(aux));
+  }
+
+  // Sums per-leg mismatch counts of one compare launch.
+  std::uint64_t compare_into(const std::vector<NxLeg>& legs_, std::uint64_t seed, unsigned long long* d_mis) {
+    if (legs_.empty()) return 0;
+    NX_CUDA(cudaMemsetAsync(d_mis, 0, sizeof(unsigned long long) * legs_.size(), aux));
+    NX_CUDA(launch_compare(legs_.data(), static_cast<int>(legs_.size()), seed, d_mis, aux));
+    launches_total += (legs_.size() + kMaxLegsPerLaunch - 1) / kMaxLegsPerLaunch;
+    std::vector<unsigned long long> h(legs_.size());
+    NX_CUDA(cudaMemcpyAsync(h.data(), d_mis, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, aux));
+    NX_CUDA(cudaStreamSynchronize(aux));
+    std::uint64_t bad = 0;
+    for (auto v : h) bad += v;
+    return bad;
+  }
+
+  std::uint64_t verify_pattern(AppId app, std::uint64_t seed) {
+    std::vector<NxLeg> direct;
+    std::vector<BlockId> paged_blocks;
+    for (BlockId b : blocks_of(app)) {
+      const TierId t = mem.block(b).loc.tier;
+      if (t == TierId::PagedHost)
+        paged_blocks.push_back(b);
+      else
+        direct.push_back(NxLeg{dev_addr(t, unit[b]), nullptr, static_cast<std::uint32_t>(b), app});
+    }
+    unsigned long long* d_mis = nullptr;
+    NX_CUDA(cudaMalloc(&d_mis, sizeof(unsigned long long) * std::max<std::size_t>(direct.size(), kBounceUnits)));
+    std::uint64_t bad = 0;
+    try {
+      bad += compare_into(direct, seed, d_mis);
+      for (std::size_t i = 0; i < paged_blocks.size(); i += kBounceUnits) {
+        const std::size_t n = std::min<std::size_t>(kBounceUnits, paged_blocks.size() - i);
+        std::vector<std::pair<void*, const void*>> copies;
+        std::vector<NxLeg> batch;
+        for (std::size_t k = 0; k < n; ++k) {
+          const BlockId b = paged_blocks[i + k];
+          copies.emplace_back(bounce + k * kBlockBytes, paged.unit(unit[b]));
+          batch.push_back(NxLeg{bounce + k * kBlockBytes, nullptr, static_cast<std::uint32_t>(b), app});
+        }
+        pool.copy_all(copies, kBlockBytes);
+        bad += compare_into(batch, seed, d_mis);
+      }
+    } catch (...) {
+      cudaFree(d_mis);
+      throw;
+    }
+    cudaFree(d_mis);
+    return bad;
+  }
+
+  // ---- lane sink ----------------------------------------------------------
+  void leg_started(int lane, std::size_t mi, TierId from, TierId to, bool) override {
+    const BlockId b = lanes->move(mi).block;
+    Leg L{mi, b, from, to, unit[b], ring_of(to).acquire(tier_name(to)), lane, false, secs_since(t0), 0};
+    const auto idx = static_cast<std::uint32_t>(legs.size());
+    legs.push_back(L);
+    trace[lane].push_back(LegTrace{b, from, to});
+    if (lane == kH2D || lane == kD2H) {
+      pending[lane].push_back(idx);
+    } else {
+      host_fifo[lane].push_back(idx);
+      pool.submit(host_addr(to, L.dst_u), host_addr(from, L.src_u), kBlockBytes, idx);
+      stats.host_bytes += kBlockBytes;
+      ++stats.host_legs;
+    }
+  }
+
+  void plan_finished() override { finished = true; }
+
+  cudaEvent_t take_event() {
+    if (events_used == events.size()) {
+      cudaEvent_t e;
+      NX_CUDA(cudaEventCreate(&e));
+      events.push_back(e);
+    }
+    return events[events_used++];
+  }
+
+  bool use_sm_kernel(int n_legs) const {
+    switch (cfg.path) {
+      case CopyPath::SmKernel: return true;
+      case CopyPath::CopyEngine: return false;
+      case CopyPath::Auto: {
+        const auto k = static_cast<std::size_t>(log2_bucket(n_legs));
+        return auto_sm.empty() ? true : auto_sm[std::min(k, auto_sm.size() - 1)];
+      }
+    }
+    return true;
+  }
+
+  NxLeg kernel_leg(const Leg& L) {
+    return NxLeg{dev_addr(L.from, L.src_u), dev_addr(L.to, L.dst_u), static_cast<std::uint32_t>(L.block), 0};
+  }
+
+  // Submits `d2h` and `h2d` legs as one batch on stream `s`.
+  void submit(int s, const std::vector<std::uint32_t>& d2h, const std::vector<std::uint32_t>& h2d) {
+    Batch B;
+    B.stream = s;
+    B.legs = d2h;
+    B.legs.insert(B.legs.end(), h2d.begin(), h2d.end());
+    B.ev_start = take_event();
+    B.ev_end = take_event();
+    B.ce = !use_sm_kernel(static_cast<int>(B.legs.size()));
+    const std::uint32_t flags = cfg.verify ? kNxVerify : 0u;
+    NX_CUDA(cudaEventRecord(B.ev_start, st[s]));
+    if (!B.ce) {
+      std::vector<NxLeg> kl;
+      kl.reserve(B.legs.size());
+      for (auto i : B.legs) kl.push_back(kernel_leg(legs[i]));
+      NX_CUDA(launch_swap(kl.data(), static_cast<int>(d2h.size()), static_cast<int>(h2d.size()), flags, ck, scratch[s],
+                          max_ctas, st[s]));
+      ++stats.launches[s];
+      ++launches_total;
+    } else {
+      // K2: copy engines, with K3 checksum launches around them.
+      std::vector<NxLeg> ckl;
+      for (auto i : d2h) ckl.push_back(NxLeg{dev_addr(legs[i].from, legs[i].src_u), nullptr, static_cast<std::uint32_t>(legs[i].block), 0});
+      if (!ckl.empty()) {
+        NX_CUDA(launch_swap(ckl.data(), static_cast<int>(ckl.size()), 0, flags, ck, scratch[s], max_ctas, st[s]));
+        ++stats.launches[s];
+        ++launches_total;
+      }
+      copy_runs(d2h, s, cudaMemcpyDeviceToHost);
+      copy_runs(h2d, s, cudaMemcpyHostToDevice);
+      ckl.clear();
+      for (auto i : h2d) ckl.push_back(NxLeg{dev_addr(legs[i].to, legs[i].dst_u), nullptr, static_cast<std::uint32_t>(legs[i].block), 0});
+      if (!ckl.empty()) {
+        NX_CUDA(launch_swap(ckl.data(), 0, static_cast<int>(ckl.size()), flags, ck, scratch[s], max_ctas, st[s]));
+        ++stats.launches[s];
+        ++launches_total;
+      }
+      ++stats.ce_batches[s];
+    }
+    NX_CUDA(cudaEventRecord(B.ev_end, st[s]));
+    stats.pcie_d2h_bytes += d2h.size() * kBlockBytes;
+    for (auto i : h2d) {
+      stats.pcie_h2d_bytes += kBlockBytes;
+      const Leg& L = legs[i];
+      h_frames[L.block] = reinterpret_cast<std::uint64_t>(arena.frame(L.dst_u));
+      if (lanes->move(L.mi).dst == TierId::Gpu) ++fetches_submitted;
+    }
+    inflight[s].push_back(std::move(B));
+    maybe_release_gate();
+  }
+
+  // cudaMemcpyAsync over runs of legs whose source and destination are both contiguous.
+  void copy_runs(const std::vector<std::uint32_t>& idx, int s, cudaMemcpyKind kind) {
+    std::size_t i = 0;
+    while (i < idx.size()) {
+      const Leg& a = legs[idx[i]];
+      auto* src = static_cast<std::uint8_t*>(dev_addr(a.from, a.src_u));
+      auto* dst = static_cast<std::uint8_t*>(dev_addr(a.to, a.dst_u));
+      std::size_t n = 1;
+      while (i + n < idx.size()) {
+        const Leg& c = legs[idx[i + n]];
+        if (dev_addr(c.from, c.src_u) != src + n * kBlockBytes || dev_addr(c.to, c.dst_u) != dst + n * kBlockBytes) break;
+        ++n;
+      }
+      NX_CUDA(cudaMemcpyAsync(dst, src, n * kBlockBytes, kind, st[s]));
+      i += n;
+    }
+  }
+
+  // Once every fetch has been submitted, publish the incoming app's frame
+  // table and open its launch gate on the H2D stream (device side).
+  void maybe_release_gate() {
+    if (gate_done || opts == nullptr || fetches_submitted < fetches_total) return;
+    gate_done = true;
+    for (ChunkId c : mem.chunks_of(incoming))
+      for (BlockId b : mem.chunk(c).blocks) {
+        const Location& loc = mem.block(b).loc;
+        if (loc.is_resident() && loc.tier == TierId::Gpu) h_frames[b] = reinterpret_cast<std::uint64_t>(arena.frame(unit[b]));
+      }
+    const std::size_t n = mem.block_count();
+    std::memcpy(h_frames_stage, h_frames, sizeof(std::uint64_t) * n);
+    NX_CUDA(cudaMemcpyAsync(d_frames, h_frames_stage, sizeof(std::uint64_t) * n, cudaMemcpyHostToDevice, st[kH2D]));
+    if (opts->gate_word != 0) {
+      if (gate_write(reinterpret_cast<CUstream>(st[kH2D]), opts->gate_word, opts->gate_value) != CUDA_SUCCESS)
+        throw SimError(Err::IoError, "cuStreamWriteValue64 failed");
+    } else if (opts->gate_event != nullptr) {
+      NX_CUDA(cudaEventRecord(opts->gate_event, st[kH2D]));
+    }
+  }
+
+  void flush() {
+    const int L = cfg.legs_per_launch;
+    if (cfg.fused_launch) {
+      while (!pending[kD2H].empty() || !pending[kH2D].empty()) {
+        if (inflight[kD2H].size() >= 2 && static_cast<int>(pending[kD2H].size() + pending[kH2D].size()) < L) break;
+        const int take_h = std::min<int>(static_cast<int>(pending[kH2D].size()), std::max(L / 2, L - static_cast<int>(pending[kD2H].size())));
+        const int take_d = std::min<int>(static_cast<int>(pending[kD2H].size()), L - take_h);
+        std::vector<std::uint32_t> d(pending[kD2H].begin(), pending[kD2H].begin() + take_d);
+        std::vector<std::uint32_t> h(pending[kH2D].begin(), pending[kH2D].begin() + take_h);
+        pending[kD2H].erase(pending[kD2H].begin(), pending[kD2H].begin() + take_d);
+        pending[kH2D].erase(pending[kH2D].begin(), pending[kH2D].begin() + take_h);
+        submit(kD2H, d, h);
+      }
+      return;
+    }
+    for (int lane : {kD2H, kH2D}) {
+      auto& p = pending[lane];
+      while (!p.empty()) {
+        // Enough queued on the stream to hide the host: wait for a full batch.
+        if (inflight[lane].size() >= 2 && static_cast<int>(p.size()) < L) break;
+        const int take = std::min<int>(static_cast<int>(p.size()), L);
+        std::vector<std::uint32_t> part(p.begin(), p.begin() + take);
+        p.erase(p.begin(), p.begin() + take);
+        if (lane == kD2H)
+          submit(kD2H, part, {});
+        else
+          submit(kH2D, {}, part);
+      }
+    }
+  }
+
+  void complete(std::uint32_t idx) {
+    Leg& L = legs[idx];
+    L.done = true;
+    ring_of(L.from).release(L.src_u);
+    unit[L.block] = L.dst_u;
+    if (L.from == TierId::Gpu) h_frames[L.block] = 0;
+    if (records) {
+      L.rec = records->size();
+      records->push_back(TransferRecord{L.t_start, secs_since(t0), L.block, L.from, L.to, kBlockBytes});
+    }
+    lanes->finish_hop(L.lane, L.mi, L.to);
+  }
+
+  bool poll() {
+    bool progress = false;
+    for (int s = 0; s < 2; ++s) {
+      while (!inflight[s].empty()) {
+        const cudaError_t e = cudaEventQuery(inflight[s].front().ev_end);
+        if (e == cudaErrorNotReady) break;
+        NX_CUDA(e);
+        Batch B = std::move(inflight[s].front());
+        inflight[s].pop_front();
+        for (auto i : B.legs) complete(i);
+        landed.push_back(std::move(B));
+        progress = true;
+      }
+    }
+    static thread_local std::vector<std::uint64_t> toks;
+    toks.clear();
+    if (pool.drain(toks)) {
+      for (auto t : toks) legs[t].done = true;  // committed below, in FIFO order
+      progress = true;
+    }
+    for (int lane = 2; lane < detail::kLaneCount; ++lane) {
+      auto& q = host_fifo[lane];
+      while (!q.empty() && legs[q.front()].done) {
+        const std::uint32_t i = q.front();
+        q.pop_front();
+        complete(i);
+      }
+    }
+    return progress;
+  }
+
+  ExecResult execute(const MigrationPlan& plan, const PlannerConfig& pcfg, const ExecOptions& o) {
+    for (const Move& m : plan.moves)
+      if (m.src == TierId::Disk || m.dst == TierId::Disk)
+        throw SimError(Err::InvalidState, "plan touches the disk tier, which the CUDA swap engine does not back");
+    ExecResult res;
+    stats = SwitchStats{};
+    stats.bytes_in = plan.bytes_in;
+    stats.bytes_out = plan.bytes_out;
+    for (auto& t : trace) t.clear();
+    legs.clear();
+    landed.clear();
+    events_used = 0;
+    records = &res.events;
+    opts = &o;
+    incoming = plan.incoming_app;
+    gate_done = false;
+    fetches_total = 0;
+    fetches_submitted = 0;
+    for (const Move& m : plan.moves)
+      if (m.dst == TierId::Gpu) ++fetches_total;
+
+    detail::LaneSet ls(mem, hw);
+    ls.set_limit(kH2D, cfg.pcie_legs_in_flight);
+    ls.set_limit(kD2H, cfg.pcie_legs_in_flight);
+    ls.set_limit(2, cfg.host_legs_in_flight);
+    ls.set_limit(3, cfg.host_legs_in_flight);
+    lanes = &ls;
+    finished = false;
+
+    t0 = Clock::now();
+    NX_CUDA(cudaEventRecord(ev0, st[kD2H]));
+    if (o.drain != nullptr) {
+      cudaEvent_t d = take_event();
+      NX_CUDA(cudaEventRecord(d, o.drain));
+      NX_CUDA(cudaStreamWaitEvent(st[kD2H], d, 0));
+      if (cfg.fused_launch) NX_CUDA(cudaStreamWaitEvent(st[kH2D], d, 0));
+    }
+    AppId owner = kNoApp;
+    for (const Move& m : plan.moves)
+      if (m.kind == MoveKind::EvictFromGpu) {
+        owner = mem.block(m.block).app;
+        break;
+      }
+    try {
+      ls.begin(plan, pcfg, /*gate_evictions=*/false, owner, this);
+      maybe_release_gate();  // no fetches at all: open immediately
+      flush();
+      auto last = Clock::now();
+      while (!finished) {
+        if (poll()) {
+          flush();
+          last = Clock::now();
+        } else {
+          if (std::chrono::duration<double>(Clock::now() - last).count() > 120.0)
+            throw InvariantViolation("swap engine made no progress for 120 s");
+          std::this_thread::yield();
+        }
+      }
+    } catch (...) {
+      lanes = nullptr;
+      cudaStreamSynchronize(st[0]);
+      cudaStreamSynchronize(st[1]);
+      throw;
+    }
+    lanes = nullptr;
+    stats.wall_s = secs_since(t0);
+    res.completion = stats.wall_s;
+    finalize_timing(res);
+    check_status();
+    return res;
+  }
+
+  // Device timestamps for the PCIe records and the per-stream kernel time.
+  void finalize_timing(ExecResult& res) {
+    double first = 1e30, last = 0;
+    for (const Batch& B : landed) {
+      float a = 0, b = 0;
+      NX_CUDA(cudaEventElapsedTime(&a, ev0, B.ev_start));
+      NX_CUDA(cudaEventElapsedTime(&b, ev0, B.ev_end));
+      const double s0 = a * 1e-3, s1 = b * 1e-3;
+      first = std::min(first, s0);
+      last = std::max(last, s1);
+      stats.kernel_s[B.stream] += s1 - s0;
+      for (auto i : B.legs) {
+        TransferRecord& r = res.events[legs[i].rec];
+        r.start = s0;
+        r.end = s1;
+      }
+    }
+    stats.device_span_s = landed.empty() ? 0.0 : last - first;
+  }
+
+  void check_status() {
+    NxDevStatus now{};
+    NX_CUDA(cudaMemcpy(&now, ck.status, sizeof(now), cudaMemcpyDeviceToHost));
+    stats.verified = now.verified - status_seen.verified;
+    stats.unverified = now.unverified - status_seen.unverified;
+    stats.mismatches = now.mismatches - status_seen.mismatches;
+    const unsigned first_bad = status_seen.n_bad;
+    status_seen = now;
+    if (stats.mismatches != 0) {
+      std::string which;
+      for (unsigned k = first_bad; k < now.n_bad && k < 64; ++k) which += " " + std::to_string(now.bad_blocks[k]);
+      throw InvariantViolation("restore checksum mismatch on " + std::to_string(stats.mismatches) + " block(s):" + which);
+    }
+  }
+};
+
+// ---- driver-API entry points for the launch gate ---------------------------
+namespace {
+using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+WriteFn g_write = nullptr;
+WaitFn g_wait = nullptr;
+bool resolve_mem_ops() {
+  static bool tried = false, ok = false;
+  if (tried) return ok;
+  tried = true;
+  cudaDriverEntryPointQueryResult q1{}, q2{};
+  void* w = nullptr;
+  void* t = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &w, cudaEnableDefault, &q1) != cudaSuccess || !w) return false;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &t, cudaEnableDefault, &q2) != cudaSuccess || !t) return false;
+  g_write = reinterpret_cast<WriteFn>(w);
+  g_wait = reinterpret_cast<WaitFn>(t);
+  ok = true;
+  return ok;
+}
+}  // namespace
+
+CUresult gate_write(CUstream s, CUdeviceptr addr, std::uint64_t v) {
+  if (!resolve_mem_ops()) return CUDA_ERROR_NOT_SUPPORTED;
+  return g_write(s, addr, v, 0);
+}
+
+CUresult gate_wait_geq(CUstream s, CUdeviceptr addr, std::uint64_t v) {
+  if (!resolve_mem_ops()) return CUDA_ERROR_NOT_SUPPORTED;
+  return g_wait(s, addr, v, CU_STREAM_WAIT_VALUE_GEQ);
+}
+
+bool gate_mem_ops_available() { return resolve_mem_ops(); }
+
+// ---- SwapEngine ---------------------------------------------------------------
+SwapEngine::SwapEngine(const EngineConfig& cfg) : impl_(std::make_unique<Impl>(cfg)) {}
+SwapEngine::~SwapEngine() = default;
+const EngineConfig& SwapEngine::config() const { return impl_->cfg; }
+MemState& SwapEngine::mem() { return impl_->mem; }
+const MemState& SwapEngine::mem() const { return impl_->mem; }
+HardwareConfig SwapEngine::hardware() const { return impl_->hw; }
+std::vector<ChunkId> SwapEngine::allocate(AppId app, Bytes size, TierId tier) { return impl_->allocate(app, size, tier); }
+Bytes SwapEngine::free_chunk(AppId app, ChunkId chunk) { return impl_->free_chunk(app, chunk); }
+void SwapEngine::fill_pattern(AppId app, std::uint64_t seed) { impl_->fill_pattern(app, seed); }
+std::uint64_t SwapEngine::verify_pattern(AppId app, std::uint64_t seed) { return impl_->verify_pattern(app, seed); }
+
+ExecResult SwapEngine::execute(const MigrationPlan& plan, const PlannerConfig& cfg, cudaStream_t drain,
+                               const GateRelease* release) {
+  ExecOptions o;
+  o.drain = drain;
+  if (release != nullptr) {
+    o.gate_word = reinterpret_cast<CUdeviceptr>(release->device_word);
+    o.gate_value = release->value;
+    o.gate_event = release->event;
+  }
+  return impl_->execute(plan, cfg, o);
+}
+
+ExecResult SwapEngine::switch_to(AppId incoming, const PlannerConfig& cfg, cudaStream_t drain) {
+  const auto t = Clock::now();
+  MigrationPlan plan = plan_switch(incoming, impl_->mem, cfg);
+  const double plan_s = secs_since(t);
+  ExecResult r = execute(plan, cfg, drain);
+  impl_->stats.plan_s = plan_s;
+  return r;
+}
+
+const SwitchStats& SwapEngine::last_stats() const { return impl_->stats; }
+const std::array<std::vector<LegTrace>, 6>& SwapEngine::lane_trace() const { return impl_->trace; }
+std::uint64_t SwapEngine::total_launches() const { return impl_->launches_total; }
+
+void* SwapEngine::frame_of(BlockId b) const {
+  const Location& loc = impl_->mem.block(b).loc;
+  if (!loc.is_resident() || loc.tier != TierId::Gpu) return nullptr;
+  return impl_->arena.frame(impl_->unit[b]);
+}
+const std::uint64_t* SwapEngine::device_frame_table() const { return impl_->d_frames; }
+
+std::uint64_t SwapEngine::block_checksum(BlockId b) const {
+  unsigned long long v = 0;
+  NX_CUDA(cudaMemcpy(&v, impl_->ck.ck_ref + b, sizeof(v), cudaMemcpyDeviceToHost));
+  return v;
+}
+
+cudaStream_t SwapEngine::stream(int lane) const { return impl_->st[lane == 0 ? kH2D : kD2H]; }
+
+void SwapEngine::read_block(BlockId b, void* dst) {
+  Impl& m = *impl_;
+  const Location& loc = m.mem.block(b).loc;
+  if (!loc.is_resident()) throw SimError(Err::InvalidState, "block in flight");
+  if (loc.tier == TierId::Gpu)
+    NX_CUDA(cudaMemcpy(dst, m.arena.frame(m.unit[b]), kBlockBytes, cudaMemcpyDeviceToHost));
+  else
+    std::memcpy(dst, m.host_addr(loc.tier, m.unit[b]), kBlockBytes);
+}
+
+void SwapEngine::poke_block(BlockId b, std::uint64_t offset, std::uint8_t value) {
+  Impl& m = *impl_;
+  const Location& loc = m.mem.block(b).loc;
+  if (!loc.is_resident()) throw SimError(Err::InvalidState, "block in flight");
+  if (offset >= kBlockBytes) throw SimError(Err::InvalidState, "offset outside the block");
+  if (loc.tier == TierId::Gpu)
+    NX_CUDA(cudaMemcpy(m.arena.frame(m.unit[b]) + offset, &value, 1, cudaMemcpyHostToDevice));
+  else
+    m.host_addr(loc.tier, m.unit[b])[offset] = value;
+}
+
+void SwapEngine::set_auto_table(const std::vector<bool>& sm_faster) { impl_->auto_sm = sm_faster; }
+
+}  // namespace nixie::b200
+
+// ---- host-link probe ----------------------------------------------------------
+namespace nixie::b200 {
+
+namespace {
+struct ProbeBufs {
+  std::uint8_t* dev[2] = {nullptr, nullptr};
+  std::uint8_t* host[2] = {nullptr, nullptr};
+  ~ProbeBufs() {
+    for (auto* p : dev)
+      if (p) cudaFree(p);
+    for (auto* p : host)
+      if (p) cudaFreeHost(p);
+  }
+};
+}  // namespace
+
+// CE and SM-kernel bandwidth of the host link, each direction alone and both
+// at once (the bidirectional figure is the roofline denominator of the swap).
+PcieProbe SwapEngine::probe_pcie(Bytes bytes, Bytes chunk) {
+  Impl& m = *impl_;
+  if (chunk < kBlockBytes || chunk % kBlockBytes) chunk = kBlockBytes;
+  bytes = std::max<Bytes>(chunk, bytes - bytes % chunk);
+  PcieProbe out;
+  out.bytes_per_direction = bytes;
+  out.chunk_bytes = chunk;
+  out.numa_node = m.numa.node;
+  ProbeBufs b;
+  for (int i = 0; i < 2; ++i) {
+    NX_CUDA(cudaMalloc(&b.dev[i], bytes));
+    NX_CUDA(cudaMemset(b.dev[i], i, bytes));
+    prefer_numa_node(m.numa.node);
+    void* h = nullptr;
+    const cudaError_t e = cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+    prefer_numa_node(-1);
+    NX_CUDA(e);
+    b.host[i] = static_cast<std::uint8_t*>(h);
+    std::memset(h, 1 + i, bytes);
+  }
+  const int legs_per_chunk = static_cast<int>(chunk / kBlockBytes);
+  // dir 0 = H2D (host[1] -> dev[1]) on st[0], dir 1 = D2H (dev[0] -> host[0]) on st[1].
+  auto issue = [&](int dir, bool sm) {
+    cudaStream_t s = m.st[dir];
+    for (Bytes off = 0; off < bytes; off += chunk) {
+      if (!sm) {
+        if (dir == 0)
+          NX_CUDA(cudaMemcpyAsync(b.dev[1] + off, b.host[1] + off, chunk, cudaMemcpyHostToDevice, s));
+        else
+          NX_CUDA(cudaMemcpyAsync(b.host[0] + off, b.dev[0] + off, chunk, cudaMemcpyDeviceToHost, s));
+        continue;
+      }
+      std::vector<NxLeg> legs;
+      for (int k = 0; k < legs_per_chunk; ++k) {
+        const Bytes o = off + static_cast<Bytes>(k) * kBlockBytes;
+        if (legs.size() == static_cast<std::size_t>(kMaxLegsPerLaunch)) {
+          NX_CUDA(launch_swap(legs.data(), dir == 1 ? static_cast<int>(legs.size()) : 0, dir == 0 ? static_cast<int>(legs.size()) : 0,
+                              kNxNoChecksum, m.ck, m.scratch[dir], m.max_ctas, s));
+          legs.clear();
+        }
+        if (dir == 0)
+          legs.push_back(NxLeg{b.host[1] + o, b.dev[1] + o, 0, 0});
+        else
+          legs.push_back(NxLeg{b.dev[0] + o, b.host[0] + o, 0, 0});
+      }
+      NX_CUDA(launch_swap(legs.data(), dir == 1 ? static_cast<int>(legs.size()) : 0, dir == 0 ? static_cast<int>(legs.size()) : 0,
+                          kNxNoChecksum, m.ck, m.scratch[dir], m.max_ctas, s));
+      ++m.launches_total;
+    }
+  };
+  cudaEvent_t ev[4];
+  for (auto& e : ev) NX_CUDA(cudaEventCreate(&e));
+  auto run = [&](bool sm, bool h2d, bool d2h, double* gbs_h2d, double* gbs_d2h, double* gbs_total) {
+    double best_h = 0, best_d = 0, best_t = 0;
+    for (int rep = 0; rep < 4; ++rep) {
+      NX_CUDA(cudaDeviceSynchronize());
+      if (h2d) NX_CUDA(cudaEventRecord(ev[0], m.st[0]));
+      if (d2h) NX_CUDA(cudaEventRecord(ev[2], m.st[1]));
+      if (h2d) issue(0, sm);
+      if (d2h) issue(1, sm);
+      if (h2d) NX_CUDA(cudaEventRecord(ev[1], m.st[0]));
+      if (d2h) NX_CUDA(cudaEventRecord(ev[3], m.st[1]));
+      NX_CUDA(cudaDeviceSynchronize());
+      float th = 0, td = 0, a = 0, z = 0;
+      if (h2d) NX_CUDA(cudaEventElapsedTime(&th, ev[0], ev[1]));
+      if (d2h) NX_CUDA(cudaEventElapsedTime(&td, ev[2], ev[3]));
+      if (rep == 0) continue;  // warm-up
+      double total = 0;
+      if (h2d && d2h) {
+        // span from the earlier start to the later end
+        NX_CUDA(cudaEventElapsedTime(&a, ev[0], ev[2]));
+        NX_CUDA(cudaEventElapsedTime(&z, ev[0], ev[3]));
+        const double span = std::max<double>(th, z) - std::min<double>(0.0, a);
+        total = 2.0 * static_cast<double>(bytes) / (span * 1e-3) / 1e9;
+      }
+      if (h2d) best_h = std::max(best_h, static_cast<double>(bytes) / (th * 1e-3) / 1e9);
+      if (d2h) best_d = std::max(best_d, static_cast<double>(bytes) / (td * 1e-3) / 1e9);
+      best_t = std::max(best_t, total);
+    }
+    if (gbs_h2d) *gbs_h2d = best_h;
+    if (gbs_d2h) *gbs_d2h = best_d;
+    if (gbs_total) *gbs_total = best_t;
+  };
+  for (int k = 0; k < 2; ++k) {
+    const bool sm = k == 1;
+    run(sm, true, false, &out.h2d[k], nullptr, nullptr);
+    run(sm, false, true, nullptr, &out.d2h[k], nullptr);
+    run(sm, true, true, &out.bidir_h2d[k], &out.bidir_d2h[k], &out.bidir_total[k]);
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return out;
+}
+
+}  // namespace nixie::b200

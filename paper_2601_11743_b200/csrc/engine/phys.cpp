@@ -1,0 +1,219 @@
+// Tier backing stores, NUMA placement and the host copy pool (phys.hpp).
+#include "phys.hpp"
+
+#include <pthread.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cctype>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+
+namespace nixie::b200 {
+
+std::string cuda_msg(cudaError_t e, const char* what) {
+  return std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+}
+
+namespace {
+
+std::string read_line(const std::string& path) {
+  std::ifstream f(path);
+  std::string s;
+  if (f) std::getline(f, s);
+  return s;
+}
+
+std::vector<int> parse_cpulist(const std::string& s) {
+  std::vector<int> cpus;
+  std::stringstream ss(s);
+  std::string part;
+  while (std::getline(ss, part, ',')) {
+    if (part.empty()) continue;
+    const auto dash = part.find('-');
+    try {
+      if (dash == std::string::npos) {
+        cpus.push_back(std::stoi(part));
+      } else {
+        const int lo = std::stoi(part.substr(0, dash)), hi = std::stoi(part.substr(dash + 1));
+        for (int c = lo; c <= hi; ++c) cpus.push_back(c);
+      }
+    } catch (const std::exception&) {
+    }
+  }
+  return cpus;
+}
+
+}  // namespace
+
+NumaInfo numa_for_device(int device) {
+  NumaInfo info;
+  char bus[64] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) return info;
+  std::string id(bus);
+  for (char& c : id) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+  // sysfs uses a 4-digit domain; CUDA may print 8.
+  if (id.size() > 12 && id.find(':') == 8) id = id.substr(4);
+  const std::string dir = "/sys/bus/pci/devices/" + id;
+  const std::string node = read_line(dir + "/numa_node");
+  try {
+    info.node = node.empty() ? -1 : std::stoi(node);
+  } catch (const std::exception&) {
+    info.node = -1;
+  }
+  info.cpus = parse_cpulist(read_line(dir + "/local_cpulist"));
+  // Keep only CPUs this process may run on.
+  cpu_set_t allowed;
+  CPU_ZERO(&allowed);
+  if (sched_getaffinity(0, sizeof(allowed), &allowed) == 0) {
+    std::vector<int> ok;
+    for (int c : info.cpus)
+      if (c >= 0 && c < CPU_SETSIZE && CPU_ISSET(c, &allowed)) ok.push_back(c);
+    info.cpus = ok;
+  }
+  return info;
+}
+
+void prefer_numa_node(int node) {
+  constexpr int kMpolDefault = 0, kMpolPreferred = 1;
+  if (node < 0) {
+    syscall(SYS_set_mempolicy, kMpolDefault, nullptr, 0);
+    return;
+  }
+  unsigned long mask[16] = {0};
+  if (node >= static_cast<int>(sizeof(mask) * 8)) return;
+  mask[node / (8 * sizeof(unsigned long))] |= 1ul << (node % (8 * sizeof(unsigned long)));
+  syscall(SYS_set_mempolicy, kMpolPreferred, mask, sizeof(mask) * 8);
+}
+
+void pin_thread_to(const std::vector<int>& cpus) {
+  if (cpus.empty()) return;
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  for (int c : cpus)
+    if (c >= 0 && c < CPU_SETSIZE) CPU_SET(c, &set);
+  pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
+}
+
+void DeviceArena::init(Bytes capacity) {
+  const auto units = static_cast<std::uint32_t>(capacity / kBlockBytes);
+  if (units > 0) NX_CUDA(cudaMalloc(&base_, static_cast<std::size_t>(units) * kBlockBytes));
+  ring.reset(units);
+}
+
+DeviceArena::~DeviceArena() {
+  if (base_) cudaFree(base_);
+}
+
+void PinnedRing::init(Bytes capacity, int numa_node) {
+  const auto units = static_cast<std::uint32_t>(capacity / kBlockBytes);
+  bytes_ = static_cast<Bytes>(units) * kBlockBytes;
+  if (units > 0) {
+    prefer_numa_node(numa_node);
+    void* p = nullptr;
+    const cudaError_t e = cudaHostAlloc(&p, bytes_, cudaHostAllocMapped | cudaHostAllocPortable);
+    prefer_numa_node(-1);
+    NX_CUDA(e);
+    host_ = static_cast<std::uint8_t*>(p);
+    void* d = nullptr;
+    NX_CUDA(cudaHostGetDevicePointer(&d, p, 0));
+    dev_ = static_cast<std::uint8_t*>(d);
+  }
+  ring.reset(units);
+}
+
+PinnedRing::~PinnedRing() {
+  if (host_) cudaFreeHost(host_);
+}
+
+void PagedStore::init(Bytes capacity) {
+  const Bytes capped = capacity == kUnbounded ? 4096 * kGiB : capacity;
+  const auto units = static_cast<std::uint32_t>(capped / kBlockBytes);
+  regions_.assign((units + kUnitsPerRegion - 1) / kUnitsPerRegion, nullptr);
+  ring.reset(units);
+}
+
+std::uint8_t* PagedStore::unit(std::uint32_t u) {
+  const std::uint32_t r = u / kUnitsPerRegion;
+  if (regions_[r] == nullptr) {
+    const std::size_t len = static_cast<std::size_t>(kUnitsPerRegion) * kBlockBytes;
+    void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) throw SimError(Err::IoError, "mmap of a paged-tier region failed");
+    madvise(p, len, MADV_HUGEPAGE);
+    regions_[r] = static_cast<std::uint8_t*>(p);
+  }
+  return regions_[r] + static_cast<std::size_t>(u % kUnitsPerRegion) * kBlockBytes;
+}
+
+PagedStore::~PagedStore() {
+  for (std::uint8_t* p : regions_)
+    if (p) munmap(p, static_cast<std::size_t>(kUnitsPerRegion) * kBlockBytes);
+}
+
+void HostCopyPool::start(int threads, const std::vector<int>& cpus) {
+  if (threads < 1) threads = 1;
+  for (int i = 0; i < threads; ++i) threads_.emplace_back(&HostCopyPool::worker, this, cpus);
+}
+
+HostCopyPool::~HostCopyPool() {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  for (auto& t : threads_) t.join();
+}
+
+void HostCopyPool::worker(std::vector<int> cpus) {
+  pin_thread_to(cpus);
+  while (true) {
+    Job j;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return stop_ || !jobs_.empty(); });
+      if (stop_ && jobs_.empty()) return;
+      j = jobs_.front();
+      jobs_.pop_front();
+    }
+    std::memcpy(j.dst, j.src, j.bytes);
+    {
+      std::lock_guard<std::mutex> lk(done_mu_);
+      done_.push_back(j.token);
+    }
+    done_count_.fetch_add(1, std::memory_order_release);
+  }
+}
+
+void HostCopyPool::submit(void* dst, const void* src, std::size_t bytes, std::uint64_t token) {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    jobs_.push_back(Job{dst, src, bytes, token});
+  }
+  cv_.notify_one();
+}
+
+bool HostCopyPool::drain(std::vector<std::uint64_t>& out) {
+  if (done_count_.load(std::memory_order_acquire) == drained_) return false;
+  std::lock_guard<std::mutex> lk(done_mu_);
+  drained_ += done_.size();
+  out.insert(out.end(), done_.begin(), done_.end());
+  done_.clear();
+  return true;
+}
+
+void HostCopyPool::copy_all(const std::vector<std::pair<void*, const void*>>& pairs, std::size_t bytes) {
+  constexpr std::uint64_t kBulkTag = 1ull << 63;
+  for (std::size_t i = 0; i < pairs.size(); ++i) submit(pairs[i].first, pairs[i].second, bytes, kBulkTag | i);
+  std::size_t got = 0;
+  std::vector<std::uint64_t> toks;
+  while (got < pairs.size()) {
+    toks.clear();
+    if (drain(toks)) got += toks.size();
+    else std::this_thread::yield();
+  }
+}
+
+}  // namespace nixie::b200

@@ -1,0 +1,143 @@
+// Physical backing of the three tiers the CUDA engine serves, and the host
+// copy pool for the pinned<->paged lanes (internal header).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "nixie/errors.hpp"
+#include "nixie/units.hpp"
+
+namespace nixie::b200 {
+
+std::string cuda_msg(cudaError_t e, const char* what);
+
+// A failed CUDA call (reported as NX_E_CUDA through the C ABI).
+class CudaFailure : public SimError {
+ public:
+  explicit CudaFailure(const std::string& what) : SimError(Err::IoError, what) {}
+};
+
+#define NX_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t nx_e_ = (call);                                                            \
+    if (nx_e_ != cudaSuccess) throw ::nixie::b200::CudaFailure(::nixie::b200::cuda_msg(nx_e_, #call)); \
+  } while (0)
+
+// A fixed set of 2 MiB units handed out FIFO (a ring: freed units go to the
+// back). acquire() failing means the registry let a tier overcommit.
+class UnitRing {
+ public:
+  void reset(std::uint32_t units) {
+    free_.clear();
+    for (std::uint32_t u = 0; u < units; ++u) free_.push_back(u);
+    units_ = units;
+  }
+  std::uint32_t acquire(const char* tier) {
+    if (free_.empty()) throw InvariantViolation(std::string(tier) + " has no free 2 MiB unit (budget overcommitted)");
+    const std::uint32_t u = free_.front();
+    free_.pop_front();
+    return u;
+  }
+  void release(std::uint32_t u) { free_.push_back(u); }
+  std::uint32_t units() const { return units_; }
+  std::size_t free_units() const { return free_.size(); }
+
+ private:
+  std::deque<std::uint32_t> free_;
+  std::uint32_t units_ = 0;
+};
+
+// NUMA placement of the GPU's host-side resources.
+struct NumaInfo {
+  int node = -1;
+  std::vector<int> cpus;  // local CPU list
+};
+NumaInfo numa_for_device(int device);
+// Prefer `node` for this thread's future page allocations (-1: default policy).
+void prefer_numa_node(int node);
+void pin_thread_to(const std::vector<int>& cpus);
+
+// tier 0: one cudaMalloc of the capped budget.
+class DeviceArena {
+ public:
+  void init(Bytes capacity);
+  ~DeviceArena();
+  std::uint8_t* frame(std::uint32_t u) const { return base_ + static_cast<std::size_t>(u) * kBlockBytes; }
+  UnitRing ring;
+
+ private:
+  std::uint8_t* base_ = nullptr;
+};
+
+// tier 1: the pinned staging ring, exactly `capacity` bytes of
+// cudaHostAlloc(mapped | portable) memory (not write-combined: host threads
+// read it on the pinned->paged lane).
+class PinnedRing {
+ public:
+  void init(Bytes capacity, int numa_node);
+  ~PinnedRing();
+  std::uint8_t* host(std::uint32_t u) const { return host_ + static_cast<std::size_t>(u) * kBlockBytes; }
+  std::uint8_t* dev(std::uint32_t u) const { return dev_ + static_cast<std::size_t>(u) * kBlockBytes; }
+  Bytes bytes() const { return bytes_; }
+  UnitRing ring;
+
+ private:
+  std::uint8_t* host_ = nullptr;
+  std::uint8_t* dev_ = nullptr;
+  Bytes bytes_ = 0;
+};
+
+// tier 2: pageable memory in 64 MiB regions mapped on first use.
+class PagedStore {
+ public:
+  void init(Bytes capacity);
+  ~PagedStore();
+  std::uint8_t* unit(std::uint32_t u);
+  UnitRing ring;
+
+ private:
+  static constexpr std::uint32_t kUnitsPerRegion = 32;
+  std::vector<std::uint8_t*> regions_;
+};
+
+// Fixed worker pool for 2 MiB host memcpy legs; completions are drained by
+// the engine thread.
+class HostCopyPool {
+ public:
+  void start(int threads, const std::vector<int>& cpus);
+  ~HostCopyPool();
+  void submit(void* dst, const void* src, std::size_t bytes, std::uint64_t token);
+  // Moves finished tokens into `out`; cheap when nothing finished.
+  bool drain(std::vector<std::uint64_t>& out);
+  // Parallel memcpy of many buffers, blocking (setup paths only).
+  void copy_all(const std::vector<std::pair<void*, const void*>>& pairs, std::size_t bytes);
+
+ private:
+  struct Job {
+    void* dst;
+    const void* src;
+    std::size_t bytes;
+    std::uint64_t token;
+  };
+  void worker(std::vector<int> cpus);
+  std::vector<std::thread> threads_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<Job> jobs_;
+  std::mutex done_mu_;
+  std::vector<std::uint64_t> done_;
+  std::atomic<std::uint64_t> done_count_{0};
+  std::uint64_t drained_ = 0;
+  bool stop_ = false;
+};
+
+}  // namespace nixie::b200

@@ -131,6 +131,11 @@ void LaneSet::commit(std::size_t mi, TierId hop) {
   check_progress();
 }
 
+void LaneSet::finish_hop(int lane, std::size_t mi, TierId hop) {
+  --lanes_[lane].inflight;
+  commit(mi, hop);
+}
+
 void LaneSet::finish() {
   if (window_held_) {
     mem_.release_window();

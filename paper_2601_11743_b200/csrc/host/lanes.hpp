@@ -59,6 +59,9 @@ class LaneSet {
   // The hop of move `mi` to `hop` has landed: commit, enqueue the next hop,
   // pump everything, detect completion / deadlock.
   void commit(std::size_t mi, TierId hop);
+  // Real executors: the copy of a hop finished, so its lane slot frees and
+  // the hop commits in one step.
+  void finish_hop(int lane, std::size_t mi, TierId hop);
   void open_eviction_gate();
   void cancel_pending();
 

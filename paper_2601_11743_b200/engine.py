@@ -1,0 +1,301 @@
+"""Python mirror of the swap-path interface (reference proj/include/nixie/*.hpp)
+over the C ABI. Method names follow the reference: allocate / free_chunk
+(MemState, mem_model.cpp:48-116), plan_switch (planner.cpp:111-216),
+switch_to = plan_switch + execute (transfer.cpp:250-271), audit
+(mem_model.cpp:274-325), and the launch gate / MLFQ grant (mlfq.cpp:132-201).
+Errors raise NixieError carrying the reference Err name.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field, fields
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from . import _lib as L
+from ._lib import NixieError, byref, c_int, c_size_t, c_uint32, c_uint64, c_uint8, c_void_p, check, lib
+
+KIB, MIB, GIB = 1 << 10, 1 << 20, 1 << 30
+BLOCK_BYTES = 2 * MIB
+SCENARIO_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "scenarios")
+
+
+@dataclass
+class EngineConfig:
+    """include/nixie/swap_engine.hpp EngineConfig."""
+    device: int = 0
+    gpu_capacity: int = 32 * GIB
+    pinned_capacity: int = 16 * GIB
+    paged_capacity: int = 96 * GIB
+    path: int = L.PATH_SM
+    pcie_legs_in_flight: int = 256
+    legs_per_launch: int = 64
+    host_threads: int = 8
+    host_legs_in_flight: int = 64
+    max_ctas: int = 0
+    fused_launch: bool = False
+    verify: bool = True
+    numa_bind: bool = True
+
+    def to_c(self) -> L.EngineConfigC:
+        c = L.EngineConfigC()
+        for f in fields(self):
+            setattr(c, f.name, int(getattr(self, f.name)))
+        return c
+
+
+@dataclass
+class PlannerConfig:
+    """reference PlannerConfig (planner.hpp:39-43)."""
+    streaming_window: int = 512 * MIB
+    pinned_budget: int = L.UNBOUNDED
+    victim_order: List[int] = field(default_factory=list)
+
+    def to_c(self) -> Tuple[L.PlannerConfigC, object]:
+        arr = (c_uint32 * max(1, len(self.victim_order)))(*self.victim_order)
+        c = L.PlannerConfigC(self.streaming_window, self.pinned_budget,
+                             ctypes.cast(arr, ctypes.POINTER(c_uint32)) if self.victim_order else None,
+                             len(self.victim_order))
+        return c, arr  # keep `arr` alive for the call
+
+
+class SwapEngine:
+    """One per-GPU Nixie instance (device arena, pinned staging ring, paged
+    store, host copy pool, two PCIe lane streams)."""
+
+    def __init__(self, config: Optional[EngineConfig] = None, **overrides):
+        cfg = config or EngineConfig()
+        for k, v in overrides.items():
+            if not hasattr(cfg, k):
+                raise TypeError(f"unknown engine option {k}")
+            setattr(cfg, k, v)
+        self.config = cfg
+        h = c_void_p()
+        check(lib.nx_engine_create(byref(cfg.to_c()), byref(h)))
+        self._h = h
+
+    # -- lifecycle --
+    def close(self) -> None:
+        if self._h:
+            lib.nx_engine_destroy(self._h)
+            self._h = c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- registry --
+    def allocate(self, app: int, size: int, tier: int = L.TIER_GPU) -> List[int]:
+        cap = (size + 128 * MIB - 1) // (128 * MIB) + 1
+        out = (c_uint64 * cap)()
+        n = c_size_t()
+        check(lib.nx_alloc(self._h, app, size, tier, out, cap, byref(n)))
+        return list(out[: n.value])
+
+    def free_chunk(self, app: int, chunk: int) -> int:
+        r = c_uint64()
+        check(lib.nx_free_chunk(self._h, app, chunk, byref(r)))
+        return r.value
+
+    def audit(self) -> None:
+        check(lib.nx_audit(self._h))
+
+    def app_bytes_resident(self, app: int) -> List[int]:
+        out = (c_uint64 * 4)()
+        check(lib.nx_app_resident(self._h, app, out))
+        return list(out)
+
+    def pinned_physical(self) -> Tuple[int, int]:
+        now, peak = c_uint64(), c_uint64()
+        check(lib.nx_pinned_physical(self._h, byref(now), byref(peak)))
+        return now.value, peak.value
+
+    def app_blocks(self, app: int) -> List[int]:
+        n = c_size_t()
+        check(lib.nx_app_blocks(self._h, app, None, 0, byref(n)))
+        out = (c_uint64 * max(1, n.value))()
+        check(lib.nx_app_blocks(self._h, app, out, n.value, byref(n)))
+        return list(out[: n.value])
+
+    # -- K4 synthetic working set --
+    def fill_pattern(self, app: int, seed: int) -> None:
+        check(lib.nx_fill_pattern(self._h, app, seed))
+
+    def verify_pattern(self, app: int, seed: int) -> int:
+        bad = c_uint64()
+        check(lib.nx_verify_pattern(self._h, app, seed, byref(bad)))
+        return bad.value
+
+    def read_block(self, block: int) -> bytes:
+        buf = ctypes.create_string_buffer(BLOCK_BYTES)
+        check(lib.nx_block_read(self._h, block, buf))
+        return buf.raw
+
+    def poke_block(self, block: int, offset: int, value: int) -> None:
+        check(lib.nx_block_poke(self._h, block, offset, value))
+
+    def block_checksum(self, block: int) -> int:
+        v = c_uint64()
+        check(lib.nx_block_checksum(self._h, block, byref(v)))
+        return v.value
+
+    def block_frame(self, block: int) -> int:
+        p = c_void_p()
+        check(lib.nx_block_frame(self._h, block, byref(p)))
+        return p.value or 0
+
+    # -- swap-engine interface --
+    def plan_switch(self, incoming: int, planner: Optional[PlannerConfig] = None) -> Tuple[str, int, int]:
+        pc, keep = (planner or PlannerConfig()).to_c()
+        n = c_size_t()
+        bi, bo = c_uint64(), c_uint64()
+        check(lib.nx_plan(self._h, incoming, byref(pc), None, 0, byref(n), byref(bi), byref(bo)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        check(lib.nx_plan(self._h, incoming, byref(pc), buf, n.value + 1, byref(n), byref(bi), byref(bo)))
+        del keep
+        return buf.value.decode(), bi.value, bo.value
+
+    def switch_to(self, incoming: int, planner: Optional[PlannerConfig] = None, drain_stream: int = 0) -> Dict:
+        pc, keep = (planner or PlannerConfig()).to_c()
+        st = L.SwitchStatsC()
+        check(lib.nx_switch(self._h, incoming, byref(pc), c_void_p(drain_stream or None), byref(st)))
+        del keep
+        return st.as_dict()
+
+    def lane_trace(self, lane: int) -> List[Tuple[int, str, str]]:
+        n = c_size_t()
+        check(lib.nx_lane_trace(self._h, lane, None, None, None, 0, byref(n)))
+        k = max(1, n.value)
+        b, s, d = (c_uint64 * k)(), (c_uint8 * k)(), (c_uint8 * k)()
+        check(lib.nx_lane_trace(self._h, lane, b, s, d, n.value, byref(n)))
+        return [(b[i], L.TIER_NAMES[s[i]], L.TIER_NAMES[d[i]]) for i in range(n.value)]
+
+    def total_launches(self) -> int:
+        return int(lib.nx_total_launches(self._h))
+
+    def lane_stream(self, lane: int) -> int:
+        return lib.nx_lane_stream(self._h, lane) or 0
+
+    # -- host link --
+    def probe_pcie(self, bytes_per_direction: int = 1 * GIB, chunk_bytes: int = 64 * MIB) -> Dict:
+        p = L.PcieProbeC()
+        check(lib.nx_probe_pcie(self._h, bytes_per_direction, chunk_bytes, byref(p)))
+        out = {}
+        for key in ("h2d", "d2h", "bidir_h2d", "bidir_d2h", "bidir_total"):
+            arr = getattr(p, key)
+            out[f"ce_{key}"] = arr[0]
+            out[f"sm_{key}"] = arr[1]
+        out.update(bytes_per_direction=p.bytes_per_direction, chunk_bytes=p.chunk_bytes, numa_node=p.numa_node)
+        return out
+
+    def set_auto_table(self, sm_faster: Sequence[bool]) -> None:
+        arr = (c_int * max(1, len(sm_faster)))(*[int(bool(x)) for x in sm_faster])
+        check(lib.nx_set_auto_table(self._h, arr, len(sm_faster)))
+
+
+class LaunchGate:
+    """MLFQ scheduler + kernel-launch gate over one engine."""
+
+    def __init__(self, engine: SwapEngine, planner: Optional[PlannerConfig] = None):
+        self.engine = engine
+        m = L.MlfqConfigC()
+        lib.nx_mlfq_config_default(byref(m))
+        pc, keep = (planner or PlannerConfig()).to_c()
+        h = c_void_p()
+        check(lib.nx_gate_create(engine._h, byref(m), byref(pc), byref(h)))
+        del keep
+        self._h = h
+
+    def close(self):
+        if self._h:
+            lib.nx_gate_destroy(self._h)
+            self._h = c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def attach(self, app: int, stream: int, now: float = 0.0) -> None:
+        check(lib.nx_gate_attach(self._h, app, c_void_p(stream or None), now))
+
+    def before_launch(self, app: int, now: float) -> bool:
+        ok = c_int()
+        check(lib.nx_gate_before_launch(self._h, app, now, byref(ok)))
+        return bool(ok.value)
+
+    def select_next(self, now: float) -> Optional[int]:
+        a = c_uint32()
+        check(lib.nx_gate_select_next(self._h, now, byref(a)))
+        return None if a.value == 0xFFFFFFFF else a.value
+
+    def context_switch(self, to: int, now: float) -> Dict:
+        st = L.SwitchStatsC()
+        check(lib.nx_gate_switch(self._h, to, now, byref(st)))
+        return st.as_dict()
+
+    def granted(self) -> Optional[int]:
+        a = c_uint32()
+        check(lib.nx_gate_granted(self._h, byref(a)))
+        return None if a.value == 0xFFFFFFFF else a.value
+
+    def app_checksum_async(self, app: int, stream: int, out_pinned: int) -> None:
+        check(lib.nx_gate_app_checksum_async(self._h, app, c_void_p(stream or None),
+                                             ctypes.cast(c_void_p(out_pinned), ctypes.POINTER(c_uint64))))
+
+
+def run_scenario_model(spec: str, legs_per_lane: int = 1) -> str:
+    """Scenario on the virtual clock (no GPU): the trace the reference would print."""
+    p, n = c_void_p(), c_size_t()
+    if legs_per_lane == 1:
+        check(lib.nx_scenario_model(spec.encode(), byref(p), byref(n)))
+    else:
+        check(lib.nx_scenario_model_lanes(spec.encode(), legs_per_lane, byref(p), byref(n)))
+    return L.take_string(p, n)
+
+
+def run_scenario_real(spec: str, seed: int = 0x4E495849, config: Optional[EngineConfig] = None, **overrides) -> str:
+    """Scenario through the CUDA engine: real copies, byte checks (V/F lines)."""
+    cfg = config or EngineConfig()
+    for k, v in overrides.items():
+        setattr(cfg, k, v)
+    p, n = c_void_p(), c_size_t()
+    check(lib.nx_scenario_real(spec.encode(), byref(cfg.to_c()), seed, byref(p), byref(n)))
+    return L.take_string(p, n)
+
+
+def load_scenario(name: str) -> str:
+    path = name if os.path.sep in name else os.path.join(SCENARIO_DIR, name if name.endswith(".scn") else name + ".scn")
+    with open(path) as f:
+        return f.read()
+
+
+def pinned_buffer(nbytes: int) -> int:
+    p = c_void_p()
+    check(lib.nx_pinned_alloc(nbytes, byref(p)))
+    return p.value
+
+
+def free_pinned(ptr: int) -> None:
+    lib.nx_pinned_free(c_void_p(ptr))
+
+
+def stream_sync(stream: int) -> None:
+    check(lib.nx_stream_sync(c_void_p(stream or None)))
+
+
+DETERMINISTIC_TAGS = ("S", "P", "L", "R", "B", "E")
+
+
+def trace_lines(trace: str, tags: Sequence[str] = DETERMINISTIC_TAGS) -> List[str]:
+    """Lines of a scenario trace whose first token is in `tags`."""
+    return [ln for ln in trace.splitlines() if ln.split(" ", 1)[0] in tags]
