@@ -41,7 +41,7 @@ struct EngineConfig {
   Bytes gpu_capacity = 32 * kGiB;     // capped device budget (consumer-GPU emulation)
   Bytes pinned_capacity = 16 * kGiB;  // enforced pinned budget
   Bytes paged_capacity = 96 * kGiB;
-  CopyPath path = CopyPath::SmKernel;
+  CopyPath path = CopyPath::Auto;
   int pcie_legs_in_flight = 256;      // per direction (x 2 MiB)
   int legs_per_launch = 64;           // max legs per K1 launch / CE batch
   int host_threads = 8;               // pinned<->paged copy workers
@@ -50,6 +50,7 @@ struct EngineConfig {
   bool fused_launch = false;          // both directions in one launch stream (warp-group split)
   bool verify = true;                 // checksum every restore
   bool numa_bind = true;              // pinned ring + workers on the GPU's NUMA node
+  int first_batch_legs = 8;           // batch-size ramp start (doubles per batch up to legs_per_launch)
 };
 
 struct SwitchStats {
@@ -63,6 +64,13 @@ struct SwitchStats {
   int ce_batches[2] = {0, 0};               // copy-engine batches per stream
   int host_legs = 0;
   std::uint64_t verified = 0, unverified = 0, mismatches = 0;
+  // Per kernel kind (CUDA events on the launching stream):
+  double k1_s = 0;      // K1 swap launches (SM path): summed durations
+  Bytes k1_bytes = 0;   // bytes they moved across PCIe
+  int k1_launches = 0;
+  double k3_s = 0;      // K3 checksum launches (CE path)
+  Bytes k3_bytes = 0;   // HBM bytes they read
+  int k3_launches = 0;
 };
 
 // Opens a launch gate on the device once the incoming app's last fetch has
@@ -90,6 +98,12 @@ struct PcieProbe {
   Bytes chunk_bytes = 0;
   int link_gen = 0, link_width = 0, link_gen_max = 0, link_width_max = 0;
   int numa_node = -1;
+};
+
+// Per-batch-size SM-kernel vs copy-engine measurement (bidirectional GB/s).
+struct Calibration {
+  std::vector<int> legs;
+  std::vector<double> sm_gbps, ce_gbps;
 };
 
 class SwapEngine {
@@ -140,9 +154,14 @@ class SwapEngine {
 
   // Measures the host link: CE and SM, H2D / D2H alone and both at once.
   PcieProbe probe_pcie(Bytes bytes_per_direction, Bytes chunk_bytes);
+  // Raw SM copy variants (csrc/cuda/copy_variants.cu): {H2D, D2H, both} GB/s.
+  std::array<double, 3> probe_copy_variant(int variant, Bytes bytes_per_direction, int ctas);
   // Per-batch-size choice for CopyPath::Auto: index k covers launches of
   // 2^k legs; true = SM kernel, false = copy engines.
   void set_auto_table(const std::vector<bool>& sm_faster);
+  // Measures both mechanisms at 1..128 legs per batch and installs the
+  // faster one per size for CopyPath::Auto.
+  Calibration calibrate(Bytes bytes_per_direction);
 
  private:
   struct Impl;

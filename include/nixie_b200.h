@@ -60,6 +60,7 @@ typedef struct nx_engine_config {
   int fused_launch;
   int verify;
   int numa_bind;
+  int first_batch_legs;
 } nx_engine_config;
 
 /* PlannerConfig (proj/include/nixie/planner.hpp:39-43). victim_order may be
@@ -81,6 +82,10 @@ typedef struct nx_switch_stats {
   /* aggregate_throughput (proj/src/transfer.cpp:7-28) over the switch's
    * GPU<->pinned records, device-timed, in bytes/s */
   double tp_to_gpu, tp_from_gpu, tp_bidir;
+  /* per kernel kind: K1 swap (SM path) and K3 checksum (CE path) */
+  double k1_s, k3_s;
+  uint64_t k1_bytes, k3_bytes;
+  int k1_launches, k3_launches;
 } nx_switch_stats;
 
 typedef struct nx_pcie_probe {
@@ -155,8 +160,14 @@ void* nx_lane_stream(nx_engine* e, int lane);
 /* ---- host link ------------------------------------------------------------ */
 /* CE and SM bandwidth, H2D / D2H alone and simultaneously. */
 int nx_probe_pcie(nx_engine* e, uint64_t bytes_per_direction, uint64_t chunk_bytes, nx_pcie_probe* out);
+/* Raw SM copy variant probe: out = {H2D, D2H, bidirectional total} GB/s. */
+int nx_probe_copy_variant(nx_engine* e, int variant, uint64_t bytes, int ctas, double out[3]);
 /* CopyPath::Auto table: sm_faster[k] for launches of 2^k legs. */
 int nx_set_auto_table(nx_engine* e, const int* sm_faster, size_t n);
+/* Measures SM kernel vs copy engines, both directions running, for batches of
+ * 1, 2, 4 ... 128 legs and installs the faster per size (CopyPath::Auto).
+ * Arrays hold 8 entries. */
+int nx_calibrate(nx_engine* e, uint64_t bytes_per_direction, double sm_gbps[8], double ce_gbps[8], int sm_faster[8]);
 
 /* ---- scheduler + launch gate (§3, §6) ---------------------------- */
 /* MlfqConfig defaults (proj/include/nixie/mlfq.hpp:13-23). */

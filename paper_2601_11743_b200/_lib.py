@@ -53,7 +53,7 @@ class EngineConfigC(Structure):
         ("device", c_int), ("gpu_capacity", c_uint64), ("pinned_capacity", c_uint64), ("paged_capacity", c_uint64),
         ("path", c_int), ("pcie_legs_in_flight", c_int), ("legs_per_launch", c_int), ("host_threads", c_int),
         ("host_legs_in_flight", c_int), ("max_ctas", c_int), ("fused_launch", c_int), ("verify", c_int),
-        ("numa_bind", c_int),
+        ("numa_bind", c_int), ("first_batch_legs", c_int),
     ]
 
 
@@ -69,7 +69,8 @@ class SwitchStatsC(Structure):
         ("kernel_s_h2d", c_double), ("kernel_s_d2h", c_double), ("launches_h2d", c_int), ("launches_d2h", c_int),
         ("ce_batches_h2d", c_int), ("ce_batches_d2h", c_int), ("host_legs", c_int), ("verified", c_uint64),
         ("unverified", c_uint64), ("mismatches", c_uint64), ("tp_to_gpu", c_double), ("tp_from_gpu", c_double),
-        ("tp_bidir", c_double),
+        ("tp_bidir", c_double), ("k1_s", c_double), ("k3_s", c_double), ("k1_bytes", c_uint64), ("k3_bytes", c_uint64),
+        ("k1_launches", c_int), ("k3_launches", c_int),
     ]
 
     def as_dict(self) -> dict:
@@ -116,7 +117,9 @@ _SIGNATURES = [
     ("nx_total_launches", c_uint64, [c_void_p]),
     ("nx_lane_stream", c_void_p, [c_void_p, c_int]),
     ("nx_probe_pcie", c_int, [c_void_p, c_uint64, c_uint64, POINTER(PcieProbeC)]),
+    ("nx_probe_copy_variant", c_int, [c_void_p, c_int, c_uint64, c_int, POINTER(c_double)]),
     ("nx_set_auto_table", c_int, [c_void_p, POINTER(c_int), c_size_t]),
+    ("nx_calibrate", c_int, [c_void_p, c_uint64, POINTER(c_double), POINTER(c_double), POINTER(c_int)]),
     ("nx_mlfq_config_default", None, [POINTER(MlfqConfigC)]),
     ("nx_gate_create", c_int, [c_void_p, POINTER(MlfqConfigC), POINTER(PlannerConfigC), POINTER(c_void_p)]),
     ("nx_gate_destroy", None, [c_void_p]),

@@ -77,6 +77,7 @@ EngineConfig to_cpp(const nx_engine_config& c) {
   o.fused_launch = c.fused_launch != 0;
   o.verify = c.verify != 0;
   o.numa_bind = c.numa_bind != 0;
+  o.first_batch_legs = c.first_batch_legs;
   return o;
 }
 
@@ -111,6 +112,12 @@ void fill_stats(const SwapEngine& eng, const ExecResult& r, nx_switch_stats* out
   out->verified = s.verified;
   out->unverified = s.unverified;
   out->mismatches = s.mismatches;
+  out->k1_s = s.k1_s;
+  out->k3_s = s.k3_s;
+  out->k1_bytes = s.k1_bytes;
+  out->k3_bytes = s.k3_bytes;
+  out->k1_launches = s.k1_launches;
+  out->k3_launches = s.k3_launches;
   if (s.device_span_s > 0) {
     double lo = 1e30, hi = 0;
     for (const TransferRecord& t : r.events)
@@ -171,6 +178,7 @@ void nx_engine_config_default(nx_engine_config* c) {
   c->fused_launch = d.fused_launch;
   c->verify = d.verify;
   c->numa_bind = d.numa_bind;
+  c->first_batch_legs = d.first_batch_legs;
 }
 
 void nx_planner_config_default(nx_planner_config* c) {
@@ -354,6 +362,27 @@ int nx_probe_pcie(nx_engine* e, uint64_t bytes, uint64_t chunk, nx_pcie_probe* o
     out->bytes_per_direction = p.bytes_per_direction;
     out->chunk_bytes = p.chunk_bytes;
     out->numa_node = p.numa_node;
+  });
+}
+
+int nx_probe_copy_variant(nx_engine* e, int variant, uint64_t bytes, int ctas, double out[3]) {
+  return guard([&] {
+    need(e, "engine");
+    need(out, "out");
+    const auto r = e->eng->probe_copy_variant(variant, bytes, ctas);
+    for (int i = 0; i < 3; ++i) out[i] = r[i];
+  });
+}
+
+int nx_calibrate(nx_engine* e, uint64_t bytes, double sm_gbps[8], double ce_gbps[8], int sm_faster[8]) {
+  return guard([&] {
+    need(e, "engine");
+    const Calibration c = e->eng->calibrate(bytes);
+    for (std::size_t k = 0; k < 8 && k < c.legs.size(); ++k) {
+      if (sm_gbps) sm_gbps[k] = c.sm_gbps[k];
+      if (ce_gbps) ce_gbps[k] = c.ce_gbps[k];
+      if (sm_faster) sm_faster[k] = c.sm_gbps[k] > c.ce_gbps[k] ? 1 : 0;
+    }
   });
 }
 

@@ -77,7 +77,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
   std::uint64_t* d_frames = nullptr;  // device frame table
   std::uint64_t* h_frames = nullptr;  // pinned mirror
   std::uint64_t* h_frames_stage = nullptr;
-  NxScratch scratch[2]{};
+  NxScratch scratch[4]{};  // [0..1] lane streams, [2..3] checksum side streams
+  cudaStream_t cks[2] = {nullptr, nullptr};
   std::uint8_t* bounce = nullptr;  // pinned, kBounceUnits slots (outside the budget)
   NxDevStatus status_seen{};
   std::vector<bool> auto_sm;
@@ -99,7 +100,24 @@ struct SwapEngine::Impl final : detail::LaneSink {
     cudaEvent_t ev_start, ev_end;
     int stream;
     bool ce;
+    bool end_on_side = false;                        // CE batch: ends on the checksum side stream
+    std::vector<std::array<cudaEvent_t, 2>> k3ev;    // CE batch: K3 launch start/end
+    Bytes k3_bytes = 0;
   };
+  std::array<int, 2> batches_sent{};  // per PCIe lane this execute (batch-size ramp)
+
+  // K3 checksum-only launch of a CE batch (record on departure, verify on arrival).
+  void k3_launch(Batch& B, const std::vector<NxLeg>& l, bool arriving, cudaStream_t cs, std::uint32_t flags) {
+    const int n = static_cast<int>(l.size());
+    cudaEvent_t a = take_event(), z = take_event();
+    NX_CUDA(cudaEventRecord(a, cs));
+    NX_CUDA(launch_swap(l.data(), arriving ? 0 : n, arriving ? n : 0, flags, ck, scratch[2 + B.stream], max_ctas, cs));
+    NX_CUDA(cudaEventRecord(z, cs));
+    B.k3ev.push_back({a, z});
+    B.k3_bytes += static_cast<Bytes>(n) * kBlockBytes;
+    ++stats.launches[B.stream];
+    ++launches_total;
+  }
   detail::LaneSet* lanes = nullptr;
   bool finished = false;
   std::vector<Leg> legs;
@@ -142,6 +160,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
     pool.start(cfg.host_threads, numa.cpus);
     for (auto& s : st) NX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     NX_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    for (auto& s : cks) NX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     NX_CUDA(cudaMalloc(&ck.status, sizeof(NxDevStatus)));
     NX_CUDA(cudaMemset(ck.status, 0, sizeof(NxDevStatus)));
     for (auto& s : scratch) {
@@ -174,6 +193,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
     if (bounce) cudaFreeHost(bounce);
     for (auto& s : st) cudaStreamDestroy(s);
     cudaStreamDestroy(aux);
+    for (auto& s : cks) cudaStreamDestroy(s);
   }
 
   // ---- per-block tables -------------------------------------------------
@@ -393,7 +413,10 @@ struct SwapEngine::Impl final : detail::LaneSink {
       case CopyPath::CopyEngine: return false;
       case CopyPath::Auto: {
         const auto k = static_cast<std::size_t>(log2_bucket(n_legs));
-        return auto_sm.empty() ? true : auto_sm[std::min(k, auto_sm.size() - 1)];
+        // Uncalibrated: the copy engines, the faster mechanism measured on
+        // B200 PCIe Gen5 x16 at every batch size; calibrate()
+        // re-measures on the box.
+        return auto_sm.empty() ? false : auto_sm[std::min(k, auto_sm.size() - 1)];
       }
     }
     return true;
@@ -423,26 +446,28 @@ struct SwapEngine::Impl final : detail::LaneSink {
       ++stats.launches[s];
       ++launches_total;
     } else {
-      // K2: copy engines, with K3 checksum launches around them.
+      // K2: the copy engines move the bytes on st[s]; the K3 checksum
+      // launches run on the side stream cks[s] so the copy stream never
+      // waits for them: the departure checksum reads the frames while the
+      // DMA reads them, the arrival check runs after the batch landed. The
+      // batch ends (and may commit) only when both are done.
+      cudaStream_t cs = cks[s];
+      NX_CUDA(cudaStreamWaitEvent(cs, B.ev_start, 0));
       std::vector<NxLeg> ckl;
       for (auto i : d2h) ckl.push_back(NxLeg{dev_addr(legs[i].from, legs[i].src_u), nullptr, static_cast<std::uint32_t>(legs[i].block), 0});
-      if (!ckl.empty()) {
-        NX_CUDA(launch_swap(ckl.data(), static_cast<int>(ckl.size()), 0, flags, ck, scratch[s], max_ctas, st[s]));
-        ++stats.launches[s];
-        ++launches_total;
-      }
+      if (!ckl.empty()) k3_launch(B, ckl, false, cs, flags);
       copy_runs(d2h, s, cudaMemcpyDeviceToHost);
       copy_runs(h2d, s, cudaMemcpyHostToDevice);
+      cudaEvent_t copied = take_event();
+      NX_CUDA(cudaEventRecord(copied, st[s]));
+      NX_CUDA(cudaStreamWaitEvent(cs, copied, 0));
       ckl.clear();
       for (auto i : h2d) ckl.push_back(NxLeg{dev_addr(legs[i].to, legs[i].dst_u), nullptr, static_cast<std::uint32_t>(legs[i].block), 0});
-      if (!ckl.empty()) {
-        NX_CUDA(launch_swap(ckl.data(), 0, static_cast<int>(ckl.size()), flags, ck, scratch[s], max_ctas, st[s]));
-        ++stats.launches[s];
-        ++launches_total;
-      }
+      if (!ckl.empty()) k3_launch(B, ckl, true, cs, flags);
       ++stats.ce_batches[s];
+      B.end_on_side = true;
     }
-    NX_CUDA(cudaEventRecord(B.ev_end, st[s]));
+    NX_CUDA(cudaEventRecord(B.ev_end, B.end_on_side ? cks[s] : st[s]));
     stats.pcie_d2h_bytes += d2h.size() * kBlockBytes;
     for (auto i : h2d) {
       stats.pcie_h2d_bytes += kBlockBytes;
@@ -511,9 +536,13 @@ struct SwapEngine::Impl final : detail::LaneSink {
     for (int lane : {kD2H, kH2D}) {
       auto& p = pending[lane];
       while (!p.empty()) {
+        // Batches ramp up from first_batch_legs so the first fetches can start
+        // (into frames the first evictions free) after a short first batch.
+        const int cap = std::min<int>(L, std::max(1, cfg.first_batch_legs) << std::min(batches_sent[lane], 12));
         // Enough queued on the stream to hide the host: wait for a full batch.
-        if (inflight[lane].size() >= 2 && static_cast<int>(p.size()) < L) break;
-        const int take = std::min<int>(static_cast<int>(p.size()), L);
+        if (inflight[lane].size() >= 2 && static_cast<int>(p.size()) < cap) break;
+        const int take = std::min<int>(static_cast<int>(p.size()), cap);
+        ++batches_sent[lane];
         std::vector<std::uint32_t> part(p.begin(), p.begin() + take);
         p.erase(p.begin(), p.begin() + take);
         if (lane == kD2H)
@@ -580,6 +609,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
     legs.clear();
     landed.clear();
     events_used = 0;
+    batches_sent = {0, 0};
     records = &res.events;
     opts = &o;
     incoming = plan.incoming_app;
@@ -630,6 +660,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
       lanes = nullptr;
       cudaStreamSynchronize(st[0]);
       cudaStreamSynchronize(st[1]);
+      cudaStreamSynchronize(cks[0]);
+      cudaStreamSynchronize(cks[1]);
       throw;
     }
     lanes = nullptr;
@@ -651,6 +683,18 @@ struct SwapEngine::Impl final : detail::LaneSink {
       first = std::min(first, s0);
       last = std::max(last, s1);
       stats.kernel_s[B.stream] += s1 - s0;
+      if (!B.ce) {
+        stats.k1_s += s1 - s0;
+        stats.k1_bytes += B.legs.size() * kBlockBytes;
+        ++stats.k1_launches;
+      }
+      for (const auto& ke : B.k3ev) {
+        float d = 0;
+        NX_CUDA(cudaEventElapsedTime(&d, ke[0], ke[1]));
+        stats.k3_s += d * 1e-3;
+        ++stats.k3_launches;
+      }
+      stats.k3_bytes += B.k3_bytes;
       for (auto i : B.legs) {
         TransferRecord& r = res.events[legs[i].rec];
         r.start = s0;
@@ -898,4 +942,92 @@ PcieProbe SwapEngine::probe_pcie(Bytes bytes, Bytes chunk) {
   return out;
 }
 
+}  // namespace nixie::b200
+
+namespace nixie::b200 {
+cudaError_t launch_raw_copy(int variant, void* dst, const void* src, std::uint64_t bytes, int ctas, cudaStream_t stream);
+
+// Raw copy-variant probe (copy_variants.cu): GB/s of H2D alone, D2H alone,
+// and the total while both run, `bytes` per direction in one launch each.
+std::array<double, 3> SwapEngine::probe_copy_variant(int variant, Bytes bytes, int ctas) {
+  Impl& m = *impl_;
+  bytes -= bytes % (1 << 20);
+  ProbeBufs b;
+  for (int i = 0; i < 2; ++i) {
+    NX_CUDA(cudaMalloc(&b.dev[i], bytes));
+    NX_CUDA(cudaMemset(b.dev[i], i, bytes));
+    void* h = nullptr;
+    NX_CUDA(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    b.host[i] = static_cast<std::uint8_t*>(h);
+    std::memset(h, 1 + i, bytes);
+  }
+  cudaEvent_t ev[4];
+  for (auto& e : ev) NX_CUDA(cudaEventCreate(&e));
+  auto go = [&](bool h2d, bool d2h) {
+    double best = 0;
+    for (int rep = 0; rep < 4; ++rep) {
+      NX_CUDA(cudaDeviceSynchronize());
+      if (h2d) NX_CUDA(cudaEventRecord(ev[0], m.st[0]));
+      if (d2h) NX_CUDA(cudaEventRecord(ev[2], m.st[1]));
+      // variant >= 10 mixes mechanisms: 10 = CE H2D + SM D2H, 11 = SM H2D + CE D2H
+      // (SM = variant 0); anything else uses `variant` for both directions.
+      const bool ce_h = variant == 10, ce_d = variant == 11;
+      const int v = variant >= 10 ? 0 : variant;
+      if (h2d) {
+        if (ce_h)
+          for (Bytes o = 0; o < bytes; o += 64 << 20)
+            NX_CUDA(cudaMemcpyAsync(b.dev[1] + o, b.host[1] + o, std::min<Bytes>(64 << 20, bytes - o), cudaMemcpyHostToDevice, m.st[0]));
+        else
+          NX_CUDA(launch_raw_copy(v, b.dev[1], b.host[1], bytes, ctas, m.st[0]));
+      }
+      if (d2h) {
+        if (ce_d)
+          for (Bytes o = 0; o < bytes; o += 64 << 20)
+            NX_CUDA(cudaMemcpyAsync(b.host[0] + o, b.dev[0] + o, std::min<Bytes>(64 << 20, bytes - o), cudaMemcpyDeviceToHost, m.st[1]));
+        else
+          NX_CUDA(launch_raw_copy(v, b.host[0], b.dev[0], bytes, ctas, m.st[1]));
+      }
+      if (h2d) NX_CUDA(cudaEventRecord(ev[1], m.st[0]));
+      if (d2h) NX_CUDA(cudaEventRecord(ev[3], m.st[1]));
+      NX_CUDA(cudaDeviceSynchronize());
+      m.launches_total += (h2d ? 1 : 0) + (d2h ? 1 : 0);
+      if (rep == 0) continue;
+      float t = 0;
+      if (h2d && d2h) {
+        float a = 0, z = 0, th = 0;
+        NX_CUDA(cudaEventElapsedTime(&th, ev[0], ev[1]));
+        NX_CUDA(cudaEventElapsedTime(&a, ev[0], ev[2]));
+        NX_CUDA(cudaEventElapsedTime(&z, ev[0], ev[3]));
+        t = std::max(th, z) - std::min(0.0f, a);
+        best = std::max(best, 2.0 * static_cast<double>(bytes) / (t * 1e-3) / 1e9);
+      } else {
+        NX_CUDA(cudaEventElapsedTime(&t, h2d ? ev[0] : ev[2], h2d ? ev[1] : ev[3]));
+        best = std::max(best, static_cast<double>(bytes) / (t * 1e-3) / 1e9);
+      }
+    }
+    return best;
+  };
+  std::array<double, 3> out{go(true, false), go(false, true), go(true, true)};
+  for (auto& e : ev) cudaEventDestroy(e);
+  return out;
+}
+}  // namespace nixie::b200
+
+namespace nixie::b200 {
+// Measured per-batch-size choice between the SM swap kernel and the copy
+// engines (both directions running, the swap's operating point).
+Calibration SwapEngine::calibrate(Bytes bytes_per_direction) {
+  Calibration c;
+  std::vector<bool> table;
+  for (int k = 0; k < 8; ++k) {
+    const Bytes chunk = kBlockBytes << k;
+    const PcieProbe p = probe_pcie(std::max<Bytes>(bytes_per_direction, 4 * chunk), chunk);
+    c.legs.push_back(1 << k);
+    c.ce_gbps.push_back(p.bidir_total[0]);
+    c.sm_gbps.push_back(p.bidir_total[1]);
+    table.push_back(p.bidir_total[1] > p.bidir_total[0]);
+  }
+  set_auto_table(table);
+  return c;
+}
 }  // namespace nixie::b200

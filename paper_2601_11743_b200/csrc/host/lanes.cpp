@@ -43,7 +43,14 @@ void LaneSet::begin(const MigrationPlan& plan, const PlannerConfig& cfg, bool ga
     return;
   }
   try_reserve_window();
+  // While the plan is loaded, a lane starts at most its first leg, exactly
+  // when the reference would (pump on every push, plan order). Extra legs
+  // are only considered once every lane's queue is known, so a lane cannot
+  // grab space another lane's first leg needs (see startable_extra).
+  loading_ = true;
   for (std::size_t i = 0; i < moves_.size(); ++i) enqueue(i);
+  loading_ = false;
+  pump_all();
   check_progress();
 }
 
@@ -75,10 +82,33 @@ bool LaneSet::startable(const MoveState& ms, TierId hop, bool* use_window) const
   return false;
 }
 
+// An extra leg (its lane already has one in flight) must leave one free block
+// of its destination tier for every other lane whose head targets that tier
+// and that has nothing in flight: with a single leg per lane the reference
+// never lets one lane take another lane's only slot, and greedy concurrency
+// would (e.g. paged->pinned fetches filling a small pinned tier before any
+// eviction can land there, while the fetched blocks wait for GPU frames only
+// those evictions free).
+bool LaneSet::extra_leaves_room(int lane, TierId hop, bool use_window) const {
+  if (use_window) return true;  // drawn from the owner's window, not ordinary space
+  const TierState& t = mem_.tier(hop);
+  if (t.unbounded()) return true;
+  std::uint64_t others = 0;
+  for (int l = 0; l < kLaneCount; ++l) {
+    if (l == lane) continue;
+    for (const auto& q : lanes_[l].q)
+      if (!q.empty() && next_hop(moves_[q.front().mi]) == hop) {
+        ++others;
+        break;
+      }
+  }
+  return t.free_bytes() >= (others + 1) * kBlockBytes;
+}
+
 // Head-of-direction pump; see lanes.hpp for why it equals ref :145-171.
 void LaneSet::pump(int lane) {
   Lane& L = lanes_[lane];
-  while (L.inflight < L.limit) {
+  while (L.inflight < L.limit && !(loading_ && L.inflight > 0)) {
     int first = 0;
     if (L.q[0].empty() || (!L.q[1].empty() && L.q[1].front().seq < L.q[0].front().seq)) first = 1;
     int pick = -1;
@@ -87,7 +117,8 @@ void LaneSet::pump(int lane) {
       const int dir = k == 0 ? first : 1 - first;
       if (L.q[dir].empty()) continue;
       const MoveState& ms = moves_[L.q[dir].front().mi];
-      if (startable(ms, next_hop(ms), &use_window)) pick = dir;
+      const TierId hop = next_hop(ms);
+      if (startable(ms, hop, &use_window) && (L.inflight == 0 || extra_leaves_room(lane, hop, use_window))) pick = dir;
     }
     if (pick < 0) return;
     const std::size_t mi = L.q[pick].front().mi;
@@ -186,7 +217,31 @@ void LaneSet::check_progress() const {
         pending = true;
         if (gated(moves_[e.mi])) return;  // waiting on the kernel-drain gate is progress
       }
-  if (pending) throw InvariantViolation("transfer deadlock: stalled legs with idle links");
+  if (pending) throw InvariantViolation("transfer deadlock: stalled legs with idle links" + describe());
+}
+
+std::string LaneSet::describe() const {
+  std::string s = " [";
+  for (int d = 0; d < kTierCount; ++d) {
+    const TierState& t = mem_.tier(tier_at_depth(d));
+    if (t.unbounded()) continue;
+    s += std::string(tier_name(t.tier)) + " cap=" + std::to_string(t.capacity / kBlockBytes) +
+         " used=" + std::to_string(t.used / kBlockBytes) + " rsv=" + std::to_string(t.reserved / kBlockBytes) +
+         " win=" + std::to_string(t.window_reserved / kBlockBytes) + "; ";
+  }
+  for (int l = 0; l < kLaneCount; ++l) {
+    const Lane& L = lanes_[l];
+    if (L.q[0].empty() && L.q[1].empty() && L.inflight == 0) continue;
+    s += "lane" + std::to_string(l) + " inflight=" + std::to_string(L.inflight) + " queued=" +
+         std::to_string(L.q[0].size() + L.q[1].size());
+    for (const auto& q : L.q)
+      if (!q.empty()) {
+        const MoveState& ms = moves_[q.front().mi];
+        s += " head=blk" + std::to_string(ms.move.block) + "(" + tier_name(ms.at) + "->" + tier_name(next_hop(ms)) + ")";
+      }
+    s += "; ";
+  }
+  return s + "]";
 }
 
 }  // namespace nixie::detail

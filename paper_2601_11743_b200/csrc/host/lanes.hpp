@@ -77,6 +77,7 @@ class LaneSet {
   std::size_t move_count() const { return moves_.size(); }
   int lane_of(TierId from, TierId to) const;
   bool window_held() const { return window_held_; }
+  std::string describe() const;  // tiers + lane heads, for deadlock reports
 
  private:
   struct MoveState {
@@ -100,6 +101,7 @@ class LaneSet {
   void pump_all();
   bool gated(const MoveState& ms) const;
   bool startable(const MoveState& ms, TierId hop, bool* use_window) const;
+  bool extra_leaves_room(int lane, TierId hop, bool use_window) const;
   void try_reserve_window();
   void check_progress() const;
   void finish();
@@ -113,6 +115,7 @@ class LaneSet {
   int on_link_ = 0;
   std::uint64_t seq_ = 0;
   bool gate_open_ = true;
+  bool loading_ = false;  // begin(): first legs only
   bool window_wanted_ = false;
   bool window_held_ = false;
   Bytes window_size_ = 0;

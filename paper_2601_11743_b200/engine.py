@@ -27,7 +27,7 @@ class EngineConfig:
     gpu_capacity: int = 32 * GIB
     pinned_capacity: int = 16 * GIB
     paged_capacity: int = 96 * GIB
-    path: int = L.PATH_SM
+    path: int = L.PATH_AUTO
     pcie_legs_in_flight: int = 256
     legs_per_launch: int = 64
     host_threads: int = 8
@@ -36,6 +36,7 @@ class EngineConfig:
     fused_launch: bool = False
     verify: bool = True
     numa_bind: bool = True
+    first_batch_legs: int = 8
 
     def to_c(self) -> L.EngineConfigC:
         c = L.EngineConfigC()
@@ -195,6 +196,14 @@ class SwapEngine:
             out[f"sm_{key}"] = arr[1]
         out.update(bytes_per_direction=p.bytes_per_direction, chunk_bytes=p.chunk_bytes, numa_node=p.numa_node)
         return out
+
+    def calibrate(self, bytes_per_direction: int = 256 * MIB) -> Dict:
+        """Measure SM kernel vs copy engines per batch size (1..128 legs) with
+        both directions running; installs the faster per size (path=AUTO)."""
+        sm, ce, pick = (ctypes.c_double * 8)(), (ctypes.c_double * 8)(), (c_int * 8)()
+        check(lib.nx_calibrate(self._h, bytes_per_direction, sm, ce, pick))
+        return {"legs": [1 << k for k in range(8)], "sm_gbps": list(sm), "ce_gbps": list(ce),
+                "sm_faster": [bool(x) for x in pick]}
 
     def set_auto_table(self, sm_faster: Sequence[bool]) -> None:
         arr = (c_int * max(1, len(sm_faster)))(*[int(bool(x)) for x in sm_faster])

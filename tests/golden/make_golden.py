@@ -1,0 +1,84 @@
+"""Regenerates tests/golden/ from the UNMODIFIED reference (oracle/_ref/ref_trace,
+built by `make -C oracle` from /root/reference/proj/src). Run in the build
+container: python tests/golden/make_golden.py
+
+Outputs
+  scenarios.json   per shipped scenario: sha256 of the full reference trace,
+                   sha256 of its deterministic lines (S P L R B E), the S/R/B/T
+                   summary lines, and the full trace when it is small
+  random_tiny.json 120 seeded random tiny scenarios: spec + full reference
+                   trace, or the reference's error class
+"""
+import glob
+import hashlib
+import json
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, os.path.dirname(HERE))
+from scenario_gen import random_scenario  # noqa: E402
+
+REF = os.path.join(ROOT, "oracle", "_ref", "ref_trace")
+DET = ("S", "P", "L", "R", "B", "E")
+
+
+def ref_run(spec: str):
+    p = subprocess.run([REF, "-"], input=spec, capture_output=True, text=True)
+    if p.returncode != 0:
+        msg = p.stderr.strip().removeprefix("ref_trace: ")
+        kind = "InvariantViolation" if msg.startswith("invariant violation") else msg.split(":", 1)[0]
+        return None, kind
+    return p.stdout, None
+
+
+SPEEDS = [(64, 32), (64, 1), (1, 64), (64, 64), (4, 200), (200, 4), (16, 32), (32, 16)]
+
+
+def retime(spec: str, pc: int, host: int) -> str:
+    body = "\n".join(ln for ln in spec.splitlines() if not ln.startswith("link"))
+    return body + f"\nlink 0 {pc}GiB/s {pc}GiB/s full\nlink 1 {host}GiB/s {host}GiB/s full\n"
+
+
+def det(trace: str) -> str:
+    return "\n".join(ln for ln in trace.splitlines() if ln.split(" ", 1)[0] in DET)
+
+
+def sha(s: str) -> str:
+    return hashlib.sha256(s.encode()).hexdigest()
+
+
+def main():
+    out = {}
+    for path in sorted(glob.glob(os.path.join(ROOT, "paper_2601_11743_b200", "scenarios", "*.scn"))):
+        spec = open(path).read()
+        trace, err = ref_run(spec)
+        assert err is None, (path, err)
+        name = os.path.basename(path)[:-4]
+        out[name] = {
+            "sha256": sha(trace),
+            "det_sha256": sha(det(trace)),
+            "summary": [ln for ln in trace.splitlines() if ln[0] in "SRBT"],
+            "lines": trace.count("\n"),
+            "trace": trace if trace.count("\n") < 3000 else None,
+        }
+    with open(os.path.join(HERE, "scenarios.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+    rnd = []
+    for seed in range(120):
+        spec = random_scenario(seed)
+        trace, err = ref_run(spec)
+        # robust: the reference completes this instance under every link timing
+        # below. Tight instances that complete only for some timings hit the
+        # reference planner's transit-lane deadlock (hard part 5a).
+        robust = err is None and all(ref_run(retime(spec, pc, host))[1] is None for pc, host in SPEEDS)
+        rnd.append({"seed": seed, "spec": spec, "trace": trace, "error": err, "robust": robust})
+    with open(os.path.join(HERE, "random_tiny.json"), "w") as f:
+        json.dump(rnd, f, indent=0)
+    print("scenarios:", len(out), "random:", len(rnd), "errors:", sum(1 for r in rnd if r["error"]))
+
+
+if __name__ == "__main__":
+    main()
