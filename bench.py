@@ -1,0 +1,374 @@
+"""Benchmark of the Nixie context-switch swap path on B200 (BASELINE.json).
+
+Metric: bidirectional swap GB/s per GPU (% of the measured simultaneous
+H2D+D2H PCIe peak); p50/p99 context-switch latency.
+
+Workload (BASELINE.json configs[1]): an interactive 16 GiB app and a 24 GiB
+background app on one B200 capped at 32 GiB, 16 GiB pinned budget; the apps
+start cold in pageable memory and alternate; a step is one steady-state
+context switch (8 GiB out of the GPU + 8 GiB in, both directions at once).
+
+Lines printed by rank 0 (one JSON line):
+  value  whole-job GB/s, device-timed (CUDA events around every PCIe launch
+         of the timed switches; inputs resident, the first-hop copies are the
+         path), summed over ranks / max-over-ranks time
+  e2e    the same bytes through the public API call (plan_switch + real
+         execute + commits, the C ABI nx_switch), host wall clock; h2d/d2h
+         bytes per step are the switch's PCIe bytes
+  roofline        the dominant kernel of the timed region (the K3 checksum
+                  kernel on the copy-engine path: HBM-bound)
+  link_roofline   the path's real bound: PCIe, against the same-run probe
+  cpu_baseline    the reference's CPU implementation of the path (see below)
+
+--impl reference: the unmodified reference's CPU path (oracle/_ref built from
+/root/reference/proj/src): plan_switch + execute of the reference library for
+the same switches plus the switch's bytes moved by host memcpy on all host
+cores (the reference models no data), on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+GIB, MIB = 1 << 30, 1 << 20
+METRIC = "bidir swap GB/s per GPU (% of PCIe peak); p50/p99 context-switch latency"
+WORKLOAD = ("c2_interactive_background: interactive 16 GiB + background 24 GiB apps alternating on one B200 "
+            "capped at 32 GiB, 16 GiB pinned budget, cold start in pageable memory, steady-state switches "
+            "(8 GiB out + 8 GiB in per switch)")
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+class Dist:
+    """Host-side barrier / max / sum across ranks (gloo; no data-path collective)."""
+
+    def __init__(self):
+        self.rank, self.world, self.local = dist_env()
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as td
+            td.init_process_group("gloo")
+            self.td = td
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def reduce(self, value: float, op: str) -> float:
+        if self.world == 1:
+            return value
+        import torch
+        t = torch.tensor([value], dtype=torch.float64)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX if op == "max" else self.td.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.td.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for ln in f:
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def pcie_link(device: int) -> dict:
+    try:
+        out = subprocess.run(["nvidia-smi", "-i", str(device), "--query-gpu=name,pcie.link.gen.current,pcie.link.gen.max,"
+                              "pcie.link.width.current,pcie.link.width.max", "--format=csv,noheader"],
+                             capture_output=True, text=True, timeout=20).stdout.strip()
+        name, g, gm, w, wm = [p.strip() for p in out.split(",")]
+        return {"gpu": name, "gen": int(g), "gen_max": int(gm), "width": int(w), "width_max": int(wm)}
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)[:80]}
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def ncu_traffic() -> dict:
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU baseline: the reference's own path on the host cores (bounded sample)
+# ---------------------------------------------------------------------------------------------
+def cpu_baseline(sample_switches: int = 2) -> dict:
+    """Reference control path (unmodified reference library: plan_switch +
+    execute, single-threaded by design) for the workload's switches, plus the
+    switch's bytes moved by host memcpy on all host cores (the reference
+    models no data; the paper's daemon copies with multiple host threads)."""
+    ref = os.path.join(ROOT, "oracle", "_ref", "ref_trace")
+    so = os.path.join(ROOT, "oracle", "_ref", "libswap_oracle.so")
+    scn = os.path.join(ROOT, "paper_2601_11743_b200", "scenarios", "c2_interactive_background.scn")
+    out = {"kind": "reference", "unit": "GB/s"}
+    if not (os.path.exists(ref) and os.path.exists(so)):
+        out.update(value=None, cores=0, sample="oracle/_ref not built")
+        return out
+    p = subprocess.run([ref, "--bench", scn, str(sample_switches)], capture_output=True, text=True, timeout=600)
+    ctl_s, ctl_bytes = p.stdout.split()
+    ctl_s, ctl_bytes = float(ctl_s), int(ctl_bytes)
+    # Byte movement: each switch copies bytes_in + bytes_out; sample one
+    # switch's worth (16 GiB) as 2 MiB blocks between two host buffers.
+    lib = ctypes.CDLL(so)
+    lib.so_copy_blocks.restype = ctypes.c_double
+    lib.so_copy_blocks.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), ctypes.c_size_t, ctypes.c_int]
+    cores = os.cpu_count() or 1
+    per_switch = ctl_bytes // max(1, sample_switches)
+    pool_bytes = min(per_switch, 4 * GIB)  # reuse a 4 GiB pool: bounded memory, same memcpy work
+    nblk = pool_bytes // (2 * MIB)
+    src = ctypes.create_string_buffer(pool_bytes)
+    dst = ctypes.create_string_buffer(pool_bytes)
+    ctypes.memset(src, 1, pool_bytes)
+    ctypes.memset(dst, 2, pool_bytes)
+    sp = (ctypes.c_void_p * nblk)(*[ctypes.addressof(src) + i * 2 * MIB for i in range(nblk)])
+    dp = (ctypes.c_void_p * nblk)(*[ctypes.addressof(dst) + i * 2 * MIB for i in range(nblk)])
+    reps = max(1, per_switch // pool_bytes)
+    copy_s = sum(lib.so_copy_blocks(dp, sp, nblk, cores) for _ in range(reps)) * (per_switch / (reps * pool_bytes))
+    per_switch_s = ctl_s / sample_switches + copy_s
+    out.update(value=per_switch / per_switch_s / 1e9, cores=cores,
+               sample=(f"{sample_switches} steady switches of the workload through the unmodified reference "
+                       f"(plan_switch+execute, 1 thread: {ctl_s / sample_switches * 1e3:.1f} ms/switch) + one switch's "
+                       f"{per_switch / GIB:.0f} GiB moved by memcpy on {cores} threads ({copy_s:.2f} s)"),
+               ms_per_switch=per_switch_s * 1e3)
+    return out
+
+
+def run_reference(args, dist: Dist):
+    if dist.rank != 0:
+        return 0
+    t0 = time.perf_counter()
+    vals = []
+    base = None
+    for _ in range(args.warmup + args.steps):
+        base = cpu_baseline(1)
+        vals.append(base["value"])
+    vals = vals[args.warmup:] if vals and vals[0] is not None else vals
+    v = statistics.mean(vals) if vals and vals[0] is not None else None
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": base.get("ms_per_switch") if base else None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "parallelism": "host cores (reference is single-threaded; memcpy on all cores)"},
+            "cpu_baseline": {**(base or {}), "value": v},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------------
+# Product arm
+# ---------------------------------------------------------------------------------------------
+def x16_exchange(path: int, switches: int = 4) -> dict:
+    """North-star latency case: 16 GiB <-> 16 GiB exchange at a 16 GiB cap."""
+    from paper_2601_11743_b200 import PlannerConfig, SwapEngine
+    from paper_2601_11743_b200._lib import TIER_GPU, TIER_PINNED
+    e = SwapEngine(gpu_capacity=16 * GIB, pinned_capacity=34 * GIB, paged_capacity=2 * GIB, path=path)
+    try:
+        e.allocate(0, 16 * GIB, TIER_GPU)
+        e.allocate(1, 16 * GIB, TIER_PINNED)
+        e.fill_pattern(0, 1)
+        e.fill_pattern(1, 1)
+        lat, dev = [], []
+        nxt = 1
+        for _ in range(switches):
+            st = e.switch_to(nxt, PlannerConfig(victim_order=[1 - nxt]))
+            assert st["mismatches"] == 0
+            lat.append(st["wall_s"] + st["plan_s"])
+            dev.append(st["device_span_s"])
+            nxt = 1 - nxt
+        bad = e.verify_pattern(0, 1) + e.verify_pattern(1, 1)
+    finally:
+        e.close()
+    return {"bytes_each_way": 16 * GIB, "latency_s": [round(x, 4) for x in lat], "device_span_s": [round(x, 4) for x in dev],
+            "byte_exact": bad == 0}
+
+
+def run_product(args, dist: Dist):
+    from paper_2601_11743_b200 import PlannerConfig, SwapEngine, load_scenario, parse_path
+    from paper_2601_11743_b200._lib import TIER_PAGED
+    device = dist.local if args.gpus > 1 else 0
+    peaks = measured_peaks()
+    path = parse_path(args.path)
+    eng = SwapEngine(device=device, gpu_capacity=32 * GIB, pinned_capacity=16 * GIB, paged_capacity=96 * GIB, path=path)
+    probe = eng.probe_pcie(1 * GIB, 64 * MIB)
+    calib = eng.calibrate(256 * MIB) if path == 0 else None
+    eng.allocate(0, 16 * GIB, TIER_PAGED)
+    eng.allocate(1, 24 * GIB, TIER_PAGED)
+    seed = 0x4E495849
+    eng.fill_pattern(0, seed)
+    eng.fill_pattern(1, seed)
+    pc = PlannerConfig(streaming_window=512 * MIB, pinned_budget=16 * GIB)
+    nxt = 0
+
+    def step():
+        nonlocal nxt
+        pc.victim_order = [1 - nxt]
+        st = eng.switch_to(nxt, pc)
+        nxt = 1 - nxt
+        return st
+
+    for _ in range(max(3, args.warmup) + 2):  # two cold switches (paged -> pinned -> GPU) + W steady ones
+        step()
+    launches0 = eng.total_launches()
+    sampler = ClockSampler(device)
+    sampler.start()
+    dist.barrier()
+    t0 = time.perf_counter()
+    stats = [step() for _ in range(args.steps)]
+    wall = time.perf_counter() - t0
+    dist.barrier()
+    clocks = sampler.stop()
+    launches = eng.total_launches() - launches0
+    bad = eng.verify_pattern(0, seed) + eng.verify_pattern(1, seed)
+    eng.audit()
+    eng.close()
+
+    bytes_rank = sum(s["bytes_in"] + s["bytes_out"] for s in stats)
+    dev_rank = sum(s["device_span_s"] for s in stats)
+    lat = sorted(s["wall_s"] + s["plan_s"] for s in stats)
+    total_bytes = dist.reduce(bytes_rank, "sum")
+    dev_max = dist.reduce(dev_rank, "max")
+    wall_max = dist.reduce(wall, "max")
+    bad_all = dist.reduce(bad, "sum")
+    x16 = x16_exchange(path) if (args.x16 and dist.rank == 0) else None
+    if dist.rank != 0:
+        return 0
+
+    value = total_bytes / dev_max / 1e9
+    e2e = total_bytes / wall_max / 1e9
+    pcie_peak = max(probe["ce_bidir_total"], probe["sm_bidir_total"])
+    per_gpu = value / args.gpus
+    k3_s = sum(s["k3_s"] for s in stats)
+    k3_b = sum(s["k3_bytes"] for s in stats)
+    k1_s = sum(s["k1_s"] for s in stats)
+    k1_b = sum(s["k1_bytes"] for s in stats)
+    k3_n = sum(s["k3_launches"] for s in stats)
+    k1_n = sum(s["k1_launches"] for s in stats)
+    traffic = ncu_traffic()
+    if k1_s > k3_s:  # SM swap kernel dominates: PCIe-bound
+        roof = {"kernel": "nx_swap_kernel (K1, fused checksum)", "bound": "pcie", "achieved": k1_b / k1_s / 1e9,
+                "peak": pcie_peak, "unit": "GB/s", "launches": k1_n, "bytes_per_launch": k1_b / max(1, k1_n),
+                "avg_launch_ms": k1_s / max(1, k1_n) * 1e3, "traffic": traffic.get("k1_dram_bytes_per_launch"),
+                "peak_source": "same-run CE simultaneous H2D+D2H probe"}
+    else:  # copy engines move the bytes; K3 checksum kernel reads HBM
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        roof = {"kernel": "nx_swap_kernel<checksum-only> (K3 record/verify)", "bound": "hbm", "achieved": k3_b / k3_s / 1e9 if k3_s else 0.0,
+                "peak": hbm, "unit": "GB/s", "launches": k3_n, "bytes_per_launch": k3_b / max(1, k3_n),
+                "avg_launch_ms": k3_s / max(1, k3_n) * 1e3, "traffic": traffic.get("k3_dram_bytes_per_launch"),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"] if roof["peak"] else None
+    base = cpu_baseline(2)
+    st0 = stats[0]
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_max / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic (splitmix64 pattern per 2 MiB block; every restore checksummed)",
+        "config": {"workload": WORKLOAD, "gpu_cap_gib": 32, "pinned_budget_gib": 16, "apps_gib": [16, 24],
+                   "bytes_per_step": bytes_rank / args.steps, "path": args.path,
+                   "l2": "inputs (8 GiB per direction per step) far exceed the 126 MB L2",
+                   "parallelism": f"{args.gpus} independent per-GPU instances, no collectives"},
+        "per_gpu_gbps": per_gpu, "pct_of_pcie_peak": per_gpu / pcie_peak * 100.0,
+        "switch_latency_ms": {"p50": statistics.median(lat) * 1e3, "p99": lat[min(len(lat) - 1, int(0.99 * len(lat)))] * 1e3,
+                              "min": lat[0] * 1e3, "max": lat[-1] * 1e3},
+        "ideal_latency_ms": max(st0["bytes_in"] / (probe["ce_bidir_h2d"] * 1e9), st0["bytes_out"] / (probe["ce_bidir_d2h"] * 1e9)) * 1e3,
+        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": sum(s["bytes_in"] for s in stats) / args.steps,
+                "d2h_bytes_per_step": sum(s["bytes_out"] for s in stats) / args.steps},
+        "roofline": roof,
+        "link_roofline": {"bound": "pcie", "achieved": per_gpu, "peak": pcie_peak, "unit": "GB/s", "frac": per_gpu / pcie_peak,
+                          "link": pcie_link(device), "peak_source": "same-run probe, 1 GiB/direction, 64 MiB chunks, max(CE, SM)"},
+        "pcie_probe": {k: (round(v, 2) if isinstance(v, float) else v) for k, v in probe.items()},
+        "calibration": calib,
+        "cpu_baseline": base,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "byte_exact": bad_all == 0,
+        "verified_restores": sum(s["verified"] for s in stats),
+        "x16_exchange": x16,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["product", "reference"], default="product")
+    ap.add_argument("--path", choices=["auto", "sm", "ce"], default="auto")
+    ap.add_argument("--no-x16", dest="x16", action="store_false")
+    args = ap.parse_args()
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            return run_reference(args, dist)
+        return run_product(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

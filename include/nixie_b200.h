@@ -189,6 +189,10 @@ int nx_gate_granted(nx_gate* g, uint32_t* app);
  * after the stream reaches it. */
 int nx_gate_app_checksum_async(nx_gate* g, uint32_t app, void* stream, uint64_t* out_pinned);
 int nx_stream_sync(void* stream);
+/* Plumbing for callers without their own CUDA runtime (tests, bindings). */
+int nx_stream_create(void** stream);
+void nx_stream_destroy(void* stream);
+int nx_stream_query(void* stream, int* done); /* *done = 1 when all queued work finished */
 int nx_pinned_alloc(size_t bytes, void** out);
 void nx_pinned_free(void* p);
 

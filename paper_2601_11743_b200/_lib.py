@@ -130,6 +130,9 @@ _SIGNATURES = [
     ("nx_gate_granted", c_int, [c_void_p, POINTER(c_uint32)]),
     ("nx_gate_app_checksum_async", c_int, [c_void_p, c_uint32, c_void_p, POINTER(c_uint64)]),
     ("nx_stream_sync", c_int, [c_void_p]),
+    ("nx_stream_create", c_int, [POINTER(c_void_p)]),
+    ("nx_stream_destroy", None, [c_void_p]),
+    ("nx_stream_query", c_int, [c_void_p, POINTER(c_int)]),
     ("nx_pinned_alloc", c_int, [c_size_t, POINTER(c_void_p)]),
     ("nx_pinned_free", None, [c_void_p]),
     ("nx_scenario_model", c_int, [c_char_p, POINTER(c_void_p), POINTER(c_size_t)]),

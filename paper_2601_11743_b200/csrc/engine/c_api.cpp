@@ -28,6 +28,7 @@ struct nx_gate {
   std::unique_ptr<LaunchGate> gate;
   unsigned long long* d_out = nullptr;  // [2] per app-checksum launch
   unsigned* d_blocks = nullptr;
+  unsigned* h_blocks = nullptr;  // pinned staging of the block list
   std::size_t blocks_cap = 0;
 };
 
@@ -429,8 +430,10 @@ int nx_gate_create(nx_engine* e, const nx_mlfq_config* mcfg, const nx_planner_co
 
 void nx_gate_destroy(nx_gate* g) {
   if (g == nullptr) return;
+  cudaDeviceSynchronize();
   cudaFree(g->d_out);
   cudaFree(g->d_blocks);
+  if (g->h_blocks) cudaFreeHost(g->h_blocks);
   delete g;
 }
 
@@ -486,18 +489,48 @@ int nx_gate_app_checksum_async(nx_gate* g, uint32_t app, void* stream, uint64_t*
       for (BlockId b : m.chunk(c).blocks) blocks.push_back(static_cast<unsigned>(b));
     auto s = static_cast<cudaStream_t>(stream);
     if (blocks.size() > g->blocks_cap) {
-      NX_CUDA(cudaStreamSynchronize(s));
+      NX_CUDA(cudaDeviceSynchronize());
       cudaFree(g->d_blocks);
+      cudaFreeHost(g->h_blocks);
       g->d_blocks = nullptr;
+      g->h_blocks = nullptr;
       NX_CUDA(cudaMalloc(&g->d_blocks, sizeof(unsigned) * blocks.size()));
+      NX_CUDA(cudaHostAlloc(&g->h_blocks, sizeof(unsigned) * blocks.size(), cudaHostAllocPortable));
       g->blocks_cap = blocks.size();
     }
-    NX_CUDA(cudaMemcpyAsync(g->d_blocks, blocks.data(), sizeof(unsigned) * blocks.size(), cudaMemcpyHostToDevice, s));
+    // Fully asynchronous: the launch may sit behind a device-side gate. The
+    // pinned staging list stays valid until the next call on this gate.
+    std::memcpy(g->h_blocks, blocks.data(), sizeof(unsigned) * blocks.size());
+    NX_CUDA(cudaMemcpyAsync(g->d_blocks, g->h_blocks, sizeof(unsigned) * blocks.size(), cudaMemcpyHostToDevice, s));
     NX_CUDA(cudaMemsetAsync(g->d_out, 0, 2 * sizeof(unsigned long long), s));
     NX_CUDA(launch_table_checksum(g->e->eng->device_frame_table(), g->d_blocks, static_cast<int>(blocks.size()), g->d_out, s));
     NX_CUDA(cudaMemcpyAsync(out_pinned, g->d_out, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    // The pageable vector must outlive the H2D copy of the block list.
-    NX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int nx_stream_create(void** out) {
+  return guard([&] {
+    need(out, "out");
+    cudaStream_t s = nullptr;
+    NX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    *out = s;
+  });
+}
+
+void nx_stream_destroy(void* stream) {
+  if (stream) cudaStreamDestroy(static_cast<cudaStream_t>(stream));
+}
+
+int nx_stream_query(void* stream, int* done) {
+  return guard([&] {
+    need(done, "done");
+    const cudaError_t e = cudaStreamQuery(static_cast<cudaStream_t>(stream));
+    if (e == cudaErrorNotReady) {
+      *done = 0;
+      return;
+    }
+    NX_CUDA(e);
+    *done = 1;
   });
 }
 

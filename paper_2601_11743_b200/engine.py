@@ -282,6 +282,11 @@ def run_scenario_real(spec: str, seed: int = 0x4E495849, config: Optional[Engine
     return L.take_string(p, n)
 
 
+def parse_path(name: str) -> int:
+    """'auto' | 'sm' | 'ce' -> PATH_* constant."""
+    return {"auto": L.PATH_AUTO, "sm": L.PATH_SM, "ce": L.PATH_CE}[name]
+
+
 def load_scenario(name: str) -> str:
     path = name if os.path.sep in name else os.path.join(SCENARIO_DIR, name if name.endswith(".scn") else name + ".scn")
     with open(path) as f:
@@ -300,6 +305,22 @@ def free_pinned(ptr: int) -> None:
 
 def stream_sync(stream: int) -> None:
     check(lib.nx_stream_sync(c_void_p(stream or None)))
+
+
+def stream_create() -> int:
+    s = c_void_p()
+    check(lib.nx_stream_create(byref(s)))
+    return s.value
+
+
+def stream_destroy(stream: int) -> None:
+    lib.nx_stream_destroy(c_void_p(stream))
+
+
+def stream_done(stream: int) -> bool:
+    d = c_int()
+    check(lib.nx_stream_query(c_void_p(stream), byref(d)))
+    return bool(d.value)
 
 
 DETERMINISTIC_TAGS = ("S", "P", "L", "R", "B", "E")

@@ -1,0 +1,150 @@
+"""CUDA engine parity on a B200 (run with -m gpu).
+
+Bit-exact bar for this byte path:
+  * every restore is byte-identical to the pre-eviction contents (K4 compare
+    against the pattern, C-oracle checksums of read-back blocks);
+  * the swap/schedule decisions of the real engine (plans, per-lane leg
+    sequences, placements, schedule events) equal the unmodified reference's
+    golden trace for the same scenario.
+"""
+import ctypes
+import hashlib
+import time
+
+import pytest
+
+from paper_2601_11743_b200 import (GIB, MIB, EngineConfig, LaunchGate, NixieError, PlannerConfig, SwapEngine,
+                                   load_scenario, run_scenario_real, trace_lines)
+from paper_2601_11743_b200 import engine as nxe
+from paper_2601_11743_b200._lib import PATH_AUTO, PATH_CE, PATH_SM, TIER_GPU, TIER_PAGED, TIER_PINNED
+
+pytestmark = pytest.mark.gpu
+SEED = 0x4E495849
+
+
+def det_sha(trace):
+    return hashlib.sha256("\n".join(trace_lines(trace)).encode()).hexdigest()
+
+
+def oracle_block_ok(eng, oracle_lib, app, block):
+    data = eng.read_block(block)
+    buf = ctypes.create_string_buffer(data, len(data))
+    assert oracle_lib.so_compare_block(buf, SEED, app, block) == 0
+    return oracle_lib.so_checksum(buf, len(data) // 8)
+
+
+def test_fill_verify_every_tier(gpu, oracle_lib):
+    with SwapEngine(gpu_capacity=64 * MIB, pinned_capacity=64 * MIB, paged_capacity=256 * MIB) as e:
+        e.allocate(0, 16 * MIB, TIER_GPU)
+        e.allocate(1, 10 * MIB, TIER_PINNED)
+        e.allocate(2, 134 * MIB, TIER_PAGED)  # two chunks, paged bounce path
+        for app in (0, 1, 2):
+            e.fill_pattern(app, SEED)
+            assert e.verify_pattern(app, SEED) == 0
+            for b in e.app_blocks(app)[:3]:
+                ck = oracle_block_ok(e, oracle_lib, app, b)
+                assert ck == oracle_lib.so_pattern_block_checksum(SEED, app, b) == e.block_checksum(b)
+        b = e.app_blocks(1)[1]
+        e.poke_block(b, 4099, 0xA5)
+        assert e.verify_pattern(1, SEED) == 1
+
+
+PATHS = [dict(path=PATH_SM), dict(path=PATH_SM, fused_launch=True), dict(path=PATH_CE), dict(path=PATH_AUTO),
+         dict(path=PATH_SM, legs_per_launch=3, pcie_legs_in_flight=5), dict(path=PATH_CE, legs_per_launch=1)]
+
+
+@pytest.mark.parametrize("opts", PATHS, ids=lambda o: "-".join(f"{k}{v}" for k, v in o.items()))
+def test_full_gpu_switch_is_byte_exact(gpu, oracle_lib, opts):
+    with SwapEngine(gpu_capacity=64 * MIB, pinned_capacity=112 * MIB, paged_capacity=64 * MIB, **opts) as e:
+        e.allocate(0, 64 * MIB, TIER_GPU)  # the incumbent fills the GPU
+        e.allocate(1, 48 * MIB, TIER_PINNED)
+        e.fill_pattern(0, SEED)
+        e.fill_pattern(1, SEED)
+        pc = PlannerConfig(streaming_window=8 * MIB, victim_order=[0])
+        plan, bi, bo = e.plan_switch(1, pc)
+        st = e.switch_to(1, pc)
+        assert (st["bytes_in"], st["bytes_out"]) == (bi, bo) == (48 * MIB, 48 * MIB)
+        assert st["verified"] == 24 and st["mismatches"] == 0 and st["unverified"] == 0
+        assert st["pcie_h2d_bytes"] == 48 * MIB and st["pcie_d2h_bytes"] == 48 * MIB
+        e.audit()
+        # Per-lane start order is the plan's order (lane FIFO).
+        moves = [ln.split() for ln in plan.splitlines()]
+        assert [b for b, *_ in e.lane_trace(0)] == [int(m[0]) for m in moves if m[4] == "fetch"]
+        assert [b for b, *_ in e.lane_trace(1)] == [int(m[0]) for m in moves if m[4] == "evict"]
+        assert e.verify_pattern(0, SEED) == 0 and e.verify_pattern(1, SEED) == 0
+        for b in e.app_blocks(1)[::7]:
+            assert oracle_block_ok(e, oracle_lib, 1, b) == oracle_lib.so_pattern_block_checksum(SEED, 1, b)
+        assert e.app_bytes_resident(1)[0] == 48 * MIB
+        st2 = e.switch_to(0, PlannerConfig(streaming_window=8 * MIB, victim_order=[1]))
+        assert st2["mismatches"] == 0 and st2["verified"] == st2["pcie_h2d_bytes"] // (2 * MIB)
+        assert e.verify_pattern(0, SEED) == 0 and e.verify_pattern(1, SEED) == 0
+        e.audit()
+
+
+@pytest.mark.parametrize("path", [PATH_SM, PATH_CE])
+@pytest.mark.parametrize("name", ["kat_planner_ordering", "small_three_apps", "small_pinned_only", "c1_two_apps_2g"])
+def test_real_engine_trace_equals_reference(gpu, golden, name, path):
+    real = run_scenario_real(load_scenario(name), seed=SEED, path=path)
+    assert det_sha(real) == golden["scenarios"][name]["det_sha256"]
+    v = [ln.split() for ln in real.splitlines() if ln.startswith("V ")]
+    f = [ln.split() for ln in real.splitlines() if ln.startswith("F ")]
+    assert v and all(x[3] == "0" for x in v), v
+    assert f and all(x[2] == "0" for x in f), f
+
+
+@pytest.mark.parametrize("path", [PATH_SM, PATH_CE])
+def test_corrupted_restore_is_detected(gpu, path):
+    with SwapEngine(gpu_capacity=32 * MIB, pinned_capacity=64 * MIB, paged_capacity=64 * MIB, path=path) as e:
+        e.allocate(0, 32 * MIB, TIER_GPU)
+        e.allocate(1, 16 * MIB, TIER_PINNED)
+        e.fill_pattern(0, SEED)
+        e.fill_pattern(1, SEED)
+        victim = e.app_blocks(1)[3]
+        e.poke_block(victim, 777, 0x5A)  # bit rot while parked in the pinned ring
+        with pytest.raises(NixieError) as err:
+            e.switch_to(1, PlannerConfig(streaming_window=4 * MIB, victim_order=[0]))
+        assert err.value.kind == "InvariantViolation"
+        assert "checksum mismatch" in str(err.value) and str(victim) in str(err.value)
+
+
+def test_launch_gate_holds_kernels_until_swap_in(gpu, oracle_lib):
+    e = SwapEngine(gpu_capacity=64 * MIB, pinned_capacity=112 * MIB, paged_capacity=64 * MIB)
+    s0, s1 = nxe.stream_create(), nxe.stream_create()
+    out = nxe.pinned_buffer(16)
+    try:
+        e.allocate(0, 64 * MIB, TIER_GPU)
+        e.allocate(1, 48 * MIB, TIER_PINNED)
+        e.fill_pattern(0, SEED)
+        e.fill_pattern(1, SEED)
+        gate = LaunchGate(e, PlannerConfig(streaming_window=8 * MIB))
+        gate.attach(0, s0, 0.0)
+        gate.attach(1, s1, 0.0)
+        gate.context_switch(0, 0.0)  # app 0 is resident: empty plan, grant only
+        assert gate.granted() == 0 and gate.before_launch(0, 0.1)
+        assert not gate.before_launch(1, 0.2)  # app 1 not resident: gated on device
+        gate.app_checksum_async(1, s1, out)
+        time.sleep(0.3)
+        assert not nxe.stream_done(s1), "app 1's kernel ran before its swap-in"
+        assert gate.select_next(0.3) == 1
+        st = gate.context_switch(1, 0.3)
+        assert st["bytes_in"] == 48 * MIB and st["mismatches"] == 0
+        nxe.stream_sync(s1)
+        res = (ctypes.c_uint64 * 2).from_address(out)
+        want = sum(oracle_lib.so_pattern_block_checksum(SEED, 1, b) for b in e.app_blocks(1)) % (1 << 64)
+        assert res[1] == 0 and res[0] == want
+        assert gate.granted() == 1 and not gate.before_launch(0, 0.5)
+        gate.close()
+    finally:
+        nxe.free_pinned(out)
+        nxe.stream_destroy(s0)
+        nxe.stream_destroy(s1)
+        e.close()
+
+
+def test_calibration_and_probe(gpu):
+    with SwapEngine(gpu_capacity=64 * MIB, pinned_capacity=64 * MIB, paged_capacity=64 * MIB) as e:
+        p = e.probe_pcie(256 * MIB, 32 * MIB)
+        for k in ("ce_h2d", "ce_d2h", "ce_bidir_total", "sm_h2d", "sm_d2h", "sm_bidir_total"):
+            assert p[k] > 5.0, p
+        c = e.calibrate(64 * MIB)
+        assert len(c["legs"]) == 8 and all(x > 1.0 for x in c["ce_gbps"] + c["sm_gbps"])
