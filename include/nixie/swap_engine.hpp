@@ -73,13 +73,15 @@ struct SwitchStats {
   int k3_launches = 0;
 };
 
-// Opens a launch gate on the device once the incoming app's last fetch has
-// been submitted: `value` is written to `device_word` on the H2D stream
-// (cuStreamWriteValue64), or `event` is recorded there if no word is given.
+// Launch-gate hook of execute(): once the incoming app's last fetch has been
+// submitted (and its frame table published), `event` is recorded on the H2D
+// stream and `callback(ctx)` runs on the calling thread. A waiter that
+// enqueues cudaStreamWaitEvent(app_stream, event) after the callback gets a
+// device-side dependency whose producer is already enqueued.
 struct GateRelease {
-  std::uint64_t* device_word = nullptr;
-  std::uint64_t value = 0;
   cudaEvent_t event = nullptr;
+  void (*callback)(void* ctx) = nullptr;
+  void* ctx = nullptr;
 };
 
 struct LegTrace {
@@ -170,25 +172,28 @@ class SwapEngine {
 
 // Kernel-launch gate (§3 steps 1-2 and 6, §4): an app's kernels run
 // only while it holds the grant and its working set is GPU-resident.
-//   * before_launch(app, stream): a granted, resident app passes. Otherwise
-//     the app's request is enqueued with the scheduler and its stream gets a
-//     device-side wait (cuStreamWaitValue64 on the app's gate word) for its
-//     next grant epoch, so the kernel it is about to launch stays queued on
-//     the GPU until the swap-in lands. No host thread blocks.
+// Thread-safe: application threads call before_launch while a scheduler
+// thread runs context_switch.
+//   * before_launch(app, now): a granted, resident app passes (true).
+//     Otherwise the app's request is enqueued with the scheduler and the
+//     calling thread is held until a switch to the app has submitted its last
+//     fetch; the app's stream then waits on the device for that fetch to land
+//     and before_launch returns false: the caller's next launch on its
+//     stream is ordered after the swap-in.
 //   * context_switch(to, now): pauses the incumbent (its later launches are
-//     gated; its queued kernels drain before any eviction starts, on the
+//     held; its queued kernels drain before any eviction starts, on the
 //     device), plans with the scheduler's victim hint, executes with real
-//     copies, grants `to`, and writes its gate word on the H2D stream after
-//     the last fetch.
+//     copies and grants `to`.
 class LaunchGate {
  public:
   LaunchGate(SwapEngine& engine, MlfqScheduler& sched, PlannerConfig cfg);
   ~LaunchGate();
 
   void attach(AppId app, cudaStream_t stream);
-  bool before_launch(AppId app, Seconds now);  // true = passed immediately
+  bool before_launch(AppId app, Seconds now, double timeout_s = 120.0);
   ExecResult context_switch(AppId to, Seconds now);
-  bool stream_mem_ops() const;  // device-side gating available
+  std::optional<AppId> select_next(Seconds now);
+  std::optional<AppId> granted();
 
  private:
   struct Impl;

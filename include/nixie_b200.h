@@ -176,9 +176,12 @@ int nx_gate_create(nx_engine* e, const nx_mlfq_config* mcfg, const nx_planner_co
 void nx_gate_destroy(nx_gate* g);
 /* MlfqScheduler::register_app (mlfq.cpp:51-57) + the app's CUDA stream. */
 int nx_gate_attach(nx_gate* g, uint32_t app, void* stream, double now);
-/* Interposed kernel launch: *passed = 1 if the app may launch now; else its
- * request is enqueued (mlfq.cpp:132-138) and its stream is gated on-device. */
-int nx_gate_before_launch(nx_gate* g, uint32_t app, double now, int* passed);
+/* Interposed kernel launch (thread-safe): *passed = 1 if the app holds the
+ * grant and is resident. Otherwise its request is enqueued (mlfq.cpp:132-138)
+ * and the calling thread is held until a switch to the app has submitted its
+ * last fetch; the app's stream then waits on the device for that fetch to
+ * land (*passed = 0). Fails with InvalidState after timeout_s. */
+int nx_gate_before_launch(nx_gate* g, uint32_t app, double now, double timeout_s, int* passed);
 /* MlfqScheduler::select_next (mlfq.cpp:144-162); *app = UINT32_MAX if none. */
 int nx_gate_select_next(nx_gate* g, double now, uint32_t* app);
 /* Pause incumbent, drain, plan, execute, grant `to`, release its gate. */

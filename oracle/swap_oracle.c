@@ -8,6 +8,13 @@
 
 #define SO_GOLDEN 0x9E3779B97F4A7C15ull
 #define SO_BLOCK_WORDS (2u * 1024u * 1024u / 8u)
+#define SO_CK_MUL 0xD6E8FEB86659FD93ull
+
+/* Checksum term of word w at word index i (paper_2601_11743_b200/csrc/cuda/nx_common.cuh). */
+static uint64_t so_ck_term(uint64_t w, uint64_t i) {
+  uint64_t t = (w ^ (i * SO_GOLDEN)) * SO_CK_MUL;
+  return t ^ (t >> 32);
+}
 
 uint64_t so_mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -27,13 +34,13 @@ void so_fill_block(uint64_t* dst, uint64_t seed, uint32_t app, uint64_t block) {
 
 uint64_t so_checksum(const uint64_t* words, size_t nwords) {
   uint64_t s = 0;
-  for (size_t i = 0; i < nwords; ++i) s += so_mix64(words[i] + (uint64_t)(i % SO_BLOCK_WORDS) * SO_GOLDEN);
+  for (size_t i = 0; i < nwords; ++i) s += so_ck_term(words[i], (uint64_t)(i % SO_BLOCK_WORDS));
   return s;
 }
 
 uint64_t so_pattern_block_checksum(uint64_t seed, uint32_t app, uint64_t block) {
   uint64_t s = 0;
-  for (uint64_t w = 0; w < SO_BLOCK_WORDS; ++w) s += so_mix64(so_pattern_word(seed, app, block, w) + w * SO_GOLDEN);
+  for (uint64_t w = 0; w < SO_BLOCK_WORDS; ++w) s += so_ck_term(so_pattern_word(seed, app, block, w), w);
   return s;
 }
 

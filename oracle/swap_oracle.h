@@ -18,7 +18,8 @@ uint64_t so_splitmix64(uint64_t x);
 uint64_t so_pattern_word(uint64_t seed, uint32_t app, uint64_t block, uint64_t word);
 /* Fills a 2 MiB block with the pattern. */
 void so_fill_block(uint64_t* dst, uint64_t seed, uint32_t app, uint64_t block);
-/* Checksum of `nwords` 64-bit words (word index restarts at 0 per block). */
+/* Checksum of `nwords` 64-bit words (word index restarts at 0 per block):
+ * sum of t ^ (t >> 32), t = (w_i ^ i*0x9E3779B97F4A7C15) * 0xD6E8FEB86659FD93. */
 uint64_t so_checksum(const uint64_t* words, size_t nwords);
 /* Checksum of the pattern block without materialising it. */
 uint64_t so_pattern_block_checksum(uint64_t seed, uint32_t app, uint64_t block);

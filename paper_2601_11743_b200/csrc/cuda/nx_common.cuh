@@ -2,7 +2,7 @@
 // working-set pattern and the per-block checksum.
 //
 // Checksum of a 2 MiB block = sum over its 64-bit words w_i (i = word index
-// within the block) of mix64(w_i + i * golden), mod 2^64. It is a sum, so any
+// within the block) of ck_term(w_i, i) (below), mod 2^64. It is a sum, so any
 // split of the block over warps, CTAs or launches reduces to the same value,
 // and the position term catches swapped or misplaced words. The swap kernel
 // computes it while the bytes stream through registers (no extra HBM pass).
@@ -38,6 +38,16 @@ NX_HD std::uint64_t pattern_word(std::uint64_t seed, std::uint32_t app, std::uin
   return splitmix64(seed ^ (static_cast<std::uint64_t>(app) << 48) ^ (block << 20) ^ w);
 }
 
-NX_HD std::uint64_t ck_term(std::uint64_t word, std::uint64_t index) { return mix64(word + index * kGolden); }
+// Checksum term of the 64-bit word at word index `index` of its block:
+// (word ^ index*golden) * kCkMul, xor-folded. Multiplying by an odd constant
+// and the fold are bijections, so any change to a word changes its term; the
+// position key makes swapped words change the sum. One 64-bit multiply per
+// word keeps the checksum well below the HBM roofline's instruction budget.
+inline constexpr std::uint64_t kCkMul = 0xD6E8FEB86659FD93ull;
+NX_HD std::uint64_t ck_term_keyed(std::uint64_t word, std::uint64_t key) {
+  const std::uint64_t t = (word ^ key) * kCkMul;
+  return t ^ (t >> 32);
+}
+NX_HD std::uint64_t ck_term(std::uint64_t word, std::uint64_t index) { return ck_term_keyed(word, index * kGolden); }
 
 }  // namespace nixie::b200

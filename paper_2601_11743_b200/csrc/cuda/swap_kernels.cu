@@ -95,6 +95,10 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
 template <bool kChecksum>
 __device__ __forceinline__ std::uint64_t stream_part(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                                      std::uint64_t nvec, std::uint64_t j0, int gt) {
+  // Position key of word 2*idx is 2*idx*golden; keys advance by constants
+  // instead of a multiply per word (vector idx = j0 + b + u*kGroupThreads).
+  constexpr std::uint64_t kKeyStepU = 2ull * kGroupThreads * kGolden;
+  std::uint64_t key = 2ull * (j0 + static_cast<std::uint64_t>(gt)) * kGolden;
   std::uint64_t acc = 0;
   for (std::uint64_t b = gt; b < nvec; b += kGroupThreads * kUnroll) {
     uint4 v[kUnroll];
@@ -106,7 +110,13 @@ __device__ __forceinline__ std::uint64_t stream_part(const uint4* __restrict__ s
     }
     if (kChecksum) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) acc += ck16(v[u], j0 + b + u * kGroupThreads);
+      for (int u = 0; u < kUnroll; ++u) {
+        const std::uint64_t w0 = static_cast<std::uint64_t>(v[u].x) | (static_cast<std::uint64_t>(v[u].y) << 32);
+        const std::uint64_t w1 = static_cast<std::uint64_t>(v[u].z) | (static_cast<std::uint64_t>(v[u].w) << 32);
+        const std::uint64_t k = key + u * kKeyStepU;
+        acc += ck_term_keyed(w0, k) + ck_term_keyed(w1, k + kGolden);
+      }
+      key += kUnroll * kKeyStepU;
     }
   }
   return acc;

@@ -34,6 +34,13 @@ struct nx_gate {
 
 namespace {
 
+// A launch gate parks application streams behind a device-side wait. With
+// the default 8 hardware work queues, streams share queues and a parked
+// stream could stall an engine stream queued behind it; 32 queues give every
+// stream of a typical instance its own. Only effective if the process has not
+// initialised CUDA before loading this library; an explicit setting wins.
+__attribute__((constructor)) void nx_widen_hw_queues() { setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0); }
+
 thread_local std::string g_err;
 
 template <typename F>
@@ -424,6 +431,9 @@ int nx_gate_create(nx_engine* e, const nx_mlfq_config* mcfg, const nx_planner_co
     g->sched->set_logging(true);
     g->gate = std::make_unique<LaunchGate>(*e->eng, *g->sched, to_cpp(pcfg));
     NX_CUDA(cudaMalloc(&g->d_out, 2 * sizeof(unsigned long long)));
+    g->blocks_cap = 1u << 20;  // 2 TiB of 2 MiB blocks: never regrown while streams may be gated
+    NX_CUDA(cudaMalloc(&g->d_blocks, sizeof(unsigned) * g->blocks_cap));
+    NX_CUDA(cudaHostAlloc(&g->h_blocks, sizeof(unsigned) * g->blocks_cap, cudaHostAllocPortable));
     *out = g.release();
   });
 }
@@ -445,10 +455,10 @@ int nx_gate_attach(nx_gate* g, uint32_t app, void* stream, double now) {
   });
 }
 
-int nx_gate_before_launch(nx_gate* g, uint32_t app, double now, int* passed) {
+int nx_gate_before_launch(nx_gate* g, uint32_t app, double now, double timeout_s, int* passed) {
   return guard([&] {
     need(g, "gate");
-    const bool ok = g->gate->before_launch(app, now);
+    const bool ok = g->gate->before_launch(app, now, timeout_s);
     if (passed) *passed = ok ? 1 : 0;
   });
 }
@@ -457,7 +467,7 @@ int nx_gate_select_next(nx_gate* g, double now, uint32_t* app) {
   return guard([&] {
     need(g, "gate");
     need(app, "app");
-    const auto n = g->sched->select_next(now);
+    const auto n = g->gate->select_next(now);
     *app = n ? *n : ~uint32_t{0};
   });
 }
@@ -474,7 +484,7 @@ int nx_gate_granted(nx_gate* g, uint32_t* app) {
   return guard([&] {
     need(g, "gate");
     need(app, "app");
-    const auto a = g->sched->granted();
+    const auto a = g->gate->granted();
     *app = a ? *a : ~uint32_t{0};
   });
 }
@@ -488,16 +498,9 @@ int nx_gate_app_checksum_async(nx_gate* g, uint32_t app, void* stream, uint64_t*
     for (ChunkId c : m.chunks_of(app))
       for (BlockId b : m.chunk(c).blocks) blocks.push_back(static_cast<unsigned>(b));
     auto s = static_cast<cudaStream_t>(stream);
-    if (blocks.size() > g->blocks_cap) {
-      NX_CUDA(cudaDeviceSynchronize());
-      cudaFree(g->d_blocks);
-      cudaFreeHost(g->h_blocks);
-      g->d_blocks = nullptr;
-      g->h_blocks = nullptr;
-      NX_CUDA(cudaMalloc(&g->d_blocks, sizeof(unsigned) * blocks.size()));
-      NX_CUDA(cudaHostAlloc(&g->h_blocks, sizeof(unsigned) * blocks.size(), cudaHostAllocPortable));
-      g->blocks_cap = blocks.size();
-    }
+    // No device-wide synchronisation here: `stream` (or another app's
+    // stream) may be parked behind a gate that only a later switch opens.
+    if (blocks.size() > g->blocks_cap) throw SimError(Err::CapacityExceeded, "app has more blocks than the gate's list");
     // Fully asynchronous: the launch may sit behind a device-side gate. The
     // pinned staging list stays valid until the next call on this gate.
     std::memcpy(g->h_blocks, blocks.data(), sizeof(unsigned) * blocks.size());

@@ -24,7 +24,6 @@
 #include <map>
 #include <thread>
 
-#include "gate_ops.hpp"
 #include "lanes.hpp"
 #include "nixie/swap_engine.hpp"
 #include "nx_kernels.h"
@@ -51,9 +50,9 @@ int log2_bucket(int n) {
 
 struct ExecOptions {
   cudaStream_t drain = nullptr;
-  CUdeviceptr gate_word = 0;  // written with gate_value on the H2D stream after the last fetch
-  std::uint64_t gate_value = 0;
-  cudaEvent_t gate_event = nullptr;  // recorded instead when stream memory ops are unavailable
+  cudaEvent_t gate_event = nullptr;              // recorded on the H2D stream after the last fetch
+  void (*gate_callback)(void*) = nullptr;        // then called (launch-gate release)
+  void* gate_ctx = nullptr;
 };
 
 struct SwapEngine::Impl final : detail::LaneSink {
@@ -69,6 +68,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   cudaStream_t aux = nullptr;
   int sm_count = 0;
   int max_ctas = 0;
+  int k3_ctas = 0;  // checksum-only launches: HBM-bound, want more resident warps
 
   // Per-block state, indexed by BlockId.
   std::vector<std::uint32_t> unit;  // frame / slot / paged unit of the block's current (source) tier
@@ -111,7 +111,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
     const int n = static_cast<int>(l.size());
     cudaEvent_t a = take_event(), z = take_event();
     NX_CUDA(cudaEventRecord(a, cs));
-    NX_CUDA(launch_swap(l.data(), arriving ? 0 : n, arriving ? n : 0, flags, ck, scratch[2 + B.stream], max_ctas, cs));
+    NX_CUDA(launch_swap(l.data(), arriving ? 0 : n, arriving ? n : 0, flags, ck, scratch[2 + B.stream], k3_ctas, cs));
     NX_CUDA(cudaEventRecord(z, cs));
     B.k3ev.push_back({a, z});
     B.k3_bytes += static_cast<Bytes>(n) * kBlockBytes;
@@ -146,6 +146,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
     NX_CUDA(cudaSetDevice(cfg.device));
     sm_count = device_sm_count(cfg.device);
     max_ctas = cfg.max_ctas > 0 ? cfg.max_ctas : 2 * std::max(sm_count, 1);
+    k3_ctas = 4 * std::max(sm_count, 1);
     if (cfg.numa_bind) numa = numa_for_device(cfg.device);
 
     hw.tier_capacity[0] = cfg.gpu_capacity;
@@ -175,8 +176,18 @@ struct SwapEngine::Impl final : detail::LaneSink {
     grow_tables(65536);
   }
 
+  // Synchronises only the engine's own streams: a device-wide sync could wait
+  // on an application stream parked behind a launch gate.
+  void sync_own() {
+    for (auto s : st) NX_CUDA(cudaStreamSynchronize(s));
+    for (auto s : cks) NX_CUDA(cudaStreamSynchronize(s));
+    NX_CUDA(cudaStreamSynchronize(aux));
+  }
+
   ~Impl() override {
-    cudaDeviceSynchronize();
+    for (auto s : st) cudaStreamSynchronize(s);
+    for (auto s : cks) cudaStreamSynchronize(s);
+    cudaStreamSynchronize(aux);
     for (cudaEvent_t e : events) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
     cudaFree(ck.ck_ref);
@@ -510,12 +521,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
     const std::size_t n = mem.block_count();
     std::memcpy(h_frames_stage, h_frames, sizeof(std::uint64_t) * n);
     NX_CUDA(cudaMemcpyAsync(d_frames, h_frames_stage, sizeof(std::uint64_t) * n, cudaMemcpyHostToDevice, st[kH2D]));
-    if (opts->gate_word != 0) {
-      if (gate_write(reinterpret_cast<CUstream>(st[kH2D]), opts->gate_word, opts->gate_value) != CUDA_SUCCESS)
-        throw SimError(Err::IoError, "cuStreamWriteValue64 failed");
-    } else if (opts->gate_event != nullptr) {
-      NX_CUDA(cudaEventRecord(opts->gate_event, st[kH2D]));
-    }
+    if (opts->gate_event != nullptr) NX_CUDA(cudaEventRecord(opts->gate_event, st[kH2D]));
+    if (opts->gate_callback != nullptr) opts->gate_callback(opts->gate_ctx);
   }
 
   void flush() {
@@ -706,7 +713,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
 
   void check_status() {
     NxDevStatus now{};
-    NX_CUDA(cudaMemcpy(&now, ck.status, sizeof(now), cudaMemcpyDeviceToHost));
+    NX_CUDA(cudaMemcpyAsync(&now, ck.status, sizeof(now), cudaMemcpyDeviceToHost, aux));
+    NX_CUDA(cudaStreamSynchronize(aux));
     stats.verified = now.verified - status_seen.verified;
     stats.unverified = now.unverified - status_seen.unverified;
     stats.mismatches = now.mismatches - status_seen.mismatches;
@@ -719,40 +727,6 @@ struct SwapEngine::Impl final : detail::LaneSink {
     }
   }
 };
-
-// ---- driver-API entry points for the launch gate ---------------------------
-namespace {
-using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
-using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
-WriteFn g_write = nullptr;
-WaitFn g_wait = nullptr;
-bool resolve_mem_ops() {
-  static bool tried = false, ok = false;
-  if (tried) return ok;
-  tried = true;
-  cudaDriverEntryPointQueryResult q1{}, q2{};
-  void* w = nullptr;
-  void* t = nullptr;
-  if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &w, cudaEnableDefault, &q1) != cudaSuccess || !w) return false;
-  if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &t, cudaEnableDefault, &q2) != cudaSuccess || !t) return false;
-  g_write = reinterpret_cast<WriteFn>(w);
-  g_wait = reinterpret_cast<WaitFn>(t);
-  ok = true;
-  return ok;
-}
-}  // namespace
-
-CUresult gate_write(CUstream s, CUdeviceptr addr, std::uint64_t v) {
-  if (!resolve_mem_ops()) return CUDA_ERROR_NOT_SUPPORTED;
-  return g_write(s, addr, v, 0);
-}
-
-CUresult gate_wait_geq(CUstream s, CUdeviceptr addr, std::uint64_t v) {
-  if (!resolve_mem_ops()) return CUDA_ERROR_NOT_SUPPORTED;
-  return g_wait(s, addr, v, CU_STREAM_WAIT_VALUE_GEQ);
-}
-
-bool gate_mem_ops_available() { return resolve_mem_ops(); }
 
 // ---- SwapEngine ---------------------------------------------------------------
 SwapEngine::SwapEngine(const EngineConfig& cfg) : impl_(std::make_unique<Impl>(cfg)) {}
@@ -771,9 +745,9 @@ ExecResult SwapEngine::execute(const MigrationPlan& plan, const PlannerConfig& c
   ExecOptions o;
   o.drain = drain;
   if (release != nullptr) {
-    o.gate_word = reinterpret_cast<CUdeviceptr>(release->device_word);
-    o.gate_value = release->value;
     o.gate_event = release->event;
+    o.gate_callback = release->callback;
+    o.gate_ctx = release->ctx;
   }
   return impl_->execute(plan, cfg, o);
 }
@@ -800,7 +774,8 @@ const std::uint64_t* SwapEngine::device_frame_table() const { return impl_->d_fr
 
 std::uint64_t SwapEngine::block_checksum(BlockId b) const {
   unsigned long long v = 0;
-  NX_CUDA(cudaMemcpy(&v, impl_->ck.ck_ref + b, sizeof(v), cudaMemcpyDeviceToHost));
+  NX_CUDA(cudaMemcpyAsync(&v, impl_->ck.ck_ref + b, sizeof(v), cudaMemcpyDeviceToHost, impl_->aux));
+  NX_CUDA(cudaStreamSynchronize(impl_->aux));
   return v;
 }
 
@@ -811,7 +786,10 @@ void SwapEngine::read_block(BlockId b, void* dst) {
   const Location& loc = m.mem.block(b).loc;
   if (!loc.is_resident()) throw SimError(Err::InvalidState, "block in flight");
   if (loc.tier == TierId::Gpu)
-    NX_CUDA(cudaMemcpy(dst, m.arena.frame(m.unit[b]), kBlockBytes, cudaMemcpyDeviceToHost));
+  {
+    NX_CUDA(cudaMemcpyAsync(dst, m.arena.frame(m.unit[b]), kBlockBytes, cudaMemcpyDeviceToHost, m.aux));
+    NX_CUDA(cudaStreamSynchronize(m.aux));
+  }
   else
     std::memcpy(dst, m.host_addr(loc.tier, m.unit[b]), kBlockBytes);
 }
@@ -822,7 +800,10 @@ void SwapEngine::poke_block(BlockId b, std::uint64_t offset, std::uint8_t value)
   if (!loc.is_resident()) throw SimError(Err::InvalidState, "block in flight");
   if (offset >= kBlockBytes) throw SimError(Err::InvalidState, "offset outside the block");
   if (loc.tier == TierId::Gpu)
-    NX_CUDA(cudaMemcpy(m.arena.frame(m.unit[b]) + offset, &value, 1, cudaMemcpyHostToDevice));
+  {
+    NX_CUDA(cudaMemcpyAsync(m.arena.frame(m.unit[b]) + offset, &value, 1, cudaMemcpyHostToDevice, m.aux));
+    NX_CUDA(cudaStreamSynchronize(m.aux));
+  }
   else
     m.host_addr(loc.tier, m.unit[b])[offset] = value;
 }
@@ -904,14 +885,14 @@ PcieProbe SwapEngine::probe_pcie(Bytes bytes, Bytes chunk) {
   auto run = [&](bool sm, bool h2d, bool d2h, double* gbs_h2d, double* gbs_d2h, double* gbs_total) {
     double best_h = 0, best_d = 0, best_t = 0;
     for (int rep = 0; rep < 4; ++rep) {
-      NX_CUDA(cudaDeviceSynchronize());
+      m.sync_own();
       if (h2d) NX_CUDA(cudaEventRecord(ev[0], m.st[0]));
       if (d2h) NX_CUDA(cudaEventRecord(ev[2], m.st[1]));
       if (h2d) issue(0, sm);
       if (d2h) issue(1, sm);
       if (h2d) NX_CUDA(cudaEventRecord(ev[1], m.st[0]));
       if (d2h) NX_CUDA(cudaEventRecord(ev[3], m.st[1]));
-      NX_CUDA(cudaDeviceSynchronize());
+      m.sync_own();
       float th = 0, td = 0, a = 0, z = 0;
       if (h2d) NX_CUDA(cudaEventElapsedTime(&th, ev[0], ev[1]));
       if (d2h) NX_CUDA(cudaEventElapsedTime(&td, ev[2], ev[3]));
@@ -966,7 +947,7 @@ std::array<double, 3> SwapEngine::probe_copy_variant(int variant, Bytes bytes, i
   auto go = [&](bool h2d, bool d2h) {
     double best = 0;
     for (int rep = 0; rep < 4; ++rep) {
-      NX_CUDA(cudaDeviceSynchronize());
+      m.sync_own();
       if (h2d) NX_CUDA(cudaEventRecord(ev[0], m.st[0]));
       if (d2h) NX_CUDA(cudaEventRecord(ev[2], m.st[1]));
       // variant >= 10 mixes mechanisms: 10 = CE H2D + SM D2H, 11 = SM H2D + CE D2H
@@ -989,7 +970,7 @@ std::array<double, 3> SwapEngine::probe_copy_variant(int variant, Bytes bytes, i
       }
       if (h2d) NX_CUDA(cudaEventRecord(ev[1], m.st[0]));
       if (d2h) NX_CUDA(cudaEventRecord(ev[3], m.st[1]));
-      NX_CUDA(cudaDeviceSynchronize());
+      m.sync_own();
       m.launches_total += (h2d ? 1 : 0) + (d2h ? 1 : 0);
       if (rep == 0) continue;
       float t = 0;

@@ -237,9 +237,12 @@ class LaunchGate:
     def attach(self, app: int, stream: int, now: float = 0.0) -> None:
         check(lib.nx_gate_attach(self._h, app, c_void_p(stream or None), now))
 
-    def before_launch(self, app: int, now: float) -> bool:
+    def before_launch(self, app: int, now: float, timeout_s: float = 120.0) -> bool:
+        """True: the app may launch now. False: it was held until its swap-in
+        was submitted and its stream now waits on the device for it to land.
+        Blocks the calling thread (ctypes releases the GIL)."""
         ok = c_int()
-        check(lib.nx_gate_before_launch(self._h, app, now, byref(ok)))
+        check(lib.nx_gate_before_launch(self._h, app, now, timeout_s, byref(ok)))
         return bool(ok.value)
 
     def select_next(self, now: float) -> Optional[int]:

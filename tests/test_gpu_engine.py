@@ -9,6 +9,7 @@ Bit-exact bar for this byte path:
 """
 import ctypes
 import hashlib
+import threading
 import time
 
 import pytest
@@ -121,18 +122,29 @@ def test_launch_gate_holds_kernels_until_swap_in(gpu, oracle_lib):
         gate.attach(1, s1, 0.0)
         gate.context_switch(0, 0.0)  # app 0 is resident: empty plan, grant only
         assert gate.granted() == 0 and gate.before_launch(0, 0.1)
-        assert not gate.before_launch(1, 0.2)  # app 1 not resident: gated on device
-        gate.app_checksum_async(1, s1, out)
+        # App 1's "interposed launch" runs on its own thread and is held there.
+        passed = {}
+
+        def app1():
+            passed["v"] = gate.before_launch(1, 0.2, timeout_s=60.0)
+            gate.app_checksum_async(1, s1, out)  # ordered after the swap-in on the device
+
+        th = threading.Thread(target=app1)
+        th.start()
         time.sleep(0.3)
-        assert not nxe.stream_done(s1), "app 1's kernel ran before its swap-in"
+        assert th.is_alive(), "app 1's launch was not held"
         assert gate.select_next(0.3) == 1
-        st = gate.context_switch(1, 0.3)
+        st = gate.context_switch(1, 0.3)  # scheduler thread: swap app 1 in
+        th.join(60)
+        assert not th.is_alive() and passed["v"] is False
         assert st["bytes_in"] == 48 * MIB and st["mismatches"] == 0
         nxe.stream_sync(s1)
         res = (ctypes.c_uint64 * 2).from_address(out)
         want = sum(oracle_lib.so_pattern_block_checksum(SEED, 1, b) for b in e.app_blocks(1)) % (1 << 64)
         assert res[1] == 0 and res[0] == want
-        assert gate.granted() == 1 and not gate.before_launch(0, 0.5)
+        assert gate.granted() == 1
+        with pytest.raises(NixieError):  # app 0 lost the grant: its launch is held (here: times out)
+            gate.before_launch(0, 0.5, timeout_s=0.2)
         gate.close()
     finally:
         nxe.free_pinned(out)
