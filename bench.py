@@ -302,6 +302,7 @@ def run_product(args, dist: Dist):
     pcie_peak = max(probe["ce_bidir_total"], probe["sm_bidir_total"])
     per_gpu = value / args.gpus
     k3_s = sum(s["k3_s"] for s in stats)
+    k3_busy = sum(s["k3_busy_s"] for s in stats)
     k3_b = sum(s["k3_bytes"] for s in stats)
     k1_s = sum(s["k1_s"] for s in stats)
     k1_b = sum(s["k1_bytes"] for s in stats)
@@ -315,10 +316,15 @@ def run_product(args, dist: Dist):
                 "peak_source": "same-run CE simultaneous H2D+D2H probe"}
     else:  # copy engines move the bytes; K3 checksum kernel reads HBM
         hbm = peaks.get("hbm_gbs", 6650.0)
-        roof = {"kernel": "nx_swap_kernel<checksum-only> (K3 record/verify)", "bound": "hbm", "achieved": k3_b / k3_s / 1e9 if k3_s else 0.0,
+        # Both lanes' K3 launches run concurrently (two side streams); the
+        # achieved HBM rate is their bytes over the union of their intervals.
+        roof = {"kernel": "nx_swap_kernel<checksum-only> (K3 record/verify)", "bound": "hbm",
+                "achieved": k3_b / k3_busy / 1e9 if k3_busy else 0.0,
+                "achieved_per_launch_avg": k3_b / k3_s / 1e9 if k3_s else 0.0,
                 "peak": hbm, "unit": "GB/s", "launches": k3_n, "bytes_per_launch": k3_b / max(1, k3_n),
-                "avg_launch_ms": k3_s / max(1, k3_n) * 1e3, "traffic": traffic.get("k3_dram_bytes_per_launch"),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
+                "avg_launch_ms": k3_s / max(1, k3_n) * 1e3, "busy_ms_per_step": k3_busy / args.steps * 1e3,
+                "traffic": traffic.get("k3_dram_bytes_per_launch"),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"] if roof["peak"] else None
     base = cpu_baseline(2)
     st0 = stats[0]

@@ -42,8 +42,8 @@ struct EngineConfig {
   Bytes pinned_capacity = 16 * kGiB;  // enforced pinned budget
   Bytes paged_capacity = 96 * kGiB;
   CopyPath path = CopyPath::Auto;
-  int pcie_legs_in_flight = 256;      // per direction (x 2 MiB)
-  int legs_per_launch = 64;           // max legs per K1 launch / CE batch
+  int pcie_legs_in_flight = 512;      // per direction (x 2 MiB)
+  int legs_per_launch = 128;          // max legs per K1 launch / CE batch (measured best)
   int host_threads = 8;               // pinned<->paged copy workers
   int host_legs_in_flight = 64;       // per host lane
   int max_ctas = 0;                   // K1 grid cap; 0 = 2 x SM count
@@ -68,7 +68,8 @@ struct SwitchStats {
   double k1_s = 0;      // K1 swap launches (SM path): summed durations
   Bytes k1_bytes = 0;   // bytes they moved across PCIe
   int k1_launches = 0;
-  double k3_s = 0;      // K3 checksum launches (CE path)
+  double k3_s = 0;      // K3 checksum launches (CE path): summed durations
+  double k3_busy_s = 0; // union of K3 launch intervals (both lanes' launches overlap)
   Bytes k3_bytes = 0;   // HBM bytes they read
   int k3_launches = 0;
 };

@@ -86,6 +86,7 @@ typedef struct nx_switch_stats {
   double k1_s, k3_s;
   uint64_t k1_bytes, k3_bytes;
   int k1_launches, k3_launches;
+  double k3_busy_s; /* union of the K3 launch intervals */
 } nx_switch_stats;
 
 typedef struct nx_pcie_probe {

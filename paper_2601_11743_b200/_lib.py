@@ -70,7 +70,7 @@ class SwitchStatsC(Structure):
         ("ce_batches_h2d", c_int), ("ce_batches_d2h", c_int), ("host_legs", c_int), ("verified", c_uint64),
         ("unverified", c_uint64), ("mismatches", c_uint64), ("tp_to_gpu", c_double), ("tp_from_gpu", c_double),
         ("tp_bidir", c_double), ("k1_s", c_double), ("k3_s", c_double), ("k1_bytes", c_uint64), ("k3_bytes", c_uint64),
-        ("k1_launches", c_int), ("k3_launches", c_int),
+        ("k1_launches", c_int), ("k3_launches", c_int), ("k3_busy_s", c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -126,6 +126,7 @@ void fill_stats(const SwapEngine& eng, const ExecResult& r, nx_switch_stats* out
   out->k3_bytes = s.k3_bytes;
   out->k1_launches = s.k1_launches;
   out->k3_launches = s.k3_launches;
+  out->k3_busy_s = s.k3_busy_s;
   if (s.device_span_s > 0) {
     double lo = 1e30, hi = 0;
     for (const TransferRecord& t : r.events)

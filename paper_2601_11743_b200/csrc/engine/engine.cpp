@@ -545,7 +545,14 @@ struct SwapEngine::Impl final : detail::LaneSink {
       while (!p.empty()) {
         // Batches ramp up from first_batch_legs so the first fetches can start
         // (into frames the first evictions free) after a short first batch.
-        const int cap = std::min<int>(L, std::max(1, cfg.first_batch_legs) << std::min(batches_sent[lane], 12));
+        int cap = std::min<int>(L, std::max(1, cfg.first_batch_legs) << std::min(batches_sent[lane], 12));
+        // Ramp down at the end of the evictions: the fetches trail the
+        // evictions by one batch (they need the frames a landed batch frees),
+        // so smaller last eviction batches shorten the fetch-only tail.
+        if (lane == kD2H) {
+          const int left = static_cast<int>(p.size() + lanes->queued(kD2H));
+          cap = std::min(cap, std::max(std::max(1, cfg.first_batch_legs), left / 4));
+        }
         // Enough queued on the stream to hide the host: wait for a full batch.
         if (inflight[lane].size() >= 2 && static_cast<int>(p.size()) < cap) break;
         const int take = std::min<int>(static_cast<int>(p.size()), cap);
@@ -682,6 +689,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   // Device timestamps for the PCIe records and the per-stream kernel time.
   void finalize_timing(ExecResult& res) {
     double first = 1e30, last = 0;
+    std::vector<std::pair<double, double>> k3_spans;
     for (const Batch& B : landed) {
       float a = 0, b = 0;
       NX_CUDA(cudaEventElapsedTime(&a, ev0, B.ev_start));
@@ -696,9 +704,11 @@ struct SwapEngine::Impl final : detail::LaneSink {
         ++stats.k1_launches;
       }
       for (const auto& ke : B.k3ev) {
-        float d = 0;
-        NX_CUDA(cudaEventElapsedTime(&d, ke[0], ke[1]));
-        stats.k3_s += d * 1e-3;
+        float a0 = 0, a1 = 0;
+        NX_CUDA(cudaEventElapsedTime(&a0, ev0, ke[0]));
+        NX_CUDA(cudaEventElapsedTime(&a1, ev0, ke[1]));
+        stats.k3_s += (a1 - a0) * 1e-3;
+        k3_spans.emplace_back(a0 * 1e-3, a1 * 1e-3);
         ++stats.k3_launches;
       }
       stats.k3_bytes += B.k3_bytes;
@@ -709,6 +719,21 @@ struct SwapEngine::Impl final : detail::LaneSink {
       }
     }
     stats.device_span_s = landed.empty() ? 0.0 : last - first;
+    // K3 launches of the two lanes overlap on the device; their busy time is
+    // the union of their intervals (bytes / busy = achieved HBM bandwidth).
+    std::sort(k3_spans.begin(), k3_spans.end());
+    double busy = 0, lo = -1, hi = -1;
+    for (const auto& [a, b] : k3_spans) {
+      if (a > hi) {
+        busy += hi - lo;
+        lo = a;
+        hi = b;
+      } else {
+        hi = std::max(hi, b);
+      }
+    }
+    busy += hi - lo;
+    stats.k3_busy_s = k3_spans.empty() ? 0.0 : busy;
   }
 
   void check_status() {

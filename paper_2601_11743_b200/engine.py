@@ -28,8 +28,8 @@ class EngineConfig:
     pinned_capacity: int = 16 * GIB
     paged_capacity: int = 96 * GIB
     path: int = L.PATH_AUTO
-    pcie_legs_in_flight: int = 256
-    legs_per_launch: int = 64
+    pcie_legs_in_flight: int = 512
+    legs_per_launch: int = 128
     host_threads: int = 8
     host_legs_in_flight: int = 64
     max_ctas: int = 0

@@ -1,0 +1,60 @@
+"""N>1 host logic on CPU: bench.py's per-rank aggregation (barrier, sum of
+bytes, max of time) over gloo with world_size 2, as torchrun would launch it.
+The swap path itself has no collective: each rank is an independent Nixie
+instance."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+WORKER = r"""
+import json, os, sys
+sys.path.insert(0, %r)
+import bench
+d = bench.Dist()
+d.barrier()
+r = d.rank
+out = {"rank": r, "world": d.world, "sum": d.reduce(10.0 + r, "sum"), "max": d.reduce(1.5 * (r + 1), "max")}
+d.barrier()
+d.close()
+print(json.dumps(out))
+""" % ROOT
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_two_rank_aggregation_over_gloo():
+    port = free_port()
+    procs = []
+    for rank in range(2):
+        env = dict(os.environ, RANK=str(rank), WORLD_SIZE="2", LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, "-c", WORKER], env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                      text=True))
+    outs = []
+    for p in procs:
+        o, e = p.communicate(timeout=240)
+        assert p.returncode == 0, e[-2000:]
+        outs.append(json.loads(o.strip().splitlines()[-1]))
+    for o in outs:
+        assert o["world"] == 2
+        assert o["sum"] == 21.0 and o["max"] == 3.0
+
+
+def test_reference_arm_nonzero_ranks_exit_cleanly():
+    """Under torchrun only rank 0 runs the reference arm; others exit 0."""
+    port = free_port()
+    env = dict(os.environ, RANK="1", WORLD_SIZE="1", LOCAL_RANK="1", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # WORLD_SIZE=1 keeps the process group out of the way; rank 1 must print nothing.
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1", "--warmup", "0"],
+                       env=env, capture_output=True, text=True, timeout=240)
+    assert p.returncode == 0 and p.stdout.strip() == ""
