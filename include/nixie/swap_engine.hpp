@@ -51,6 +51,7 @@ struct EngineConfig {
   bool verify = true;                 // checksum every restore
   bool numa_bind = true;              // pinned ring + workers on the GPU's NUMA node
   int first_batch_legs = 8;           // batch-size ramp start (doubles per batch up to legs_per_launch)
+  bool k3_tma = true;                 // CE-path checksum pass on the TMA pipeline (else the LDG loop)
 };
 
 struct SwitchStats {
@@ -165,6 +166,8 @@ class SwapEngine {
   // Measures both mechanisms at 1..128 legs per batch and installs the
   // faster one per size for CopyPath::Auto.
   Calibration calibrate(Bytes bytes_per_direction);
+  // K3 launch duration (us) for 1, 2, 4 ... 128 legs: [0] TMA pipeline, [1] LDG loop.
+  std::vector<std::array<double, 2>> probe_checksum_launch();
 
  private:
   struct Impl;

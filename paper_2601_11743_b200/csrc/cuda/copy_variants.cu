@@ -10,6 +10,7 @@
 #include <cstdint>
 
 #include "nx_common.cuh"
+#include "nx_tma.cuh"
 
 namespace nixie::b200 {
 
@@ -45,50 +46,6 @@ __global__ void __launch_bounds__(256) nx_raw_ldg_kernel(const uint4* __restrict
   }
 }
 
-__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
-  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, unsigned bytes, std::uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(smem)),
-               "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void bulk_store(void* gmem, const void* smem, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)), "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
 // One thread per CTA drives a kStages-deep ring of kChunk-byte stages over the
 // CTA's contiguous share of [src, src + bytes).
 template <int kChunk, int kStages>
@@ -102,7 +59,7 @@ __global__ void __launch_bounds__(32) nx_raw_tma_kernel(const std::uint8_t* __re
   const std::uint64_t c1 = c0 + per < nchunks ? c0 + per : nchunks;
   if (threadIdx.x != 0 || c0 >= c1) return;
   for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  mbar_fence_init();
   const std::uint64_t n = c1 - c0;
   for (std::uint64_t i = 0; i < n && i < static_cast<std::uint64_t>(kStages); ++i) {
     mbar_expect_tx(&full[i], kChunk);
@@ -124,7 +81,20 @@ __global__ void __launch_bounds__(32) nx_raw_tma_kernel(const std::uint8_t* __re
   bulk_wait_all();
 }
 
+__global__ void nx_spin_kernel(unsigned ns) {
+  const unsigned long long t0 = clock64();
+  (void)t0;
+  for (unsigned waited = 0; waited < ns; waited += 1000) __nanosleep(1000);
+}
+
 }  // namespace
+
+// Keeps a stream busy for ~ns so that events recorded after it time the next
+// kernel alone, not the host's launch latency (timing probes only).
+cudaError_t launch_spin(unsigned ns, cudaStream_t stream) {
+  nx_spin_kernel<<<1, 32, 0, stream>>>(ns);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_raw_copy(int variant, void* dst, const void* src, std::uint64_t bytes, int ctas, cudaStream_t stream) {
   switch (variant) {

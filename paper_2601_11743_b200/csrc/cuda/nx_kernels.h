@@ -42,6 +42,7 @@ struct NxCkTables {
 struct NxScratch {
   unsigned long long* part_sums;  // [kMaxLegsPerLaunch << kMaxPartsLog2]
   unsigned int* part_count;       // [kMaxLegsPerLaunch], self-resetting
+  unsigned long long* leg_acc;    // [kMaxLegsPerLaunch], zero at rest (TMA checksum), self-resetting
 };
 
 enum NxSwapFlags : std::uint32_t {
@@ -56,6 +57,13 @@ enum NxSwapFlags : std::uint32_t {
 // are checksum-only (K3). Returns the launch error.
 cudaError_t launch_swap(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t flags, const NxCkTables& ck,
                         const NxScratch& scratch, int max_ctas, cudaStream_t stream);
+
+// K3 on the TMA pipeline: checksum-only pass over `n` legs of HBM frames
+// (legs[i].src), recorded (arriving = false) or verified (arriving = true).
+// One CTA per SM: a producer thread streams 32 KiB cp.async.bulk chunks into
+// a 6-stage shared-memory ring, 16 consumer warps checksum from shared memory.
+cudaError_t launch_checksum_tma(const NxLeg* legs, int n, bool arriving, std::uint32_t flags, const NxCkTables& ck,
+                                const NxScratch& scratch, int ctas, cudaStream_t stream);
 
 // K4: pattern fill (records checksums, marks them valid) and compare (adds
 // the number of mismatching 16-byte vectors per leg into mismatches[i]).

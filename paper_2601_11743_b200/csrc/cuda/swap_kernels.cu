@@ -29,20 +29,26 @@
 
 #include "nx_common.cuh"
 #include "nx_kernels.h"
+#include "nx_tma.cuh"
 
 namespace nixie::b200 {
 
 namespace {
 
-struct SwapParams {
-  NxLeg legs[kMaxLegsPerLaunch];
+// Kernel parameter block sized for up to N legs. Launches pick the smallest
+// N that fits: the block is copied into every launch, so a 6 KB block for a
+// 1-leg launch is pure overhead.
+template <int N>
+struct SwapParamsT {
   NxCkTables ck;
   NxScratch scratch;
   std::uint32_t n_d2h;
   std::uint32_t n_h2d;
   std::uint32_t parts_log2;
   std::uint32_t flags;
+  NxLeg legs[N];
 };
+using SwapParams = SwapParamsT<kMaxLegsPerLaunch>;
 
 struct FillParams {
   NxLeg legs[kMaxLegsPerLaunch];
@@ -124,7 +130,8 @@ __device__ __forceinline__ std::uint64_t stream_part(const uint4* __restrict__ s
 
 // Final checksum of leg `li` (all parts summed): record on departure, check
 // on arrival.
-__device__ void finish_leg(const SwapParams& p, std::uint32_t li, unsigned long long sum, bool arriving) {
+template <class P>
+__device__ void finish_leg(const P& p, std::uint32_t li, unsigned long long sum, bool arriving) {
   const std::uint32_t blk = p.legs[li].block;
   if (!arriving) {
     p.ck.ck_ref[blk] = sum;
@@ -145,8 +152,8 @@ __device__ void finish_leg(const SwapParams& p, std::uint32_t li, unsigned long 
   }
 }
 
-template <bool kChecksum>
-__global__ void __launch_bounds__(2 * kGroupThreads) nx_swap_kernel(const __grid_constant__ SwapParams p) {
+template <bool kChecksum, class P>
+__global__ void __launch_bounds__(2 * kGroupThreads) nx_swap_kernel(const __grid_constant__ P p) {
   __shared__ unsigned long long red[2][4];
   const int group = threadIdx.x / kGroupThreads;
   const int gt = threadIdx.x % kGroupThreads;
@@ -235,6 +242,114 @@ __global__ void __launch_bounds__(256) nx_pattern_kernel(const __grid_constant__
   }
 }
 
+// K3 on the TMA pipeline. The chunks of all legs form one sequence; CTA b
+// takes the contiguous, balanced range [total*b/grid, total*(b+1)/grid), so
+// every SM gets the same bytes whatever the leg count. The last warp's lane 0
+// is the producer (bulk loads into a kStages ring, full/empty mbarriers); the
+// consume. A leg split across CTAs is combined by the CTA that completes its
+// chunk count (threadfence + counter, accumulator reset for the next launch).
+constexpr int kTmaChunk = 32 << 10;
+constexpr int kTmaStages = 6;
+constexpr int kTmaConsumers = 512;  // 16 consumer warps: the checksum must keep up with ~23 B/clk/SM of HBM
+constexpr std::uint32_t kTmaChunksPerLeg = kBlockBytesDev / kTmaChunk;
+
+template <class P>
+__device__ void tma_flush(const P& p, std::uint32_t base, std::uint32_t leg, std::uint32_t chunks,
+                          unsigned long long acc, bool arriving, unsigned long long* red) {
+  acc = warp_sum(acc);
+  const int warp = threadIdx.x / 32;
+  if ((threadIdx.x & 31) == 0) red[warp] = acc;
+  asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
+  if (threadIdx.x == 0) {
+    unsigned long long part = 0;
+    for (int w = 0; w < kTmaConsumers / 32; ++w) part += red[w];
+    atomicAdd(&p.scratch.leg_acc[base + leg], part);
+    __threadfence();
+    const unsigned before = atomicAdd(&p.scratch.part_count[base + leg], chunks);
+    if (before + chunks == kTmaChunksPerLeg) {
+      __threadfence();
+      const unsigned long long total = atomicExch(&p.scratch.leg_acc[base + leg], 0ull);
+      p.scratch.part_count[base + leg] = 0u;
+      finish_leg(p, base + leg, total, arriving);
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
+}
+
+template <class P>
+__global__ void __launch_bounds__(kTmaConsumers + 32, 1) nx_checksum_tma_kernel(const __grid_constant__ P p) {
+  extern __shared__ __align__(1024) std::uint8_t ring[];
+  __shared__ __align__(8) std::uint64_t full[kTmaStages];
+  __shared__ __align__(8) std::uint64_t empty[kTmaStages];
+  __shared__ unsigned long long red[kTmaConsumers / 32];
+  const bool arriving = p.n_h2d != 0;
+  const std::uint32_t base = arriving ? p.n_d2h : 0u;
+  const std::uint64_t total = static_cast<std::uint64_t>(arriving ? p.n_h2d : p.n_d2h) * kTmaChunksPerLeg;
+  const std::uint64_t c0 = total * blockIdx.x / gridDim.x;
+  const std::uint64_t c1 = total * (blockIdx.x + 1) / gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaConsumers / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (c0 >= c1) return;
+  const std::uint64_t n = c1 - c0;
+  const int warp = threadIdx.x / 32;
+
+  if (warp == kTmaConsumers / 32) {  // producer warp
+    if ((threadIdx.x & 31) == 0) {
+      for (std::uint64_t i = 0; i < n; ++i) {
+        const int s = static_cast<int>(i % kTmaStages);
+        if (i >= static_cast<std::uint64_t>(kTmaStages))
+          mbar_wait(&empty[s], static_cast<unsigned>((i / kTmaStages - 1) & 1));
+        const std::uint64_t c = c0 + i;
+        const auto* src = static_cast<const std::uint8_t*>(p.legs[base + c / kTmaChunksPerLeg].src) +
+                          (c % kTmaChunksPerLeg) * static_cast<std::uint64_t>(kTmaChunk);
+        mbar_expect_tx(&full[s], kTmaChunk);
+        bulk_load(ring + s * kTmaChunk, src, kTmaChunk, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // Consumers: thread t reads vectors t, t+256, ... of each 32 KiB chunk.
+  constexpr int kVecsPerThread = kTmaChunk / 16 / kTmaConsumers;
+  constexpr std::uint64_t kKeyStep = 2ull * kTmaConsumers * kGolden;
+  std::uint32_t leg = static_cast<std::uint32_t>(c0 / kTmaChunksPerLeg);
+  std::uint32_t seg_chunks = 0;
+  unsigned long long acc = 0;
+  for (std::uint64_t i = 0; i < n; ++i) {
+    const std::uint64_t c = c0 + i;
+    const auto li = static_cast<std::uint32_t>(c / kTmaChunksPerLeg);
+    if (li != leg) {
+      tma_flush(p, base, leg, seg_chunks, acc, arriving, red);
+      leg = li;
+      seg_chunks = 0;
+      acc = 0;
+    }
+    const int s = static_cast<int>(i % kTmaStages);
+    mbar_wait(&full[s], static_cast<unsigned>((i / kTmaStages) & 1));
+    const uint4* v = reinterpret_cast<const uint4*>(ring + s * kTmaChunk);
+    const std::uint64_t vbase = (c % kTmaChunksPerLeg) * static_cast<std::uint64_t>(kTmaChunk / 16);
+    std::uint64_t key = 2ull * (vbase + threadIdx.x) * kGolden;
+#pragma unroll
+    for (int k = 0; k < kVecsPerThread; ++k) {
+      const uint4 x = v[threadIdx.x + k * kTmaConsumers];
+      const std::uint64_t w0 = static_cast<std::uint64_t>(x.x) | (static_cast<std::uint64_t>(x.y) << 32);
+      const std::uint64_t w1 = static_cast<std::uint64_t>(x.z) | (static_cast<std::uint64_t>(x.w) << 32);
+      acc += ck_term_keyed(w0, key) + ck_term_keyed(w1, key + kGolden);
+      key += kKeyStep;
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+    ++seg_chunks;
+  }
+  tma_flush(p, base, leg, seg_chunks, acc, arriving, red);
+}
+
 int parts_log2_for(int n_legs, int groups_wanted) {
   int k = 0;
   while (k < kMaxPartsLog2 && (n_legs << k) < groups_wanted) ++k;
@@ -249,11 +364,12 @@ int device_sm_count(int device) {
   return sms;
 }
 
-cudaError_t launch_swap(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t flags, const NxCkTables& ck,
-                        const NxScratch& scratch, int max_ctas, cudaStream_t stream) {
-  if (n_d2h < 0 || n_h2d < 0 || n_d2h + n_h2d > kMaxLegsPerLaunch) return cudaErrorInvalidValue;
-  if (n_d2h + n_h2d == 0) return cudaSuccess;
-  SwapParams p;
+namespace {
+
+template <int N>
+cudaError_t launch_swap_n(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t flags, const NxCkTables& ck,
+                          const NxScratch& scratch, int max_ctas, cudaStream_t stream) {
+  SwapParamsT<N> p;
   for (int i = 0; i < n_d2h + n_h2d; ++i) p.legs[i] = legs[i];
   p.ck = ck;
   p.scratch = scratch;
@@ -270,10 +386,58 @@ cudaError_t launch_swap(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t f
   if (ctas > max_ctas) ctas = max_ctas;
   if (ctas < 1) ctas = 1;
   if (flags & kNxNoChecksum)
-    nx_swap_kernel<false><<<ctas, 2 * kGroupThreads, 0, stream>>>(p);
+    nx_swap_kernel<false, SwapParamsT<N>><<<ctas, 2 * kGroupThreads, 0, stream>>>(p);
   else
-    nx_swap_kernel<true><<<ctas, 2 * kGroupThreads, 0, stream>>>(p);
+    nx_swap_kernel<true, SwapParamsT<N>><<<ctas, 2 * kGroupThreads, 0, stream>>>(p);
   return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t launch_checksum_tma_n(const NxLeg* legs, int n, bool arriving, std::uint32_t flags, const NxCkTables& ck,
+                                  const NxScratch& scratch, int ctas, cudaStream_t stream) {
+  static bool configured = false;
+  constexpr int kSmem = kTmaStages * kTmaChunk;
+  if (!configured) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(nx_checksum_tma_kernel<SwapParamsT<N>>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  SwapParamsT<N> p;
+  for (int i = 0; i < n; ++i) p.legs[i] = legs[i];
+  p.ck = ck;
+  p.scratch = scratch;
+  p.n_d2h = arriving ? 0u : static_cast<std::uint32_t>(n);
+  p.n_h2d = arriving ? static_cast<std::uint32_t>(n) : 0u;
+  p.parts_log2 = 0;
+  p.flags = flags;
+  const int chunks = n * static_cast<int>(kTmaChunksPerLeg);
+  if (ctas > chunks) ctas = chunks;
+  nx_checksum_tma_kernel<SwapParamsT<N>><<<ctas, kTmaConsumers + 32, kSmem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_swap(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t flags, const NxCkTables& ck,
+                        const NxScratch& scratch, int max_ctas, cudaStream_t stream) {
+  if (n_d2h < 0 || n_h2d < 0 || n_d2h + n_h2d > kMaxLegsPerLaunch) return cudaErrorInvalidValue;
+  const int n = n_d2h + n_h2d;
+  if (n == 0) return cudaSuccess;
+  if (n <= 8) return launch_swap_n<8>(legs, n_d2h, n_h2d, flags, ck, scratch, max_ctas, stream);
+  if (n <= 32) return launch_swap_n<32>(legs, n_d2h, n_h2d, flags, ck, scratch, max_ctas, stream);
+  if (n <= 128) return launch_swap_n<128>(legs, n_d2h, n_h2d, flags, ck, scratch, max_ctas, stream);
+  return launch_swap_n<kMaxLegsPerLaunch>(legs, n_d2h, n_h2d, flags, ck, scratch, max_ctas, stream);
+}
+
+cudaError_t launch_checksum_tma(const NxLeg* legs, int n, bool arriving, std::uint32_t flags, const NxCkTables& ck,
+                                const NxScratch& scratch, int ctas, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  if (n > kMaxLegsPerLaunch) return cudaErrorInvalidValue;
+  if (n <= 8) return launch_checksum_tma_n<8>(legs, n, arriving, flags, ck, scratch, ctas, stream);
+  if (n <= 32) return launch_checksum_tma_n<32>(legs, n, arriving, flags, ck, scratch, ctas, stream);
+  if (n <= 128) return launch_checksum_tma_n<128>(legs, n, arriving, flags, ck, scratch, ctas, stream);
+  return launch_checksum_tma_n<kMaxLegsPerLaunch>(legs, n, arriving, flags, ck, scratch, ctas, stream);
 }
 
 cudaError_t launch_fill(const NxLeg* legs, int n, std::uint64_t seed, const NxCkTables& ck, cudaStream_t stream) {

@@ -86,6 +86,7 @@ EngineConfig to_cpp(const nx_engine_config& c) {
   o.verify = c.verify != 0;
   o.numa_bind = c.numa_bind != 0;
   o.first_batch_legs = c.first_batch_legs;
+  o.k3_tma = c.k3_tma != 0;
   return o;
 }
 
@@ -188,6 +189,7 @@ void nx_engine_config_default(nx_engine_config* c) {
   c->verify = d.verify;
   c->numa_bind = d.numa_bind;
   c->first_batch_legs = d.first_batch_legs;
+  c->k3_tma = d.k3_tma;
 }
 
 void nx_planner_config_default(nx_planner_config* c) {
@@ -391,6 +393,18 @@ int nx_calibrate(nx_engine* e, uint64_t bytes, double sm_gbps[8], double ce_gbps
       if (sm_gbps) sm_gbps[k] = c.sm_gbps[k];
       if (ce_gbps) ce_gbps[k] = c.ce_gbps[k];
       if (sm_faster) sm_faster[k] = c.sm_gbps[k] > c.ce_gbps[k] ? 1 : 0;
+    }
+  });
+}
+
+int nx_probe_checksum_launch(nx_engine* e, double us[16]) {
+  return guard([&] {
+    need(e, "engine");
+    need(us, "us");
+    const auto r = e->eng->probe_checksum_launch();
+    for (std::size_t k = 0; k < r.size() && k < 8; ++k) {
+      us[2 * k] = r[k][0];
+      us[2 * k + 1] = r[k][1];
     }
   });
 }

@@ -111,7 +111,10 @@ struct SwapEngine::Impl final : detail::LaneSink {
     const int n = static_cast<int>(l.size());
     cudaEvent_t a = take_event(), z = take_event();
     NX_CUDA(cudaEventRecord(a, cs));
-    NX_CUDA(launch_swap(l.data(), arriving ? 0 : n, arriving ? n : 0, flags, ck, scratch[2 + B.stream], k3_ctas, cs));
+    if (cfg.k3_tma)
+      NX_CUDA(launch_checksum_tma(l.data(), n, arriving, flags, ck, scratch[2 + B.stream], sm_count, cs));
+    else
+      NX_CUDA(launch_swap(l.data(), arriving ? 0 : n, arriving ? n : 0, flags, ck, scratch[2 + B.stream], k3_ctas, cs));
     NX_CUDA(cudaEventRecord(z, cs));
     B.k3ev.push_back({a, z});
     B.k3_bytes += static_cast<Bytes>(n) * kBlockBytes;
@@ -168,6 +171,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
       NX_CUDA(cudaMalloc(&s.part_sums, sizeof(unsigned long long) * (kMaxLegsPerLaunch << kMaxPartsLog2)));
       NX_CUDA(cudaMalloc(&s.part_count, sizeof(unsigned int) * kMaxLegsPerLaunch));
       NX_CUDA(cudaMemset(s.part_count, 0, sizeof(unsigned int) * kMaxLegsPerLaunch));
+      NX_CUDA(cudaMalloc(&s.leg_acc, sizeof(unsigned long long) * kMaxLegsPerLaunch));
+      NX_CUDA(cudaMemset(s.leg_acc, 0, sizeof(unsigned long long) * kMaxLegsPerLaunch));
     }
     void* b = nullptr;
     NX_CUDA(cudaHostAlloc(&b, static_cast<std::size_t>(kBounceUnits) * kBlockBytes, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -200,6 +205,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
     for (auto& s : scratch) {
       cudaFree(s.part_sums);
       cudaFree(s.part_count);
+      cudaFree(s.leg_acc);
     }
     if (bounce) cudaFreeHost(bounce);
     for (auto& s : st) cudaStreamDestroy(s);
@@ -952,6 +958,7 @@ PcieProbe SwapEngine::probe_pcie(Bytes bytes, Bytes chunk) {
 
 namespace nixie::b200 {
 cudaError_t launch_raw_copy(int variant, void* dst, const void* src, std::uint64_t bytes, int ctas, cudaStream_t stream);
+cudaError_t launch_spin(unsigned ns, cudaStream_t stream);
 
 // Raw copy-variant probe (copy_variants.cu): GB/s of H2D alone, D2H alone,
 // and the total while both run, `bytes` per direction in one launch each.
@@ -1022,6 +1029,49 @@ std::array<double, 3> SwapEngine::probe_copy_variant(int variant, Bytes bytes, i
 namespace nixie::b200 {
 // Measured per-batch-size choice between the SM swap kernel and the copy
 // engines (both directions running, the swap's operating point).
+// K3 launch timing for 1, 2, 4 ... 128 legs over a scratch HBM buffer
+// (CUDA events, median of 9): microseconds per launch, [0] TMA, [1] LDG.
+std::vector<std::array<double, 2>> SwapEngine::probe_checksum_launch() {
+  Impl& m = *impl_;
+  constexpr int kMax = 128;
+  std::uint8_t* buf = nullptr;
+  NX_CUDA(cudaMalloc(&buf, kMax * kBlockBytes));
+  NX_CUDA(cudaMemset(buf, 7, kMax * kBlockBytes));
+  cudaEvent_t a, z;
+  NX_CUDA(cudaEventCreate(&a));
+  NX_CUDA(cudaEventCreate(&z));
+  std::vector<std::array<double, 2>> out;
+  for (int n = 1; n <= kMax; n *= 2) {
+    std::vector<NxLeg> legs;
+    for (int i = 0; i < n; ++i) legs.push_back(NxLeg{buf + static_cast<std::size_t>(i) * kBlockBytes, nullptr, static_cast<std::uint32_t>(i), 0});
+    std::array<double, 2> r{};
+    for (int variant = 0; variant < 2; ++variant) {
+      std::vector<double> t;
+      for (int rep = 0; rep < 10; ++rep) {
+        NX_CUDA(launch_spin(200000, m.aux));  // host finishes enqueueing before the GPU reaches `a`
+        NX_CUDA(cudaEventRecord(a, m.aux));
+        if (variant == 0)
+          NX_CUDA(launch_checksum_tma(legs.data(), n, false, 0, m.ck, m.scratch[2], m.sm_count, m.aux));
+        else
+          NX_CUDA(launch_swap(legs.data(), n, 0, 0, m.ck, m.scratch[2], m.k3_ctas, m.aux));
+        NX_CUDA(cudaEventRecord(z, m.aux));
+        NX_CUDA(cudaEventSynchronize(z));
+        float ms = 0;
+        NX_CUDA(cudaEventElapsedTime(&ms, a, z));
+        if (rep > 0) t.push_back(ms * 1e3);
+        ++m.launches_total;
+      }
+      std::sort(t.begin(), t.end());
+      r[variant] = t[t.size() / 2];
+    }
+    out.push_back(r);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(z);
+  cudaFree(buf);
+  return out;
+}
+
 Calibration SwapEngine::calibrate(Bytes bytes_per_direction) {
   Calibration c;
   std::vector<bool> table;

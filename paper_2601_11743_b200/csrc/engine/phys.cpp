@@ -178,6 +178,8 @@ void HostCopyPool::worker(std::vector<int> cpus) {
       j = jobs_.front();
       jobs_.pop_front();
     }
+    // Plain memcpy: measured equal to 32-byte streaming stores on the B200
+    // hosts (the pinned<->paged lanes are host-DRAM-bound either way).
     std::memcpy(j.dst, j.src, j.bytes);
     {
       std::lock_guard<std::mutex> lk(done_mu_);

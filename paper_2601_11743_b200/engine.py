@@ -37,6 +37,7 @@ class EngineConfig:
     verify: bool = True
     numa_bind: bool = True
     first_batch_legs: int = 8
+    k3_tma: bool = True
 
     def to_c(self) -> L.EngineConfigC:
         c = L.EngineConfigC()
