@@ -5,8 +5,9 @@ H2D+D2H PCIe peak); p50/p99 context-switch latency.
 
 Workload (BASELINE.json configs[1]): an interactive 16 GiB app and a 24 GiB
 background app on one B200 capped at 32 GiB, 16 GiB pinned budget; the apps
-start cold in pageable memory and alternate; a step is one steady-state
-context switch (8 GiB out of the GPU + 8 GiB in, both directions at once).
+alternate; a step is one steady-state context switch (8 GiB out of the GPU +
+8 GiB in, both directions at once). The cold start from pageable memory and
+the full scenario are parity-tested in tests/test_gpu_scale.py.
 
 Lines printed by rank 0 (one JSON line):
   value  whole-job GB/s, device-timed (CUDA events around every PCIe launch
@@ -43,8 +44,7 @@ sys.path.insert(0, ROOT)
 GIB, MIB = 1 << 30, 1 << 20
 METRIC = "bidir swap GB/s per GPU (% of PCIe peak); p50/p99 context-switch latency"
 WORKLOAD = ("c2_interactive_background: interactive 16 GiB + background 24 GiB apps alternating on one B200 "
-            "capped at 32 GiB, 16 GiB pinned budget, cold start in pageable memory, steady-state switches "
-            "(8 GiB out + 8 GiB in per switch)")
+            "capped at 32 GiB, 16 GiB pinned budget, steady-state switches (8 GiB out + 8 GiB in per switch)")
 
 
 def dist_env():
@@ -133,6 +133,33 @@ def pcie_link(device: int) -> dict:
         return {"gpu": name, "gen": int(g), "gen_max": int(gm), "width": int(w), "width_max": int(wm)}
     except Exception as e:  # noqa: BLE001
         return {"error": str(e)[:80]}
+
+
+def settle_host_link(eng, limit_s: float = 30.0) -> dict:
+    """Before warm-up: short bidirectional CE probes until two consecutive
+    readings agree within 3% (host-side background work, e.g. reclaim after a
+    large free, or a neighbour's burst, has passed), at most `limit_s`."""
+    t0 = time.perf_counter()
+    readings = []
+    while time.perf_counter() - t0 < limit_s:
+        readings.append(round(eng.probe_pcie(256 * MIB, 64 * MIB)["ce_bidir_total"], 2))
+        if len(readings) >= 2 and abs(readings[-1] - readings[-2]) <= 0.03 * readings[-1]:
+            break
+    return {"readings_gbps": readings, "secs": round(time.perf_counter() - t0, 2)}
+
+
+def check_host_memory(dist: "Dist") -> None:
+    """Each rank pins 16 GiB (+ 2 GiB of probe/bounce buffers); refuse to start
+    rather than drive the host out of memory under torchrun."""
+    try:
+        with open("/proc/meminfo") as f:
+            avail = {ln.split(":")[0]: int(ln.split()[1]) * 1024 for ln in f}.get("MemAvailable", 0)
+    except OSError:
+        return
+    per_node = int(os.environ.get("LOCAL_WORLD_SIZE", str(dist.world)))
+    need = per_node * 20 * GIB
+    if avail and avail < need:
+        raise SystemExit(f"bench: {per_node} ranks need ~{need / GIB:.0f} GiB of host memory, {avail / GIB:.0f} GiB available")
 
 
 def measured_peaks() -> dict:
@@ -248,15 +275,20 @@ def x16_exchange(path: int, switches: int = 4) -> dict:
 
 def run_product(args, dist: Dist):
     from paper_2601_11743_b200 import PlannerConfig, SwapEngine, load_scenario, parse_path
-    from paper_2601_11743_b200._lib import TIER_PAGED
+    from paper_2601_11743_b200._lib import TIER_GPU, TIER_PINNED
     device = dist.local if args.gpus > 1 else 0
     peaks = measured_peaks()
     path = parse_path(args.path)
-    eng = SwapEngine(device=device, gpu_capacity=32 * GIB, pinned_capacity=16 * GIB, paged_capacity=96 * GIB, path=path)
+    check_host_memory(dist)
+    eng = SwapEngine(device=device, gpu_capacity=32 * GIB, pinned_capacity=16 * GIB, paged_capacity=2 * GIB, path=path)
     probe = eng.probe_pcie(1 * GIB, 64 * MIB)
     calib = eng.calibrate(256 * MIB) if path == 0 else None
-    eng.allocate(0, 16 * GIB, TIER_PAGED)
-    eng.allocate(1, 24 * GIB, TIER_PAGED)
+    # Steady state only involves the GPU and the pinned ring, so the apps are
+    # placed directly (no pageable cold start): the interactive app on the
+    # GPU, the background app's 24 GiB as 16 GiB on the GPU + 8 GiB pinned.
+    eng.allocate(0, 16 * GIB, TIER_GPU)
+    eng.allocate(1, 16 * GIB, TIER_GPU)
+    eng.allocate(1, 8 * GIB, TIER_PINNED)
     seed = 0x4E495849
     eng.fill_pattern(0, seed)
     eng.fill_pattern(1, seed)
@@ -270,7 +302,8 @@ def run_product(args, dist: Dist):
         nxt = 1 - nxt
         return st
 
-    for _ in range(max(3, args.warmup) + 2):  # two cold switches (paged -> pinned -> GPU) + W steady ones
+    settle = settle_host_link(eng)
+    for _ in range(max(3, args.warmup)):  # W warm-up switches (the first reaches the steady 8 <-> 8 GiB state)
         step()
     launches0 = eng.total_launches()
     sampler = ClockSampler(device)
@@ -282,6 +315,7 @@ def run_product(args, dist: Dist):
     dist.barrier()
     clocks = sampler.stop()
     launches = eng.total_launches() - launches0
+    probe_after = eng.probe_pcie(1 * GIB, 64 * MIB)
     bad = eng.verify_pattern(0, seed) + eng.verify_pattern(1, seed)
     eng.audit()
     eng.close()
@@ -299,7 +333,10 @@ def run_product(args, dist: Dist):
 
     value = total_bytes / dev_max / 1e9
     e2e = total_bytes / wall_max / 1e9
-    pcie_peak = max(probe["ce_bidir_total"], probe["sm_bidir_total"])
+    # Denominator: the better of the probes right before and right after the
+    # timed region (shared hosts: neighbours' DRAM/PCIe load moves both).
+    pcie_peak = max(probe["ce_bidir_total"], probe["sm_bidir_total"], probe_after["ce_bidir_total"],
+                    probe_after["sm_bidir_total"])
     per_gpu = value / args.gpus
     k3_s = sum(s["k3_s"] for s in stats)
     k3_busy = sum(s["k3_busy_s"] for s in stats)
@@ -346,6 +383,8 @@ def run_product(args, dist: Dist):
         "link_roofline": {"bound": "pcie", "achieved": per_gpu, "peak": pcie_peak, "unit": "GB/s", "frac": per_gpu / pcie_peak,
                           "link": pcie_link(device), "peak_source": "same-run probe, 1 GiB/direction, 64 MiB chunks, max(CE, SM)"},
         "pcie_probe": {k: (round(v, 2) if isinstance(v, float) else v) for k, v in probe.items()},
+        "pcie_probe_after": {k: round(probe_after[k], 2) for k in ("ce_bidir_total", "ce_bidir_h2d", "ce_bidir_d2h", "sm_bidir_total")},
+        "settle": settle,
         "calibration": calib,
         "cpu_baseline": base,
         "gpu_launches": launches,
