@@ -340,6 +340,7 @@ def run_product(args, dist: Dist):
     per_gpu = value / args.gpus
     k3_s = sum(s["k3_s"] for s in stats)
     k3_busy = sum(s["k3_busy_s"] for s in stats)
+    k3_kernel = sum(s["k3_kernel_s"] for s in stats)
     k3_b = sum(s["k3_bytes"] for s in stats)
     k1_s = sum(s["k1_s"] for s in stats)
     k1_b = sum(s["k1_bytes"] for s in stats)
@@ -358,6 +359,9 @@ def run_product(args, dist: Dist):
         roof = {"kernel": "nx_swap_kernel<checksum-only> (K3 record/verify)", "bound": "hbm",
                 "achieved": k3_b / k3_busy / 1e9 if k3_busy else 0.0,
                 "achieved_per_launch_avg": k3_b / k3_s / 1e9 if k3_s else 0.0,
+                # in-kernel %globaltimer spans (first CTA start .. last CTA end): excludes
+                # the stream/front-end delays the events include
+                "achieved_kernel_clock": k3_b / k3_kernel / 1e9 if k3_kernel else None,
                 "peak": hbm, "unit": "GB/s", "launches": k3_n, "bytes_per_launch": k3_b / max(1, k3_n),
                 "avg_launch_ms": k3_s / max(1, k3_n) * 1e3, "busy_ms_per_step": k3_busy / args.steps * 1e3,
                 "traffic": traffic.get("k3_dram_bytes_per_launch"),

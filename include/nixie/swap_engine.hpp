@@ -64,6 +64,7 @@ struct SwitchStats {
   int launches[2] = {0, 0};                 // K1/K3 kernel launches per stream
   int ce_batches[2] = {0, 0};               // copy-engine batches per stream
   int host_legs = 0;
+  int ce_calls = 0;                         // cudaMemcpyAsync calls (contiguous runs) of the CE batches
   std::uint64_t verified = 0, unverified = 0, mismatches = 0;
   // Per kernel kind (CUDA events on the launching stream):
   double k1_s = 0;      // K1 swap launches (SM path): summed durations
@@ -71,6 +72,7 @@ struct SwitchStats {
   int k1_launches = 0;
   double k3_s = 0;      // K3 checksum launches (CE path): summed durations
   double k3_busy_s = 0; // union of K3 launch intervals (both lanes' launches overlap)
+  double k3_kernel_s = 0;  // summed in-kernel spans (%globaltimer, first CTA start .. last CTA end)
   Bytes k3_bytes = 0;   // HBM bytes they read
   int k3_launches = 0;
 };
@@ -84,6 +86,13 @@ struct GateRelease {
   cudaEvent_t event = nullptr;
   void (*callback)(void* ctx) = nullptr;
   void* ctx = nullptr;
+};
+
+// One K3 checksum launch of the last execute (device times from its start).
+struct K3Launch {
+  double start_s, end_s;
+  int legs;
+  int lane;  // 0 = arrivals (verify), 1 = departures (record)
 };
 
 struct LegTrace {
@@ -143,6 +152,7 @@ class SwapEngine {
   const SwitchStats& last_stats() const;
   const std::array<std::vector<LegTrace>, 6>& lane_trace() const;  // per lane, start order, last execute
   std::uint64_t total_launches() const;  // kernels this engine has launched (all kinds)
+  const std::vector<K3Launch>& k3_launches() const;  // last execute
 
   // Device pointer of the frame holding a GPU-resident block; device table
   // of frame pointers indexed by BlockId (0 when not on the GPU), refreshed

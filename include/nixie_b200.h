@@ -87,7 +87,9 @@ typedef struct nx_switch_stats {
   double k1_s, k3_s;
   uint64_t k1_bytes, k3_bytes;
   int k1_launches, k3_launches;
-  double k3_busy_s; /* union of the K3 launch intervals */
+  double k3_busy_s;   /* union of the K3 launch intervals (CUDA events) */
+  double k3_kernel_s; /* summed in-kernel K3 spans (%globaltimer) */
+  int ce_calls;       /* cudaMemcpyAsync calls of the CE batches */
 } nx_switch_stats;
 
 typedef struct nx_pcie_probe {
@@ -156,6 +158,9 @@ int nx_switch(nx_engine* e, uint32_t incoming, const nx_planner_config* cfg, voi
  * transfer.cpp:39-45), in start order. */
 int nx_lane_trace(nx_engine* e, int lane, uint64_t* blocks, uint8_t* src, uint8_t* dst, size_t cap, size_t* n);
 uint64_t nx_total_launches(nx_engine* e);
+/* K3 checksum launches of the last switch: device start/end (s, from the
+ * switch start), legs per launch, lane (0 arrivals, 1 departures). */
+int nx_k3_trace(nx_engine* e, double* start_s, double* end_s, int* legs, int* lane, size_t cap, size_t* n);
 /* cudaStream_t of a PCIe lane: 0 = H2D, 1 = D2H. */
 void* nx_lane_stream(nx_engine* e, int lane);
 

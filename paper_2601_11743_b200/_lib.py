@@ -70,7 +70,8 @@ class SwitchStatsC(Structure):
         ("ce_batches_h2d", c_int), ("ce_batches_d2h", c_int), ("host_legs", c_int), ("verified", c_uint64),
         ("unverified", c_uint64), ("mismatches", c_uint64), ("tp_to_gpu", c_double), ("tp_from_gpu", c_double),
         ("tp_bidir", c_double), ("k1_s", c_double), ("k3_s", c_double), ("k1_bytes", c_uint64), ("k3_bytes", c_uint64),
-        ("k1_launches", c_int), ("k3_launches", c_int), ("k3_busy_s", c_double),
+        ("k1_launches", c_int), ("k3_launches", c_int), ("k3_busy_s", c_double), ("k3_kernel_s", c_double),
+        ("ce_calls", c_int),
     ]
 
     def as_dict(self) -> dict:
@@ -115,6 +116,8 @@ _SIGNATURES = [
     ("nx_lane_trace", c_int, [c_void_p, c_int, POINTER(c_uint64), POINTER(c_uint8), POINTER(c_uint8), c_size_t,
                               POINTER(c_size_t)]),
     ("nx_total_launches", c_uint64, [c_void_p]),
+    ("nx_k3_trace", c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_int), POINTER(c_int), c_size_t,
+                            POINTER(c_size_t)]),
     ("nx_lane_stream", c_void_p, [c_void_p, c_int]),
     ("nx_probe_pcie", c_int, [c_void_p, c_uint64, c_uint64, POINTER(PcieProbeC)]),
     ("nx_probe_copy_variant", c_int, [c_void_p, c_int, c_uint64, c_int, POINTER(c_double)]),

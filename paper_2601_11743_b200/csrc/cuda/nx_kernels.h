@@ -37,7 +37,14 @@ struct NxCkTables {
   unsigned long long* ck_seen;  // checksum observed at the last arrival on the GPU
   unsigned int* ck_valid;       // 1 if ck_ref is meaningful
   NxDevStatus* status;
+  // Device-clock span of each K3 launch (%globaltimer ns): first CTA start
+  // (atomicMin, preset to ~0) and last CTA end (atomicMax, preset to 0).
+  unsigned long long* kstart;
+  unsigned long long* kend;
 };
+
+inline constexpr std::uint32_t kNoClockSlot = 0xFFFFFFFFu;
+inline constexpr int kClockSlots = 8192;
 
 struct NxScratch {
   unsigned long long* part_sums;  // [kMaxLegsPerLaunch << kMaxPartsLog2]
@@ -63,7 +70,8 @@ cudaError_t launch_swap(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t f
 // One CTA per SM: a producer thread streams 32 KiB cp.async.bulk chunks into
 // a 6-stage shared-memory ring, 16 consumer warps checksum from shared memory.
 cudaError_t launch_checksum_tma(const NxLeg* legs, int n, bool arriving, std::uint32_t flags, const NxCkTables& ck,
-                                const NxScratch& scratch, int ctas, cudaStream_t stream);
+                                const NxScratch& scratch, int ctas, cudaStream_t stream,
+                                std::uint32_t clock_slot = kNoClockSlot);
 
 // K4: pattern fill (records checksums, marks them valid) and compare (adds
 // the number of mismatching 16-byte vectors per leg into mismatches[i]).

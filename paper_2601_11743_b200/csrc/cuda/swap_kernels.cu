@@ -46,8 +46,15 @@ struct SwapParamsT {
   std::uint32_t n_h2d;
   std::uint32_t parts_log2;
   std::uint32_t flags;
+  std::uint32_t clock_slot;  // kNoClockSlot: no device-clock stamps
   NxLeg legs[N];
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 using SwapParams = SwapParamsT<kMaxLegsPerLaunch>;
 
 struct FillParams {
@@ -296,6 +303,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) nx_checksum_tma_kernel(
   }
   __syncthreads();
   if (c0 >= c1) return;
+  if (threadIdx.x == 0 && p.clock_slot != kNoClockSlot) atomicMin(&p.ck.kstart[p.clock_slot], global_ns());
   const std::uint64_t n = c1 - c0;
   const int warp = threadIdx.x / 32;
 
@@ -347,7 +355,8 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) nx_checksum_tma_kernel(
     if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
     ++seg_chunks;
   }
-  tma_flush(p, base, leg, seg_chunks, acc, arriving, red);
+  tma_flush(p, base, leg, seg_chunks, acc, arriving, red);  // ends with a consumer barrier
+  if (threadIdx.x == 0 && p.clock_slot != kNoClockSlot) atomicMax(&p.ck.kend[p.clock_slot], global_ns());
 }
 
 int parts_log2_for(int n_legs, int groups_wanted) {
@@ -376,6 +385,7 @@ cudaError_t launch_swap_n(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t
   p.n_d2h = static_cast<std::uint32_t>(n_d2h);
   p.n_h2d = static_cast<std::uint32_t>(n_h2d);
   p.flags = flags;
+  p.clock_slot = kNoClockSlot;
   const bool fused = n_d2h > 0 && n_h2d > 0;
   // Aim for one work item per warp group of the capped grid.
   const int groups = fused ? max_ctas : 2 * max_ctas;
@@ -394,7 +404,7 @@ cudaError_t launch_swap_n(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t
 
 template <int N>
 cudaError_t launch_checksum_tma_n(const NxLeg* legs, int n, bool arriving, std::uint32_t flags, const NxCkTables& ck,
-                                  const NxScratch& scratch, int ctas, cudaStream_t stream) {
+                                  const NxScratch& scratch, int ctas, cudaStream_t stream, std::uint32_t clock_slot) {
   static bool configured = false;
   constexpr int kSmem = kTmaStages * kTmaChunk;
   if (!configured) {
@@ -410,6 +420,7 @@ cudaError_t launch_checksum_tma_n(const NxLeg* legs, int n, bool arriving, std::
   p.n_d2h = arriving ? 0u : static_cast<std::uint32_t>(n);
   p.n_h2d = arriving ? static_cast<std::uint32_t>(n) : 0u;
   p.parts_log2 = 0;
+  p.clock_slot = (ck.kstart != nullptr && ck.kend != nullptr) ? clock_slot : kNoClockSlot;
   p.flags = flags;
   const int chunks = n * static_cast<int>(kTmaChunksPerLeg);
   if (ctas > chunks) ctas = chunks;
@@ -431,13 +442,13 @@ cudaError_t launch_swap(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t f
 }
 
 cudaError_t launch_checksum_tma(const NxLeg* legs, int n, bool arriving, std::uint32_t flags, const NxCkTables& ck,
-                                const NxScratch& scratch, int ctas, cudaStream_t stream) {
+                                const NxScratch& scratch, int ctas, cudaStream_t stream, std::uint32_t slot) {
   if (n <= 0) return cudaSuccess;
   if (n > kMaxLegsPerLaunch) return cudaErrorInvalidValue;
-  if (n <= 8) return launch_checksum_tma_n<8>(legs, n, arriving, flags, ck, scratch, ctas, stream);
-  if (n <= 32) return launch_checksum_tma_n<32>(legs, n, arriving, flags, ck, scratch, ctas, stream);
-  if (n <= 128) return launch_checksum_tma_n<128>(legs, n, arriving, flags, ck, scratch, ctas, stream);
-  return launch_checksum_tma_n<kMaxLegsPerLaunch>(legs, n, arriving, flags, ck, scratch, ctas, stream);
+  if (n <= 8) return launch_checksum_tma_n<8>(legs, n, arriving, flags, ck, scratch, ctas, stream, slot);
+  if (n <= 32) return launch_checksum_tma_n<32>(legs, n, arriving, flags, ck, scratch, ctas, stream, slot);
+  if (n <= 128) return launch_checksum_tma_n<128>(legs, n, arriving, flags, ck, scratch, ctas, stream, slot);
+  return launch_checksum_tma_n<kMaxLegsPerLaunch>(legs, n, arriving, flags, ck, scratch, ctas, stream, slot);
 }
 
 cudaError_t launch_fill(const NxLeg* legs, int n, std::uint64_t seed, const NxCkTables& ck, cudaStream_t stream) {

@@ -128,6 +128,8 @@ void fill_stats(const SwapEngine& eng, const ExecResult& r, nx_switch_stats* out
   out->k1_launches = s.k1_launches;
   out->k3_launches = s.k3_launches;
   out->k3_busy_s = s.k3_busy_s;
+  out->k3_kernel_s = s.k3_kernel_s;
+  out->ce_calls = s.ce_calls;
   if (s.device_span_s > 0) {
     double lo = 1e30, hi = 0;
     for (const TransferRecord& t : r.events)
@@ -355,6 +357,20 @@ int nx_lane_trace(nx_engine* e, int lane, uint64_t* blocks, uint8_t* src, uint8_
 }
 
 uint64_t nx_total_launches(nx_engine* e) { return e ? e->eng->total_launches() : 0; }
+
+int nx_k3_trace(nx_engine* e, double* start_s, double* end_s, int* legs, int* lane, size_t cap, size_t* n) {
+  return guard([&] {
+    need(e, "engine");
+    const auto& t = e->eng->k3_launches();
+    for (size_t i = 0; i < t.size() && i < cap; ++i) {
+      if (start_s) start_s[i] = t[i].start_s;
+      if (end_s) end_s[i] = t[i].end_s;
+      if (legs) legs[i] = t[i].legs;
+      if (lane) lane[i] = t[i].lane;
+    }
+    if (n) *n = t.size();
+  });
+}
 void* nx_lane_stream(nx_engine* e, int lane) { return e ? static_cast<void*>(e->eng->stream(lane)) : nullptr; }
 
 int nx_probe_pcie(nx_engine* e, uint64_t bytes, uint64_t chunk, nx_pcie_probe* out) {

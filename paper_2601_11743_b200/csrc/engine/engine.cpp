@@ -102,9 +102,12 @@ struct SwapEngine::Impl final : detail::LaneSink {
     bool ce;
     bool end_on_side = false;                        // CE batch: ends on the checksum side stream
     std::vector<std::array<cudaEvent_t, 2>> k3ev;    // CE batch: K3 launch start/end
+    std::vector<std::uint32_t> k3slot;               // device-clock slot per K3 launch
     Bytes k3_bytes = 0;
   };
   std::array<int, 2> batches_sent{};  // per PCIe lane this execute (batch-size ramp)
+  std::vector<K3Launch> k3_trace;     // last execute's K3 launches (device times)
+  std::uint32_t k3_slots_used = 0;    // device-clock slots handed out this execute
 
   // K3 checksum-only launch of a CE batch (record on departure, verify on arrival).
   void k3_launch(Batch& B, const std::vector<NxLeg>& l, bool arriving, cudaStream_t cs, std::uint32_t flags) {
@@ -112,11 +115,13 @@ struct SwapEngine::Impl final : detail::LaneSink {
     cudaEvent_t a = take_event(), z = take_event();
     NX_CUDA(cudaEventRecord(a, cs));
     if (cfg.k3_tma)
-      NX_CUDA(launch_checksum_tma(l.data(), n, arriving, flags, ck, scratch[2 + B.stream], sm_count, cs));
+      NX_CUDA(launch_checksum_tma(l.data(), n, arriving, flags, ck, scratch[2 + B.stream], sm_count, cs,
+                                  k3_slots_used < kClockSlots ? k3_slots_used : kNoClockSlot));
     else
       NX_CUDA(launch_swap(l.data(), arriving ? 0 : n, arriving ? n : 0, flags, ck, scratch[2 + B.stream], k3_ctas, cs));
     NX_CUDA(cudaEventRecord(z, cs));
     B.k3ev.push_back({a, z});
+    B.k3slot.push_back(cfg.k3_tma && k3_slots_used < kClockSlots ? k3_slots_used++ : kNoClockSlot);
     B.k3_bytes += static_cast<Bytes>(n) * kBlockBytes;
     ++stats.launches[B.stream];
     ++launches_total;
@@ -166,6 +171,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
     NX_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
     for (auto& s : cks) NX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     NX_CUDA(cudaMalloc(&ck.status, sizeof(NxDevStatus)));
+    NX_CUDA(cudaMalloc(&ck.kstart, sizeof(unsigned long long) * kClockSlots));
+    NX_CUDA(cudaMalloc(&ck.kend, sizeof(unsigned long long) * kClockSlots));
     NX_CUDA(cudaMemset(ck.status, 0, sizeof(NxDevStatus)));
     for (auto& s : scratch) {
       NX_CUDA(cudaMalloc(&s.part_sums, sizeof(unsigned long long) * (kMaxLegsPerLaunch << kMaxPartsLog2)));
@@ -199,6 +206,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
     cudaFree(ck.ck_seen);
     cudaFree(ck.ck_valid);
     cudaFree(ck.status);
+    cudaFree(ck.kstart);
+    cudaFree(ck.kend);
     cudaFree(d_frames);
     if (h_frames) cudaFreeHost(h_frames);
     if (h_frames_stage) cudaFreeHost(h_frames_stage);
@@ -510,6 +519,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
         ++n;
       }
       NX_CUDA(cudaMemcpyAsync(dst, src, n * kBlockBytes, kind, st[s]));
+      ++stats.ce_calls;
       i += n;
     }
   }
@@ -630,6 +640,10 @@ struct SwapEngine::Impl final : detail::LaneSink {
     landed.clear();
     events_used = 0;
     batches_sent = {0, 0};
+    k3_slots_used = 0;
+    NX_CUDA(cudaMemsetAsync(ck.kstart, 0xFF, sizeof(unsigned long long) * kClockSlots, aux));
+    NX_CUDA(cudaMemsetAsync(ck.kend, 0, sizeof(unsigned long long) * kClockSlots, aux));
+    NX_CUDA(cudaStreamSynchronize(aux));
     records = &res.events;
     opts = &o;
     incoming = plan.incoming_app;
@@ -696,6 +710,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   void finalize_timing(ExecResult& res) {
     double first = 1e30, last = 0;
     std::vector<std::pair<double, double>> k3_spans;
+    k3_trace.clear();
     for (const Batch& B : landed) {
       float a = 0, b = 0;
       NX_CUDA(cudaEventElapsedTime(&a, ev0, B.ev_start));
@@ -715,6 +730,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
         NX_CUDA(cudaEventElapsedTime(&a1, ev0, ke[1]));
         stats.k3_s += (a1 - a0) * 1e-3;
         k3_spans.emplace_back(a0 * 1e-3, a1 * 1e-3);
+        k3_trace.push_back(K3Launch{a0 * 1e-3, a1 * 1e-3, static_cast<int>(B.k3_bytes / kBlockBytes / B.k3ev.size()), B.stream});
         ++stats.k3_launches;
       }
       stats.k3_bytes += B.k3_bytes;
@@ -740,6 +756,17 @@ struct SwapEngine::Impl final : detail::LaneSink {
     }
     busy += hi - lo;
     stats.k3_busy_s = k3_spans.empty() ? 0.0 : busy;
+
+    // Kernel-only K3 time from the in-kernel %globaltimer stamps (first CTA
+    // start .. last CTA end per launch), free of stream/front-end delays.
+    if (k3_slots_used > 0) {
+      std::vector<unsigned long long> ks(k3_slots_used), ke(k3_slots_used);
+      NX_CUDA(cudaMemcpyAsync(ks.data(), ck.kstart, sizeof(unsigned long long) * k3_slots_used, cudaMemcpyDeviceToHost, aux));
+      NX_CUDA(cudaMemcpyAsync(ke.data(), ck.kend, sizeof(unsigned long long) * k3_slots_used, cudaMemcpyDeviceToHost, aux));
+      NX_CUDA(cudaStreamSynchronize(aux));
+      for (std::uint32_t i = 0; i < k3_slots_used; ++i)
+        if (ke[i] > ks[i] && ks[i] != ~0ull) stats.k3_kernel_s += (ke[i] - ks[i]) * 1e-9;
+    }
   }
 
   void check_status() {
@@ -795,6 +822,7 @@ ExecResult SwapEngine::switch_to(AppId incoming, const PlannerConfig& cfg, cudaS
 const SwitchStats& SwapEngine::last_stats() const { return impl_->stats; }
 const std::array<std::vector<LegTrace>, 6>& SwapEngine::lane_trace() const { return impl_->trace; }
 std::uint64_t SwapEngine::total_launches() const { return impl_->launches_total; }
+const std::vector<K3Launch>& SwapEngine::k3_launches() const { return impl_->k3_trace; }
 
 void* SwapEngine::frame_of(BlockId b) const {
   const Location& loc = impl_->mem.block(b).loc;

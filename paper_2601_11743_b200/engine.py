@@ -183,6 +183,16 @@ class SwapEngine:
     def total_launches(self) -> int:
         return int(lib.nx_total_launches(self._h))
 
+    def k3_trace(self) -> List[Tuple[float, float, int, int]]:
+        """(start_s, end_s, legs, lane) of the last switch's checksum launches."""
+        n = c_size_t()
+        check(lib.nx_k3_trace(self._h, None, None, None, None, 0, byref(n)))
+        k = max(1, n.value)
+        a, z = (ctypes.c_double * k)(), (ctypes.c_double * k)()
+        g, l = (c_int * k)(), (c_int * k)()
+        check(lib.nx_k3_trace(self._h, a, z, g, l, n.value, byref(n)))
+        return [(a[i], z[i], g[i], l[i]) for i in range(n.value)]
+
     def lane_stream(self, lane: int) -> int:
         return lib.nx_lane_stream(self._h, lane) or 0
 
