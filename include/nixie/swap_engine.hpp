@@ -204,10 +204,19 @@ class LaunchGate {
   ~LaunchGate();
 
   void attach(AppId app, cudaStream_t stream);
+  // Returns holding the app's launch lock; call after_launch(app) once the
+  // kernel is enqueued (a pause waits for it).
   bool before_launch(AppId app, Seconds now, double timeout_s = 120.0);
+  void after_launch(AppId app);
+  // Blocking-call brackets and other API activity (idleness, §6.1).
+  void api_event(AppId app, Seconds now, ApiEventKind kind);
   ExecResult context_switch(AppId to, Seconds now);
+  // One scheduler tick: infer_all, then switch to select_next() if the GPU
+  // has no holder, the holder is idle, or should_preempt fires.
+  std::optional<AppId> tick(Seconds now);
   std::optional<AppId> select_next(Seconds now);
   std::optional<AppId> granted();
+  std::uint64_t switches() const;
 
  private:
   struct Impl;

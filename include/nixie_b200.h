@@ -191,6 +191,19 @@ int nx_gate_attach(nx_gate* g, uint32_t app, void* stream, double now);
  * last fetch; the app's stream then waits on the device for that fetch to
  * land (*passed = 0). Fails with InvalidState after timeout_s. */
 int nx_gate_before_launch(nx_gate* g, uint32_t app, double now, double timeout_s, int* passed);
+/* Must follow every successful nx_gate_before_launch once the kernel is
+ * enqueued: releases the app's launch lock (a pause waits for it). */
+int nx_gate_after_launch(nx_gate* g, uint32_t app);
+/* MlfqScheduler::on_api_event (mlfq.cpp:71-85): 0 NonBlockingReturn,
+ * 1 BlockingEnter, 2 BlockingExit. */
+int nx_gate_api_event(nx_gate* g, uint32_t app, double now, int kind);
+/* One scheduler tick: infer_all, then a switch if the GPU has
+ * no holder, the holder is idle or should_preempt fires; *switched_to =
+ * UINT32_MAX when nothing switched. */
+int nx_gate_tick(nx_gate* g, double now, uint32_t* switched_to);
+uint64_t nx_gate_switches(nx_gate* g);
+/* Synthetic application kernel: occupies one warp for ~ns on `stream`. */
+int nx_launch_busy_kernel(void* stream, uint64_t ns);
 /* MlfqScheduler::select_next (mlfq.cpp:144-162); *app = UINT32_MAX if none. */
 int nx_gate_select_next(nx_gate* g, double now, uint32_t* app);
 /* Pause incumbent, drain, plan, execute, grant `to`, release its gate. */

@@ -129,6 +129,11 @@ _SIGNATURES = [
     ("nx_gate_destroy", None, [c_void_p]),
     ("nx_gate_attach", c_int, [c_void_p, c_uint32, c_void_p, c_double]),
     ("nx_gate_before_launch", c_int, [c_void_p, c_uint32, c_double, c_double, POINTER(c_int)]),
+    ("nx_gate_after_launch", c_int, [c_void_p, c_uint32]),
+    ("nx_gate_api_event", c_int, [c_void_p, c_uint32, c_double, c_int]),
+    ("nx_gate_tick", c_int, [c_void_p, c_double, POINTER(c_uint32)]),
+    ("nx_gate_switches", c_uint64, [c_void_p]),
+    ("nx_launch_busy_kernel", c_int, [c_void_p, c_uint64]),
     ("nx_gate_select_next", c_int, [c_void_p, c_double, POINTER(c_uint32)]),
     ("nx_gate_switch", c_int, [c_void_p, c_uint32, c_double, POINTER(SwitchStatsC)]),
     ("nx_gate_granted", c_int, [c_void_p, POINTER(c_uint32)]),

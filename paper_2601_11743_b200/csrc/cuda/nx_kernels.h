@@ -87,6 +87,8 @@ int device_sm_count(int device);
 namespace nixie::b200 {
 // Launch-gate test kernel: out[0] += sum of block checksums read through the
 // frame table, out[1] += number of blocks with no frame.
+// One warp busy for ~ns (timing probes; synthetic application kernels).
+cudaError_t launch_spin(unsigned ns, cudaStream_t stream);
 cudaError_t launch_table_checksum(const std::uint64_t* table, const unsigned* blocks, int n, unsigned long long* out,
                                   cudaStream_t stream);
 }  // namespace nixie::b200

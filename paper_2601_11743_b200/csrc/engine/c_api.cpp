@@ -494,6 +494,37 @@ int nx_gate_before_launch(nx_gate* g, uint32_t app, double now, double timeout_s
   });
 }
 
+int nx_gate_after_launch(nx_gate* g, uint32_t app) {
+  return guard([&] {
+    need(g, "gate");
+    g->gate->after_launch(app);
+  });
+}
+
+int nx_gate_api_event(nx_gate* g, uint32_t app, double now, int kind) {
+  return guard([&] {
+    need(g, "gate");
+    if (kind < 0 || kind > 2) throw std::invalid_argument("bad api event kind");
+    g->gate->api_event(app, now, static_cast<ApiEventKind>(kind));
+  });
+}
+
+int nx_gate_tick(nx_gate* g, double now, uint32_t* switched_to) {
+  return guard([&] {
+    need(g, "gate");
+    const auto s = g->gate->tick(now);
+    if (switched_to) *switched_to = s ? *s : ~uint32_t{0};
+  });
+}
+
+uint64_t nx_gate_switches(nx_gate* g) { return g ? g->gate->switches() : 0; }
+
+int nx_launch_busy_kernel(void* stream, uint64_t ns) {
+  return guard([&] {
+    NX_CUDA(launch_spin(static_cast<unsigned>(std::min<uint64_t>(ns, 4000000000ull)), static_cast<cudaStream_t>(stream)));
+  });
+}
+
 int nx_gate_select_next(nx_gate* g, double now, uint32_t* app) {
   return guard([&] {
     need(g, "gate");

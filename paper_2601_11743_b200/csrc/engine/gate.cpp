@@ -12,16 +12,19 @@
 // that fetch. The app's kernel therefore starts the moment its data lands,
 // without a host round trip. The event wait is enqueued after the work that
 // completes it, so it cannot deadlock through a shared hardware queue (a
-// value-wait enqueued before the producer can). The incumbent drain is
-// likewise device-side: the engine's D2H stream waits for an event recorded
-// on the incumbent's stream. Reference anchors: grant =
+// value-wait enqueued before the producer can). Check-and-launch is atomic
+// w.r.t. a pause: before_launch returns holding the app's launch lock until
+// after_launch, and a pause takes that lock before it records the drain event
+// the evictions wait for (the shim's "blocks new launches and synchronizes
+// outstanding kernels"). Reference anchors: grant =
 // MlfqScheduler::on_grant_start (proj/src/mlfq.cpp:188-194), drain = the
-// eviction gate (proj/src/transfer.cpp:82-87, 126-129).
+// eviction gate (proj/src/transfer.cpp:82-87, 126-129), tick = SPEC.md:354.
 #include <cuda_runtime.h>
 
 #include <chrono>
 #include <condition_variable>
 #include <map>
+#include <memory>
 #include <mutex>
 
 #include "nixie/swap_engine.hpp"
@@ -33,15 +36,20 @@ struct LaunchGate::Impl {
   SwapEngine& eng;
   MlfqScheduler& sched;
   PlannerConfig cfg;
-  std::mutex mu;  // guards the scheduler and the maps below
+  std::mutex mu;  // guards the scheduler and the maps below; taken after a launch lock
   std::condition_variable cv;
   std::map<AppId, cudaStream_t> streams;
-  std::map<AppId, cudaEvent_t> landed;          // recorded after an app's last fetch
-  std::map<AppId, std::uint64_t> released;      // swap-ins submitted (grant epochs)
+  std::map<AppId, cudaEvent_t> landed;                 // recorded after an app's last fetch
+  std::map<AppId, cudaEvent_t> drained;                // recorded on the app's stream at pause
+  std::map<AppId, std::uint64_t> released;             // swap-ins submitted (grant epochs)
+  std::map<AppId, std::unique_ptr<std::mutex>> launch; // check-and-launch atomicity
+  std::uint64_t switches = 0;
+  AppId incoming = kNoApp;  // swap-in submitted, grant not yet recorded
 
   Impl(SwapEngine& e, MlfqScheduler& s, PlannerConfig c) : eng(e), sched(s), cfg(std::move(c)) {}
   ~Impl() {
     for (auto& kv : landed) cudaEventDestroy(kv.second);
+    for (auto& kv : drained) cudaEventDestroy(kv.second);
   }
 
   static void on_release(void* ctx) {
@@ -49,8 +57,16 @@ struct LaunchGate::Impl {
     {
       std::lock_guard<std::mutex> lk(p->first->mu);
       p->first->released[p->second] += 1;
+      p->first->incoming = p->second;
     }
     p->first->cv.notify_all();
+  }
+
+  std::mutex& launch_lock(AppId app) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = launch.find(app);
+    if (it == launch.end()) throw SimError(Err::UnknownApp, "launch gate: app " + std::to_string(app) + " not attached");
+    return *it->second;
   }
 };
 
@@ -62,56 +78,107 @@ void LaunchGate::attach(AppId app, cudaStream_t stream) {
   Impl& g = *impl_;
   std::lock_guard<std::mutex> lk(g.mu);
   if (!g.landed.count(app)) {
-    cudaEvent_t ev;
-    NX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    g.landed[app] = ev;
+    cudaEvent_t a, b;
+    NX_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    NX_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    g.landed[app] = a;
+    g.drained[app] = b;
     g.released[app] = 0;
+    g.launch[app] = std::make_unique<std::mutex>();
   }
   g.streams[app] = stream;
 }
 
 bool LaunchGate::before_launch(AppId app, Seconds now, double timeout_s) {
   Impl& g = *impl_;
-  std::unique_lock<std::mutex> lk(g.mu);
-  auto it = g.streams.find(app);
-  if (it == g.streams.end()) throw SimError(Err::UnknownApp, "launch gate: app " + std::to_string(app) + " not attached");
-  g.sched.on_api_event(app, now, ApiEventKind::NonBlockingReturn);
-  if (g.sched.granted() == app && g.eng.mem().app_fully_resident(app, TierId::Gpu)) return true;
-  g.sched.enqueue_request(app, now);
-  const std::uint64_t ticket = g.released[app];
-  const bool ok = g.cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return g.released[app] > ticket; });
-  if (!ok) throw SimError(Err::InvalidState, "launch gate: app " + std::to_string(app) + " was not scheduled within the timeout");
-  NX_CUDA(cudaStreamWaitEvent(it->second, g.landed[app], 0));
-  return false;
+  std::mutex& lmu = g.launch_lock(app);
+  lmu.lock();  // held until after_launch: a pause cannot slip between check and launch
+  try {
+    std::unique_lock<std::mutex> lk(g.mu);
+    g.sched.on_api_event(app, now, ApiEventKind::NonBlockingReturn);
+    if (g.sched.granted() == app && g.eng.mem().app_fully_resident(app, TierId::Gpu)) return true;
+    if (g.incoming == app) {  // its swap-in is submitted: order the launch after it lands
+      NX_CUDA(cudaStreamWaitEvent(g.streams[app], g.landed[app], 0));
+      return false;
+    }
+    g.sched.enqueue_request(app, now);
+    const std::uint64_t ticket = g.released[app];
+    const bool ok = g.cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return g.released[app] > ticket; });
+    if (!ok) throw SimError(Err::InvalidState, "launch gate: app " + std::to_string(app) + " was not scheduled within the timeout");
+    NX_CUDA(cudaStreamWaitEvent(g.streams[app], g.landed[app], 0));
+    return false;
+  } catch (...) {
+    lmu.unlock();
+    throw;
+  }
+}
+
+void LaunchGate::after_launch(AppId app) { impl_->launch_lock(app).unlock(); }
+
+void LaunchGate::api_event(AppId app, Seconds now, ApiEventKind kind) {
+  std::lock_guard<std::mutex> lk(impl_->mu);
+  impl_->sched.on_api_event(app, now, kind);
 }
 
 ExecResult LaunchGate::context_switch(AppId to, Seconds now) {
   Impl& g = *impl_;
   MigrationPlan plan;
-  cudaStream_t drain = nullptr;
   GateRelease rel;
   std::pair<Impl*, AppId> ctx{&g, to};
+  std::optional<AppId> incumbent;
   {
     std::lock_guard<std::mutex> lk(g.mu);
     if (!g.streams.count(to)) throw SimError(Err::UnknownApp, "launch gate: app " + std::to_string(to) + " not attached");
-    const std::optional<AppId> incumbent = g.sched.granted();
+    incumbent = g.sched.granted();
     if (incumbent == to) return ExecResult{};
-    if (incumbent) {
-      g.sched.on_grant_end(*incumbent, now);  // pause: its next launches are held
-      auto it = g.streams.find(*incumbent);
-      if (it != g.streams.end()) drain = it->second;
+  }
+  if (incumbent) {
+    // Pause: no launch of the incumbent is in progress while its grant ends
+    // and the drain point is recorded on its stream.
+    std::lock_guard<std::mutex> launch_guard(g.launch_lock(*incumbent));
+    std::lock_guard<std::mutex> lk(g.mu);
+    g.sched.on_grant_end(*incumbent, now);
+    auto it = g.streams.find(*incumbent);
+    if (it != g.streams.end()) {
+      NX_CUDA(cudaEventRecord(g.drained[*incumbent], it->second));
+      for (int lane = 0; lane < 2; ++lane) NX_CUDA(cudaStreamWaitEvent(g.eng.stream(lane), g.drained[*incumbent], 0));
     }
+  }
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
     g.cfg.eviction_policy.victim_order = g.sched.victim_hint();
     plan = plan_switch(to, g.eng.mem(), g.cfg);
     rel.event = g.landed[to];
     rel.callback = &Impl::on_release;
     rel.ctx = &ctx;
   }
-  ExecResult r = g.eng.execute(plan, g.cfg, drain, &rel);
+  ExecResult r = g.eng.execute(plan, g.cfg, nullptr, &rel);
   std::lock_guard<std::mutex> lk(g.mu);
   g.sched.clear_request(to);
   g.sched.on_grant_start(to, now + r.completion);
+  g.incoming = kNoApp;
+  ++g.switches;
   return r;
+}
+
+// One scheduler tick (MlfqConfig::tick): Algorithm-1 inference
+// for every app, then a switch to select_next() when the GPU has no holder,
+// when the holder has gone idle (no API activity and not blocked in a call
+// for > idle_threshold) while others wait, or when should_preempt fires.
+std::optional<AppId> LaunchGate::tick(Seconds now) {
+  Impl& g = *impl_;
+  std::optional<AppId> next;
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    g.sched.infer_all(now);
+    next = g.sched.select_next(now);
+    if (!next) return std::nullopt;
+    const std::optional<AppId> holder = g.sched.granted();
+    const bool go = !holder || g.sched.is_idle(*holder, now) || g.sched.should_preempt(*holder, now);
+    if (!go) return std::nullopt;
+  }
+  context_switch(*next, now);
+  return next;
 }
 
 std::optional<AppId> LaunchGate::select_next(Seconds now) {
@@ -123,5 +190,7 @@ std::optional<AppId> LaunchGate::granted() {
   std::lock_guard<std::mutex> lk(impl_->mu);
   return impl_->sched.granted();
 }
+
+std::uint64_t LaunchGate::switches() const { return impl_->switches; }
 
 }  // namespace nixie::b200

@@ -251,10 +251,40 @@ class LaunchGate:
     def before_launch(self, app: int, now: float, timeout_s: float = 120.0) -> bool:
         """True: the app may launch now. False: it was held until its swap-in
         was submitted and its stream now waits on the device for it to land.
-        Blocks the calling thread (ctypes releases the GIL)."""
+        Blocks the calling thread (ctypes releases the GIL). Returns holding
+        the app's launch lock: call after_launch(app) once the kernel is
+        enqueued (or use `with gate.launching(app, now):`)."""
         ok = c_int()
         check(lib.nx_gate_before_launch(self._h, app, now, timeout_s, byref(ok)))
         return bool(ok.value)
+
+    def after_launch(self, app: int) -> None:
+        check(lib.nx_gate_after_launch(self._h, app))
+
+    def launching(self, app: int, now: float, timeout_s: float = 120.0):
+        gate = self
+
+        class _Launch:
+            def __enter__(self_):
+                self_.passed = gate.before_launch(app, now, timeout_s)
+                return self_
+
+            def __exit__(self_, *exc):
+                gate.after_launch(app)
+
+        return _Launch()
+
+    def api_event(self, app: int, now: float, kind: int) -> None:
+        """0 NonBlockingReturn, 1 BlockingEnter, 2 BlockingExit (mlfq.cpp:71-85)."""
+        check(lib.nx_gate_api_event(self._h, app, now, kind))
+
+    def tick(self, now: float) -> Optional[int]:
+        a = c_uint32()
+        check(lib.nx_gate_tick(self._h, now, byref(a)))
+        return None if a.value == 0xFFFFFFFF else a.value
+
+    def switches(self) -> int:
+        return int(lib.nx_gate_switches(self._h))
 
     def select_next(self, now: float) -> Optional[int]:
         a = c_uint32()
@@ -329,6 +359,11 @@ def stream_create() -> int:
 
 def stream_destroy(stream: int) -> None:
     lib.nx_stream_destroy(c_void_p(stream))
+
+
+def launch_busy_kernel(stream: int, ns: int) -> None:
+    """Synthetic application kernel: one warp busy for ~ns on `stream`."""
+    check(lib.nx_launch_busy_kernel(c_void_p(stream or None), ns))
 
 
 def stream_done(stream: int) -> bool:

@@ -122,12 +122,14 @@ def test_launch_gate_holds_kernels_until_swap_in(gpu, oracle_lib):
         gate.attach(1, s1, 0.0)
         gate.context_switch(0, 0.0)  # app 0 is resident: empty plan, grant only
         assert gate.granted() == 0 and gate.before_launch(0, 0.1)
+        gate.after_launch(0)
         # App 1's "interposed launch" runs on its own thread and is held there.
         passed = {}
 
         def app1():
-            passed["v"] = gate.before_launch(1, 0.2, timeout_s=60.0)
-            gate.app_checksum_async(1, s1, out)  # ordered after the swap-in on the device
+            with gate.launching(1, 0.2, timeout_s=60.0) as launch:
+                passed["v"] = launch.passed
+                gate.app_checksum_async(1, s1, out)  # ordered after the swap-in on the device
 
         th = threading.Thread(target=app1)
         th.start()
