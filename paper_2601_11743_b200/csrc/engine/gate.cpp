@@ -36,7 +36,8 @@ struct LaunchGate::Impl {
   SwapEngine& eng;
   MlfqScheduler& sched;
   PlannerConfig cfg;
-  std::mutex mu;  // guards the scheduler and the maps below; taken after a launch lock
+  std::mutex switch_mu;  // one context switch at a time (the engine has a single control loop)
+  std::mutex mu;         // guards the scheduler and the maps below; taken after a launch lock
   std::condition_variable cv;
   std::map<AppId, cudaStream_t> streams;
   std::map<AppId, cudaEvent_t> landed;                 // recorded after an app's last fetch
@@ -122,6 +123,7 @@ void LaunchGate::api_event(AppId app, Seconds now, ApiEventKind kind) {
 
 ExecResult LaunchGate::context_switch(AppId to, Seconds now) {
   Impl& g = *impl_;
+  std::lock_guard<std::mutex> serial(g.switch_mu);
   MigrationPlan plan;
   GateRelease rel;
   std::pair<Impl*, AppId> ctx{&g, to};

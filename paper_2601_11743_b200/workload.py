@@ -119,6 +119,7 @@ def run_workload(apps: List[AppSpec], horizon_s: float = 30.0, gpu_gib: int = 32
             t.start()
         time.sleep(horizon_s)
         stop.set()
+        threads[-1].join()  # the scheduler thread: from here on this thread ticks
         # A held app thread only wakes when it is scheduled: keep ticking
         # until every app thread has left.
         deadline = time.perf_counter() + 120

@@ -17,8 +17,8 @@ def test_three_app_mix_under_mlfq(gpu):
 
 
 def test_small_mix_fast_switches(gpu):
-    """Tiny working sets: the gate/scheduler loop itself sustains frequent switches."""
-    apps = [AppSpec(0, "a", 0.25, burst=2, kernel_ms=5, think_s=0.05), AppSpec(1, "b", 0.25, burst=2, kernel_ms=5, think_s=0.05),
-            AppSpec(2, "c", 0.25, burst=3, kernel_ms=5, think_s=0.0)]
+    """Small working sets that do not all fit the 1 GiB GPU: frequent real swaps."""
+    apps = [AppSpec(0, "a", 0.5, burst=2, kernel_ms=5, think_s=0.2), AppSpec(1, "b", 0.5, burst=2, kernel_ms=5, think_s=0.2),
+            AppSpec(2, "c", 0.5, burst=3, kernel_ms=5, think_s=0.2)]  # all idle > 100 ms between requests
     r = run_workload(apps, horizon_s=4.0, gpu_gib=1, pinned_gib=1, paged_gib=2)
-    assert r["errors"] == [] and r["byte_exact"] and r["switches"] >= 5
+    assert r["errors"] == [] and r["byte_exact"] and r["switches"] >= 4
