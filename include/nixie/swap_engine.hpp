@@ -52,6 +52,7 @@ struct EngineConfig {
   bool numa_bind = true;              // pinned ring + workers on the GPU's NUMA node
   int first_batch_legs = 8;           // batch-size ramp start (doubles per batch up to legs_per_launch)
   bool k3_tma = true;                 // CE-path checksum pass on the TMA pipeline (else the LDG loop)
+  bool exportable_arena = false;      // GPU tier = one VMM allocation shims can import (interposer daemon)
 };
 
 struct SwitchStats {
@@ -159,6 +160,12 @@ class SwapEngine {
   // on the H2D stream at the end of every execute.
   void* frame_of(BlockId block) const;
   const std::uint64_t* device_frame_table() const;
+  // Frame number (offset / 2 MiB into the arena) of a GPU-resident block, or
+  // -1. With EngineConfig::exportable_arena every frame is its own physical
+  // allocation and arena_export_fd(k) returns a new POSIX descriptor of frame
+  // k (caller closes it): a shim imports it and maps it at its own address.
+  std::int64_t frame_index(BlockId block) const;
+  int arena_export_fd(std::uint32_t frame) const;
   std::uint64_t block_checksum(BlockId block) const;  // last recorded departure checksum
   // Test access to a resident block's bytes wherever it lives.
   void read_block(BlockId block, void* host_dst);

@@ -1,0 +1,663 @@
+// nixied — the Nixie daemon for unmodified CUDA applications (PAPER.md:114-116,
+// "a centralized system service ... performs global coordination and
+// enforces multiplexing policies").
+//
+// One daemon per GPU. It owns:
+//   * the allocation registry (MemState, proj/src/mem_model.cpp) and the GPU
+//     tier as ONE exportable VMM allocation (csrc/engine/vmm.hpp); every
+//     application's shim imports it and maps 2 MiB frames under the stable
+//     virtual range it reserved at cudaMalloc time;
+//   * the MLFQ scheduler (proj/src/mlfq.cpp) fed from the shims' control
+//     pages (launch counts, blocking calls: PAPER.md §6.1);
+//   * the swap engine (csrc/engine/engine.cpp): a context switch is
+//     plan_switch (proj/src/planner.cpp:111-216) executed with real copies,
+//     both PCIe directions at once, every restore checksum-verified.
+//
+// A context switch (PAPER.md:116 steps 3-6):
+//   Pause(incumbent)   its shim clears the execution flag, waits for
+//                      launches in progress, synchronises its context,
+//                      acks Drained
+//   plan_switch        victim order = the scheduler's hint
+//   Unmap(victims)     owners of evicted blocks drop those mappings (acked
+//                      before any frame is handed to another application)
+//   execute            the swap engine: evictions and fetches at once
+//   Grant(incoming)    frame list for every chunk; the shim maps what moved,
+//                      sets the execution flag, acks Granted
+// The daemon loop is single-threaded: every decision and
+// registry mutation happens here, in arrival order.
+#include <fcntl.h>
+#include <poll.h>
+#include <signal.h>
+#include <sys/mman.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cinttypes>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <optional>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "nixie/swap_engine.hpp"
+#include "nixie_ipc.hpp"
+
+using namespace nixie;
+using namespace nixie::b200;
+namespace ipc = nixie::ipc;
+
+namespace {
+
+volatile sig_atomic_t g_stop = 0;
+void on_signal(int) { g_stop = 1; }
+
+struct Options {
+  std::string socket_path = "/tmp/nixie.sock";
+  std::string log_path;
+  EngineConfig eng;
+  PlannerConfig planner;
+  MlfqConfig mlfq;
+  Bytes min_bytes = kBlockBytes;  // smaller allocations pass through
+  double ack_timeout_s = 60.0;
+  int exit_after_apps = 0;         // exit once this many apps have come and gone (tests)
+};
+
+Bytes parse_size(const char* s) {
+  char* end = nullptr;
+  const double v = std::strtod(s, &end);
+  std::string u = end ? end : "";
+  double mul = 1;
+  if (u == "K" || u == "KiB") mul = 1024.0;
+  else if (u == "M" || u == "MiB") mul = 1024.0 * 1024;
+  else if (u == "G" || u == "GiB" || u.empty()) mul = 1024.0 * 1024 * 1024;
+  return static_cast<Bytes>(v * mul);
+}
+
+void usage() {
+  std::fprintf(stderr,
+               "usage: nixied [--socket PATH] [--device N] [--gpu SIZE] [--pinned SIZE] [--paged SIZE]\n"
+               "              [--window SIZE] [--min-bytes SIZE] [--path auto|ce|sm] [--host-threads N]\n"
+               "              [--tick-ms X] [--idle-ms X] [--allot-s X] [--preempt-s X] [--log FILE]\n"
+               "              [--exit-after-apps N]\n"
+               "sizes take a K/M/G suffix (GiB when bare). The daemon serves LD_PRELOAD=libnixie_shim.so apps\n"
+               "that set NIXIE_SOCKET=PATH.\n");
+}
+
+bool parse_args(int argc, char** argv, Options& o) {
+  o.eng.gpu_capacity = 32 * kGiB;
+  o.eng.pinned_capacity = 16 * kGiB;
+  o.eng.paged_capacity = 96 * kGiB;
+  o.eng.path = CopyPath::CopyEngine;
+  o.eng.exportable_arena = true;
+  for (int i = 1; i < argc; ++i) {
+    const std::string a = argv[i];
+    auto val = [&]() -> const char* {
+      if (i + 1 >= argc) throw SimError(Err::ParseError, "missing value for " + a);
+      return argv[++i];
+    };
+    if (a == "--socket") o.socket_path = val();
+    else if (a == "--device") o.eng.device = std::atoi(val());
+    else if (a == "--gpu") o.eng.gpu_capacity = parse_size(val()) / kBlockBytes * kBlockBytes;
+    else if (a == "--pinned") o.eng.pinned_capacity = parse_size(val()) / kBlockBytes * kBlockBytes;
+    else if (a == "--paged") o.eng.paged_capacity = parse_size(val()) / kBlockBytes * kBlockBytes;
+    else if (a == "--window") o.planner.streaming_window = parse_size(val());
+    else if (a == "--min-bytes") o.min_bytes = parse_size(val());
+    else if (a == "--host-threads") o.eng.host_threads = std::atoi(val());
+    else if (a == "--tick-ms") o.mlfq.tick = std::atof(val()) / 1000.0;
+    else if (a == "--idle-ms") o.mlfq.idle_threshold = std::atof(val()) / 1000.0;
+    else if (a == "--allot-s") o.mlfq.base_allotment = std::atof(val());
+    else if (a == "--preempt-s") o.mlfq.base_preemption = std::atof(val());
+    else if (a == "--log") o.log_path = val();
+    else if (a == "--exit-after-apps") o.exit_after_apps = std::atoi(val());
+    else if (a == "--path") {
+      const std::string p = val();
+      o.eng.path = p == "sm" ? CopyPath::SmKernel : p == "auto" ? CopyPath::Auto : CopyPath::CopyEngine;
+    } else if (a == "-h" || a == "--help") {
+      usage();
+      std::exit(0);
+    } else {
+      usage();
+      return false;
+    }
+  }
+  o.mlfq.validate();
+  return true;
+}
+
+class Daemon {
+ public:
+  explicit Daemon(const Options& o) : opt_(o), eng_(o.eng), sched_(o.mlfq) {
+    sched_.set_logging(true);
+    t0_ = ipc::mono_ns();
+    if (!o.log_path.empty()) {
+      log_ = std::fopen(o.log_path.c_str(), "w");
+      if (!log_) throw SimError(Err::IoError, "cannot open log " + o.log_path);
+    }
+  }
+  ~Daemon() {
+    for (auto& [id, a] : apps_) close_app(a);
+    for (int fd : pending_) ::close(fd);
+    if (listen_fd_ >= 0) ::close(listen_fd_);
+    ::unlink(opt_.socket_path.c_str());
+    if (log_) std::fclose(log_);
+  }
+
+  void listen_on() {
+    listen_fd_ = ::socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+    sockaddr_un addr{};
+    addr.sun_family = AF_UNIX;
+    if (opt_.socket_path.size() >= sizeof(addr.sun_path)) throw SimError(Err::ValidationError, "socket path too long");
+    std::strcpy(addr.sun_path, opt_.socket_path.c_str());
+    ::unlink(opt_.socket_path.c_str());
+    if (::bind(listen_fd_, reinterpret_cast<sockaddr*>(&addr), sizeof(addr)) != 0 || ::listen(listen_fd_, 64) != 0)
+      throw SimError(Err::IoError, "cannot listen on " + opt_.socket_path + ": " + std::strerror(errno));
+    std::fprintf(stderr, "[nixied] listening on %s  gpu %.1f GiB  pinned %.1f GiB  path %s\n", opt_.socket_path.c_str(),
+                 double(opt_.eng.gpu_capacity) / kGiB, double(opt_.eng.pinned_capacity) / kGiB,
+                 opt_.eng.path == CopyPath::SmKernel ? "sm" : opt_.eng.path == CopyPath::Auto ? "auto" : "ce");
+    std::fflush(stderr);
+  }
+
+  int run() {
+    Seconds next_tick = now() + opt_.mlfq.tick;
+    while (!g_stop) {
+      std::vector<pollfd> fds;
+      fds.push_back({listen_fd_, POLLIN, 0});
+      for (int fd : pending_) fds.push_back({fd, POLLIN, 0});
+      for (auto& [id, a] : apps_) {
+        if (!a.alive) continue;
+        fds.push_back({a.rpc, POLLIN, 0});
+        if (a.ev >= 0) fds.push_back({a.ev, POLLIN, 0});
+      }
+      const int wait_ms = std::max(0, static_cast<int>((next_tick - now()) * 1000.0));
+      const int n = ::poll(fds.data(), fds.size(), wait_ms);
+      if (n < 0 && errno != EINTR) throw SimError(Err::IoError, std::string("poll: ") + std::strerror(errno));
+      if (n > 0) {
+        for (const pollfd& p : fds) {
+          if (!p.revents) continue;
+          if (p.fd == listen_fd_) {
+            const int c = ::accept4(listen_fd_, nullptr, nullptr, SOCK_CLOEXEC);
+            if (c >= 0) pending_.push_back(c);
+          } else if (std::find(pending_.begin(), pending_.end(), p.fd) != pending_.end()) {
+            on_pending(p.fd);
+          } else {
+            on_app_fd(p.fd);
+          }
+        }
+      }
+      reap();
+      if (now() >= next_tick) {
+        tick();
+        next_tick = now() + opt_.mlfq.tick;
+      }
+      if (opt_.exit_after_apps > 0 && gone_ >= opt_.exit_after_apps && live_apps() == 0) break;
+    }
+    write_summary();
+    return 0;
+  }
+
+ private:
+  struct App {
+    AppId id = 0;
+    int rpc = -1, ev = -1;
+    int pid = 0;
+    std::string name;
+    int ctl_fd = -1;
+    ipc::CtlPage* ctl = nullptr;
+    bool alive = true;
+    std::uint64_t seen_launches = 0;
+    bool seen_blocking = false;
+    std::uint64_t active_launch_mark = 0;
+  };
+
+  Seconds now() const { return static_cast<double>(ipc::mono_ns() - t0_) * 1e-9; }
+  Seconds to_daemon_time(std::uint64_t ns) const { return ns > t0_ ? static_cast<double>(ns - t0_) * 1e-9 : 0.0; }
+
+  int live_apps() const {
+    int n = 0;
+    for (const auto& kv : apps_) n += kv.second.alive ? 1 : 0;
+    return n;
+  }
+
+  void close_app(App& a) {
+    if (a.rpc >= 0) ::close(a.rpc);
+    if (a.ev >= 0) ::close(a.ev);
+    if (a.ctl) ::munmap(a.ctl, 4096);
+    if (a.ctl_fd >= 0) ::close(a.ctl_fd);
+    a.rpc = a.ev = a.ctl_fd = -1;
+    a.ctl = nullptr;
+  }
+
+  App* app_by_fd(int fd) {
+    for (auto& [id, a] : apps_)
+      if (a.alive && (a.rpc == fd || a.ev == fd)) return &a;
+    return nullptr;
+  }
+
+  // ---- connections ---------------------------------------------------------
+  void on_pending(int fd) {
+    pending_.erase(std::find(pending_.begin(), pending_.end(), fd));
+    ipc::Msg type;
+    std::vector<std::uint8_t> body;
+    if (!ipc::recv_msg(fd, type, body)) {
+      ::close(fd);
+      return;
+    }
+    ipc::Reader r{body};
+    if (type == ipc::Msg::Hello) {
+      const auto req = r.get<ipc::HelloReq>();
+      if (!r.ok) {
+        ::close(fd);
+        return;
+      }
+      hello(fd, req);
+    } else if (type == ipc::Msg::EventHello) {
+      const auto req = r.get<ipc::EventHelloReq>();
+      auto it = apps_.find(req.app);
+      if (!r.ok || it == apps_.end() || it->second.ev >= 0) {
+        ::close(fd);
+        return;
+      }
+      it->second.ev = fd;
+    } else {
+      ::close(fd);
+    }
+  }
+
+  void hello(int fd, const ipc::HelloReq& req) {
+    App a;
+    a.id = next_app_++;
+    a.rpc = fd;
+    a.pid = req.pid;
+    a.name.assign(req.name, strnlen(req.name, sizeof(req.name)));
+    a.ctl_fd = ::memfd_create("nixie-ctl", MFD_CLOEXEC);
+    if (a.ctl_fd < 0 || ::ftruncate(a.ctl_fd, 4096) != 0) throw SimError(Err::IoError, "memfd_create for the control page");
+    void* p = ::mmap(nullptr, 4096, PROT_READ | PROT_WRITE, MAP_SHARED, a.ctl_fd, 0);
+    if (p == MAP_FAILED) throw SimError(Err::IoError, "mmap control page");
+    a.ctl = new (p) ipc::CtlPage();
+    sched_.register_app(a.id, now());
+    ipc::HelloRep rep{};
+    rep.status = req.device == opt_.eng.device ? 0 : 1;
+    rep.app = a.id;
+    rep.gpu_budget = opt_.eng.gpu_capacity;
+    rep.block_bytes = kBlockBytes;
+    rep.arena_bytes = opt_.eng.gpu_capacity;
+    rep.min_bytes = opt_.min_bytes;
+    rep.device = opt_.eng.device;
+    const std::uint32_t frames = static_cast<std::uint32_t>(opt_.eng.gpu_capacity / kBlockBytes);
+    rep.frames = frames;
+    bool ok = ipc::send_msg(fd, ipc::Msg::Hello, &rep, sizeof(rep)) && ipc::send_fds(fd, &a.ctl_fd, 1);
+    std::vector<int> batch;
+    for (std::uint32_t f = 0; f < frames && ok; f += ipc::kFdBatch) {
+      const std::uint32_t n = std::min<std::uint32_t>(ipc::kFdBatch, frames - f);
+      batch.clear();
+      for (std::uint32_t k = 0; k < n; ++k) batch.push_back(eng_.arena_export_fd(f + k));
+      ok = ipc::send_fds(fd, batch.data(), static_cast<int>(n));
+      for (int x : batch) ::close(x);
+    }
+    apps_[a.id] = a;
+    if (!ok) apps_[a.id].alive = false;
+    note("{\"t\": %.6f, \"event\": \"hello\", \"app\": %u, \"pid\": %d, \"name\": \"%s\"}", now(), a.id, a.pid, a.name.c_str());
+  }
+
+  void on_app_fd(int fd) {
+    App* a = app_by_fd(fd);
+    if (!a) return;
+    ipc::Msg type;
+    std::vector<std::uint8_t> body;
+    if (!ipc::recv_msg(fd, type, body)) {
+      a->alive = false;  // reaped below
+      return;
+    }
+    if (fd == a->ev) {  // unsolicited event-socket traffic outside a switch: protocol error
+      a->alive = false;
+      return;
+    }
+    try {
+      rpc(*a, type, body);
+    } catch (const InvariantViolation&) {
+      throw;
+    } catch (const std::exception& e) {
+      std::fprintf(stderr, "[nixied] app %u: %s\n", a->id, e.what());
+      ipc::StatusRep st{100, 0};
+      ipc::send_msg(a->rpc, ipc::Msg::Status, &st, sizeof(st));
+    }
+  }
+
+  // Apps whose sockets closed: their memory returns to the registry.
+  void reap() {
+    for (auto& [id, a] : apps_) {
+      if (a.alive || a.rpc < 0) continue;
+      if (sched_.granted() == id) sched_.on_grant_end(id, now());
+      sched_.clear_request(id);
+      const std::vector<ChunkId> chunks = eng_.mem().chunks_of(id);
+      for (ChunkId c : chunks) eng_.free_chunk(id, c);
+      close_app(a);
+      ++gone_;
+      note("{\"t\": %.6f, \"event\": \"bye\", \"app\": %u, \"chunks_freed\": %zu}", now(), id, chunks.size());
+    }
+  }
+
+  // ---- requests --------------------------------------------------------------
+  void rpc(App& a, ipc::Msg type, const std::vector<std::uint8_t>& body) {
+    ipc::Reader r{body};
+    switch (type) {
+      case ipc::Msg::Alloc: {
+        const auto req = r.get<ipc::AllocReq>();
+        alloc(a, req.bytes);
+        break;
+      }
+      case ipc::Msg::Free: {
+        const auto n = r.get<std::uint32_t>();
+        int status = 0;
+        for (std::uint32_t i = 0; i < n && r.ok; ++i) {
+          const auto c = r.get<std::uint32_t>();
+          try {
+            eng_.free_chunk(a.id, c);
+          } catch (const SimError&) {
+            status = 1;
+          }
+        }
+        ipc::StatusRep st{status, 0};
+        ipc::send_msg(a.rpc, ipc::Msg::Status, &st, sizeof(st));
+        break;
+      }
+      case ipc::Msg::Acquire: {
+        ipc::StatusRep st{0, 0};
+        ipc::send_msg(a.rpc, ipc::Msg::Status, &st, sizeof(st));
+        if (sched_.granted() != a.id) {
+          sched_.enqueue_request(a.id, now());
+          decide(now());
+        }
+        break;
+      }
+      case ipc::Msg::Stats: {
+        ipc::StatsRep s{switches_, bytes_in_, bytes_out_, mismatches_, verified_};
+        ipc::send_msg(a.rpc, ipc::Msg::Stats, &s, sizeof(s));
+        break;
+      }
+      default:
+        a.alive = false;
+    }
+  }
+
+  // cudaMalloc >= min_bytes (MemState::allocate, proj/src/mem_model.cpp:48-86).
+  // Placement: the GPU when it has room; otherwise the holder's allocation
+  // is brought in by an in-place plan (other apps' blocks are evicted), and
+  // a waiting app's allocation starts in pageable memory (its next grant
+  // fetches it). An app's footprint may not exceed the GPU budget
+  // (the planner's precondition).
+  void alloc(App& a, Bytes bytes) {
+    MemState& mem = eng_.mem();
+    const Bytes fp = footprint_for(bytes);
+    ipc::AllocRep rep{};
+    if (bytes == 0 || mem.app_footprint(a.id) + fp > opt_.eng.gpu_capacity) {
+      rep.status = 2;
+      ipc::send_msg(a.rpc, ipc::Msg::Alloc, &rep, sizeof(rep));
+      return;
+    }
+    const bool holder = sched_.granted() == a.id;
+    TierId tier = TierId::Gpu;
+    if (mem.tier(TierId::Gpu).free_bytes() < fp) {
+      tier = mem.tier(TierId::PagedHost).free_bytes() >= fp ? TierId::PagedHost : TierId::PinnedHost;
+      if (mem.tier(tier).free_bytes() < fp) {
+        rep.status = 2;
+        ipc::send_msg(a.rpc, ipc::Msg::Alloc, &rep, sizeof(rep));
+        return;
+      }
+    }
+    const std::vector<ChunkId> chunks = eng_.allocate(a.id, bytes, tier);
+    if (holder && tier != TierId::Gpu) fetch_in_place(a.id);
+    std::vector<std::uint32_t> ids, frames;
+    for (ChunkId c : chunks) {
+      ids.push_back(static_cast<std::uint32_t>(c));
+      for (BlockId b : mem.chunk(c).blocks) {
+        const std::int64_t f = eng_.frame_index(b);
+        frames.push_back(f < 0 ? ipc::kNoFrame : static_cast<std::uint32_t>(f));
+      }
+    }
+    rep.n_chunks = static_cast<std::uint32_t>(ids.size());
+    rep.n_blocks = static_cast<std::uint32_t>(frames.size());
+    rep.footprint = fp;
+    rep.epoch = ++epoch_;
+    ipc::Writer w;
+    w.put(rep);
+    w.put_u32s(ids);
+    w.put_u32s(frames);
+    ipc::send_msg(a.rpc, ipc::Msg::Alloc, w.buf);
+  }
+
+  // ---- activity (the shims' control pages) -> MLFQ inputs ---------------------
+  void poll_activity(Seconds t, Seconds dt) {
+    for (auto& [id, a] : apps_) {
+      if (!a.alive || !a.ctl) continue;
+      const std::uint64_t launches = a.ctl->launches.load(std::memory_order_acquire);
+      const bool blocking = a.ctl->blocking.load(std::memory_order_acquire) > 0;
+      const Seconds t_api = std::min(t, to_daemon_time(a.ctl->last_api_ns.load(std::memory_order_acquire)));
+      const Seconds t_blk = std::min(t, to_daemon_time(a.ctl->last_block_ns.load(std::memory_order_acquire)));
+      if (blocking && !a.seen_blocking) sched_.on_api_event(id, t_blk, ApiEventKind::BlockingEnter);
+      if (!blocking && a.seen_blocking) sched_.on_api_event(id, t_blk, ApiEventKind::BlockingExit);
+      if (launches != a.seen_launches) sched_.on_api_event(id, t_api, ApiEventKind::NonBlockingReturn);
+      // The holder's busy time drives demotion (t_a in Algorithm 1).
+      if (dt > 0 && sched_.granted() == id && (blocking || launches != a.active_launch_mark)) sched_.add_execution(id, dt);
+      a.active_launch_mark = launches;
+      a.seen_launches = launches;
+      a.seen_blocking = blocking;
+    }
+  }
+
+  void tick() {
+    const Seconds t = now();
+    poll_activity(t, last_tick_ > 0 ? t - last_tick_ : 0.0);
+    last_tick_ = t;
+    decide(t);
+  }
+
+  // SPEC.md:354 tick rule (as LaunchGate::tick): switch to select_next() when
+  // nobody holds the GPU, when the holder has gone idle, or when
+  // should_preempt fires.
+  void decide(Seconds t) {
+    poll_activity(t, 0.0);
+    sched_.infer_all(t);
+    const std::optional<AppId> next = sched_.select_next(t);
+    if (!next) return;
+    const std::optional<AppId> holder = sched_.granted();
+    const bool go = !holder || sched_.is_idle(*holder, t) || sched_.should_preempt(*holder, t);
+    if (go) context_switch(*next, t);
+  }
+
+  // ---- acks on the event socket ------------------------------------------------
+  bool wait_ack(App& a, ipc::Msg want, std::vector<std::uint8_t>& body) {
+    if (!a.alive || a.ev < 0) return false;
+    pollfd p{a.ev, POLLIN, 0};
+    const int n = ::poll(&p, 1, static_cast<int>(opt_.ack_timeout_s * 1000));
+    ipc::Msg type;
+    if (n <= 0 || !ipc::recv_msg(a.ev, type, body) || type != want) {
+      std::fprintf(stderr, "[nixied] app %u: no %u ack (dropping the app)\n", a.id, static_cast<unsigned>(want));
+      a.alive = false;
+      return false;
+    }
+    return true;
+  }
+
+  // Sends Unmap for every GPU block the plan evicts, grouped by owner.
+  std::vector<AppId> send_unmaps(const MigrationPlan& plan) {
+    const MemState& mem = eng_.mem();
+    std::map<AppId, std::vector<std::uint32_t>> per_app;
+    for (const Move& m : plan.moves) {
+      if (m.src != TierId::Gpu) continue;
+      const Block& b = mem.block(m.block);
+      const std::vector<BlockId>& blocks = mem.chunk(b.chunk).blocks;
+      const auto idx = static_cast<std::uint32_t>(std::find(blocks.begin(), blocks.end(), m.block) - blocks.begin());
+      auto& v = per_app[b.app];
+      v.push_back(static_cast<std::uint32_t>(b.chunk));
+      v.push_back(idx);
+    }
+    std::vector<AppId> waiting;
+    for (auto& [app, pairs] : per_app) {
+      auto it = apps_.find(app);
+      if (it == apps_.end() || !it->second.alive || it->second.ev < 0) continue;
+      ipc::UnmapMsg um{++epoch_, static_cast<std::uint32_t>(pairs.size() / 2), 0};
+      ipc::Writer w;
+      w.put(um);
+      w.put_u32s(pairs);
+      if (ipc::send_msg(it->second.ev, ipc::Msg::Unmap, w.buf)) waiting.push_back(app);
+      else it->second.alive = false;
+    }
+    return waiting;
+  }
+
+  void collect_unmaps(const std::vector<AppId>& waiting) {
+    std::vector<std::uint8_t> body;
+    for (AppId app : waiting) wait_ack(apps_.at(app), ipc::Msg::Unmapped, body);
+  }
+
+  void account(const ExecResult&) {
+    const SwitchStats& s = eng_.last_stats();
+    bytes_in_ += s.pcie_h2d_bytes;
+    bytes_out_ += s.pcie_d2h_bytes;
+    verified_ += s.verified;
+    mismatches_ += s.mismatches;
+  }
+
+  // The holder allocated past the GPU's free space: its new blocks come in
+  // and other apps' blocks go out; the holder keeps running (its resident
+  // blocks do not move: plan_switch never evicts the incoming app).
+  void fetch_in_place(AppId app) {
+    PlannerConfig cfg = opt_.planner;
+    cfg.eviction_policy.victim_order = sched_.victim_hint();
+    const MigrationPlan plan = plan_switch(app, eng_.mem(), cfg);
+    const std::vector<AppId> waiting = send_unmaps(plan);
+    const ExecResult r = eng_.execute(plan, cfg);
+    collect_unmaps(waiting);
+    account(r);
+    note("{\"t\": %.6f, \"event\": \"fetch_in_place\", \"app\": %u, \"bytes_in\": %" PRIu64 ", \"bytes_out\": %" PRIu64 "}",
+         now(), app, plan.bytes_in, plan.bytes_out);
+  }
+
+  void context_switch(AppId to, Seconds t) {
+    App& in = apps_.at(to);
+    if (!in.alive || in.ev < 0) {
+      sched_.clear_request(to);
+      return;
+    }
+    const std::uint64_t t_start = ipc::mono_ns();
+    const std::optional<AppId> holder = sched_.granted();
+    std::vector<std::uint8_t> body;
+    // (3) pause the incumbent and drain its kernels.
+    if (holder) {
+      App& h = apps_.at(*holder);
+      ipc::EpochMsg pm{++epoch_};
+      if (h.alive && h.ev >= 0 && ipc::send_msg(h.ev, ipc::Msg::Pause, &pm, sizeof(pm))) wait_ack(h, ipc::Msg::Drained, body);
+      sched_.on_grant_end(*holder, t);
+    }
+    const std::uint64_t t_drained = ipc::mono_ns();
+    // (4) plan + real copies, victims unmapping concurrently.
+    PlannerConfig cfg = opt_.planner;
+    cfg.eviction_policy.victim_order = sched_.victim_hint();
+    const MigrationPlan plan = plan_switch(to, eng_.mem(), cfg);
+    const std::uint64_t t_planned = ipc::mono_ns();
+    const std::vector<AppId> waiting = send_unmaps(plan);
+    const ExecResult r = eng_.execute(plan, cfg);
+    const std::uint64_t t_copied = ipc::mono_ns();
+    collect_unmaps(waiting);
+    account(r);
+    const std::uint64_t t_unmapped = ipc::mono_ns();
+    // (5) grant: the incoming shim maps its frames and sets its flag.
+    ipc::Writer w;
+    const std::vector<ChunkId>& chunks = eng_.mem().chunks_of(to);
+    w.put(ipc::GrantMsg{++epoch_, static_cast<std::uint32_t>(chunks.size()), 0});
+    for (ChunkId c : chunks) {
+      const std::vector<BlockId>& blocks = eng_.mem().chunk(c).blocks;
+      w.put(static_cast<std::uint32_t>(c));
+      w.put(static_cast<std::uint32_t>(blocks.size()));
+      for (BlockId b : blocks) {
+        const std::int64_t f = eng_.frame_index(b);
+        if (f < 0) throw InvariantViolation("grant: block " + std::to_string(b) + " of app " + std::to_string(to) + " is not GPU-resident");
+        w.put(static_cast<std::uint32_t>(f));
+      }
+    }
+    ipc::GrantedMsg gm{};
+    if (ipc::send_msg(in.ev, ipc::Msg::Grant, w.buf) && wait_ack(in, ipc::Msg::Granted, body) && body.size() >= sizeof(gm))
+      std::memcpy(&gm, body.data(), sizeof(gm));
+    const std::uint64_t t_end = ipc::mono_ns();
+    sched_.clear_request(to);
+    const Seconds granted_at = t + static_cast<double>(t_end - t_start) * 1e-9;
+    sched_.on_grant_start(to, granted_at);
+    sched_.on_api_event(to, granted_at, ApiEventKind::NonBlockingReturn);  // its held launch resumes now
+    ++switches_;
+    const SwitchStats& s = eng_.last_stats();
+    auto ms = [](std::uint64_t a, std::uint64_t b) { return static_cast<double>(b - a) * 1e-6; };
+    note("{\"t\": %.6f, \"event\": \"switch\", \"from\": %d, \"to\": %u, \"bytes_in\": %" PRIu64 ", \"bytes_out\": %" PRIu64
+         ", \"pcie_h2d\": %" PRIu64 ", \"pcie_d2h\": %" PRIu64 ", \"host_bytes\": %" PRIu64
+         ", \"pause_ms\": %.3f, \"plan_ms\": %.3f, \"copy_ms\": %.3f, \"unmap_wait_ms\": %.3f, \"grant_ms\": %.3f"
+         ", \"map_ms\": %.3f, \"map_calls\": %" PRIu64 ", \"total_ms\": %.3f, \"device_span_ms\": %.3f"
+         ", \"verified\": %" PRIu64 ", \"unverified\": %" PRIu64 ", \"mismatches\": %" PRIu64 "}",
+         t, holder ? static_cast<int>(*holder) : -1, to, plan.bytes_in, plan.bytes_out, s.pcie_h2d_bytes, s.pcie_d2h_bytes,
+         s.host_bytes, ms(t_start, t_drained), ms(t_drained, t_planned), ms(t_planned, t_copied), ms(t_copied, t_unmapped),
+         ms(t_unmapped, t_end), static_cast<double>(gm.map_ns) * 1e-6, gm.map_calls, ms(t_start, t_end),
+         s.device_span_s * 1e3, s.verified, s.unverified, s.mismatches);
+  }
+
+  template <typename... A>
+  void note(const char* fmt, A... args) {
+    if (!log_) return;
+    std::fprintf(log_, fmt, args...);
+    std::fputc('\n', log_);
+    std::fflush(log_);
+  }
+
+  void write_summary() {
+    note("{\"event\": \"summary\", \"switches\": %" PRIu64 ", \"pcie_bytes_in\": %" PRIu64 ", \"pcie_bytes_out\": %" PRIu64
+         ", \"verified\": %" PRIu64 ", \"mismatches\": %" PRIu64 ", \"apps\": %u}",
+         switches_, bytes_in_, bytes_out_, verified_, mismatches_, next_app_);
+    for (const SchedLogRow& row : sched_.log())
+      note("{\"event\": \"sched\", \"t\": %.6f, \"app\": %u, \"what\": \"%s\", \"level\": %d}", row.time, row.app,
+           row.event.c_str(), row.level);
+  }
+
+  Options opt_;
+  SwapEngine eng_;
+  MlfqScheduler sched_;
+  int listen_fd_ = -1;
+  std::vector<int> pending_;
+  std::map<AppId, App> apps_;
+  AppId next_app_ = 0;
+  int gone_ = 0;
+  std::uint64_t epoch_ = 0;
+  std::uint64_t t0_ = 0;
+  Seconds last_tick_ = 0;
+  std::uint64_t switches_ = 0, bytes_in_ = 0, bytes_out_ = 0, verified_ = 0, mismatches_ = 0;
+  std::FILE* log_ = nullptr;
+};
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  Options opt;
+  try {
+    if (!parse_args(argc, argv, opt)) return 1;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "nixied: %s\n", e.what());
+    return 1;
+  }
+  signal(SIGINT, on_signal);
+  signal(SIGTERM, on_signal);
+  signal(SIGPIPE, SIG_IGN);
+  try {
+    Daemon d(opt);
+    d.listen_on();
+    return d.run();
+  } catch (const InvariantViolation& e) {
+    std::fprintf(stderr, "nixied: invariant violation: %s\n", e.what());
+    return 2;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "nixied: %s\n", e.what());
+    return 1;
+  }
+}

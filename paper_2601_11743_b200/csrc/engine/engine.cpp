@@ -163,7 +163,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
     hw.tier_capacity[3] = 0;
     hw.apply_to(mem);
 
-    arena.init(cfg.gpu_capacity);
+    arena.init(cfg.gpu_capacity, cfg.exportable_arena, cfg.device);
     pinned.init(cfg.pinned_capacity, numa.node);
     paged.init(cfg.paged_capacity);
     pool.start(cfg.host_threads, numa.cpus);
@@ -830,6 +830,18 @@ void* SwapEngine::frame_of(BlockId b) const {
   return impl_->arena.frame(impl_->unit[b]);
 }
 const std::uint64_t* SwapEngine::device_frame_table() const { return impl_->d_frames; }
+
+std::int64_t SwapEngine::frame_index(BlockId b) const {
+  const Location& loc = impl_->mem.block(b).loc;
+  if (!loc.is_resident() || loc.tier != TierId::Gpu) return -1;
+  return impl_->unit[b];
+}
+
+int SwapEngine::arena_export_fd(std::uint32_t frame) const {
+  const int fd = impl_->arena.export_fd(frame);
+  if (fd < 0) throw SimError(Err::InvalidState, "the arena is not exportable (EngineConfig::exportable_arena)");
+  return fd;
+}
 
 std::uint64_t SwapEngine::block_checksum(BlockId b) const {
   unsigned long long v = 0;

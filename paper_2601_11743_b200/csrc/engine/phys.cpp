@@ -1,5 +1,6 @@
 // Tier backing stores, NUMA placement and the host copy pool (phys.hpp).
 #include "phys.hpp"
+#include "vmm.hpp"
 
 #include <pthread.h>
 #include <sched.h>
@@ -98,15 +99,29 @@ void pin_thread_to(const std::vector<int>& cpus) {
   pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
 }
 
-void DeviceArena::init(Bytes capacity) {
+void DeviceArena::init(Bytes capacity, bool exportable, int device) {
   const auto units = static_cast<std::uint32_t>(capacity / kBlockBytes);
-  if (units > 0) NX_CUDA(cudaMalloc(&base_, static_cast<std::size_t>(units) * kBlockBytes));
+  if (units > 0) {
+    if (exportable) {
+      vmm_ = new ExportableArena();
+      vmm_->init(device, static_cast<Bytes>(units) * kBlockBytes);
+      base_ = vmm_->base();
+    } else {
+      NX_CUDA(cudaMalloc(&base_, static_cast<std::size_t>(units) * kBlockBytes));
+    }
+  }
   ring.reset(units);
 }
 
 DeviceArena::~DeviceArena() {
-  if (base_) cudaFree(base_);
+  if (vmm_) {
+    delete vmm_;
+  } else if (base_) {
+    cudaFree(base_);
+  }
 }
+
+int DeviceArena::export_fd(std::uint32_t frame) const { return vmm_ ? vmm_->export_fd(frame) : -1; }
 
 void PinnedRing::init(Bytes capacity, int numa_node) {
   const auto units = static_cast<std::uint32_t>(capacity / kBlockBytes);

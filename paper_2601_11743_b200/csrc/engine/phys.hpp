@@ -66,16 +66,23 @@ NumaInfo numa_for_device(int device);
 void prefer_numa_node(int node);
 void pin_thread_to(const std::vector<int>& cpus);
 
-// tier 0: one cudaMalloc of the capped budget.
+class ExportableArena;
+
+// tier 0: one allocation of the capped budget: cudaMalloc, or (exportable,
+// for the interposer daemon) one VMM allocation whose handle the shims import
+// to map frames at their applications' stable virtual addresses (vmm.hpp).
 class DeviceArena {
  public:
-  void init(Bytes capacity);
+  void init(Bytes capacity, bool exportable = false, int device = 0);
   ~DeviceArena();
   std::uint8_t* frame(std::uint32_t u) const { return base_ + static_cast<std::size_t>(u) * kBlockBytes; }
+  std::uint8_t* base() const { return base_; }
+  int export_fd(std::uint32_t frame) const;  // -1 unless exportable
   UnitRing ring;
 
  private:
   std::uint8_t* base_ = nullptr;
+  ExportableArena* vmm_ = nullptr;
 };
 
 // tier 1: the pinned staging ring, exactly `capacity` bytes of

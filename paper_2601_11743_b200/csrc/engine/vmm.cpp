@@ -1,0 +1,94 @@
+// Exportable VMM arena (vmm.hpp).
+#include "vmm.hpp"
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "phys.hpp"
+
+namespace nixie::b200 {
+
+namespace {
+
+template <typename F>
+void resolve(F& fn, const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  NX_CUDA(cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q));
+  if (!p || q != cudaDriverEntryPointSuccess) throw CudaFailure(std::string("driver entry point ") + name + " unavailable");
+  fn = reinterpret_cast<F>(p);
+}
+
+void check(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return;
+  const char* s = "unknown";
+  if (vmm_api().get_error_string) vmm_api().get_error_string(r, &s);
+  throw CudaFailure(std::string(what) + ": CUresult " + std::to_string(static_cast<int>(r)) + " (" + s + ")");
+}
+
+}  // namespace
+
+const VmmApi& vmm_api() {
+  static const VmmApi api = [] {
+    VmmApi a;
+    resolve(a.mem_create, "cuMemCreate");
+    resolve(a.mem_release, "cuMemRelease");
+    resolve(a.addr_reserve, "cuMemAddressReserve");
+    resolve(a.addr_free, "cuMemAddressFree");
+    resolve(a.map, "cuMemMap");
+    resolve(a.unmap, "cuMemUnmap");
+    resolve(a.set_access, "cuMemSetAccess");
+    resolve(a.granularity, "cuMemGetAllocationGranularity");
+    resolve(a.export_handle, "cuMemExportToShareableHandle");
+    resolve(a.get_error_string, "cuGetErrorString");
+    return a;
+  }();
+  return api;
+}
+
+void ExportableArena::init(int device, Bytes bytes) {
+  const VmmApi& v = vmm_api();
+  NX_CUDA(cudaFree(nullptr));  // the primary context is current on this thread
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t gran = 0;
+  check(v.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM), "cuMemGetAllocationGranularity");
+  if (gran == 0 || kBlockBytes % gran != 0)
+    throw CudaFailure("VMM granularity " + std::to_string(gran) + " does not divide the 2 MiB frame");
+  bytes_ = bytes / kBlockBytes * kBlockBytes;
+  const auto n = static_cast<std::uint32_t>(bytes_ / kBlockBytes);
+  check(v.addr_reserve(&va_, bytes_, kBlockBytes, 0, 0), "cuMemAddressReserve(arena)");
+  handles_.resize(n, 0);
+  for (std::uint32_t f = 0; f < n; ++f) {
+    check(v.mem_create(&handles_[f], kBlockBytes, &prop, 0), "cuMemCreate(exportable frame)");
+    check(v.map(va_ + static_cast<CUdeviceptr>(f) * kBlockBytes, kBlockBytes, 0, handles_[f], 0), "cuMemMap(frame)");
+    mapped_ = f + 1;
+  }
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  check(v.set_access(va_, bytes_, &acc, 1), "cuMemSetAccess(arena)");
+}
+
+ExportableArena::~ExportableArena() {
+  if (!va_) return;
+  const VmmApi& v = vmm_api();
+  for (std::uint32_t f = 0; f < mapped_; ++f) v.unmap(va_ + static_cast<CUdeviceptr>(f) * kBlockBytes, kBlockBytes);
+  for (CUmemGenericAllocationHandle h : handles_)
+    if (h) v.mem_release(h);
+  v.addr_free(va_, bytes_);
+}
+
+int ExportableArena::export_fd(std::uint32_t f) const {
+  if (f >= handles_.size()) throw SimError(Err::InvalidState, "export of frame " + std::to_string(f) + " out of range");
+  int fd = -1;
+  check(vmm_api().export_handle(&fd, handles_[f], CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0), "cuMemExportToShareableHandle");
+  return fd;
+}
+
+}  // namespace nixie::b200

@@ -1,0 +1,66 @@
+// CUDA virtual-memory-management (VMM) helpers for the exportable device
+// arena (internal header).
+//
+// The interposer path (csrc/shim, csrc/daemon) needs the GPU tier's frames to
+// be mappable into every application's own address space at stable virtual
+// addresses ("reserve GPU virtual addresses, and map these
+// addresses to different physical allocations before and after chunk
+// migrations"; modeled in the reference by Chunk::logical_base,
+// proj/include/nixie/mem_model.hpp:72). The daemon therefore backs each 2 MiB
+// frame of the arena with its own cuMemCreate allocation, exportable as a
+// POSIX file descriptor; each shim imports every frame once at start-up and
+// maps frames under its applications' reserved ranges as blocks move.
+//
+// Driver entry points are resolved at run time through the runtime's
+// cudaGetDriverEntryPoint, so the product library still loads without a
+// driver (the CPU tests dlopen it).
+#pragma once
+
+#include <cuda.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "nixie/units.hpp"
+
+namespace nixie::b200 {
+
+struct VmmApi {
+  CUresult (*mem_create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+  CUresult (*mem_release)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*addr_reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*addr_free)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  CUresult (*export_handle)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long) = nullptr;
+  CUresult (*get_error_string)(CUresult, const char**) = nullptr;
+};
+
+// Resolved once; throws CudaFailure when an entry point is missing.
+const VmmApi& vmm_api();
+
+// The GPU tier as exportable 2 MiB physical allocations (one per frame:
+// cuMemMap maps a handle only from offset 0, so a frame that must be mapped on
+// its own at an application's address needs its own handle), mapped
+// contiguously at a fresh virtual range of this process.
+class ExportableArena {
+ public:
+  void init(int device, Bytes bytes);
+  ~ExportableArena();
+  std::uint8_t* base() const { return reinterpret_cast<std::uint8_t*>(va_); }
+  Bytes bytes() const { return bytes_; }
+  std::uint32_t frames() const { return static_cast<std::uint32_t>(handles_.size()); }
+  // A new descriptor for frame `f`'s physical allocation (the caller owns
+  // it; it is sent to a shim with SCM_RIGHTS and closed).
+  int export_fd(std::uint32_t f) const;
+
+ private:
+  std::vector<CUmemGenericAllocationHandle> handles_;
+  CUdeviceptr va_ = 0;
+  Bytes bytes_ = 0;
+  std::uint32_t mapped_ = 0;
+};
+
+}  // namespace nixie::b200

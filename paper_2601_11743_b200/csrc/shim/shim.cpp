@@ -1,0 +1,750 @@
+// libnixie_shim.so — the Nixie shim: LD_PRELOAD it into an
+// unmodified CUDA application (one that links the CUDA runtime dynamically)
+// and set NIXIE_SOCKET to a running nixied's socket.
+//
+// Interposed ("memory allocation and free ... kernel/graph
+// launches ... APIs that implicitly allocate memory ... memory usage"):
+//   cudaMalloc / cudaFree, cuMemAlloc_v2 / cuMemFree_v2
+//       allocations >= min_bytes (2 MiB) become daemon chunks: the shim
+//       reserves a stable virtual range (cuMemAddressReserve) and maps the
+//       daemon's arena frames under it (each frame is a 2 MiB physical
+//       allocation the shim imported once at start-up) whenever the blocks
+//       are GPU-resident; smaller
+//       ones pass through. Reference registry anchor:
+//       MemState::allocate / free_chunk (proj/src/mem_model.cpp:48-116),
+//       Chunk::logical_base (proj/include/nixie/mem_model.hpp:72).
+//   cudaLaunchKernel[_ptsz], cudaLaunchKernelExC[_ptsz],
+//   cudaLaunchCooperativeKernel[_ptsz], cudaGraphLaunch[_ptsz], cuLaunchKernel,
+//   cudaMemcpy[Async], cudaMemcpy2D[Async], cudaMemset[Async]
+//       the launch gate (PAPER.md:116 steps 1-2 and 6): pass while the
+//       execution flag is set; otherwise ask the daemon (Acquire) and hold
+//       the calling thread until a Grant has mapped the app's frames.
+//   cudaDeviceSynchronize, cudaStreamSynchronize, cudaEventSynchronize,
+//   cudaMemcpy (sync)
+//       blocking-call brackets for the MLFQ's idleness test (§6.1).
+//   cudaStreamBeginCapture / cudaStreamEndCapture
+//       capture guard: launches into a capturing stream are
+//       not gated and a pause waits for captures to end before it calls any
+//       CUDA API.
+//   cudaMemGetInfo
+//       reports the daemon's budget as total and budget - own usage as free
+//       (PAPER.md:147).
+//
+// The shim never copies application data: the daemon's swap engine moves
+// every byte (both PCIe directions at once) through its own mapping of the
+// same physical frames; the shim only maps, unmaps and gates.
+#include <cuda.h>
+#include <cuda_runtime_api.h>
+#include <dlfcn.h>
+#include <sys/mman.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <thread>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "nixie_ipc.hpp"
+
+// Per-thread-default-stream variants (declared by cuda_runtime_api.h only
+// when that mode is compiled in; libcudart exports them regardless).
+extern "C" {
+cudaError_t cudaLaunchKernel_ptsz(const void*, dim3, dim3, void**, size_t, cudaStream_t);
+cudaError_t cudaLaunchKernelExC_ptsz(const cudaLaunchConfig_t*, const void*, void**);
+cudaError_t cudaLaunchCooperativeKernel_ptsz(const void*, dim3, dim3, void**, size_t, cudaStream_t);
+cudaError_t cudaGraphLaunch_ptsz(cudaGraphExec_t, cudaStream_t);
+cudaError_t cudaMemcpyAsync_ptsz(void*, const void*, size_t, cudaMemcpyKind, cudaStream_t);
+cudaError_t cudaMemsetAsync_ptsz(void*, int, size_t, cudaStream_t);
+}
+
+namespace ipc = nixie::ipc;
+
+namespace {
+
+constexpr std::uint64_t kBlock = 2ull << 20;
+
+// ---- real entry points --------------------------------------------------------
+void* cudart_handle() {
+  static void* h = [] {
+    void* p = dlopen("libcudart.so.12", RTLD_NOW | RTLD_NOLOAD);
+    if (!p) p = dlopen("libcudart.so", RTLD_NOW | RTLD_NOLOAD);
+    return p;
+  }();
+  return h;
+}
+
+void* real_sym(const char* name) {
+  void* p = dlsym(RTLD_NEXT, name);
+  if (!p && cudart_handle()) p = dlsym(cudart_handle(), name);
+  if (!p) {
+    static void* cuda = dlopen("libcuda.so.1", RTLD_NOW);
+    if (cuda) p = dlsym(cuda, name);
+  }
+  if (!p) {
+    std::fprintf(stderr, "[nixie-shim] cannot resolve %s\n", name);
+    std::abort();
+  }
+  return p;
+}
+
+#define REAL(name) \
+  static auto real_##name = reinterpret_cast<decltype(&::name)>(real_sym(#name))
+
+// Driver entry points the shim itself uses (never the interposed names).
+struct Drv {
+  CUresult (*import_handle)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType);
+  CUresult (*addr_reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+  CUresult (*addr_free)(CUdeviceptr, size_t);
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+  CUresult (*unmap)(CUdeviceptr, size_t);
+  CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+  CUresult (*ctx_get_current)(CUcontext*);
+  CUresult (*ctx_set_current)(CUcontext);
+};
+
+Drv& drv() {
+  static Drv d = [] {
+    Drv x{};
+    void* h = dlopen("libcuda.so.1", RTLD_NOW);
+    if (!h) {
+      std::fprintf(stderr, "[nixie-shim] libcuda.so.1 not found\n");
+      std::abort();
+    }
+    auto get = [h](const char* n) {
+      void* p = dlsym(h, n);
+      if (!p) {
+        std::fprintf(stderr, "[nixie-shim] libcuda lacks %s\n", n);
+        std::abort();
+      }
+      return p;
+    };
+    x.import_handle = reinterpret_cast<decltype(x.import_handle)>(get("cuMemImportFromShareableHandle"));
+    x.addr_reserve = reinterpret_cast<decltype(x.addr_reserve)>(get("cuMemAddressReserve"));
+    x.addr_free = reinterpret_cast<decltype(x.addr_free)>(get("cuMemAddressFree"));
+    x.map = reinterpret_cast<decltype(x.map)>(get("cuMemMap"));
+    x.unmap = reinterpret_cast<decltype(x.unmap)>(get("cuMemUnmap"));
+    x.set_access = reinterpret_cast<decltype(x.set_access)>(get("cuMemSetAccess"));
+    x.ctx_get_current = reinterpret_cast<decltype(x.ctx_get_current)>(get("cuCtxGetCurrent"));
+    x.ctx_set_current = reinterpret_cast<decltype(x.ctx_set_current)>(get("cuCtxSetCurrent"));
+    return x;
+  }();
+  return d;
+}
+
+void die(const char* what, CUresult r = CUDA_SUCCESS) {
+  std::fprintf(stderr, "[nixie-shim] fatal: %s (CUresult %d)\n", what, static_cast<int>(r));
+  std::abort();
+}
+
+// ---- state ----------------------------------------------------------------------
+struct ChunkMap {
+  CUdeviceptr va = 0;                 // 0 until the allocating thread registers it
+  std::uint32_t nblocks = 0;
+  std::uint64_t epoch = 0;            // newest daemon message applied to `want`
+  std::vector<std::uint32_t> want;    // desired frame per block (kNoFrame = not on the GPU)
+  std::vector<std::uint32_t> have;    // frame mapped at each block now
+};
+
+struct Region {
+  CUdeviceptr va = 0;
+  std::uint64_t reserved = 0;  // 2 MiB rounded
+  std::vector<std::uint32_t> chunks;
+};
+
+struct Shim {
+  bool active = false;
+  int device = 0;
+  std::uint32_t app = 0;
+  std::uint64_t budget = 0, min_bytes = kBlock;
+  int rpc = -1, ev = -1;
+  ipc::CtlPage* ctl = nullptr;
+  std::vector<CUmemGenericAllocationHandle> frames;  // imported arena frames
+  CUcontext ctx = nullptr;
+
+  std::mutex rpc_mu;            // one request in flight on the rpc socket
+  std::mutex mu;                // regions, chunks, granted (slow paths)
+  std::condition_variable cv;
+  std::map<CUdeviceptr, Region> regions;
+  std::unordered_map<std::uint32_t, ChunkMap> chunks;
+  std::unordered_set<std::uint32_t> dead_chunks;
+  std::map<void*, std::size_t> small;  // passthrough allocations (for cudaMemGetInfo)
+  std::uint64_t managed_bytes = 0, small_bytes = 0;
+
+  std::atomic<bool> granted{false};
+  std::atomic<int> inflight{0};
+  std::atomic<int> capturing{0};
+};
+
+// Never destroyed: the listener thread may still run while the process exits.
+Shim& g = *new Shim;
+std::once_flag g_once;
+thread_local int t_capturing = 0;  // this thread began a stream capture
+thread_local int t_in_shim = 0;    // re-entrancy guard
+
+void now_api() {
+  if (g.ctl) g.ctl->last_api_ns.store(ipc::mono_ns(), std::memory_order_release);
+}
+
+void ensure_ctx() {
+  CUcontext cur = nullptr;
+  drv().ctx_get_current(&cur);
+  if (cur != g.ctx && g.ctx) drv().ctx_set_current(g.ctx);
+}
+
+void listener();
+
+int connect_to(const char* path) {
+  const int fd = ::socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+  sockaddr_un addr{};
+  addr.sun_family = AF_UNIX;
+  std::strncpy(addr.sun_path, path, sizeof(addr.sun_path) - 1);
+  if (::connect(fd, reinterpret_cast<sockaddr*>(&addr), sizeof(addr)) != 0) {
+    ::close(fd);
+    return -1;
+  }
+  return fd;
+}
+
+void init_once() {
+  const char* path = std::getenv("NIXIE_SOCKET");
+  if (!path || !*path) return;  // inactive: pure passthrough
+  t_in_shim++;
+  REAL(cudaFree);
+  REAL(cudaGetDevice);
+  real_cudaFree(nullptr);  // primary context current on this thread
+  real_cudaGetDevice(&g.device);
+  drv().ctx_get_current(&g.ctx);
+  g.rpc = connect_to(path);
+  if (g.rpc < 0) {
+    std::fprintf(stderr, "[nixie-shim] cannot connect to %s\n", path);
+    std::abort();
+  }
+  ipc::HelloReq req{};
+  req.pid = getpid();
+  req.device = g.device;
+  FILE* f = std::fopen("/proc/self/comm", "r");
+  if (f) {
+    if (!std::fgets(req.name, sizeof(req.name), f)) req.name[0] = 0;
+    std::fclose(f);
+    req.name[strcspn(req.name, "\n")] = 0;
+  }
+  ipc::Msg type;
+  std::vector<std::uint8_t> body;
+  int ctl_fd = -1;
+  if (!ipc::send_msg(g.rpc, ipc::Msg::Hello, &req, sizeof(req)) || !ipc::recv_msg(g.rpc, type, body) ||
+      type != ipc::Msg::Hello || body.size() < sizeof(ipc::HelloRep) || !ipc::recv_fds(g.rpc, &ctl_fd, 1))
+    die("hello with the daemon failed");
+  ipc::HelloRep rep;
+  std::memcpy(&rep, body.data(), sizeof(rep));
+  if (rep.status != 0) die("the daemon serves another device");
+  g.app = rep.app;
+  g.budget = rep.gpu_budget;
+  g.min_bytes = rep.min_bytes;
+  g.frames.resize(rep.frames, 0);
+  std::vector<int> fds(ipc::kFdBatch);
+  for (std::uint64_t f = 0; f < rep.frames; f += ipc::kFdBatch) {
+    const int n = static_cast<int>(std::min<std::uint64_t>(ipc::kFdBatch, rep.frames - f));
+    if (!ipc::recv_fds(g.rpc, fds.data(), n)) die("receiving the arena's frame descriptors");
+    for (int k = 0; k < n; ++k) {
+      const CUresult r = drv().import_handle(&g.frames[f + k], reinterpret_cast<void*>(static_cast<std::uintptr_t>(fds[k])),
+                                             CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+      if (r != CUDA_SUCCESS) die("cuMemImportFromShareableHandle(frame)", r);
+      ::close(fds[k]);
+    }
+  }
+  void* p = ::mmap(nullptr, 4096, PROT_READ | PROT_WRITE, MAP_SHARED, ctl_fd, 0);
+  if (p == MAP_FAILED) die("mmap control page");
+  ::close(ctl_fd);
+  g.ctl = static_cast<ipc::CtlPage*>(p);
+  g.ev = connect_to(path);
+  ipc::EventHelloReq eh{g.app, 0};
+  if (g.ev < 0 || !ipc::send_msg(g.ev, ipc::Msg::EventHello, &eh, sizeof(eh))) die("event connection");
+  g.active = true;
+  std::thread(listener).detach();
+  t_in_shim--;
+}
+
+bool active() {
+  std::call_once(g_once, init_once);
+  return g.active;
+}
+
+// ---- mapping ---------------------------------------------------------------------
+CUmemAccessDesc access_desc() {
+  CUmemAccessDesc a{};
+  a.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  a.location.id = g.device;
+  a.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  return a;
+}
+
+// Makes the chunk's mappings equal `want` (caller holds g.mu): one cuMemMap
+// per 2 MiB block (each frame is its own physical allocation) and one
+// cuMemSetAccess per run of newly mapped blocks. Returns cuMemMap calls made.
+std::uint64_t sync_chunk(ChunkMap& c) {
+  if (!c.va) return 0;
+  ensure_ctx();
+  c.have.resize(c.nblocks, ipc::kNoFrame);
+  const std::uint64_t t0 = ipc::mono_ns();
+  for (std::uint32_t i = 0; i < c.nblocks; ++i) {
+    if (c.have[i] == ipc::kNoFrame || c.have[i] == c.want[i]) continue;
+    const CUresult e = drv().unmap(c.va + i * kBlock, kBlock);
+    if (e != CUDA_SUCCESS) die("cuMemUnmap", e);
+    c.have[i] = ipc::kNoFrame;
+  }
+  const std::uint64_t t1 = ipc::mono_ns();
+  std::uint64_t calls = 0;
+  const CUmemAccessDesc acc = access_desc();
+  for (std::uint32_t i = 0; i < c.nblocks;) {
+    if (c.want[i] == ipc::kNoFrame || c.have[i] == c.want[i]) {
+      ++i;
+      continue;
+    }
+    std::uint32_t n = 0;
+    while (i + n < c.nblocks && c.want[i + n] != ipc::kNoFrame && c.have[i + n] == ipc::kNoFrame) {
+      const std::uint32_t f = c.want[i + n];
+      if (f >= g.frames.size()) die("grant names a frame outside the arena");
+      const CUresult e = drv().map(c.va + (i + n) * kBlock, kBlock, 0, g.frames[f], 0);
+      if (e != CUDA_SUCCESS) die("cuMemMap", e);
+      c.have[i + n] = f;
+      ++n;
+      ++calls;
+    }
+    const CUresult e = drv().set_access(c.va + i * kBlock, static_cast<size_t>(n) * kBlock, &acc, 1);
+    if (e != CUDA_SUCCESS) die("cuMemSetAccess", e);
+    i += n;
+  }
+  const std::uint64_t t2 = ipc::mono_ns();
+  if (g.ctl) {
+    g.ctl->unmap_ns.fetch_add(t1 - t0, std::memory_order_relaxed);
+    g.ctl->map_ns.fetch_add(t2 - t1, std::memory_order_relaxed);
+  }
+  return calls;
+}
+
+ChunkMap& chunk_entry(std::uint32_t id, std::uint32_t nblocks) {
+  ChunkMap& c = g.chunks[id];
+  if (c.want.size() < nblocks) {
+    c.nblocks = nblocks;
+    c.want.resize(nblocks, ipc::kNoFrame);
+  }
+  return c;
+}
+
+// ---- event socket: Pause / Unmap / Grant ----------------------------------------------
+void on_pause(const std::vector<std::uint8_t>& body) {
+  ipc::EpochMsg m{};
+  std::memcpy(&m, body.data(), std::min(body.size(), sizeof(m)));
+  const std::uint64_t t0 = ipc::mono_ns();
+  g.granted.store(false, std::memory_order_seq_cst);
+  if (g.ctl) g.ctl->granted.store(0);
+  while (g.inflight.load(std::memory_order_seq_cst) != 0 || g.capturing.load() != 0) std::this_thread::yield();
+  REAL(cudaDeviceSynchronize);
+  t_in_shim++;
+  ensure_ctx();
+  real_cudaDeviceSynchronize();  // outstanding kernels finish before any eviction
+  t_in_shim--;
+  if (g.ctl) g.ctl->drain_ns.fetch_add(ipc::mono_ns() - t0, std::memory_order_relaxed);
+  ipc::send_msg(g.ev, ipc::Msg::Drained, &m, sizeof(m));
+}
+
+void on_unmap(const std::vector<std::uint8_t>& body) {
+  ipc::Reader r{body};
+  const auto m = r.get<ipc::UnmapMsg>();
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    std::unordered_map<std::uint32_t, bool> touched;
+    for (std::uint32_t i = 0; i < m.n && r.ok; ++i) {
+      const auto chunk = r.get<std::uint32_t>();
+      const auto blk = r.get<std::uint32_t>();
+      if (g.dead_chunks.count(chunk)) continue;
+      ChunkMap& c = chunk_entry(chunk, blk + 1);
+      if (m.epoch <= c.epoch) continue;
+      c.want[blk] = ipc::kNoFrame;
+      touched[chunk] = true;
+    }
+    for (auto& kv : touched) {
+      ChunkMap& c = g.chunks[kv.first];
+      c.epoch = m.epoch;
+      sync_chunk(c);
+    }
+  }
+  ipc::EpochMsg ack{m.epoch};
+  ipc::send_msg(g.ev, ipc::Msg::Unmapped, &ack, sizeof(ack));
+}
+
+void on_grant(const std::vector<std::uint8_t>& body) {
+  ipc::Reader r{body};
+  const auto m = r.get<ipc::GrantMsg>();
+  const std::uint64_t t0 = ipc::mono_ns();
+  std::uint64_t calls = 0;
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    for (std::uint32_t k = 0; k < m.n_chunks && r.ok; ++k) {
+      const auto id = r.get<std::uint32_t>();
+      const auto n = r.get<std::uint32_t>();
+      std::vector<std::uint32_t> frames(n);
+      for (auto& f : frames) f = r.get<std::uint32_t>();
+      if (g.dead_chunks.count(id)) continue;
+      ChunkMap& c = chunk_entry(id, n);
+      if (m.epoch <= c.epoch) continue;
+      c.want = frames;
+      c.epoch = m.epoch;
+      calls += sync_chunk(c);
+    }
+    g.granted.store(true, std::memory_order_seq_cst);
+    if (g.ctl) g.ctl->granted.store(1);
+  }
+  g.cv.notify_all();
+  ipc::GrantedMsg ack{m.epoch, ipc::mono_ns() - t0, calls};
+  ipc::send_msg(g.ev, ipc::Msg::Granted, &ack, sizeof(ack));
+}
+
+void listener() {
+  t_in_shim++;
+  REAL(cudaSetDevice);
+  REAL(cudaFree);
+  real_cudaSetDevice(g.device);
+  real_cudaFree(nullptr);
+  ensure_ctx();
+  ipc::Msg type;
+  std::vector<std::uint8_t> body;
+  while (ipc::recv_msg(g.ev, type, body)) {
+    switch (type) {
+      case ipc::Msg::Pause: on_pause(body); break;
+      case ipc::Msg::Unmap: on_unmap(body); break;
+      case ipc::Msg::Grant: on_grant(body); break;
+      default:
+        std::fprintf(stderr, "[nixie-shim] unexpected event %u\n", static_cast<unsigned>(type));
+    }
+  }
+  // The daemon went away: keep the application alive only if it holds its
+  // memory; otherwise any further gated call would hang forever.
+  std::fprintf(stderr, "[nixie-shim] daemon connection closed\n");
+  std::_Exit(3);
+}
+
+// ---- rpc ----------------------------------------------------------------------------
+bool rpc(ipc::Msg type, const void* p, std::size_t n, ipc::Msg& rtype, std::vector<std::uint8_t>& body) {
+  std::lock_guard<std::mutex> lk(g.rpc_mu);
+  return ipc::send_msg(g.rpc, type, p, n) && ipc::recv_msg(g.rpc, rtype, body);
+}
+
+// ---- the gate -------------------------------------------------------------------------
+// Held at the gate: the thread waits for the GPU like a blocking call (the
+// MLFQ must not see a waiting app as idle the moment it is granted).
+void acquire_slow() {
+  const std::uint64_t t0 = ipc::mono_ns();
+  g.ctl->blocking.fetch_add(1, std::memory_order_acq_rel);
+  g.ctl->last_block_ns.store(t0, std::memory_order_release);
+  std::unique_lock<std::mutex> lk(g.mu);
+  auto last_ask = std::chrono::steady_clock::now() - std::chrono::hours(1);
+  while (!g.granted.load(std::memory_order_seq_cst)) {
+    if (std::chrono::steady_clock::now() - last_ask > std::chrono::seconds(1)) {
+      lk.unlock();
+      ipc::Msg rt;
+      std::vector<std::uint8_t> body;
+      if (!rpc(ipc::Msg::Acquire, nullptr, 0, rt, body)) die("acquire: daemon connection lost");
+      last_ask = std::chrono::steady_clock::now();
+      lk.lock();
+      continue;
+    }
+    g.cv.wait_for(lk, std::chrono::milliseconds(200));
+  }
+  const std::uint64_t t1 = ipc::mono_ns();
+  g.ctl->last_block_ns.store(t1, std::memory_order_release);
+  g.ctl->last_api_ns.store(t1, std::memory_order_release);
+  g.ctl->blocking.fetch_sub(1, std::memory_order_acq_rel);
+  if (g.ctl) {
+    g.ctl->gate_waits.fetch_add(1, std::memory_order_relaxed);
+    g.ctl->gate_wait_ns.fetch_add(ipc::mono_ns() - t0, std::memory_order_relaxed);
+  }
+}
+
+// Entry of every gated call: returns true holding an in-flight slot (a pause
+// waits for it), false when the call need not be gated.
+bool gate_enter() {
+  if (t_in_shim || !active() || t_capturing) return false;
+  for (;;) {
+    g.inflight.fetch_add(1, std::memory_order_seq_cst);
+    if (g.granted.load(std::memory_order_seq_cst)) break;
+    g.inflight.fetch_sub(1, std::memory_order_seq_cst);
+    acquire_slow();
+  }
+  g.ctl->launches.fetch_add(1, std::memory_order_relaxed);
+  return true;
+}
+
+struct Gate {
+  bool held;
+  Gate() : held(gate_enter()) {}
+  ~Gate() {
+    if (held) {
+      g.inflight.fetch_sub(1, std::memory_order_seq_cst);
+      now_api();
+    }
+  }
+};
+
+struct Blocking {
+  bool on;
+  Blocking() : on(!t_in_shim && active()) {
+    if (on) {
+      g.ctl->blocking.fetch_add(1, std::memory_order_acq_rel);
+      g.ctl->last_block_ns.store(ipc::mono_ns(), std::memory_order_release);
+    }
+  }
+  ~Blocking() {
+    if (on) {
+      const std::uint64_t t = ipc::mono_ns();
+      g.ctl->last_block_ns.store(t, std::memory_order_release);
+      g.ctl->last_api_ns.store(t, std::memory_order_release);
+      g.ctl->blocking.fetch_sub(1, std::memory_order_acq_rel);
+    }
+  }
+};
+
+// ---- allocation -------------------------------------------------------------------------
+int managed_alloc(void** out, std::size_t bytes) {
+  const std::uint64_t reserved = (bytes + kBlock - 1) / kBlock * kBlock;
+  ensure_ctx();
+  CUdeviceptr va = 0;
+  CUresult e = drv().addr_reserve(&va, reserved, kBlock, 0, 0);
+  if (e != CUDA_SUCCESS) return 2;
+  ipc::AllocReq req{bytes};
+  ipc::Msg rt;
+  std::vector<std::uint8_t> body;
+  if (!rpc(ipc::Msg::Alloc, &req, sizeof(req), rt, body) || rt != ipc::Msg::Alloc || body.size() < sizeof(ipc::AllocRep))
+    die("alloc: daemon connection lost");
+  ipc::Reader r{body};
+  const auto rep = r.get<ipc::AllocRep>();
+  if (rep.status != 0) {
+    drv().addr_free(va, reserved);
+    return 2;
+  }
+  std::vector<std::uint32_t> ids(rep.n_chunks), frames(rep.n_blocks);
+  for (auto& x : ids) x = r.get<std::uint32_t>();
+  for (auto& x : frames) x = r.get<std::uint32_t>();
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    Region reg{va, reserved, ids};
+    // MemState::allocate splits a request into <= 128 MiB chunks of 2 MiB
+    // blocks, in order (proj/src/mem_model.cpp:48-86): chunk k covers the
+    // next blocks of the range.
+    std::uint32_t off = 0;
+    const std::uint64_t per_chunk = 64;  // kChunkMaxBytes / kBlockBytes
+    const auto total = static_cast<std::uint32_t>(reserved / kBlock);
+    if (frames.size() != total) die("alloc: the daemon's block count differs from the reserved range");
+    for (std::uint32_t id : ids) {
+      const auto n = static_cast<std::uint32_t>(std::min<std::uint64_t>(per_chunk, total - off));
+      ChunkMap& c = chunk_entry(id, n);
+      c.va = va + static_cast<CUdeviceptr>(off) * kBlock;
+      if (rep.epoch > c.epoch) {
+        c.want.assign(frames.begin() + off, frames.begin() + off + n);
+        c.epoch = rep.epoch;
+      }
+      sync_chunk(c);
+      off += n;
+    }
+    g.regions[va] = reg;
+    g.managed_bytes += reserved;
+  }
+  *out = reinterpret_cast<void*>(va);
+  return 0;
+}
+
+// Returns true if `p` was a managed range (and frees it).
+bool managed_free(void* p) {
+  const auto va = reinterpret_cast<CUdeviceptr>(p);
+  std::vector<std::uint32_t> ids;
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    auto it = g.regions.find(va);
+    if (it == g.regions.end()) return false;
+    ids = it->second.chunks;
+  }
+  if (g.granted.load()) {  // cudaFree's implicit synchronisation
+    REAL(cudaDeviceSynchronize);
+    t_in_shim++;
+    real_cudaDeviceSynchronize();
+    t_in_shim--;
+  }
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    auto it = g.regions.find(va);
+    if (it == g.regions.end()) return true;
+    for (std::uint32_t id : ids) {
+      ChunkMap& c = g.chunks[id];
+      std::fill(c.want.begin(), c.want.end(), ipc::kNoFrame);
+      sync_chunk(c);
+      g.chunks.erase(id);
+      g.dead_chunks.insert(id);
+    }
+    drv().addr_free(va, it->second.reserved);
+    g.managed_bytes -= it->second.reserved;
+    g.regions.erase(it);
+  }
+  ipc::Writer w;
+  w.put(static_cast<std::uint32_t>(ids.size()));
+  w.put_u32s(ids);
+  ipc::Msg rt;
+  std::vector<std::uint8_t> body;
+  if (!rpc(ipc::Msg::Free, w.buf.data(), w.buf.size(), rt, body)) die("free: daemon connection lost");
+  return true;
+}
+
+}  // namespace
+
+// =================================================================================
+// Interposed CUDA runtime API
+// =================================================================================
+extern "C" {
+
+cudaError_t cudaMalloc(void** devPtr, size_t size) {
+  REAL(cudaMalloc);
+  if (t_in_shim || !active() || size < g.min_bytes) {
+    const cudaError_t e = real_cudaMalloc(devPtr, size);
+    if (e == cudaSuccess && g.active && !t_in_shim) {
+      std::lock_guard<std::mutex> lk(g.mu);
+      g.small[*devPtr] = size;
+      g.small_bytes += size;
+    }
+    return e;
+  }
+  return managed_alloc(devPtr, size) == 0 ? cudaSuccess : cudaErrorMemoryAllocation;
+}
+
+cudaError_t cudaFree(void* devPtr) {
+  REAL(cudaFree);
+  if (t_in_shim || !devPtr || !active()) return real_cudaFree(devPtr);
+  if (managed_free(devPtr)) return cudaSuccess;
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    auto it = g.small.find(devPtr);
+    if (it != g.small.end()) {
+      g.small_bytes -= it->second;
+      g.small.erase(it);
+    }
+  }
+  return real_cudaFree(devPtr);
+}
+
+cudaError_t cudaMemGetInfo(size_t* free_b, size_t* total_b) {
+  REAL(cudaMemGetInfo);
+  if (t_in_shim || !active()) return real_cudaMemGetInfo(free_b, total_b);
+  std::lock_guard<std::mutex> lk(g.mu);
+  const std::uint64_t used = g.managed_bytes + g.small_bytes;
+  if (total_b) *total_b = g.budget;
+  if (free_b) *free_b = used >= g.budget ? 0 : g.budget - used;
+  return cudaSuccess;
+}
+
+#define GATED(ret, name, params, args) \
+  ret name params {                    \
+    REAL(name);                        \
+    Gate gate_;                        \
+    return real_##name args;           \
+  }
+
+GATED(cudaError_t, cudaLaunchKernel, (const void* f, dim3 g_, dim3 b, void** a, size_t s, cudaStream_t st), (f, g_, b, a, s, st))
+GATED(cudaError_t, cudaLaunchKernel_ptsz, (const void* f, dim3 g_, dim3 b, void** a, size_t s, cudaStream_t st), (f, g_, b, a, s, st))
+GATED(cudaError_t, cudaLaunchKernelExC, (const cudaLaunchConfig_t* c, const void* f, void** a), (c, f, a))
+GATED(cudaError_t, cudaLaunchKernelExC_ptsz, (const cudaLaunchConfig_t* c, const void* f, void** a), (c, f, a))
+GATED(cudaError_t, cudaLaunchCooperativeKernel, (const void* f, dim3 g_, dim3 b, void** a, size_t s, cudaStream_t st), (f, g_, b, a, s, st))
+GATED(cudaError_t, cudaLaunchCooperativeKernel_ptsz, (const void* f, dim3 g_, dim3 b, void** a, size_t s, cudaStream_t st), (f, g_, b, a, s, st))
+GATED(cudaError_t, cudaGraphLaunch, (cudaGraphExec_t e, cudaStream_t st), (e, st))
+GATED(cudaError_t, cudaGraphLaunch_ptsz, (cudaGraphExec_t e, cudaStream_t st), (e, st))
+GATED(cudaError_t, cudaMemcpyAsync, (void* d, const void* s, size_t n, cudaMemcpyKind k, cudaStream_t st), (d, s, n, k, st))
+GATED(cudaError_t, cudaMemcpyAsync_ptsz, (void* d, const void* s, size_t n, cudaMemcpyKind k, cudaStream_t st), (d, s, n, k, st))
+GATED(cudaError_t, cudaMemcpy2DAsync, (void* d, size_t dp, const void* s, size_t sp, size_t w, size_t h, cudaMemcpyKind k, cudaStream_t st), (d, dp, s, sp, w, h, k, st))
+GATED(cudaError_t, cudaMemsetAsync, (void* d, int v, size_t n, cudaStream_t st), (d, v, n, st))
+GATED(cudaError_t, cudaMemsetAsync_ptsz, (void* d, int v, size_t n, cudaStream_t st), (d, v, n, st))
+GATED(cudaError_t, cudaMemset, (void* d, int v, size_t n), (d, v, n))
+GATED(cudaError_t, cudaMemcpy2D, (void* d, size_t dp, const void* s, size_t sp, size_t w, size_t h, cudaMemcpyKind k), (d, dp, s, sp, w, h, k))
+
+cudaError_t cudaMemcpy(void* d, const void* s, size_t n, cudaMemcpyKind k) {
+  REAL(cudaMemcpy);
+  Gate gate_;
+  Blocking b_;
+  return real_cudaMemcpy(d, s, n, k);
+}
+
+cudaError_t cudaDeviceSynchronize(void) {
+  REAL(cudaDeviceSynchronize);
+  Blocking b_;
+  return real_cudaDeviceSynchronize();
+}
+
+cudaError_t cudaStreamSynchronize(cudaStream_t st) {
+  REAL(cudaStreamSynchronize);
+  Blocking b_;
+  return real_cudaStreamSynchronize(st);
+}
+
+cudaError_t cudaEventSynchronize(cudaEvent_t ev) {
+  REAL(cudaEventSynchronize);
+  Blocking b_;
+  return real_cudaEventSynchronize(ev);
+}
+
+cudaError_t cudaStreamBeginCapture(cudaStream_t st, cudaStreamCaptureMode mode) {
+  REAL(cudaStreamBeginCapture);
+  // Capture records work; the app must hold the GPU when the graph is later
+  // launched (gated), not while it is built.
+  const cudaError_t e = real_cudaStreamBeginCapture(st, mode);
+  if (e == cudaSuccess && !t_in_shim) {
+    ++t_capturing;
+    g.capturing.fetch_add(1);
+  }
+  return e;
+}
+
+cudaError_t cudaStreamEndCapture(cudaStream_t st, cudaGraph_t* graph) {
+  REAL(cudaStreamEndCapture);
+  const cudaError_t e = real_cudaStreamEndCapture(st, graph);
+  if (!t_in_shim && t_capturing > 0) {
+    --t_capturing;
+    g.capturing.fetch_sub(1);
+  }
+  return e;
+}
+
+// ---- driver API (applications that call it directly through the PLT) ----------------
+CUresult cuMemAlloc_v2(CUdeviceptr* dptr, size_t bytes) {
+  REAL(cuMemAlloc_v2);
+  if (t_in_shim || !active() || bytes < g.min_bytes) return real_cuMemAlloc_v2(dptr, bytes);
+  void* p = nullptr;
+  if (managed_alloc(&p, bytes) != 0) return CUDA_ERROR_OUT_OF_MEMORY;
+  *dptr = reinterpret_cast<CUdeviceptr>(p);
+  return CUDA_SUCCESS;
+}
+
+CUresult cuMemFree_v2(CUdeviceptr dptr) {
+  REAL(cuMemFree_v2);
+  if (t_in_shim || !dptr || !active()) return real_cuMemFree_v2(dptr);
+  if (managed_free(reinterpret_cast<void*>(dptr))) return CUDA_SUCCESS;
+  return real_cuMemFree_v2(dptr);
+}
+
+CUresult cuLaunchKernel(CUfunction f, unsigned gx, unsigned gy, unsigned gz, unsigned bx, unsigned by, unsigned bz,
+                        unsigned smem, CUstream st, void** params, void** extra) {
+  REAL(cuLaunchKernel);
+  Gate gate_;
+  return real_cuLaunchKernel(f, gx, gy, gz, bx, by, bz, smem, st, params, extra);
+}
+
+// Introspection for tests: 1 when the shim is connected to a daemon.
+int nixie_shim_active(void) { return active() ? 1 : 0; }
+unsigned nixie_shim_app(void) { return active() ? g.app : 0xFFFFFFFFu; }
+
+}  // extern "C"

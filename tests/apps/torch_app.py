@@ -1,0 +1,37 @@
+"""An ordinary PyTorch program used to test the interposer: it allocates
+device tensors, runs elementwise kernels, synchronises, thinks, and checks
+its tensors at the end. It knows nothing about Nixie (run it with
+LD_PRELOAD=libnixie_shim.so NIXIE_SOCKET=...). Prints one JSON line."""
+import json
+import sys
+import time
+
+import torch
+
+
+def main():
+    mib = float(sys.argv[1]) if len(sys.argv) > 1 else 1024
+    iters = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    think = float(sys.argv[3]) if len(sys.argv) > 3 else 0.2
+    bufs = 4
+    n = int(mib * (1 << 20) / 4 / bufs)
+    free_b, total_b = torch.cuda.mem_get_info()
+    xs = [torch.full((n,), k * 1000, dtype=torch.int32, device="cuda") for k in range(bufs)]
+    lat = []
+    for it in range(iters):
+        t0 = time.perf_counter()
+        for x in xs:
+            x.add_(1)
+        torch.cuda.synchronize()
+        lat.append((time.perf_counter() - t0) * 1e3)
+        time.sleep(think)
+    bad = 0
+    for k, x in enumerate(xs):
+        bad += int((x != k * 1000 + iters).sum().item())
+    print(json.dumps({"name": "torch_app", "bytes": n * 4 * bufs, "iters": iters, "mismatch": bad,
+                      "memgetinfo": [free_b, total_b], "iter_ms_max": max(lat)}))
+    return 0 if bad == 0 else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

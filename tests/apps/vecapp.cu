@@ -1,0 +1,117 @@
+// nx_vecapp — an ordinary CUDA application used to test the interposer
+// (libnixie_shim.so + nixied). It knows nothing about Nixie: it allocates
+// with cudaMalloc, launches kernels with <<<>>>, synchronises, thinks, and at
+// the end copies everything back and checks it on the host. Built with
+// `-cudart shared` so LD_PRELOAD can interpose the runtime.
+//
+//   nx_vecapp --mib N --buffers K --iters I --think-ms T --seed S [--name X]
+//
+// Every word of every buffer holds hash(seed, buffer, index) + iteration; each
+// iteration's kernel checks the expected value and increments it, so a byte
+// lost or misplaced across a context switch is counted (device errors) and
+// the final host check compares every word. Prints one JSON line.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+__host__ __device__ inline std::uint32_t mix(std::uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return static_cast<std::uint32_t>(x ^ (x >> 31));
+}
+
+__host__ __device__ inline std::uint32_t expect(std::uint64_t seed, int buf, std::uint64_t i) {
+  return mix(seed ^ (static_cast<std::uint64_t>(buf) << 48) ^ i);
+}
+
+__global__ void fill(std::uint32_t* p, std::uint64_t n, std::uint64_t seed, int buf) {
+  for (std::uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = expect(seed, buf, i);
+}
+
+__global__ void step(std::uint32_t* p, std::uint64_t n, std::uint64_t seed, int buf, std::uint32_t iter,
+                     unsigned long long* errors) {
+  unsigned long long bad = 0;
+  for (std::uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const std::uint32_t want = expect(seed, buf, i) + iter;
+    const std::uint32_t v = p[i];
+    bad += v != want;
+    p[i] = v + 1;
+  }
+  if (bad) atomicAdd(errors, bad);
+}
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) {                                                                    \
+      std::fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+      std::exit(2);                                                                             \
+    }                                                                                           \
+  } while (0)
+
+int main(int argc, char** argv) {
+  double mib = 512;
+  int buffers = 4, iters = 10;
+  double think_ms = 50;
+  std::uint64_t seed = 1;
+  std::string name = "vecapp";
+  for (int i = 1; i + 1 < argc; i += 2) {
+    const std::string a = argv[i];
+    if (a == "--mib") mib = std::atof(argv[i + 1]);
+    else if (a == "--buffers") buffers = std::atoi(argv[i + 1]);
+    else if (a == "--iters") iters = std::atoi(argv[i + 1]);
+    else if (a == "--think-ms") think_ms = std::atof(argv[i + 1]);
+    else if (a == "--seed") seed = std::strtoull(argv[i + 1], nullptr, 0);
+    else if (a == "--name") name = argv[i + 1];
+  }
+  const auto t_start = std::chrono::steady_clock::now();
+  const std::uint64_t bytes_each = static_cast<std::uint64_t>(mib * 1048576.0 / buffers) / 4 * 4;
+  const std::uint64_t n = bytes_each / 4;
+  std::vector<std::uint32_t*> buf(buffers);
+  for (auto& p : buf) CK(cudaMalloc(&p, bytes_each));
+  unsigned long long* d_err = nullptr;  // a small allocation (passes through)
+  CK(cudaMalloc(&d_err, sizeof(unsigned long long)));
+  CK(cudaMemset(d_err, 0, sizeof(unsigned long long)));
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  for (int b = 0; b < buffers; ++b) fill<<<1184, 256>>>(buf[b], n, seed, b);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  std::vector<double> lat;
+  for (int it = 0; it < iters; ++it) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int b = 0; b < buffers; ++b) step<<<1184, 256>>>(buf[b], n, seed, b, static_cast<std::uint32_t>(it), d_err);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    lat.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    if (think_ms > 0) std::this_thread::sleep_for(std::chrono::duration<double, std::milli>(think_ms));
+  }
+  unsigned long long dev_errors = 0;
+  CK(cudaMemcpy(&dev_errors, d_err, sizeof(dev_errors), cudaMemcpyDeviceToHost));
+  std::uint64_t host_mismatch = 0;
+  std::vector<std::uint32_t> h(n);
+  for (int b = 0; b < buffers; ++b) {
+    CK(cudaMemcpy(h.data(), buf[b], bytes_each, cudaMemcpyDeviceToHost));
+    for (std::uint64_t i = 0; i < n; ++i) host_mismatch += h[i] != expect(seed, b, i) + static_cast<std::uint32_t>(iters);
+  }
+  for (auto p : buf) CK(cudaFree(p));
+  CK(cudaFree(d_err));
+  std::vector<double> s = lat;
+  std::sort(s.begin(), s.end());
+  auto q = [&](double f) { return s.empty() ? 0.0 : s[std::min(s.size() - 1, static_cast<std::size_t>(f * s.size()))]; };
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  std::printf("{\"name\": \"%s\", \"bytes\": %llu, \"iters\": %d, \"device_errors\": %llu, \"host_mismatch\": %llu, "
+              "\"memgetinfo\": [%zu, %zu], \"iter_ms\": {\"p50\": %.3f, \"p99\": %.3f, \"max\": %.3f}, \"wall_s\": %.3f}\n",
+              name.c_str(), static_cast<unsigned long long>(bytes_each * buffers), iters, dev_errors,
+              static_cast<unsigned long long>(host_mismatch), free_b, total_b, q(0.5), q(0.99), s.empty() ? 0.0 : s.back(), wall);
+  return dev_errors == 0 && host_mismatch == 0 ? 0 : 1;
+}

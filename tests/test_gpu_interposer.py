@@ -1,0 +1,85 @@
+"""Unmodified CUDA applications under the interposer:
+lib/nixied + LD_PRELOAD=lib/libnixie_shim.so.
+
+Applications: tests/apps/vecapp.cu (C++/CUDA, cudaMalloc + <<<>>>), and
+tests/apps/torch_app.py (PyTorch elementwise). Their combined working sets
+exceed the daemon's GPU budget, so they can only finish if the daemon swaps
+them in and out: each app checks every word of its data on the device every
+iteration and on the host at the end, and the daemon verifies every restore
+by checksum (mismatches would fail the switch)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2601_11743_b200.interpose import NIXIED, SHIM, VECAPP, Daemon, run_apps  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _vec(mib, iters, think_ms, seed, name):
+    return [VECAPP, "--mib", str(mib), "--buffers", "6", "--iters", str(iters), "--think-ms", str(think_ms),
+            "--seed", str(seed), "--name", name]
+
+
+def _save(name, d, res):
+    """Keeps the daemon log and app outputs (gpurun_out/ is merged back from the GPU box)."""
+    out = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(out):
+        with open(os.path.join(out, f"interposer_{name}.jsonl"), "w") as f:
+            for r in d.records():
+                f.write(json.dumps(r) + "\n")
+            for r in res:
+                f.write(json.dumps({"event": "app", "rc": r["rc"], "out": r["out"], "stderr": r["stderr"][-500:]}) + "\n")
+
+
+def _check(res, d):
+    for r in res:
+        assert r["rc"] == 0, (r["stderr"], d.stderr())
+        assert r["out"] is not None, r["stdout"]
+
+
+def test_two_vecapps_oversubscribed():
+    """2 x 3 GiB on a 4 GiB budget: every iteration after a think gap needs a
+    switch. Byte-exact (device + host checks), every restore verified."""
+    with Daemon(gpu="4G", pinned="4G", paged="16G") as d:
+        res = run_apps(d, [_vec(3072, 6, 250, 11, "a"), _vec(3072, 6, 250, 22, "b")], timeout=600)
+        _save("two_vecapps", d, res)
+        _check(res, d)
+        sw = d.switches()
+    d.stop()
+    for r in res:
+        assert r["out"]["device_errors"] == 0 and r["out"]["host_mismatch"] == 0
+    assert len(sw) >= 3, sw
+    assert all(s["mismatches"] == 0 for s in sw)
+    assert sum(s["verified"] for s in sw) > 0
+    assert sum(s["pcie_h2d"] for s in sw) > 0 and sum(s["pcie_d2h"] for s in sw) > 0
+    # both directions in the same switch (bidirectional swap)
+    assert any(s["pcie_h2d"] > 0 and s["pcie_d2h"] > 0 for s in sw)
+
+
+def test_memgetinfo_reports_budget():
+    with Daemon(gpu="6G", pinned="2G", paged="8G") as d:
+        res = run_apps(d, [_vec(1024, 1, 0, 3, "m")], timeout=300)
+        _check(res, d)
+    free_b, total_b = res[0]["out"]["memgetinfo"]
+    assert total_b == 6 << 30
+    assert free_b <= total_b - (1 << 30)
+
+
+def test_three_apps_with_torch():
+    """A PyTorch program and two CUDA programs share a 5 GiB budget."""
+    with Daemon(gpu="5G", pinned="4G", paged="16G") as d:
+        res = run_apps(d, [_vec(2048, 5, 200, 5, "a"), [sys.executable, os.path.join(ROOT, "tests", "apps", "torch_app.py"),
+                                                           "2048", "5", "0.2"], _vec(2048, 5, 200, 6, "c")], timeout=900)
+        _save("torch_mix", d, res)
+        _check(res, d)
+        sw = d.switches()
+    assert res[1]["out"]["mismatch"] == 0
+    assert res[1]["out"]["memgetinfo"][1] == 5 << 30
+    assert len(sw) >= 3 and all(s["mismatches"] == 0 for s in sw)
