@@ -52,7 +52,21 @@ struct EngineConfig {
   bool numa_bind = true;              // pinned ring + workers on the GPU's NUMA node
   int first_batch_legs = 8;           // batch-size ramp start (doubles per batch up to legs_per_launch)
   bool k3_tma = true;                 // CE-path checksum pass on the TMA pipeline (else the LDG loop)
-  bool exportable_arena = false;      // GPU tier = one VMM allocation shims can import (interposer daemon)
+  bool exportable_arena = false;      // GPU tier = exportable VMM slabs shims can import (interposer daemon)
+  Bytes arena_slab_bytes = 128 * kMiB; // exportable arena: bytes per physical allocation (a multiple of 2 MiB)
+  Bytes gpu_physical = 0;             // arena bytes (0 = gpu_capacity); the registry still enforces gpu_capacity
+};
+
+// Physical placement of blocks arriving on the GPU tier. Default (no placer):
+// any free 2 MiB frame of the arena, FIFO. The interposer daemon installs one
+// that keeps each application's 128 MiB virtual slabs backed by whole
+// physical slabs (csrc/daemon/daemon.cpp), so a restore maps one slab per
+// 64 blocks into the application instead of one frame per block.
+class FramePlacer {
+ public:
+  virtual ~FramePlacer() = default;
+  virtual std::uint32_t acquire(BlockId block) = 0;                // frame for a block about to land on the GPU
+  virtual void release(BlockId block, std::uint32_t frame) = 0;    // the block left the GPU (or was freed)
 };
 
 struct SwitchStats {
@@ -161,11 +175,15 @@ class SwapEngine {
   void* frame_of(BlockId block) const;
   const std::uint64_t* device_frame_table() const;
   // Frame number (offset / 2 MiB into the arena) of a GPU-resident block, or
-  // -1. With EngineConfig::exportable_arena every frame is its own physical
-  // allocation and arena_export_fd(k) returns a new POSIX descriptor of frame
-  // k (caller closes it): a shim imports it and maps it at its own address.
+  // -1. With EngineConfig::exportable_arena the arena is a row of physical
+  // slabs of arena_slab_bytes; arena_export_fd(s) returns a new POSIX
+  // descriptor of slab s (caller closes it): a shim imports it and maps it at
+  // its own address (frames s * slab_frames ... belong to slab s).
   std::int64_t frame_index(BlockId block) const;
-  int arena_export_fd(std::uint32_t frame) const;
+  int arena_export_fd(std::uint32_t slab) const;
+  std::uint32_t arena_frames() const;  // physical 2 MiB frames in the arena
+  // Not owned; nullptr restores the default. Install before any GPU allocation.
+  void set_frame_placer(FramePlacer* placer);
   std::uint64_t block_checksum(BlockId block) const;  // last recorded departure checksum
   // Test access to a resident block's bytes wherever it lives.
   void read_block(BlockId block, void* host_dst);

@@ -34,6 +34,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <deque>
+#include <utility>
 #include <cinttypes>
 #include <cstdio>
 #include <cstdlib>
@@ -66,6 +68,7 @@ struct Options {
   Bytes min_bytes = kBlockBytes;  // smaller allocations pass through
   double ack_timeout_s = 60.0;
   int exit_after_apps = 0;         // exit once this many apps have come and gone (tests)
+  int phys_slack_slabs = 16;       // physical slabs beyond the budget (partly resident slabs)
 };
 
 Bytes parse_size(const char* s) {
@@ -84,7 +87,7 @@ void usage() {
                "usage: nixied [--socket PATH] [--device N] [--gpu SIZE] [--pinned SIZE] [--paged SIZE]\n"
                "              [--window SIZE] [--min-bytes SIZE] [--path auto|ce|sm] [--host-threads N]\n"
                "              [--tick-ms X] [--idle-ms X] [--allot-s X] [--preempt-s X] [--log FILE]\n"
-               "              [--exit-after-apps N]\n"
+               "              [--phys-slack SLABS] [--exit-after-apps N]\n"
                "sizes take a K/M/G suffix (GiB when bare). The daemon serves LD_PRELOAD=libnixie_shim.so apps\n"
                "that set NIXIE_SOCKET=PATH.\n");
 }
@@ -115,6 +118,7 @@ bool parse_args(int argc, char** argv, Options& o) {
     else if (a == "--preempt-s") o.mlfq.base_preemption = std::atof(val());
     else if (a == "--log") o.log_path = val();
     else if (a == "--exit-after-apps") o.exit_after_apps = std::atoi(val());
+    else if (a == "--phys-slack") o.phys_slack_slabs = std::atoi(val());
     else if (a == "--path") {
       const std::string p = val();
       o.eng.path = p == "sm" ? CopyPath::SmKernel : p == "auto" ? CopyPath::Auto : CopyPath::CopyEngine;
@@ -127,12 +131,106 @@ bool parse_args(int argc, char** argv, Options& o) {
     }
   }
   o.mlfq.validate();
+  const Bytes slab = static_cast<Bytes>(ipc::kSlabBlocks) * kBlockBytes;
+  o.eng.arena_slab_bytes = slab;
+  o.eng.gpu_physical = (o.eng.gpu_capacity + slab - 1) / slab * slab + static_cast<Bytes>(std::max(o.phys_slack_slabs, 0)) * slab;
   return true;
 }
 
+// GPU frame placement for the interposer: each application's 128 MiB virtual
+// slab (ipc::kSlabBlocks blocks of its shim's range) is backed by one whole
+// physical slab while any of its blocks is on the GPU, at the block's slot.
+// The registry still charges 2 MiB per resident block against the budget;
+// the arena holds `slack` extra slabs for slabs that are partly resident
+// (an eviction boundary inside a slab, or small allocations sharing one).
+class SlabPlacer final : public FramePlacer {
+ public:
+  using Key = std::pair<AppId, std::uint32_t>;  // (app, vslab)
+
+  explicit SlabPlacer(std::uint32_t slabs) {
+    for (std::uint32_t p = 0; p < slabs; ++p) free_.push_back(p);
+  }
+
+  // Blocks first .. first+n-1 (about to be created by MemState::allocate, in
+  // order) sit at range blocks va_block .. of `app`.
+  void expect(BlockId first, std::uint64_t n, AppId app, std::uint64_t va_block) {
+    if (app_.size() < first + n) {
+      app_.resize(first + n);
+      vpos_.resize(first + n);
+    }
+    for (std::uint64_t k = 0; k < n; ++k) {
+      app_[first + k] = app;
+      vpos_[first + k] = va_block + k;
+    }
+  }
+
+  std::uint32_t acquire(BlockId b) override {
+    if (b >= app_.size()) throw InvariantViolation("slab placer: block " + std::to_string(b) + " has no virtual placement");
+    Slab& s = slabs_[key(b)];
+    if (s.phys == ipc::kNoFrame) {
+      if (free_.empty())
+        throw InvariantViolation("slab placer: every physical slab is in use (raise --phys-slack; partly resident slabs: " +
+                                 std::to_string(partial()) + ")");
+      s.phys = free_.front();
+      free_.pop_front();
+    }
+    ++s.count;
+    return s.phys * ipc::kSlabBlocks + static_cast<std::uint32_t>(vpos_[b] % ipc::kSlabBlocks);
+  }
+
+  void release(BlockId b, std::uint32_t frame) override {
+    const Key k = key(b);
+    Slab& s = slabs_[k];
+    if (s.count == 0 || frame / ipc::kSlabBlocks != s.phys) throw InvariantViolation("slab placer: release of an unplaced block");
+    if (--s.count == 0) {
+      free_.push_back(s.phys);
+      s.phys = ipc::kNoFrame;
+      released_.push_back(k);
+    }
+  }
+
+  // vslabs that lost their physical slab since the last call.
+  std::vector<Key> take_released() { return std::exchange(released_, {}); }
+
+  // Every backed vslab of `app`.
+  std::vector<ipc::SlabMap> backed(AppId app) const {
+    std::vector<ipc::SlabMap> out;
+    for (auto it = slabs_.lower_bound(Key{app, 0}); it != slabs_.end() && it->first.first == app; ++it)
+      if (it->second.phys != ipc::kNoFrame) out.push_back(ipc::SlabMap{it->first.second, it->second.phys});
+    return out;
+  }
+
+  ipc::SlabMap map_of(AppId app, std::uint32_t vslab) const {
+    auto it = slabs_.find(Key{app, vslab});
+    return ipc::SlabMap{vslab, it == slabs_.end() ? ipc::kNoFrame : it->second.phys};
+  }
+
+  std::uint64_t partial() const {
+    std::uint64_t n = 0;
+    for (const auto& kv : slabs_) n += kv.second.phys != ipc::kNoFrame && kv.second.count < ipc::kSlabBlocks;
+    return n;
+  }
+  std::size_t free_slabs() const { return free_.size(); }
+
+ private:
+  struct Slab {
+    std::uint32_t phys = ipc::kNoFrame;
+    std::uint32_t count = 0;  // blocks placed in it
+  };
+  Key key(BlockId b) const { return Key{app_[b], static_cast<std::uint32_t>(vpos_[b] / ipc::kSlabBlocks)}; }
+
+  std::vector<AppId> app_;
+  std::vector<std::uint64_t> vpos_;
+  std::map<Key, Slab> slabs_;
+  std::deque<std::uint32_t> free_;
+  std::vector<Key> released_;
+};
+
 class Daemon {
  public:
-  explicit Daemon(const Options& o) : opt_(o), eng_(o.eng), sched_(o.mlfq) {
+  explicit Daemon(const Options& o)
+      : opt_(o), eng_(o.eng), sched_(o.mlfq), placer_(eng_.arena_frames() / ipc::kSlabBlocks) {
+    eng_.set_frame_placer(&placer_);
     sched_.set_logging(true);
     t0_ = ipc::mono_ns();
     if (!o.log_path.empty()) {
@@ -157,8 +255,9 @@ class Daemon {
     ::unlink(opt_.socket_path.c_str());
     if (::bind(listen_fd_, reinterpret_cast<sockaddr*>(&addr), sizeof(addr)) != 0 || ::listen(listen_fd_, 64) != 0)
       throw SimError(Err::IoError, "cannot listen on " + opt_.socket_path + ": " + std::strerror(errno));
-    std::fprintf(stderr, "[nixied] listening on %s  gpu %.1f GiB  pinned %.1f GiB  path %s\n", opt_.socket_path.c_str(),
-                 double(opt_.eng.gpu_capacity) / kGiB, double(opt_.eng.pinned_capacity) / kGiB,
+    std::fprintf(stderr, "[nixied] listening on %s  gpu %.1f GiB (physical %.1f GiB)  pinned %.1f GiB  path %s\n",
+                 opt_.socket_path.c_str(), double(opt_.eng.gpu_capacity) / kGiB, double(opt_.eng.gpu_physical) / kGiB,
+                 double(opt_.eng.pinned_capacity) / kGiB,
                  opt_.eng.path == CopyPath::SmKernel ? "sm" : opt_.eng.path == CopyPath::Auto ? "auto" : "ce");
     std::fflush(stderr);
   }
@@ -286,15 +385,16 @@ class Daemon {
     rep.app = a.id;
     rep.gpu_budget = opt_.eng.gpu_capacity;
     rep.block_bytes = kBlockBytes;
-    rep.arena_bytes = opt_.eng.gpu_capacity;
     rep.min_bytes = opt_.min_bytes;
     rep.device = opt_.eng.device;
-    const std::uint32_t frames = static_cast<std::uint32_t>(opt_.eng.gpu_capacity / kBlockBytes);
-    rep.frames = frames;
+    const std::uint32_t slabs = eng_.arena_frames() / ipc::kSlabBlocks;
+    rep.slabs = slabs;
+    rep.slab_bytes = static_cast<std::uint64_t>(ipc::kSlabBlocks) * kBlockBytes;
+    rep.arena_bytes = rep.slabs * rep.slab_bytes;
     bool ok = ipc::send_msg(fd, ipc::Msg::Hello, &rep, sizeof(rep)) && ipc::send_fds(fd, &a.ctl_fd, 1);
     std::vector<int> batch;
-    for (std::uint32_t f = 0; f < frames && ok; f += ipc::kFdBatch) {
-      const std::uint32_t n = std::min<std::uint32_t>(ipc::kFdBatch, frames - f);
+    for (std::uint32_t f = 0; f < slabs && ok; f += ipc::kFdBatch) {
+      const std::uint32_t n = std::min<std::uint32_t>(ipc::kFdBatch, slabs - f);
       batch.clear();
       for (std::uint32_t k = 0; k < n; ++k) batch.push_back(eng_.arena_export_fd(f + k));
       ok = ipc::send_fds(fd, batch.data(), static_cast<int>(n));
@@ -337,6 +437,7 @@ class Daemon {
       sched_.clear_request(id);
       const std::vector<ChunkId> chunks = eng_.mem().chunks_of(id);
       for (ChunkId c : chunks) eng_.free_chunk(id, c);
+      placer_.take_released();  // its slabs return to the pool; nobody to unmap them
       close_app(a);
       ++gone_;
       note("{\"t\": %.6f, \"event\": \"bye\", \"app\": %u, \"chunks_freed\": %zu}", now(), id, chunks.size());
@@ -349,7 +450,7 @@ class Daemon {
     switch (type) {
       case ipc::Msg::Alloc: {
         const auto req = r.get<ipc::AllocReq>();
-        alloc(a, req.bytes);
+        alloc(a, req.bytes, req.va_block);
         break;
       }
       case ipc::Msg::Free: {
@@ -363,8 +464,17 @@ class Daemon {
             status = 1;
           }
         }
-        ipc::StatusRep st{status, 0};
-        ipc::send_msg(a.rpc, ipc::Msg::Status, &st, sizeof(st));
+        // Slabs the free emptied: the shim unmaps them (its reply carries them).
+        std::vector<std::uint32_t> mine;
+        for (const auto& k : placer_.take_released()) {
+          if (k.first == a.id) mine.push_back(k.second);
+          else throw InvariantViolation("free released another app's slab");
+        }
+        ipc::FreeRep rep{status, static_cast<std::uint32_t>(mine.size()), ++epoch_};
+        ipc::Writer w;
+        w.put(rep);
+        w.put_u32s(mine);
+        ipc::send_msg(a.rpc, ipc::Msg::Free, w.buf);
         break;
       }
       case ipc::Msg::Acquire: {
@@ -392,7 +502,7 @@ class Daemon {
   // a waiting app's allocation starts in pageable memory (its next grant
   // fetches it). An app's footprint may not exceed the GPU budget
   // (the planner's precondition).
-  void alloc(App& a, Bytes bytes) {
+  void alloc(App& a, Bytes bytes, std::uint64_t va_block) {
     MemState& mem = eng_.mem();
     const Bytes fp = footprint_for(bytes);
     ipc::AllocRep rep{};
@@ -411,24 +521,23 @@ class Daemon {
         return;
       }
     }
+    const std::uint64_t nblk = fp / kBlockBytes;
+    placer_.expect(mem.block_count(), nblk, a.id, va_block);
     const std::vector<ChunkId> chunks = eng_.allocate(a.id, bytes, tier);
     if (holder && tier != TierId::Gpu) fetch_in_place(a.id);
-    std::vector<std::uint32_t> ids, frames;
-    for (ChunkId c : chunks) {
-      ids.push_back(static_cast<std::uint32_t>(c));
-      for (BlockId b : mem.chunk(c).blocks) {
-        const std::int64_t f = eng_.frame_index(b);
-        frames.push_back(f < 0 ? ipc::kNoFrame : static_cast<std::uint32_t>(f));
-      }
-    }
+    std::vector<std::uint32_t> ids;
+    for (ChunkId c : chunks) ids.push_back(static_cast<std::uint32_t>(c));
+    std::vector<ipc::SlabMap> slabs;
+    for (std::uint64_t v = va_block / ipc::kSlabBlocks; v <= (va_block + nblk - 1) / ipc::kSlabBlocks; ++v)
+      slabs.push_back(placer_.map_of(a.id, static_cast<std::uint32_t>(v)));
     rep.n_chunks = static_cast<std::uint32_t>(ids.size());
-    rep.n_blocks = static_cast<std::uint32_t>(frames.size());
+    rep.n_slabs = static_cast<std::uint32_t>(slabs.size());
     rep.footprint = fp;
     rep.epoch = ++epoch_;
     ipc::Writer w;
     w.put(rep);
     w.put_u32s(ids);
-    w.put_u32s(frames);
+    for (const auto& m : slabs) w.put(m);
     ipc::send_msg(a.rpc, ipc::Msg::Alloc, w.buf);
   }
 
@@ -485,36 +594,22 @@ class Daemon {
     return true;
   }
 
-  // Sends Unmap for every GPU block the plan evicts, grouped by owner.
-  std::vector<AppId> send_unmaps(const MigrationPlan& plan) {
-    const MemState& mem = eng_.mem();
+  // After a plan ran: owners of vslabs whose physical slab was released unmap
+  // them. No ack is needed: only applications that cannot launch (paused
+  // or waiting) lose slabs, and the next Grant to them follows on the same
+  // socket.
+  void send_unmaps() {
     std::map<AppId, std::vector<std::uint32_t>> per_app;
-    for (const Move& m : plan.moves) {
-      if (m.src != TierId::Gpu) continue;
-      const Block& b = mem.block(m.block);
-      const std::vector<BlockId>& blocks = mem.chunk(b.chunk).blocks;
-      const auto idx = static_cast<std::uint32_t>(std::find(blocks.begin(), blocks.end(), m.block) - blocks.begin());
-      auto& v = per_app[b.app];
-      v.push_back(static_cast<std::uint32_t>(b.chunk));
-      v.push_back(idx);
-    }
-    std::vector<AppId> waiting;
-    for (auto& [app, pairs] : per_app) {
+    for (const auto& k : placer_.take_released()) per_app[k.first].push_back(k.second);
+    for (auto& [app, vs] : per_app) {
       auto it = apps_.find(app);
       if (it == apps_.end() || !it->second.alive || it->second.ev < 0) continue;
-      ipc::UnmapMsg um{++epoch_, static_cast<std::uint32_t>(pairs.size() / 2), 0};
+      if (sched_.granted() == app) throw InvariantViolation("the grant holder lost a physical slab");
       ipc::Writer w;
-      w.put(um);
-      w.put_u32s(pairs);
-      if (ipc::send_msg(it->second.ev, ipc::Msg::Unmap, w.buf)) waiting.push_back(app);
-      else it->second.alive = false;
+      w.put(ipc::SlabsMsg{++epoch_, static_cast<std::uint32_t>(vs.size()), 0});
+      w.put_u32s(vs);
+      if (!ipc::send_msg(it->second.ev, ipc::Msg::Unmap, w.buf)) it->second.alive = false;
     }
-    return waiting;
-  }
-
-  void collect_unmaps(const std::vector<AppId>& waiting) {
-    std::vector<std::uint8_t> body;
-    for (AppId app : waiting) wait_ack(apps_.at(app), ipc::Msg::Unmapped, body);
   }
 
   void account(const ExecResult&) {
@@ -532,9 +627,8 @@ class Daemon {
     PlannerConfig cfg = opt_.planner;
     cfg.eviction_policy.victim_order = sched_.victim_hint();
     const MigrationPlan plan = plan_switch(app, eng_.mem(), cfg);
-    const std::vector<AppId> waiting = send_unmaps(plan);
     const ExecResult r = eng_.execute(plan, cfg);
-    collect_unmaps(waiting);
+    send_unmaps();
     account(r);
     note("{\"t\": %.6f, \"event\": \"fetch_in_place\", \"app\": %u, \"bytes_in\": %" PRIu64 ", \"bytes_out\": %" PRIu64 "}",
          now(), app, plan.bytes_in, plan.bytes_out);
@@ -562,26 +656,18 @@ class Daemon {
     cfg.eviction_policy.victim_order = sched_.victim_hint();
     const MigrationPlan plan = plan_switch(to, eng_.mem(), cfg);
     const std::uint64_t t_planned = ipc::mono_ns();
-    const std::vector<AppId> waiting = send_unmaps(plan);
     const ExecResult r = eng_.execute(plan, cfg);
     const std::uint64_t t_copied = ipc::mono_ns();
-    collect_unmaps(waiting);
+    send_unmaps();
     account(r);
     const std::uint64_t t_unmapped = ipc::mono_ns();
-    // (5) grant: the incoming shim maps its frames and sets its flag.
+    // (5) grant: the incoming shim maps its slabs and sets its flag.
+    const std::vector<ipc::SlabMap> slabs = placer_.backed(to);
     ipc::Writer w;
-    const std::vector<ChunkId>& chunks = eng_.mem().chunks_of(to);
-    w.put(ipc::GrantMsg{++epoch_, static_cast<std::uint32_t>(chunks.size()), 0});
-    for (ChunkId c : chunks) {
-      const std::vector<BlockId>& blocks = eng_.mem().chunk(c).blocks;
-      w.put(static_cast<std::uint32_t>(c));
-      w.put(static_cast<std::uint32_t>(blocks.size()));
-      for (BlockId b : blocks) {
-        const std::int64_t f = eng_.frame_index(b);
-        if (f < 0) throw InvariantViolation("grant: block " + std::to_string(b) + " of app " + std::to_string(to) + " is not GPU-resident");
-        w.put(static_cast<std::uint32_t>(f));
-      }
-    }
+    w.put(ipc::SlabsMsg{++epoch_, static_cast<std::uint32_t>(slabs.size()), 0});
+    for (const auto& m : slabs) w.put(m);
+    if (!eng_.mem().app_fully_resident(to, TierId::Gpu))
+      throw InvariantViolation("grant: app " + std::to_string(to) + " is not GPU-resident after its switch");
     ipc::GrantedMsg gm{};
     if (ipc::send_msg(in.ev, ipc::Msg::Grant, w.buf) && wait_ack(in, ipc::Msg::Granted, body) && body.size() >= sizeof(gm))
       std::memcpy(&gm, body.data(), sizeof(gm));
@@ -596,12 +682,13 @@ class Daemon {
     note("{\"t\": %.6f, \"event\": \"switch\", \"from\": %d, \"to\": %u, \"bytes_in\": %" PRIu64 ", \"bytes_out\": %" PRIu64
          ", \"pcie_h2d\": %" PRIu64 ", \"pcie_d2h\": %" PRIu64 ", \"host_bytes\": %" PRIu64
          ", \"pause_ms\": %.3f, \"plan_ms\": %.3f, \"copy_ms\": %.3f, \"unmap_wait_ms\": %.3f, \"grant_ms\": %.3f"
-         ", \"map_ms\": %.3f, \"map_calls\": %" PRIu64 ", \"total_ms\": %.3f, \"device_span_ms\": %.3f"
-         ", \"verified\": %" PRIu64 ", \"unverified\": %" PRIu64 ", \"mismatches\": %" PRIu64 "}",
+         ", \"map_ms\": %.3f, \"map_calls\": %" PRIu64 ", \"unmap_calls\": %" PRIu64 ", \"total_ms\": %.3f, \"device_span_ms\": %.3f"
+         ", \"verified\": %" PRIu64 ", \"unverified\": %" PRIu64 ", \"mismatches\": %" PRIu64
+         ", \"partial_slabs\": %" PRIu64 ", \"free_slabs\": %zu}",
          t, holder ? static_cast<int>(*holder) : -1, to, plan.bytes_in, plan.bytes_out, s.pcie_h2d_bytes, s.pcie_d2h_bytes,
          s.host_bytes, ms(t_start, t_drained), ms(t_drained, t_planned), ms(t_planned, t_copied), ms(t_copied, t_unmapped),
-         ms(t_unmapped, t_end), static_cast<double>(gm.map_ns) * 1e-6, gm.map_calls, ms(t_start, t_end),
-         s.device_span_s * 1e3, s.verified, s.unverified, s.mismatches);
+         ms(t_unmapped, t_end), static_cast<double>(gm.map_ns) * 1e-6, gm.map_calls, gm.unmap_calls, ms(t_start, t_end),
+         s.device_span_s * 1e3, s.verified, s.unverified, s.mismatches, placer_.partial(), placer_.free_slabs());
   }
 
   template <typename... A>
@@ -624,6 +711,7 @@ class Daemon {
   Options opt_;
   SwapEngine eng_;
   MlfqScheduler sched_;
+  SlabPlacer placer_;
   int listen_fd_ = -1;
   std::vector<int> pending_;
   std::map<AppId, App> apps_;

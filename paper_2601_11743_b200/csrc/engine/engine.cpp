@@ -61,6 +61,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   HardwareConfig hw;
   NumaInfo numa;
   DeviceArena arena;
+  FramePlacer* placer = nullptr;
   PinnedRing pinned;
   PagedStore paged;
   HostCopyPool pool;
@@ -163,7 +164,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
     hw.tier_capacity[3] = 0;
     hw.apply_to(mem);
 
-    arena.init(cfg.gpu_capacity, cfg.exportable_arena, cfg.device);
+    arena.init(cfg.gpu_physical ? cfg.gpu_physical : cfg.gpu_capacity, cfg.exportable_arena, cfg.device, cfg.arena_slab_bytes);
     pinned.init(cfg.pinned_capacity, numa.node);
     paged.init(cfg.paged_capacity);
     pool.start(cfg.host_threads, numa.cpus);
@@ -265,6 +266,15 @@ struct SwapEngine::Impl final : detail::LaneSink {
     }
   }
 
+  std::uint32_t take_unit(TierId t, BlockId b) {
+    if (t == TierId::Gpu && placer) return placer->acquire(b);
+    return ring_of(t).acquire(tier_name(t));
+  }
+  void give_unit(TierId t, BlockId b, std::uint32_t u) {
+    if (t == TierId::Gpu && placer) return placer->release(b, u);
+    ring_of(t).release(u);
+  }
+
   // Device-visible address of a unit (GPU frame or mapped pinned slot).
   void* dev_addr(TierId t, std::uint32_t u) {
     if (t == TierId::Gpu) return arena.frame(u);
@@ -285,9 +295,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
     const std::size_t last = mem.block_count();
     grow_tables(last);
     unit.resize(last);
-    UnitRing& ring = ring_of(tier);
     for (std::size_t b = first; b < last; ++b) {
-      unit[b] = ring.acquire(tier_name(tier));
+      unit[b] = take_unit(tier, b);
       h_frames[b] = tier == TierId::Gpu ? reinterpret_cast<std::uint64_t>(arena.frame(unit[b])) : 0;
     }
     if (tier == TierId::PagedHost)  // touch now, not inside a timed switch
@@ -303,7 +312,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
       for (BlockId b : mem.chunk(c).blocks) where.emplace_back(b, mem.block(b).loc.tier);
     const Bytes released = mem.free_chunk(app, c);  // throws before any physical change
     for (auto [b, t] : where) {
-      ring_of(t).release(unit[b]);
+      give_unit(t, b, unit[b]);
       h_frames[b] = 0;
     }
     return released;
@@ -408,7 +417,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   // ---- lane sink ----------------------------------------------------------
   void leg_started(int lane, std::size_t mi, TierId from, TierId to, bool) override {
     const BlockId b = lanes->move(mi).block;
-    Leg L{mi, b, from, to, unit[b], ring_of(to).acquire(tier_name(to)), lane, false, secs_since(t0), 0};
+    Leg L{mi, b, from, to, unit[b], take_unit(to, b), lane, false, secs_since(t0), 0};
     const auto idx = static_cast<std::uint32_t>(legs.size());
     legs.push_back(L);
     trace[lane].push_back(LegTrace{b, from, to});
@@ -586,7 +595,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   void complete(std::uint32_t idx) {
     Leg& L = legs[idx];
     L.done = true;
-    ring_of(L.from).release(L.src_u);
+    give_unit(L.from, L.block, L.src_u);
     unit[L.block] = L.dst_u;
     if (L.from == TierId::Gpu) h_frames[L.block] = 0;
     if (records) {
@@ -837,8 +846,11 @@ std::int64_t SwapEngine::frame_index(BlockId b) const {
   return impl_->unit[b];
 }
 
-int SwapEngine::arena_export_fd(std::uint32_t frame) const {
-  const int fd = impl_->arena.export_fd(frame);
+std::uint32_t SwapEngine::arena_frames() const { return impl_->arena.ring.units(); }
+void SwapEngine::set_frame_placer(FramePlacer* placer) { impl_->placer = placer; }
+
+int SwapEngine::arena_export_fd(std::uint32_t slab) const {
+  const int fd = impl_->arena.export_fd(slab);
   if (fd < 0) throw SimError(Err::InvalidState, "the arena is not exportable (EngineConfig::exportable_arena)");
   return fd;
 }

@@ -99,12 +99,12 @@ void pin_thread_to(const std::vector<int>& cpus) {
   pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
 }
 
-void DeviceArena::init(Bytes capacity, bool exportable, int device) {
+void DeviceArena::init(Bytes capacity, bool exportable, int device, Bytes slab_bytes) {
   const auto units = static_cast<std::uint32_t>(capacity / kBlockBytes);
   if (units > 0) {
     if (exportable) {
       vmm_ = new ExportableArena();
-      vmm_->init(device, static_cast<Bytes>(units) * kBlockBytes);
+      vmm_->init(device, static_cast<Bytes>(units) * kBlockBytes, slab_bytes ? slab_bytes : kBlockBytes);
       base_ = vmm_->base();
     } else {
       NX_CUDA(cudaMalloc(&base_, static_cast<std::size_t>(units) * kBlockBytes));
@@ -121,7 +121,7 @@ DeviceArena::~DeviceArena() {
   }
 }
 
-int DeviceArena::export_fd(std::uint32_t frame) const { return vmm_ ? vmm_->export_fd(frame) : -1; }
+int DeviceArena::export_fd(std::uint32_t slab) const { return vmm_ ? vmm_->export_fd(slab) : -1; }
 
 void PinnedRing::init(Bytes capacity, int numa_node) {
   const auto units = static_cast<std::uint32_t>(capacity / kBlockBytes);

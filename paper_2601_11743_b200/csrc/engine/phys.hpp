@@ -73,11 +73,11 @@ class ExportableArena;
 // to map frames at their applications' stable virtual addresses (vmm.hpp).
 class DeviceArena {
  public:
-  void init(Bytes capacity, bool exportable = false, int device = 0);
+  void init(Bytes capacity, bool exportable = false, int device = 0, Bytes slab_bytes = 0);
   ~DeviceArena();
   std::uint8_t* frame(std::uint32_t u) const { return base_ + static_cast<std::size_t>(u) * kBlockBytes; }
   std::uint8_t* base() const { return base_; }
-  int export_fd(std::uint32_t frame) const;  // -1 unless exportable
+  int export_fd(std::uint32_t slab) const;  // -1 unless exportable
   UnitRing ring;
 
  private:

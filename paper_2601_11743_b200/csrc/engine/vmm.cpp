@@ -47,7 +47,7 @@ const VmmApi& vmm_api() {
   return api;
 }
 
-void ExportableArena::init(int device, Bytes bytes) {
+void ExportableArena::init(int device, Bytes bytes, Bytes slab_bytes) {
   const VmmApi& v = vmm_api();
   NX_CUDA(cudaFree(nullptr));  // the primary context is current on this thread
   CUmemAllocationProp prop{};
@@ -59,13 +59,16 @@ void ExportableArena::init(int device, Bytes bytes) {
   check(v.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM), "cuMemGetAllocationGranularity");
   if (gran == 0 || kBlockBytes % gran != 0)
     throw CudaFailure("VMM granularity " + std::to_string(gran) + " does not divide the 2 MiB frame");
-  bytes_ = bytes / kBlockBytes * kBlockBytes;
-  const auto n = static_cast<std::uint32_t>(bytes_ / kBlockBytes);
-  check(v.addr_reserve(&va_, bytes_, kBlockBytes, 0, 0), "cuMemAddressReserve(arena)");
+  if (slab_bytes == 0 || slab_bytes % kBlockBytes || bytes % slab_bytes)
+    throw SimError(Err::ValidationError, "exportable arena: bytes must be a multiple of the slab, the slab of 2 MiB");
+  slab_ = slab_bytes;
+  bytes_ = bytes;
+  const auto n = static_cast<std::uint32_t>(bytes_ / slab_);
+  check(v.addr_reserve(&va_, bytes_, slab_, 0, 0), "cuMemAddressReserve(arena)");
   handles_.resize(n, 0);
   for (std::uint32_t f = 0; f < n; ++f) {
-    check(v.mem_create(&handles_[f], kBlockBytes, &prop, 0), "cuMemCreate(exportable frame)");
-    check(v.map(va_ + static_cast<CUdeviceptr>(f) * kBlockBytes, kBlockBytes, 0, handles_[f], 0), "cuMemMap(frame)");
+    check(v.mem_create(&handles_[f], slab_, &prop, 0), "cuMemCreate(exportable slab)");
+    check(v.map(va_ + static_cast<CUdeviceptr>(f) * slab_, slab_, 0, handles_[f], 0), "cuMemMap(slab)");
     mapped_ = f + 1;
   }
   CUmemAccessDesc acc{};
@@ -78,14 +81,14 @@ void ExportableArena::init(int device, Bytes bytes) {
 ExportableArena::~ExportableArena() {
   if (!va_) return;
   const VmmApi& v = vmm_api();
-  for (std::uint32_t f = 0; f < mapped_; ++f) v.unmap(va_ + static_cast<CUdeviceptr>(f) * kBlockBytes, kBlockBytes);
+  for (std::uint32_t f = 0; f < mapped_; ++f) v.unmap(va_ + static_cast<CUdeviceptr>(f) * slab_, slab_);
   for (CUmemGenericAllocationHandle h : handles_)
     if (h) v.mem_release(h);
   v.addr_free(va_, bytes_);
 }
 
 int ExportableArena::export_fd(std::uint32_t f) const {
-  if (f >= handles_.size()) throw SimError(Err::InvalidState, "export of frame " + std::to_string(f) + " out of range");
+  if (f >= handles_.size()) throw SimError(Err::InvalidState, "export of slab " + std::to_string(f) + " out of range");
   int fd = -1;
   check(vmm_api().export_handle(&fd, handles_[f], CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0), "cuMemExportToShareableHandle");
   return fd;

@@ -41,25 +41,30 @@ struct VmmApi {
 // Resolved once; throws CudaFailure when an entry point is missing.
 const VmmApi& vmm_api();
 
-// The GPU tier as exportable 2 MiB physical allocations (one per frame:
-// cuMemMap maps a handle only from offset 0, so a frame that must be mapped on
-// its own at an application's address needs its own handle), mapped
-// contiguously at a fresh virtual range of this process.
+// The GPU tier as a row of exportable physical slabs (cuMemMap maps a handle
+// only from offset 0, so whatever an application maps on its own must be its
+// own allocation), mapped contiguously at a fresh virtual range of this
+// process. On the pool's B200s the driver charges ~0.1-0.4 ms of
+// cuMemSetAccess and ~0.08 ms of cuMemUnmap per mapping whatever its size,
+// and 5-7 ms to export/import a handle (tools/vmm_probe.cu,
+// profiles/r01_vmm_probe.txt), so slabs are large (128 MiB = 64 frames).
 class ExportableArena {
  public:
-  void init(int device, Bytes bytes);
+  void init(int device, Bytes bytes, Bytes slab_bytes);
   ~ExportableArena();
   std::uint8_t* base() const { return reinterpret_cast<std::uint8_t*>(va_); }
   Bytes bytes() const { return bytes_; }
-  std::uint32_t frames() const { return static_cast<std::uint32_t>(handles_.size()); }
-  // A new descriptor for frame `f`'s physical allocation (the caller owns
+  std::uint32_t slabs() const { return static_cast<std::uint32_t>(handles_.size()); }
+  Bytes slab_bytes() const { return slab_; }
+  // A new descriptor for slab `s`'s physical allocation (the caller owns
   // it; it is sent to a shim with SCM_RIGHTS and closed).
-  int export_fd(std::uint32_t f) const;
+  int export_fd(std::uint32_t s) const;
 
  private:
   std::vector<CUmemGenericAllocationHandle> handles_;
   CUdeviceptr va_ = 0;
   Bytes bytes_ = 0;
+  Bytes slab_ = 0;
   std::uint32_t mapped_ = 0;
 };
 

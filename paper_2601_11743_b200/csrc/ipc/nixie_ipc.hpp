@@ -40,20 +40,33 @@ constexpr std::uint32_t kNoFrame = 0xFFFFFFFFu;
 constexpr int kFdBatch = 250;  // SCM_RIGHTS carries at most 253 descriptors
 
 enum class Msg : std::uint32_t {
-  Hello = 1,     // rpc  shim->d : HelloReq            reply HelloRep, fd [ctl], then the frames'
-                 //                                     fds in batches of kFdBatch (frame order)
-  EventHello,    // event shim->d: EventHelloReq       (no reply)
-  Alloc,         // rpc  shim->d : AllocReq            reply AllocRep + u32 chunk ids + u32 frames (one per block)
-  Free,          // rpc  shim->d : u32 n + u32 chunk ids; reply Status
-  Acquire,       // rpc  shim->d : (empty)             reply Status (queued; Grant follows on the event socket)
+  Hello = 1,     // rpc  shim->d : HelloReq   reply HelloRep, fd [ctl], then the arena slabs' fds in
+                 //                            batches of kFdBatch (slab order)
+  EventHello,    // event shim->d: EventHelloReq (no reply)
+  Alloc,         // rpc  shim->d : AllocReq   reply AllocRep + u32 chunk ids + SlabMap[n_slabs]
+  Free,          // rpc  shim->d : u32 n + u32 chunk ids; reply FreeRep + u32 released vslabs
+  Acquire,       // rpc  shim->d : (empty)    reply Status (queued; a Grant follows on the event socket)
   Status,        // reply: StatusRep
-  Pause,         // event d->shim: EpochMsg  -> shim stops launches, drains, acks Drained
+  Pause,         // event d->shim: EpochMsg -> shim stops launches, drains, acks Drained
   Drained,       // event shim->d: EpochMsg
-  Unmap,         // event d->shim: UnmapMsg + (u32 chunk, u32 block index) pairs -> ack Unmapped
-  Unmapped,      // event shim->d: EpochMsg
-  Grant,         // event d->shim: GrantMsg + per chunk {u32 chunk, u32 n, u32 frames[n]} -> ack Granted
+  Unmap,         // event d->shim: SlabsMsg + u32 vslabs (their physical slab was released; no ack)
+  Grant,         // event d->shim: SlabsMsg + SlabMap[n] (every mapped vslab of the app) -> ack Granted
   Granted,       // event shim->d: GrantedMsg
-  Stats,         // rpc  shim->d : (empty) reply StatsRep
+  Stats,         // rpc  shim->d : (empty)    reply StatsRep
+};
+
+// Virtual slabs: a shim reserves one large virtual range and places its
+// managed allocations in it at 2 MiB granularity; vslab k is the 128 MiB
+// (kSlabBlocks frames) window k of that range. The daemon backs every vslab
+// that holds a GPU-resident block with one physical slab of its arena, so the
+// shim maps whole slabs (one mapping per 64 blocks), and block j of an
+// allocation placed at range block v lives in frame phys * kSlabBlocks +
+// (v + j) % kSlabBlocks.
+constexpr std::uint32_t kSlabBlocks = 64;
+
+struct SlabMap {
+  std::uint32_t vslab;
+  std::uint32_t phys;  // kNoFrame: not backed
 };
 
 struct Header {
@@ -72,8 +85,9 @@ struct HelloRep {
   std::uint32_t app;
   std::uint64_t gpu_budget;    // bytes the app may see as device memory (cudaMemGetInfo total)
   std::uint64_t block_bytes;   // 2 MiB
-  std::uint64_t arena_bytes;   // GPU tier bytes (frames x 2 MiB)
-  std::uint64_t frames;        // exported frame allocations that follow
+  std::uint64_t arena_bytes;   // physical bytes of the arena (slabs x slab_bytes)
+  std::uint64_t slabs;         // exported slab allocations that follow
+  std::uint64_t slab_bytes;
   std::uint64_t min_bytes;     // allocations below this pass through to cudaMalloc
   std::int32_t device;
   std::int32_t pad;
@@ -84,11 +98,12 @@ struct EventHelloReq {
 };
 struct AllocReq {
   std::uint64_t bytes;
+  std::uint64_t va_block;  // placement in the shim's range, in 2 MiB blocks
 };
 struct AllocRep {
   std::int32_t status;  // 0 ok, 2 out of memory, other: SimError code + 100
   std::uint32_t n_chunks;
-  std::uint32_t n_blocks;
+  std::uint32_t n_slabs;  // SlabMap entries that follow the chunk ids
   std::uint32_t pad;
   std::uint64_t footprint;  // bytes charged (2 MiB rounded)
   std::uint64_t epoch;      // daemon message sequence at reply time (orders it
@@ -101,20 +116,21 @@ struct StatusRep {
 struct EpochMsg {
   std::uint64_t epoch;
 };
-struct UnmapMsg {
+struct SlabsMsg {
   std::uint64_t epoch;
-  std::uint32_t n;  // (chunk, block-in-chunk) pairs
+  std::uint32_t n;
   std::uint32_t pad;
 };
-struct GrantMsg {
+struct FreeRep {
+  std::int32_t status;
+  std::uint32_t n;  // released vslabs that follow
   std::uint64_t epoch;
-  std::uint32_t n_chunks;
-  std::uint32_t pad;
 };
 struct GrantedMsg {
   std::uint64_t epoch;
   std::uint64_t map_ns;       // shim-side mapping time
   std::uint64_t map_calls;    // cuMemMap calls made
+  std::uint64_t unmap_calls;  // cuMemUnmap calls made
 };
 struct StatsRep {
   std::uint64_t switches;

@@ -6,10 +6,10 @@
 // launches ... APIs that implicitly allocate memory ... memory usage"):
 //   cudaMalloc / cudaFree, cuMemAlloc_v2 / cuMemFree_v2
 //       allocations >= min_bytes (2 MiB) become daemon chunks: the shim
-//       reserves a stable virtual range (cuMemAddressReserve) and maps the
-//       daemon's arena frames under it (each frame is a 2 MiB physical
-//       allocation the shim imported once at start-up) whenever the blocks
-//       are GPU-resident; smaller
+//       are placed in a virtual range the shim reserved once (stable
+//       addresses); every 128 MiB virtual slab of it that holds GPU-resident
+//       blocks is mapped to one physical slab of the daemon's arena (imported
+//       once at start-up), so a restore costs one mapping per 64 blocks; smaller
 //       ones pass through. Reference registry anchor:
 //       MemState::allocate / free_chunk (proj/src/mem_model.cpp:48-116),
 //       Chunk::logical_base (proj/include/nixie/mem_model.hpp:72).
@@ -18,7 +18,7 @@
 //   cudaMemcpy[Async], cudaMemcpy2D[Async], cudaMemset[Async]
 //       the launch gate (PAPER.md:116 steps 1-2 and 6): pass while the
 //       execution flag is set; otherwise ask the daemon (Acquire) and hold
-//       the calling thread until a Grant has mapped the app's frames.
+//       the calling thread until a Grant has mapped the app's slabs.
 //   cudaDeviceSynchronize, cudaStreamSynchronize, cudaEventSynchronize,
 //   cudaMemcpy (sync)
 //       blocking-call brackets for the MLFQ's idleness test (§6.1).
@@ -32,7 +32,7 @@
 //
 // The shim never copies application data: the daemon's swap engine moves
 // every byte (both PCIe directions at once) through its own mapping of the
-// same physical frames; the shim only maps, unmaps and gates.
+// same physical slabs; the shim only maps, unmaps and gates.
 #include <cuda.h>
 #include <cuda_runtime_api.h>
 #include <dlfcn.h>
@@ -147,17 +147,16 @@ void die(const char* what, CUresult r = CUDA_SUCCESS) {
 }
 
 // ---- state ----------------------------------------------------------------------
-struct ChunkMap {
-  CUdeviceptr va = 0;                 // 0 until the allocating thread registers it
-  std::uint32_t nblocks = 0;
-  std::uint64_t epoch = 0;            // newest daemon message applied to `want`
-  std::vector<std::uint32_t> want;    // desired frame per block (kNoFrame = not on the GPU)
-  std::vector<std::uint32_t> have;    // frame mapped at each block now
+// A virtual slab (ipc::kSlabBlocks x 2 MiB window of the shim's range) and
+// the physical arena slab mapped under it.
+struct VSlab {
+  std::uint32_t want = ipc::kNoFrame;  // physical slab the daemon placed it on (kNoFrame: none)
+  std::uint32_t have = ipc::kNoFrame;  // physical slab mapped now
+  std::uint64_t epoch = 0;             // newest daemon message applied to `want`
 };
 
 struct Region {
-  CUdeviceptr va = 0;
-  std::uint64_t reserved = 0;  // 2 MiB rounded
+  std::uint64_t first = 0, blocks = 0;  // placement in the range, 2 MiB blocks
   std::vector<std::uint32_t> chunks;
 };
 
@@ -165,18 +164,20 @@ struct Shim {
   bool active = false;
   int device = 0;
   std::uint32_t app = 0;
-  std::uint64_t budget = 0, min_bytes = kBlock;
+  std::uint64_t budget = 0, min_bytes = kBlock, slab_bytes = 0;
   int rpc = -1, ev = -1;
   ipc::CtlPage* ctl = nullptr;
-  std::vector<CUmemGenericAllocationHandle> frames;  // imported arena frames
+  std::vector<CUmemGenericAllocationHandle> slabs;  // imported arena slabs
   CUcontext ctx = nullptr;
+  CUdeviceptr range = 0;          // reserved once; managed allocations live here
+  std::uint64_t range_blocks = 0;
 
   std::mutex rpc_mu;            // one request in flight on the rpc socket
-  std::mutex mu;                // regions, chunks, granted (slow paths)
+  std::mutex mu;                // everything below (slow paths only)
   std::condition_variable cv;
+  std::map<std::uint64_t, std::uint64_t> free_runs;  // range blocks: start -> length
   std::map<CUdeviceptr, Region> regions;
-  std::unordered_map<std::uint32_t, ChunkMap> chunks;
-  std::unordered_set<std::uint32_t> dead_chunks;
+  std::unordered_map<std::uint32_t, VSlab> vslabs;
   std::map<void*, std::size_t> small;  // passthrough allocations (for cudaMemGetInfo)
   std::uint64_t managed_bytes = 0, small_bytes = 0;
 
@@ -184,6 +185,8 @@ struct Shim {
   std::atomic<int> inflight{0};
   std::atomic<int> capturing{0};
 };
+
+constexpr std::uint64_t kRangeBytes = 1ull << 40;  // 1 TiB of virtual space per process
 
 // Never destroyed: the listener thread may still run while the process exits.
 Shim& g = *new Shim;
@@ -250,17 +253,25 @@ void init_once() {
   g.app = rep.app;
   g.budget = rep.gpu_budget;
   g.min_bytes = rep.min_bytes;
-  g.frames.resize(rep.frames, 0);
+  g.slab_bytes = rep.slab_bytes;
+  if (g.slab_bytes != ipc::kSlabBlocks * kBlock) die("the daemon's slab size differs from this shim's");
+  g.slabs.resize(rep.slabs, 0);
   std::vector<int> fds(ipc::kFdBatch);
-  for (std::uint64_t f = 0; f < rep.frames; f += ipc::kFdBatch) {
-    const int n = static_cast<int>(std::min<std::uint64_t>(ipc::kFdBatch, rep.frames - f));
-    if (!ipc::recv_fds(g.rpc, fds.data(), n)) die("receiving the arena's frame descriptors");
+  for (std::uint64_t f = 0; f < rep.slabs; f += ipc::kFdBatch) {
+    const int n = static_cast<int>(std::min<std::uint64_t>(ipc::kFdBatch, rep.slabs - f));
+    if (!ipc::recv_fds(g.rpc, fds.data(), n)) die("receiving the arena's slab descriptors");
     for (int k = 0; k < n; ++k) {
-      const CUresult r = drv().import_handle(&g.frames[f + k], reinterpret_cast<void*>(static_cast<std::uintptr_t>(fds[k])),
+      const CUresult r = drv().import_handle(&g.slabs[f + k], reinterpret_cast<void*>(static_cast<std::uintptr_t>(fds[k])),
                                              CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
-      if (r != CUDA_SUCCESS) die("cuMemImportFromShareableHandle(frame)", r);
+      if (r != CUDA_SUCCESS) die("cuMemImportFromShareableHandle(slab)", r);
       ::close(fds[k]);
     }
+  }
+  {
+    const CUresult r = drv().addr_reserve(&g.range, kRangeBytes, g.slab_bytes, 0, 0);
+    if (r != CUDA_SUCCESS) die("cuMemAddressReserve(range)", r);
+    g.range_blocks = kRangeBytes / kBlock;
+    g.free_runs[0] = g.range_blocks;
   }
   void* p = ::mmap(nullptr, 4096, PROT_READ | PROT_WRITE, MAP_SHARED, ctl_fd, 0);
   if (p == MAP_FAILED) die("mmap control page");
@@ -288,57 +299,44 @@ CUmemAccessDesc access_desc() {
   return a;
 }
 
-// Makes the chunk's mappings equal `want` (caller holds g.mu): one cuMemMap
-// per 2 MiB block (each frame is its own physical allocation) and one
-// cuMemSetAccess per run of newly mapped blocks. Returns cuMemMap calls made.
-std::uint64_t sync_chunk(ChunkMap& c) {
-  if (!c.va) return 0;
+// Makes vslab v's mapping equal `want` (caller holds g.mu): one cuMemUnmap
+// and/or one cuMemMap + cuMemSetAccess of a whole slab.
+void sync_vslab(std::uint32_t v, VSlab& s, std::uint64_t& maps, std::uint64_t& unmaps) {
+  if (s.have == s.want) return;
   ensure_ctx();
-  c.have.resize(c.nblocks, ipc::kNoFrame);
+  const CUdeviceptr va = g.range + static_cast<CUdeviceptr>(v) * g.slab_bytes;
   const std::uint64_t t0 = ipc::mono_ns();
-  for (std::uint32_t i = 0; i < c.nblocks; ++i) {
-    if (c.have[i] == ipc::kNoFrame || c.have[i] == c.want[i]) continue;
-    const CUresult e = drv().unmap(c.va + i * kBlock, kBlock);
+  if (s.have != ipc::kNoFrame) {
+    const CUresult e = drv().unmap(va, g.slab_bytes);
     if (e != CUDA_SUCCESS) die("cuMemUnmap", e);
-    c.have[i] = ipc::kNoFrame;
+    s.have = ipc::kNoFrame;
+    ++unmaps;
   }
   const std::uint64_t t1 = ipc::mono_ns();
-  std::uint64_t calls = 0;
-  const CUmemAccessDesc acc = access_desc();
-  for (std::uint32_t i = 0; i < c.nblocks;) {
-    if (c.want[i] == ipc::kNoFrame || c.have[i] == c.want[i]) {
-      ++i;
-      continue;
-    }
-    std::uint32_t n = 0;
-    while (i + n < c.nblocks && c.want[i + n] != ipc::kNoFrame && c.have[i + n] == ipc::kNoFrame) {
-      const std::uint32_t f = c.want[i + n];
-      if (f >= g.frames.size()) die("grant names a frame outside the arena");
-      const CUresult e = drv().map(c.va + (i + n) * kBlock, kBlock, 0, g.frames[f], 0);
-      if (e != CUDA_SUCCESS) die("cuMemMap", e);
-      c.have[i + n] = f;
-      ++n;
-      ++calls;
-    }
-    const CUresult e = drv().set_access(c.va + i * kBlock, static_cast<size_t>(n) * kBlock, &acc, 1);
+  if (s.want != ipc::kNoFrame) {
+    if (s.want >= g.slabs.size()) die("the daemon named a slab outside the arena");
+    CUresult e = drv().map(va, g.slab_bytes, 0, g.slabs[s.want], 0);
+    if (e != CUDA_SUCCESS) die("cuMemMap", e);
+    const CUmemAccessDesc acc = access_desc();
+    e = drv().set_access(va, g.slab_bytes, &acc, 1);
     if (e != CUDA_SUCCESS) die("cuMemSetAccess", e);
-    i += n;
+    s.have = s.want;
+    ++maps;
   }
   const std::uint64_t t2 = ipc::mono_ns();
   if (g.ctl) {
     g.ctl->unmap_ns.fetch_add(t1 - t0, std::memory_order_relaxed);
     g.ctl->map_ns.fetch_add(t2 - t1, std::memory_order_relaxed);
   }
-  return calls;
 }
 
-ChunkMap& chunk_entry(std::uint32_t id, std::uint32_t nblocks) {
-  ChunkMap& c = g.chunks[id];
-  if (c.want.size() < nblocks) {
-    c.nblocks = nblocks;
-    c.want.resize(nblocks, ipc::kNoFrame);
-  }
-  return c;
+// Applies a daemon placement if it is newer than what the vslab has seen.
+void place(std::uint32_t v, std::uint32_t phys, std::uint64_t epoch, std::uint64_t& maps, std::uint64_t& unmaps) {
+  VSlab& s = g.vslabs[v];
+  if (epoch <= s.epoch) return;
+  s.want = phys;
+  s.epoch = epoch;
+  sync_vslab(v, s, maps, unmaps);
 }
 
 // ---- event socket: Pause / Unmap / Grant ----------------------------------------------
@@ -360,53 +358,33 @@ void on_pause(const std::vector<std::uint8_t>& body) {
 
 void on_unmap(const std::vector<std::uint8_t>& body) {
   ipc::Reader r{body};
-  const auto m = r.get<ipc::UnmapMsg>();
-  {
-    std::lock_guard<std::mutex> lk(g.mu);
-    std::unordered_map<std::uint32_t, bool> touched;
-    for (std::uint32_t i = 0; i < m.n && r.ok; ++i) {
-      const auto chunk = r.get<std::uint32_t>();
-      const auto blk = r.get<std::uint32_t>();
-      if (g.dead_chunks.count(chunk)) continue;
-      ChunkMap& c = chunk_entry(chunk, blk + 1);
-      if (m.epoch <= c.epoch) continue;
-      c.want[blk] = ipc::kNoFrame;
-      touched[chunk] = true;
-    }
-    for (auto& kv : touched) {
-      ChunkMap& c = g.chunks[kv.first];
-      c.epoch = m.epoch;
-      sync_chunk(c);
-    }
-  }
-  ipc::EpochMsg ack{m.epoch};
-  ipc::send_msg(g.ev, ipc::Msg::Unmapped, &ack, sizeof(ack));
+  const auto m = r.get<ipc::SlabsMsg>();
+  std::uint64_t maps = 0, unmaps = 0;
+  std::lock_guard<std::mutex> lk(g.mu);
+  for (std::uint32_t i = 0; i < m.n && r.ok; ++i) place(r.get<std::uint32_t>(), ipc::kNoFrame, m.epoch, maps, unmaps);
 }
 
 void on_grant(const std::vector<std::uint8_t>& body) {
   ipc::Reader r{body};
-  const auto m = r.get<ipc::GrantMsg>();
+  const auto m = r.get<ipc::SlabsMsg>();
   const std::uint64_t t0 = ipc::mono_ns();
-  std::uint64_t calls = 0;
+  std::uint64_t maps = 0, unmaps = 0;
   {
     std::lock_guard<std::mutex> lk(g.mu);
-    for (std::uint32_t k = 0; k < m.n_chunks && r.ok; ++k) {
-      const auto id = r.get<std::uint32_t>();
-      const auto n = r.get<std::uint32_t>();
-      std::vector<std::uint32_t> frames(n);
-      for (auto& f : frames) f = r.get<std::uint32_t>();
-      if (g.dead_chunks.count(id)) continue;
-      ChunkMap& c = chunk_entry(id, n);
-      if (m.epoch <= c.epoch) continue;
-      c.want = frames;
-      c.epoch = m.epoch;
-      calls += sync_chunk(c);
+    std::unordered_set<std::uint32_t> listed;
+    for (std::uint32_t k = 0; k < m.n && r.ok; ++k) {
+      const auto sm = r.get<ipc::SlabMap>();
+      listed.insert(sm.vslab);
+      place(sm.vslab, sm.phys, m.epoch, maps, unmaps);
     }
+    // The grant lists every backed vslab of the app: anything else is stale.
+    for (auto& [v, st] : g.vslabs)
+      if (!listed.count(v) && st.have != ipc::kNoFrame && m.epoch > st.epoch) place(v, ipc::kNoFrame, m.epoch, maps, unmaps);
     g.granted.store(true, std::memory_order_seq_cst);
     if (g.ctl) g.ctl->granted.store(1);
   }
   g.cv.notify_all();
-  ipc::GrantedMsg ack{m.epoch, ipc::mono_ns() - t0, calls};
+  ipc::GrantedMsg ack{m.epoch, ipc::mono_ns() - t0, maps, unmaps};
   ipc::send_msg(g.ev, ipc::Msg::Granted, &ack, sizeof(ack));
 }
 
@@ -515,63 +493,82 @@ struct Blocking {
 };
 
 // ---- allocation -------------------------------------------------------------------------
+// First fit in the range (caller holds g.mu); allocations of 64 MiB or more
+// start on a slab boundary so they do not straddle more slabs than needed.
+bool take_range(std::uint64_t n, std::uint64_t& start) {
+  const std::uint64_t align = n >= ipc::kSlabBlocks / 2 ? ipc::kSlabBlocks : 1;
+  for (auto it = g.free_runs.begin(); it != g.free_runs.end(); ++it) {
+    const std::uint64_t s0 = (it->first + align - 1) / align * align;
+    if (s0 + n > it->first + it->second) continue;
+    const std::uint64_t run_start = it->first, run_len = it->second;
+    g.free_runs.erase(it);
+    if (s0 > run_start) g.free_runs[run_start] = s0 - run_start;
+    if (s0 + n < run_start + run_len) g.free_runs[s0 + n] = run_start + run_len - (s0 + n);
+    start = s0;
+    return true;
+  }
+  return false;
+}
+
+void give_range(std::uint64_t start, std::uint64_t n) {
+  auto next = g.free_runs.lower_bound(start);
+  if (next != g.free_runs.end() && start + n == next->first) {
+    n += next->second;
+    next = g.free_runs.erase(next);
+  }
+  if (next != g.free_runs.begin()) {
+    auto prev = std::prev(next);
+    if (prev->first + prev->second == start) {
+      prev->second += n;
+      return;
+    }
+  }
+  g.free_runs[start] = n;
+}
+
 int managed_alloc(void** out, std::size_t bytes) {
-  const std::uint64_t reserved = (bytes + kBlock - 1) / kBlock * kBlock;
-  ensure_ctx();
-  CUdeviceptr va = 0;
-  CUresult e = drv().addr_reserve(&va, reserved, kBlock, 0, 0);
-  if (e != CUDA_SUCCESS) return 2;
-  ipc::AllocReq req{bytes};
+  const std::uint64_t n = (bytes + kBlock - 1) / kBlock;
+  std::uint64_t first = 0;
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    if (!take_range(n, first)) return 2;
+  }
+  ipc::AllocReq req{bytes, first};
   ipc::Msg rt;
   std::vector<std::uint8_t> body;
   if (!rpc(ipc::Msg::Alloc, &req, sizeof(req), rt, body) || rt != ipc::Msg::Alloc || body.size() < sizeof(ipc::AllocRep))
     die("alloc: daemon connection lost");
   ipc::Reader r{body};
   const auto rep = r.get<ipc::AllocRep>();
+  std::lock_guard<std::mutex> lk(g.mu);
   if (rep.status != 0) {
-    drv().addr_free(va, reserved);
+    give_range(first, n);
     return 2;
   }
-  std::vector<std::uint32_t> ids(rep.n_chunks), frames(rep.n_blocks);
-  for (auto& x : ids) x = r.get<std::uint32_t>();
-  for (auto& x : frames) x = r.get<std::uint32_t>();
-  {
-    std::lock_guard<std::mutex> lk(g.mu);
-    Region reg{va, reserved, ids};
-    // MemState::allocate splits a request into <= 128 MiB chunks of 2 MiB
-    // blocks, in order (proj/src/mem_model.cpp:48-86): chunk k covers the
-    // next blocks of the range.
-    std::uint32_t off = 0;
-    const std::uint64_t per_chunk = 64;  // kChunkMaxBytes / kBlockBytes
-    const auto total = static_cast<std::uint32_t>(reserved / kBlock);
-    if (frames.size() != total) die("alloc: the daemon's block count differs from the reserved range");
-    for (std::uint32_t id : ids) {
-      const auto n = static_cast<std::uint32_t>(std::min<std::uint64_t>(per_chunk, total - off));
-      ChunkMap& c = chunk_entry(id, n);
-      c.va = va + static_cast<CUdeviceptr>(off) * kBlock;
-      if (rep.epoch > c.epoch) {
-        c.want.assign(frames.begin() + off, frames.begin() + off + n);
-        c.epoch = rep.epoch;
-      }
-      sync_chunk(c);
-      off += n;
-    }
-    g.regions[va] = reg;
-    g.managed_bytes += reserved;
+  Region reg{first, n, {}};
+  for (std::uint32_t k = 0; k < rep.n_chunks; ++k) reg.chunks.push_back(r.get<std::uint32_t>());
+  std::uint64_t maps = 0, unmaps = 0;
+  for (std::uint32_t k = 0; k < rep.n_slabs && r.ok; ++k) {
+    const auto sm = r.get<ipc::SlabMap>();
+    place(sm.vslab, sm.phys, rep.epoch, maps, unmaps);
   }
+  const CUdeviceptr va = g.range + first * kBlock;
+  g.regions[va] = reg;
+  g.managed_bytes += n * kBlock;
   *out = reinterpret_cast<void*>(va);
   return 0;
 }
 
-// Returns true if `p` was a managed range (and frees it).
+// Returns true if `p` was a managed allocation (and frees it).
 bool managed_free(void* p) {
   const auto va = reinterpret_cast<CUdeviceptr>(p);
-  std::vector<std::uint32_t> ids;
+  Region reg;
   {
     std::lock_guard<std::mutex> lk(g.mu);
     auto it = g.regions.find(va);
     if (it == g.regions.end()) return false;
-    ids = it->second.chunks;
+    reg = it->second;
+    g.regions.erase(it);
   }
   if (g.granted.load()) {  // cudaFree's implicit synchronisation
     REAL(cudaDeviceSynchronize);
@@ -579,27 +576,20 @@ bool managed_free(void* p) {
     real_cudaDeviceSynchronize();
     t_in_shim--;
   }
-  {
-    std::lock_guard<std::mutex> lk(g.mu);
-    auto it = g.regions.find(va);
-    if (it == g.regions.end()) return true;
-    for (std::uint32_t id : ids) {
-      ChunkMap& c = g.chunks[id];
-      std::fill(c.want.begin(), c.want.end(), ipc::kNoFrame);
-      sync_chunk(c);
-      g.chunks.erase(id);
-      g.dead_chunks.insert(id);
-    }
-    drv().addr_free(va, it->second.reserved);
-    g.managed_bytes -= it->second.reserved;
-    g.regions.erase(it);
-  }
   ipc::Writer w;
-  w.put(static_cast<std::uint32_t>(ids.size()));
-  w.put_u32s(ids);
+  w.put(static_cast<std::uint32_t>(reg.chunks.size()));
+  w.put_u32s(reg.chunks);
   ipc::Msg rt;
   std::vector<std::uint8_t> body;
-  if (!rpc(ipc::Msg::Free, w.buf.data(), w.buf.size(), rt, body)) die("free: daemon connection lost");
+  if (!rpc(ipc::Msg::Free, w.buf.data(), w.buf.size(), rt, body) || rt != ipc::Msg::Free || body.size() < sizeof(ipc::FreeRep))
+    die("free: daemon connection lost");
+  ipc::Reader r{body};
+  const auto rep = r.get<ipc::FreeRep>();
+  std::lock_guard<std::mutex> lk(g.mu);
+  std::uint64_t maps = 0, unmaps = 0;
+  for (std::uint32_t k = 0; k < rep.n && r.ok; ++k) place(r.get<std::uint32_t>(), ipc::kNoFrame, rep.epoch, maps, unmaps);
+  give_range(reg.first, reg.blocks);
+  g.managed_bytes -= reg.blocks * kBlock;
   return true;
 }
 
