@@ -20,6 +20,7 @@
 
 #include <array>
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -184,6 +185,10 @@ class SwapEngine {
   std::uint32_t arena_frames() const;  // physical 2 MiB frames in the arena
   // Not owned; nullptr restores the default. Install before any GPU allocation.
   void set_frame_placer(FramePlacer* placer);
+  // Called on the thread running execute() whenever legs have committed (the
+  // interposer daemon maps the incoming app's slabs while copies continue).
+  // It must not call back into the engine.
+  void set_progress_hook(std::function<void()> hook);
   std::uint64_t block_checksum(BlockId block) const;  // last recorded departure checksum
   // Test access to a resident block's bytes wherever it lives.
   void read_block(BlockId block, void* host_dst);

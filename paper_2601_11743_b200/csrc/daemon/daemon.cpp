@@ -174,7 +174,7 @@ class SlabPlacer final : public FramePlacer {
       s.phys = free_.front();
       free_.pop_front();
     }
-    ++s.count;
+    if (s.count++ == 0) assigned_.push_back(key(b));
     return s.phys * ipc::kSlabBlocks + static_cast<std::uint32_t>(vpos_[b] % ipc::kSlabBlocks);
   }
 
@@ -188,6 +188,9 @@ class SlabPlacer final : public FramePlacer {
       released_.push_back(k);
     }
   }
+
+  // vslabs that got a physical slab since the last call.
+  std::vector<Key> take_assigned() { return std::exchange(assigned_, {}); }
 
   // vslabs that lost their physical slab since the last call.
   std::vector<Key> take_released() { return std::exchange(released_, {}); }
@@ -224,6 +227,7 @@ class SlabPlacer final : public FramePlacer {
   std::map<Key, Slab> slabs_;
   std::deque<std::uint32_t> free_;
   std::vector<Key> released_;
+  std::vector<Key> assigned_;
 };
 
 class Daemon {
@@ -231,6 +235,7 @@ class Daemon {
   explicit Daemon(const Options& o)
       : opt_(o), eng_(o.eng), sched_(o.mlfq), placer_(eng_.arena_frames() / ipc::kSlabBlocks) {
     eng_.set_frame_placer(&placer_);
+    eng_.set_progress_hook([this] { send_maps(); });
     sched_.set_logging(true);
     t0_ = ipc::mono_ns();
     if (!o.log_path.empty()) {
@@ -594,6 +599,25 @@ class Daemon {
     return true;
   }
 
+  // While a plan runs: the incoming app maps the slabs its blocks are landing
+  // in (it cannot launch until the Grant, so the bytes need not be there yet),
+  // and victims drop released ones, overlapping the driver's per-mapping
+  // cost with the copies. A slab is reassigned only after its release, and
+  // every message to one shim is ordered on its event socket.
+  void send_maps() {
+    std::map<AppId, std::vector<ipc::SlabMap>> per_app;
+    for (const auto& k : placer_.take_assigned()) per_app[k.first].push_back(placer_.map_of(k.first, k.second));
+    for (auto& [app, ms] : per_app) {
+      auto it = apps_.find(app);
+      if (it == apps_.end() || !it->second.alive || it->second.ev < 0) continue;
+      ipc::Writer w;
+      w.put(ipc::SlabsMsg{++epoch_, static_cast<std::uint32_t>(ms.size()), 0});
+      for (const auto& m : ms) w.put(m);
+      if (!ipc::send_msg(it->second.ev, ipc::Msg::Map, w.buf)) it->second.alive = false;
+    }
+    send_unmaps();
+  }
+
   // After a plan ran: owners of vslabs whose physical slab was released unmap
   // them. No ack is needed: only applications that cannot launch (paused
   // or waiting) lose slabs, and the next Grant to them follows on the same
@@ -628,7 +652,7 @@ class Daemon {
     cfg.eviction_policy.victim_order = sched_.victim_hint();
     const MigrationPlan plan = plan_switch(app, eng_.mem(), cfg);
     const ExecResult r = eng_.execute(plan, cfg);
-    send_unmaps();
+    send_maps();
     account(r);
     note("{\"t\": %.6f, \"event\": \"fetch_in_place\", \"app\": %u, \"bytes_in\": %" PRIu64 ", \"bytes_out\": %" PRIu64 "}",
          now(), app, plan.bytes_in, plan.bytes_out);
@@ -658,7 +682,7 @@ class Daemon {
     const std::uint64_t t_planned = ipc::mono_ns();
     const ExecResult r = eng_.execute(plan, cfg);
     const std::uint64_t t_copied = ipc::mono_ns();
-    send_unmaps();
+    send_maps();
     account(r);
     const std::uint64_t t_unmapped = ipc::mono_ns();
     // (5) grant: the incoming shim maps its slabs and sets its flag.

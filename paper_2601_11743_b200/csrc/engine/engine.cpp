@@ -20,6 +20,7 @@
 #include <array>
 #include <chrono>
 #include <cstring>
+#include <functional>
 #include <deque>
 #include <map>
 #include <thread>
@@ -62,6 +63,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   NumaInfo numa;
   DeviceArena arena;
   FramePlacer* placer = nullptr;
+  std::function<void()> progress;  // called on the engine thread after commits
   PinnedRing pinned;
   PagedStore paged;
   HostCopyPool pool;
@@ -692,6 +694,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
       while (!finished) {
         if (poll()) {
           flush();
+          if (progress) progress();
           last = Clock::now();
         } else {
           if (std::chrono::duration<double>(Clock::now() - last).count() > 120.0)
@@ -848,6 +851,7 @@ std::int64_t SwapEngine::frame_index(BlockId b) const {
 
 std::uint32_t SwapEngine::arena_frames() const { return impl_->arena.ring.units(); }
 void SwapEngine::set_frame_placer(FramePlacer* placer) { impl_->placer = placer; }
+void SwapEngine::set_progress_hook(std::function<void()> hook) { impl_->progress = std::move(hook); }
 
 int SwapEngine::arena_export_fd(std::uint32_t slab) const {
   const int fd = impl_->arena.export_fd(slab);

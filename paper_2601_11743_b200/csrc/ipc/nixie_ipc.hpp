@@ -53,6 +53,7 @@ enum class Msg : std::uint32_t {
   Grant,         // event d->shim: SlabsMsg + SlabMap[n] (every mapped vslab of the app) -> ack Granted
   Granted,       // event shim->d: GrantedMsg
   Stats,         // rpc  shim->d : (empty)    reply StatsRep
+  Map,           // event d->shim: SlabsMsg + SlabMap[n] (slabs placed while the switch runs; no ack)
 };
 
 // Virtual slabs: a shim reserves one large virtual range and places its

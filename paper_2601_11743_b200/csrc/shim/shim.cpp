@@ -141,7 +141,17 @@ Drv& drv() {
   return d;
 }
 
+struct Shim;
+extern Shim& g;
+bool exiting();
+
+thread_local bool t_listener = false;
+
 void die(const char* what, CUresult r = CUDA_SUCCESS) {
+  // At exit the driver tears down under the listener thread: not an error;
+  // the thread parks and the process finishes exiting with its own status.
+  if (t_listener && (r == CUDA_ERROR_DEINITIALIZED || exiting()))
+    for (;;) pause();
   std::fprintf(stderr, "[nixie-shim] fatal: %s (CUresult %d)\n", what, static_cast<int>(r));
   std::abort();
 }
@@ -182,6 +192,7 @@ struct Shim {
   std::uint64_t managed_bytes = 0, small_bytes = 0;
 
   std::atomic<bool> granted{false};
+  std::atomic<bool> exiting{false};  // the process is exiting: the driver may be torn down
   std::atomic<int> inflight{0};
   std::atomic<int> capturing{0};
 };
@@ -190,6 +201,7 @@ constexpr std::uint64_t kRangeBytes = 1ull << 40;  // 1 TiB of virtual space per
 
 // Never destroyed: the listener thread may still run while the process exits.
 Shim& g = *new Shim;
+bool exiting() { return g.exiting.load(); }
 std::once_flag g_once;
 thread_local int t_capturing = 0;  // this thread began a stream capture
 thread_local int t_in_shim = 0;    // re-entrancy guard
@@ -281,6 +293,7 @@ void init_once() {
   ipc::EventHelloReq eh{g.app, 0};
   if (g.ev < 0 || !ipc::send_msg(g.ev, ipc::Msg::EventHello, &eh, sizeof(eh))) die("event connection");
   g.active = true;
+  std::atexit([] { g.exiting.store(true); });
   std::thread(listener).detach();
   t_in_shim--;
 }
@@ -364,6 +377,17 @@ void on_unmap(const std::vector<std::uint8_t>& body) {
   for (std::uint32_t i = 0; i < m.n && r.ok; ++i) place(r.get<std::uint32_t>(), ipc::kNoFrame, m.epoch, maps, unmaps);
 }
 
+void on_map(const std::vector<std::uint8_t>& body) {
+  ipc::Reader r{body};
+  const auto m = r.get<ipc::SlabsMsg>();
+  std::uint64_t maps = 0, unmaps = 0;
+  std::lock_guard<std::mutex> lk(g.mu);
+  for (std::uint32_t i = 0; i < m.n && r.ok; ++i) {
+    const auto sm = r.get<ipc::SlabMap>();
+    place(sm.vslab, sm.phys, m.epoch, maps, unmaps);
+  }
+}
+
 void on_grant(const std::vector<std::uint8_t>& body) {
   ipc::Reader r{body};
   const auto m = r.get<ipc::SlabsMsg>();
@@ -389,6 +413,7 @@ void on_grant(const std::vector<std::uint8_t>& body) {
 }
 
 void listener() {
+  t_listener = true;
   t_in_shim++;
   REAL(cudaSetDevice);
   REAL(cudaFree);
@@ -402,6 +427,7 @@ void listener() {
       case ipc::Msg::Pause: on_pause(body); break;
       case ipc::Msg::Unmap: on_unmap(body); break;
       case ipc::Msg::Grant: on_grant(body); break;
+      case ipc::Msg::Map: on_map(body); break;
       default:
         std::fprintf(stderr, "[nixie-shim] unexpected event %u\n", static_cast<unsigned>(type));
     }
