@@ -4,7 +4,7 @@
 // the end copies everything back and checks it on the host. Built with
 // `-cudart shared` so LD_PRELOAD can interpose the runtime.
 //
-//   nx_vecapp --mib N --buffers K --iters I --think-ms T --seed S [--name X]
+//   nx_vecapp --mib N --buffers K --iters I --think-ms T --seed S [--name X] [--host-check 0|1]
 //
 // Every word of every buffer holds hash(seed, buffer, index) + iteration; each
 // iteration's kernel checks the expected value and increments it, so a byte
@@ -64,6 +64,7 @@ int main(int argc, char** argv) {
   double think_ms = 50;
   std::uint64_t seed = 1;
   std::string name = "vecapp";
+  int host_check = 1;
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string a = argv[i];
     if (a == "--mib") mib = std::atof(argv[i + 1]);
@@ -72,6 +73,7 @@ int main(int argc, char** argv) {
     else if (a == "--think-ms") think_ms = std::atof(argv[i + 1]);
     else if (a == "--seed") seed = std::strtoull(argv[i + 1], nullptr, 0);
     else if (a == "--name") name = argv[i + 1];
+    else if (a == "--host-check") host_check = std::atoi(argv[i + 1]);
   }
   const auto t_start = std::chrono::steady_clock::now();
   const std::uint64_t bytes_each = static_cast<std::uint64_t>(mib * 1048576.0 / buffers) / 4 * 4;
@@ -98,8 +100,8 @@ int main(int argc, char** argv) {
   unsigned long long dev_errors = 0;
   CK(cudaMemcpy(&dev_errors, d_err, sizeof(dev_errors), cudaMemcpyDeviceToHost));
   std::uint64_t host_mismatch = 0;
-  std::vector<std::uint32_t> h(n);
-  for (int b = 0; b < buffers; ++b) {
+  std::vector<std::uint32_t> h(host_check ? n : 0);
+  for (int b = 0; b < buffers && host_check; ++b) {
     CK(cudaMemcpy(h.data(), buf[b], bytes_each, cudaMemcpyDeviceToHost));
     for (std::uint64_t i = 0; i < n; ++i) host_mismatch += h[i] != expect(seed, b, i) + static_cast<std::uint32_t>(iters);
   }
@@ -110,8 +112,8 @@ int main(int argc, char** argv) {
   auto q = [&](double f) { return s.empty() ? 0.0 : s[std::min(s.size() - 1, static_cast<std::size_t>(f * s.size()))]; };
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   std::printf("{\"name\": \"%s\", \"bytes\": %llu, \"iters\": %d, \"device_errors\": %llu, \"host_mismatch\": %llu, "
-              "\"memgetinfo\": [%zu, %zu], \"iter_ms\": {\"p50\": %.3f, \"p99\": %.3f, \"max\": %.3f}, \"wall_s\": %.3f}\n",
+              "\"host_checked\": %d, \"memgetinfo\": [%zu, %zu], \"iter_ms\": {\"p50\": %.3f, \"p99\": %.3f, \"max\": %.3f}, \"wall_s\": %.3f}\n",
               name.c_str(), static_cast<unsigned long long>(bytes_each * buffers), iters, dev_errors,
-              static_cast<unsigned long long>(host_mismatch), free_b, total_b, q(0.5), q(0.99), s.empty() ? 0.0 : s.back(), wall);
+              static_cast<unsigned long long>(host_mismatch), host_check, free_b, total_b, q(0.5), q(0.99), s.empty() ? 0.0 : s.back(), wall);
   return dev_errors == 0 && host_mismatch == 0 ? 0 : 1;
 }
