@@ -1,0 +1,59 @@
+"""Host-side checks of the interposer (no GPU): the shim exports exactly the
+CUDA entry points it interposes (include/nixie_shim.h) and nothing of its
+statically linked C++ runtime, is inert without NIXIE_SOCKET, and the daemon
+binary parses its command line."""
+import os
+import re
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2601_11743_b200.interpose import NIXIED, SHIM, VECAPP  # noqa: E402
+
+INTERPOSED = {
+    "cudaMalloc", "cudaFree", "cuMemAlloc_v2", "cuMemFree_v2", "cudaMemGetInfo",
+    "cudaLaunchKernel", "cudaLaunchKernel_ptsz", "cudaLaunchKernelExC", "cudaLaunchKernelExC_ptsz",
+    "cudaLaunchCooperativeKernel", "cudaLaunchCooperativeKernel_ptsz", "cudaGraphLaunch", "cudaGraphLaunch_ptsz",
+    "cuLaunchKernel", "cudaMemcpy", "cudaMemcpyAsync", "cudaMemcpyAsync_ptsz", "cudaMemcpy2D", "cudaMemcpy2DAsync",
+    "cudaMemset", "cudaMemsetAsync", "cudaMemsetAsync_ptsz",
+    "cudaDeviceSynchronize", "cudaStreamSynchronize", "cudaEventSynchronize",
+    "cudaStreamBeginCapture", "cudaStreamEndCapture",
+}
+
+
+def exported(path):
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True, check=True).stdout
+    return {ln.split()[-1] for ln in out.splitlines() if re.search(r" [TW] ", ln)}
+
+
+def test_shim_exports_exactly_the_interposed_api():
+    syms = exported(SHIM)
+    assert syms == INTERPOSED | {"nixie_shim_active", "nixie_shim_app"}, sorted(syms ^ (INTERPOSED | {"nixie_shim_active", "nixie_shim_app"}))
+    header = open(os.path.join(ROOT, "include", "nixie_shim.h")).read()
+    for s in INTERPOSED:
+        base = s.replace("_ptsz", "")
+        assert base in header, f"{s} not documented in include/nixie_shim.h"
+
+
+def test_shim_is_inert_without_a_daemon():
+    code = ("import ctypes, os; os.environ.pop('NIXIE_SOCKET', None); "
+            f"s = ctypes.CDLL({SHIM!r}); s.nixie_shim_app.restype = ctypes.c_uint; "
+            "print(s.nixie_shim_active(), s.nixie_shim_app())")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.split() == ["0", str(0xFFFFFFFF)]
+
+
+def test_daemon_cli():
+    r = subprocess.run([NIXIED, "--help"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and "--socket" in r.stderr and "--phys-slack" in r.stderr
+    r = subprocess.run([NIXIED, "--bogus"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 1
+
+
+def test_test_app_links_the_shared_runtime():
+    """LD_PRELOAD can only interpose a dynamically linked CUDA runtime."""
+    out = subprocess.run(["readelf", "-d", VECAPP], capture_output=True, text=True, check=True).stdout
+    assert "libcudart.so" in out
