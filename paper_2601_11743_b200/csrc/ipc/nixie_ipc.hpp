@@ -152,6 +152,8 @@ struct alignas(64) CtlPage {
   std::atomic<std::uint64_t> map_ns;          // total mapping time
   std::atomic<std::uint64_t> unmap_ns;        // total unmapping time
   std::atomic<std::uint64_t> drain_ns;        // total pause-drain time
+  std::atomic<std::uint64_t> table_launches;  // gated calls that came through cuGetProcAddress entry
+                                              // points directly (not via an interposed runtime call)
 };
 static_assert(sizeof(CtlPage) <= 4096, "control page fits one page");
 

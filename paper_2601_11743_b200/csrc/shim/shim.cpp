@@ -204,6 +204,7 @@ Shim& g = *new Shim;
 bool exiting() { return g.exiting.load(); }
 std::once_flag g_once;
 thread_local int t_capturing = 0;  // this thread began a stream capture
+thread_local int t_gate_depth = 0; // this thread holds a gate slot (nested gated calls pass)
 thread_local int t_in_shim = 0;    // re-entrancy guard
 
 void now_api() {
@@ -478,7 +479,7 @@ void acquire_slow() {
 // Entry of every gated call: returns true holding an in-flight slot (a pause
 // waits for it), false when the call need not be gated.
 bool gate_enter() {
-  if (t_in_shim || !active() || t_capturing) return false;
+  if (t_in_shim || t_gate_depth || !active() || t_capturing) return false;
   for (;;) {
     g.inflight.fetch_add(1, std::memory_order_seq_cst);
     if (g.granted.load(std::memory_order_seq_cst)) break;
@@ -489,11 +490,17 @@ bool gate_enter() {
   return true;
 }
 
+// A runtime call the shim gates reaches the driver through cudart's entry
+// table, which the shim also wraps (cuGetProcAddress below): the nested
+// driver call passes on the outer call's slot (t_gate_depth).
 struct Gate {
   bool held;
-  Gate() : held(gate_enter()) {}
+  Gate() : held(gate_enter()) {
+    if (held) ++t_gate_depth;
+  }
   ~Gate() {
     if (held) {
+      --t_gate_depth;
       g.inflight.fetch_sub(1, std::memory_order_seq_cst);
       now_api();
     }
@@ -619,7 +626,163 @@ bool managed_free(void* p) {
   return true;
 }
 
+// ---- driver entry points handed out by cuGetProcAddress -----------------------------
+// Libraries that link the CUDA runtime statically (cuBLAS, cuDNN) and cudart
+// itself reach the driver through cuGetProcAddress, not the PLT. The shim
+// wraps dlsym's answer for cuGetProcAddress and returns gated wrappers for
+// the launch and async-copy entry points (legacy and per-thread-stream
+// variants); everything else is returned untouched.
+// Each (symbol, real pointer) pair gets its own wrapper slot: libraries built
+// against different CUDA versions may receive different implementations for
+// the same name (and the per-thread-stream flavour is another pointer).
+constexpr int kSlots = 8;
+
+#define NX_DRV(id, ret, params, args)                                                       \
+  ret(*real_##id[kSlots]) params = {};                                                      \
+  template <int K>                                                                          \
+  ret wrap_##id params {                                                                    \
+    Gate gate_;                                                                             \
+    if (gate_.held) g.ctl->table_launches.fetch_add(1, std::memory_order_relaxed);          \
+    return real_##id[K] args;                                                               \
+  }                                                                                         \
+  void* const wraps_##id[kSlots] = {                                                        \
+      reinterpret_cast<void*>(&wrap_##id<0>), reinterpret_cast<void*>(&wrap_##id<1>),       \
+      reinterpret_cast<void*>(&wrap_##id<2>), reinterpret_cast<void*>(&wrap_##id<3>),       \
+      reinterpret_cast<void*>(&wrap_##id<4>), reinterpret_cast<void*>(&wrap_##id<5>),       \
+      reinterpret_cast<void*>(&wrap_##id<6>), reinterpret_cast<void*>(&wrap_##id<7>)};
+
+NX_DRV(LaunchKernel, CUresult,
+       (CUfunction f, unsigned gx, unsigned gy, unsigned gz, unsigned bx, unsigned by, unsigned bz, unsigned sm,
+        CUstream st, void** p, void** e),
+       (f, gx, gy, gz, bx, by, bz, sm, st, p, e))
+NX_DRV(LaunchKernelEx, CUresult, (const CUlaunchConfig* c, CUfunction f, void** p, void** e), (c, f, p, e))
+NX_DRV(LaunchCoop, CUresult,
+       (CUfunction f, unsigned gx, unsigned gy, unsigned gz, unsigned bx, unsigned by, unsigned bz, unsigned sm,
+        CUstream st, void** p),
+       (f, gx, gy, gz, bx, by, bz, sm, st, p))
+NX_DRV(GraphLaunch, CUresult, (CUgraphExec e, CUstream st), (e, st))
+NX_DRV(MemcpyAsync, CUresult, (CUdeviceptr d, CUdeviceptr s, size_t n, CUstream st), (d, s, n, st))
+NX_DRV(MemcpyHtoDAsync, CUresult, (CUdeviceptr d, const void* s, size_t n, CUstream st), (d, s, n, st))
+NX_DRV(MemcpyDtoHAsync, CUresult, (void* d, CUdeviceptr s, size_t n, CUstream st), (d, s, n, st))
+NX_DRV(MemcpyDtoDAsync, CUresult, (CUdeviceptr d, CUdeviceptr s, size_t n, CUstream st), (d, s, n, st))
+NX_DRV(MemsetD8Async, CUresult, (CUdeviceptr d, unsigned char v, size_t n, CUstream st), (d, v, n, st))
+NX_DRV(MemsetD32Async, CUresult, (CUdeviceptr d, unsigned v, size_t n, CUstream st), (d, v, n, st))
+
+struct DrvWrap {
+  const char* name;
+  void** real;        // kSlots real pointers
+  void* const* wrap;  // kSlots wrappers
+};
+
+#define NX_ENTRY(id, sym) \
+  DrvWrap { sym, reinterpret_cast<void**>(real_##id), wraps_##id }
+
+const DrvWrap kDrvWraps[] = {
+    NX_ENTRY(LaunchKernel, "cuLaunchKernel"),       NX_ENTRY(LaunchKernelEx, "cuLaunchKernelEx"),
+    NX_ENTRY(LaunchCoop, "cuLaunchCooperativeKernel"), NX_ENTRY(GraphLaunch, "cuGraphLaunch"),
+    NX_ENTRY(MemcpyAsync, "cuMemcpyAsync"),         NX_ENTRY(MemcpyHtoDAsync, "cuMemcpyHtoDAsync"),
+    NX_ENTRY(MemcpyDtoHAsync, "cuMemcpyDtoHAsync"), NX_ENTRY(MemcpyDtoDAsync, "cuMemcpyDtoDAsync"),
+    NX_ENTRY(MemsetD8Async, "cuMemsetD8Async"),     NX_ENTRY(MemsetD32Async, "cuMemsetD32Async"),
+};
+
+std::mutex g_drv_mu;
+
+// Replaces *pfn with a gated wrapper when `symbol` is one of ours. The real
+// pointer is kept per (symbol, stream flavour); a library asking twice gets
+// the same answer.
+bool debug_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("NIXIE_SHIM_DEBUG");
+    return e && *e == '1';
+  }();
+  return on;
+}
+
+void wrap_proc(const char* symbol, void** pfn, cuuint64_t flags) {
+  if (!symbol || !pfn || !*pfn) return;
+  for (const DrvWrap& w : kDrvWraps) {
+    if (std::strcmp(symbol, w.name) != 0) continue;
+    std::lock_guard<std::mutex> lk(g_drv_mu);
+    for (int k = 0; k < kSlots; ++k) {
+      if (*pfn == w.wrap[k]) return;  // already ours
+      if (w.real[k] == nullptr) w.real[k] = *pfn;
+      if (w.real[k] == *pfn) {
+        if (debug_on())
+          std::fprintf(stderr, "[nixie-shim] wrapped %s (flags %llu) slot %d\n", symbol, static_cast<unsigned long long>(flags), k);
+        *pfn = w.wrap[k];
+        return;
+      }
+    }
+    std::fprintf(stderr, "[nixie-shim] warning: %s has more than %d implementations; not gated\n", symbol, kSlots);
+    return;
+  }
+}
+
+using GetProcV2 = CUresult (*)(const char*, void**, int, cuuint64_t, CUdriverProcAddressQueryResult*);
+using GetProcV1 = CUresult (*)(const char*, void**, int, cuuint64_t);
+GetProcV2 real_gpa_v2 = nullptr;
+GetProcV1 real_gpa_v1 = nullptr;
+CUresult wrap_gpa_v1(const char* symbol, void** pfn, int ver, cuuint64_t flags);
+
+CUresult wrap_gpa_v2(const char* symbol, void** pfn, int ver, cuuint64_t flags, CUdriverProcAddressQueryResult* st) {
+  const CUresult r = real_gpa_v2(symbol, pfn, ver, flags, st);
+  if (debug_on()) std::fprintf(stderr, "[nixie-shim] gpa %s ver %d flags %llu -> %d\n", symbol, ver, static_cast<unsigned long long>(flags), static_cast<int>(r));
+  if (r == CUDA_SUCCESS && symbol) {
+    if (std::strcmp(symbol, "cuGetProcAddress") == 0) {
+      if (ver >= 12000) {
+        real_gpa_v2 = real_gpa_v2 ? real_gpa_v2 : reinterpret_cast<GetProcV2>(*pfn);
+        *pfn = reinterpret_cast<void*>(&wrap_gpa_v2);
+      } else {
+        real_gpa_v1 = reinterpret_cast<GetProcV1>(*pfn);
+        *pfn = reinterpret_cast<void*>(&wrap_gpa_v1);
+      }
+    } else {
+      wrap_proc(symbol, pfn, flags);
+    }
+  }
+  return r;
+}
+
+CUresult wrap_gpa_v1(const char* symbol, void** pfn, int ver, cuuint64_t flags) {
+  const CUresult r = real_gpa_v1(symbol, pfn, ver, flags);
+  if (debug_on()) std::fprintf(stderr, "[nixie-shim] gpa1 %s ver %d flags %llu -> %d\n", symbol, ver, static_cast<unsigned long long>(flags), static_cast<int>(r));
+  if (r == CUDA_SUCCESS) wrap_proc(symbol, pfn, flags);
+  return r;
+}
+
+using DlsymFn = void* (*)(void*, const char*);
+DlsymFn real_dlsym() {
+  static DlsymFn f = [] {
+    auto p = reinterpret_cast<DlsymFn>(dlvsym(RTLD_NEXT, "dlsym", "GLIBC_2.34"));
+    if (!p) p = reinterpret_cast<DlsymFn>(dlvsym(RTLD_NEXT, "dlsym", "GLIBC_2.2.5"));
+    return p;
+  }();
+  return f;
+}
+
 }  // namespace
+
+// The one libc entry point the shim wraps: libraries find the driver with
+// dlopen("libcuda.so.1") + dlsym("cuGetProcAddress[_v2]").
+extern "C" void* dlsym(void* handle, const char* name) {
+  void* p = real_dlsym()(handle, name);
+  if (!p || std::strncmp(name, "cu", 2) != 0) return p;
+  if (std::strncmp(name, "cuGetProcAddress", 16) != 0) {
+    // Direct lookups of the gated entry points (launchers that dlopen libcuda).
+    wrap_proc(name, &p, 0);
+    return p;
+  }
+  if (debug_on()) std::fprintf(stderr, "[nixie-shim] dlsym(%s)\n", name);
+  if (std::strcmp(name, "cuGetProcAddress_v2") == 0) {
+    if (!real_gpa_v2) real_gpa_v2 = reinterpret_cast<GetProcV2>(p);
+    return reinterpret_cast<void*>(&wrap_gpa_v2);
+  }
+  if (std::strcmp(name, "cuGetProcAddress") == 0) {
+    if (!real_gpa_v1) real_gpa_v1 = reinterpret_cast<GetProcV1>(p);
+    return reinterpret_cast<void*>(&wrap_gpa_v1);
+  }
+  return p;
+}
 
 // =================================================================================
 // Interposed CUDA runtime API

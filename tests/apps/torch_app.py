@@ -17,20 +17,29 @@ def main():
     n = int(mib * (1 << 20) / 4 / bufs)
     free_b, total_b = torch.cuda.mem_get_info()
     xs = [torch.full((n,), k * 1000, dtype=torch.int32, device="cuda") for k in range(bufs)]
+    # cuBLAS work: its kernels reach the driver through cuGetProcAddress, not
+    # the runtime's PLT entry points (the shim gates them too).
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(2048, 2048, device="cuda", generator=g)
+    b = torch.randn(2048, 2048, device="cuda", generator=g)
+    ref = (a @ b).double().sum().item()
+    mm_bad = 0
     lat = []
     for it in range(iters):
         t0 = time.perf_counter()
         for x in xs:
             x.add_(1)
+        c = a @ b
         torch.cuda.synchronize()
+        mm_bad += int(abs(c.double().sum().item() - ref) > 1e-6 * max(1.0, abs(ref)))
         lat.append((time.perf_counter() - t0) * 1e3)
         time.sleep(think)
     bad = 0
     for k, x in enumerate(xs):
         bad += int((x != k * 1000 + iters).sum().item())
-    print(json.dumps({"name": "torch_app", "bytes": n * 4 * bufs, "iters": iters, "mismatch": bad,
+    print(json.dumps({"name": "torch_app", "bytes": n * 4 * bufs, "iters": iters, "mismatch": bad, "matmul_mismatch": mm_bad,
                       "memgetinfo": [free_b, total_b], "iter_ms_max": max(lat)}))
-    return 0 if bad == 0 else 1
+    return 0 if bad == 0 and mm_bad == 0 else 1
 
 
 if __name__ == "__main__":

@@ -4,12 +4,13 @@
 // the end copies everything back and checks it on the host. Built with
 // `-cudart shared` so LD_PRELOAD can interpose the runtime.
 //
-//   nx_vecapp --mib N --buffers K --iters I --think-ms T --seed S [--name X] [--host-check 0|1]
+//   nx_vecapp --mib N --buffers K --iters I --think-ms T --seed S [--name X] [--host-check 0|1] [--driver 0|1]
 //
 // Every word of every buffer holds hash(seed, buffer, index) + iteration; each
 // iteration's kernel checks the expected value and increments it, so a byte
 // lost or misplaced across a context switch is counted (device errors) and
 // the final host check compares every word. Prints one JSON line.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -65,6 +66,7 @@ int main(int argc, char** argv) {
   std::uint64_t seed = 1;
   std::string name = "vecapp";
   int host_check = 1;
+  int driver = 0;  // 1: launch `step` through the driver API (cuLaunchKernel from cudaGetDriverEntryPoint)
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string a = argv[i];
     if (a == "--mib") mib = std::atof(argv[i + 1]);
@@ -74,6 +76,7 @@ int main(int argc, char** argv) {
     else if (a == "--seed") seed = std::strtoull(argv[i + 1], nullptr, 0);
     else if (a == "--name") name = argv[i + 1];
     else if (a == "--host-check") host_check = std::atoi(argv[i + 1]);
+    else if (a == "--driver") driver = std::atoi(argv[i + 1]);
   }
   const auto t_start = std::chrono::steady_clock::now();
   const std::uint64_t bytes_each = static_cast<std::uint64_t>(mib * 1048576.0 / buffers) / 4 * 4;
@@ -88,10 +91,37 @@ int main(int argc, char** argv) {
   for (int b = 0; b < buffers; ++b) fill<<<1184, 256>>>(buf[b], n, seed, b);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
+  using LaunchFn = CUresult (*)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
+                                void**, void**);
+  LaunchFn cu_launch = nullptr;
+  CUfunction step_fn = nullptr;
+  if (driver) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CK(cudaGetDriverEntryPoint("cuLaunchKernel", &p, cudaEnableDefault, &q));
+    cu_launch = reinterpret_cast<LaunchFn>(p);
+    cudaFunction_t f = nullptr;
+    CK(cudaGetFuncBySymbol(&f, reinterpret_cast<const void*>(&step)));
+    step_fn = reinterpret_cast<CUfunction>(f);
+  }
   std::vector<double> lat;
   for (int it = 0; it < iters; ++it) {
     const auto t0 = std::chrono::steady_clock::now();
-    for (int b = 0; b < buffers; ++b) step<<<1184, 256>>>(buf[b], n, seed, b, static_cast<std::uint32_t>(it), d_err);
+    for (int b = 0; b < buffers; ++b) {
+      if (driver) {
+        std::uint32_t* pb = buf[b];
+        std::uint64_t nn = n, sd = seed;
+        int bb = b;
+        std::uint32_t itv = static_cast<std::uint32_t>(it);
+        void* args[] = {&pb, &nn, &sd, &bb, &itv, &d_err};
+        if (cu_launch(step_fn, 1184, 1, 1, 256, 1, 1, 0, nullptr, args, nullptr) != CUDA_SUCCESS) {
+          std::fprintf(stderr, "cuLaunchKernel failed\n");
+          return 2;
+        }
+      } else {
+        step<<<1184, 256>>>(buf[b], n, seed, b, static_cast<std::uint32_t>(it), d_err);
+      }
+    }
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     lat.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());

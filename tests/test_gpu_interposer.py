@@ -63,6 +63,24 @@ def test_two_vecapps_oversubscribed():
     assert any(s["pcie_h2d"] > 0 and s["pcie_d2h"] > 0 for s in sw)
 
 
+def test_driver_api_launches_are_gated():
+    """One app launches through the driver API (cuLaunchKernel obtained with
+    cudaGetDriverEntryPoint, i.e. cuGetProcAddress); the shim's wrapped entry
+    table gates those launches like runtime ones."""
+    with Daemon(gpu="4G", pinned="4G", paged="16G") as d:
+        res = run_apps(d, [_vec(3072, 5, 250, 31, "drv") + ["--driver", "1"], _vec(3072, 5, 250, 32, "rt")], timeout=600)
+        _save("driver_api", d, res)
+        _check(res, d)
+        recs = d.records()
+    byes = {r["app"]: r for r in recs if r.get("event") == "bye"}
+    assert len(byes) == 2
+    assert max(b["table_launches"] for b in byes.values()) >= 5 * 6
+    assert min(b["table_launches"] for b in byes.values()) == 0
+    assert len([r for r in recs if r.get("event") == "switch"]) >= 3
+    for r in res:
+        assert r["out"]["device_errors"] == 0 and r["out"]["host_mismatch"] == 0
+
+
 def test_memgetinfo_reports_budget():
     with Daemon(gpu="6G", pinned="2G", paged="8G") as d:
         res = run_apps(d, [_vec(1024, 1, 0, 3, "m")], timeout=300)
@@ -73,13 +91,14 @@ def test_memgetinfo_reports_budget():
 
 
 def test_three_apps_with_torch():
-    """A PyTorch program and two CUDA programs share a 5 GiB budget."""
+    """A PyTorch program (elementwise + cuBLAS matmul) and two CUDA programs
+    share a 5 GiB budget."""
     with Daemon(gpu="5G", pinned="4G", paged="16G") as d:
         res = run_apps(d, [_vec(2048, 5, 200, 5, "a"), [sys.executable, os.path.join(ROOT, "tests", "apps", "torch_app.py"),
                                                            "2048", "5", "0.2"], _vec(2048, 5, 200, 6, "c")], timeout=900)
         _save("torch_mix", d, res)
         _check(res, d)
         sw = d.switches()
-    assert res[1]["out"]["mismatch"] == 0
+    assert res[1]["out"]["mismatch"] == 0 and res[1]["out"]["matmul_mismatch"] == 0
     assert res[1]["out"]["memgetinfo"][1] == 5 << 30
     assert len(sw) >= 3 and all(s["mismatches"] == 0 for s in sw)

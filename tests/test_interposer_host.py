@@ -30,7 +30,8 @@ def exported(path):
 
 def test_shim_exports_exactly_the_interposed_api():
     syms = exported(SHIM)
-    assert syms == INTERPOSED | {"nixie_shim_active", "nixie_shim_app"}, sorted(syms ^ (INTERPOSED | {"nixie_shim_active", "nixie_shim_app"}))
+    want = INTERPOSED | {"nixie_shim_active", "nixie_shim_app", "dlsym"}
+    assert syms == want, sorted(syms ^ want)
     header = open(os.path.join(ROOT, "include", "nixie_shim.h")).read()
     for s in INTERPOSED:
         base = s.replace("_ptsz", "")
