@@ -233,6 +233,15 @@ int nx_scenario_model_lanes(const char* spec, int legs_per_lane, char** trace, s
  * with the pattern (seed) up front; after each switch the incoming app is
  * verified byte-exact (`V k app bad` lines) and at the end every app is. */
 int nx_scenario_real(const char* spec, const nx_engine_config* cfg, uint64_t seed, char** trace, size_t* len);
+/* An MLFQ-driven workload (include/nixie_workload/workload_sim.hpp grammar:
+ * interactive / batch apps, launch gate, scheduler ticks) on
+ * the virtual clock. Replaces the reference's (absent) workload-sim `run`
+ * (SPEC.md:455); its reference twin is oracle/_ref/ref_workload. */
+int nx_workload_model(const char* spec, char** trace, size_t* len);
+/* Same workload with every planned switch executed by the CUDA engine (real
+ * bytes; decisions keep the virtual clock). Adds `M k differing-blocks`,
+ * `V k app bad ...` and final `F app bad` lines. */
+int nx_workload_real(const char* spec, const nx_engine_config* cfg, uint64_t seed, char** trace, size_t* len);
 void nx_free(void* p);
 
 #ifdef __cplusplus

@@ -147,6 +147,8 @@ _SIGNATURES = [
     ("nx_scenario_model", c_int, [c_char_p, POINTER(c_void_p), POINTER(c_size_t)]),
     ("nx_scenario_model_lanes", c_int, [c_char_p, c_int, POINTER(c_void_p), POINTER(c_size_t)]),
     ("nx_scenario_real", c_int, [c_char_p, POINTER(EngineConfigC), c_uint64, POINTER(c_void_p), POINTER(c_size_t)]),
+    ("nx_workload_model", c_int, [c_char_p, POINTER(c_void_p), POINTER(c_size_t)]),
+    ("nx_workload_real", c_int, [c_char_p, POINTER(EngineConfigC), c_uint64, POINTER(c_void_p), POINTER(c_size_t)]),
     ("nx_free", None, [c_void_p]),
 ]
 

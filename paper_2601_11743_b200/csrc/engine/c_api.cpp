@@ -11,6 +11,8 @@
 #include <string>
 
 #include "nixie/scenario.hpp"
+#include "nixie/workload.hpp"
+#include <nixie_workload/workload_sim.hpp>
 #include "nixie/swap_engine.hpp"
 #include "nx_kernels.h"
 #include "phys.hpp"
@@ -664,6 +666,70 @@ int nx_scenario_real(const char* spec, const nx_engine_config* cfg, uint64_t see
     };
     std::string out = drive_scenario(sc, runner);
     for (const ScenarioApp& a : sc.apps)
+      out += "F " + std::to_string(a.id) + " " + std::to_string(eng.verify_pattern(a.id, seed)) + "\n";
+    *trace = dup_out(out, len);
+  });
+}
+
+int nx_workload_model(const char* spec, char** trace, size_t* len) {
+  return guard([&] {
+    need(spec, "spec");
+    need(trace, "trace");
+    *trace = dup_out(run_workload_model(spec), len);
+  });
+}
+
+// The workload's decisions follow the virtual clock (the model's completion
+// of each switch, computed on a copy of the registry), while the CUDA engine
+// moves the bytes of every planned switch; after each switch the engine's
+// placement must equal the model's (`M` line) and the incoming app must be
+// byte-exact (`V` line).
+int nx_workload_real(const char* spec, const nx_engine_config* cfg, uint64_t seed, char** trace, size_t* len) {
+  return guard([&] {
+    need(spec, "spec");
+    need(cfg, "cfg");
+    need(trace, "trace");
+    const workload::Spec ws = workload::parse(spec);
+    EngineConfig ec = to_cpp(*cfg);
+    ec.gpu_capacity = ws.hw.tier_capacity[0];
+    ec.pinned_capacity = ws.hw.tier_capacity[1];
+    ec.paged_capacity = ws.hw.tier_capacity[2];
+    SwapEngine eng(ec);
+    std::string extra;
+    std::size_t k = 0;
+    workload::Runner runner = [&](const MigrationPlan& plan, MemState& mem, const HardwareConfig& hw, const PlannerConfig& pc,
+                                  Seconds now, std::array<std::vector<std::array<std::uint64_t, 3>>, 6>& lanes) {
+      MemState model = mem;
+      const ExecResult m = execute(plan, model, hw, pc, now);
+      eng.execute(plan, pc);
+      const auto& t = eng.lane_trace();
+      for (int l = 0; l < 6; ++l)
+        for (const LegTrace& x : t[l])
+          lanes[l].push_back({x.block, static_cast<std::uint64_t>(x.src), static_cast<std::uint64_t>(x.dst)});
+      std::uint64_t differ = 0;
+      for (std::size_t b = 0; b < mem.block_count(); ++b)
+        if (mem.block(b).alive && mem.block(b).loc.tier != model.block(b).loc.tier) ++differ;
+      const SwitchStats& s = eng.last_stats();
+      AppId incoming = kNoApp;
+      for (const Move& mv : plan.moves)
+        if (mv.kind == MoveKind::FetchForIncoming) {
+          incoming = mem.block(mv.block).app;
+          break;
+        }
+      extra += "M " + std::to_string(k) + " " + std::to_string(differ) + "\n";
+      if (incoming != kNoApp)
+        extra += "V " + std::to_string(k) + " " + std::to_string(incoming) + " " + std::to_string(eng.verify_pattern(incoming, seed)) +
+                 " verified " + std::to_string(s.verified) + " unverified " + std::to_string(s.unverified) + "\n";
+      ++k;
+      return m.completion;
+    };
+    workload::Engine we(ws, eng.mem(), runner);
+    const workload::Result r = we.run([&](AppId a, Bytes size, TierId tier) {
+      eng.allocate(a, size, tier);
+      eng.fill_pattern(a, seed);
+    });
+    std::string out = r.trace + extra;
+    for (const workload::AppSpec& a : ws.apps)
       out += "F " + std::to_string(a.id) + " " + std::to_string(eng.verify_pattern(a.id, seed)) + "\n";
     *trace = dup_out(out, len);
   });

@@ -326,6 +326,25 @@ def run_scenario_real(spec: str, seed: int = 0x4E495849, config: Optional[Engine
     return L.take_string(p, n)
 
 
+def run_workload_model(spec: str) -> str:
+    """MLFQ-driven workload on the virtual clock (no GPU); its reference twin is
+    oracle/_ref/ref_workload (same engine over the reference library)."""
+    p, n = c_void_p(), c_size_t()
+    check(lib.nx_workload_model(spec.encode(), byref(p), byref(n)))
+    return L.take_string(p, n)
+
+
+def run_workload_real(spec: str, seed: int = 0x4E495849, config: Optional[EngineConfig] = None, **overrides) -> str:
+    """The same workload with every switch's bytes moved by the CUDA engine
+    (M/V/F lines: placement vs the model, byte checks)."""
+    cfg = config or EngineConfig()
+    for k, v in overrides.items():
+        setattr(cfg, k, v)
+    p, n = c_void_p(), c_size_t()
+    check(lib.nx_workload_real(spec.encode(), byref(cfg.to_c()), seed, byref(p), byref(n)))
+    return L.take_string(p, n)
+
+
 def parse_path(name: str) -> int:
     """'auto' | 'sm' | 'ce' -> PATH_* constant."""
     return {"auto": L.PATH_AUTO, "sm": L.PATH_SM, "ce": L.PATH_CE}[name]

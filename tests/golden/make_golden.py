@@ -8,6 +8,12 @@ Outputs
                    summary lines, and the full trace when it is small
   random_tiny.json 120 seeded random tiny scenarios: spec + full reference
                    trace, or the reference's error class
+  workloads.json   MLFQ-driven workloads through oracle/_ref/ref_workload (the
+                   shared workload engine over the reference): config 3
+                   (paper_2601_11743_b200/workloads/*.wl) and 60 seeded random
+                   small ones: sha256 of the trace (or the error class) and the
+                   X/S/Q summary lines of config 3
+(`--workloads` regenerates only workloads.json.)
 """
 import glob
 import hashlib
@@ -20,6 +26,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, os.path.dirname(HERE))
 from scenario_gen import random_scenario  # noqa: E402
+from workload_gen import random_workload  # noqa: E402
 
 REF = os.path.join(ROOT, "oracle", "_ref", "ref_trace")
 DET = ("S", "P", "L", "R", "B", "E")
@@ -80,5 +87,36 @@ def main():
     print("scenarios:", len(out), "random:", len(rnd), "errors:", sum(1 for r in rnd if r["error"]))
 
 
+REF_WL = os.path.join(ROOT, "oracle", "_ref", "ref_workload")
+
+
+def ref_workload(spec: str):
+    p = subprocess.run([REF_WL, "-"], input=spec, capture_output=True, text=True)
+    if p.returncode != 0:
+        return None, p.stderr.strip().removeprefix("ref_workload: ").split(":", 1)[0]
+    return p.stdout, None
+
+
+def main_workloads():
+    out = {"c3": {}, "random": {}}
+    for path in sorted(glob.glob(os.path.join(ROOT, "paper_2601_11743_b200", "workloads", "*.wl"))):
+        trace, err = ref_workload(open(path).read())
+        assert err is None, (path, err)
+        out["c3"][os.path.basename(path)] = {"sha256": sha(trace),
+                                             "summary": [ln for ln in trace.splitlines() if ln[0] in "XSQ"]}
+    for seed in range(60):
+        spec = random_workload(seed)
+        trace, err = ref_workload(spec)
+        out["random"][str(seed)] = {"spec_sha256": sha(spec), "sha256": sha(trace) if trace else None, "error": err}
+    with open(os.path.join(HERE, "workloads.json"), "w") as f:
+        json.dump(out, f, indent=0, sort_keys=True)
+    print("workloads: c3", len(out["c3"]), "random", len(out["random"]),
+          "errors", sum(1 for r in out["random"].values() if r["error"]))
+
+
 if __name__ == "__main__":
-    main()
+    if "--workloads" in sys.argv:
+        main_workloads()
+    else:
+        main()
+        main_workloads()

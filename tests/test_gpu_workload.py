@@ -22,3 +22,38 @@ def test_small_mix_fast_switches(gpu):
             AppSpec(2, "c", 0.5, burst=3, kernel_ms=5, think_s=0.2)]  # all idle > 100 ms between requests
     r = run_workload(apps, horizon_s=4.0, gpu_gib=1, pinned_gib=1, paged_gib=2)
     assert r["errors"] == [] and r["byte_exact"] and r["switches"] >= 4
+
+
+C3_SMALL = """
+# config 3 scaled down 8x (capacities and working sets), same MLFQ constants
+capacity gpu 4GiB
+capacity pinned 2GiB
+capacity paged 32GiB
+link 0 64GiB/s 64GiB/s full
+link 1 32GiB/s 32GiB/s full
+dispatch 5e-6
+mlfq 4 8 4 0.1 0.01
+seed 0x4E495849
+horizon 40
+interactive 0 2GiB paged 0.0 3 5 0.02 0.1
+interactive 1 3GiB paged 0.3 12 40 0.05 0.1
+batch 2 1536MiB paged 0.6 0.04 16
+"""
+
+
+def test_mlfq_workload_real_bytes_follow_reference_decisions(gpu):
+    """The config-3 workload's decisions on the virtual clock (identical to the
+    reference's, tests/test_parity_workload.py) with every switch's bytes moved
+    by the CUDA engine: same trace, the engine's placement equals the model's
+    after every switch, every restore byte-exact."""
+    from paper_2601_11743_b200 import run_workload_model, run_workload_real
+    model = run_workload_model(C3_SMALL)
+    real = run_workload_real(C3_SMALL)
+    core = [ln for ln in real.splitlines() if ln[0] not in "MVF"]
+    assert core == model.splitlines()
+    ms = [ln.split() for ln in real.splitlines() if ln.startswith("M ")]
+    vs = [ln.split() for ln in real.splitlines() if ln.startswith("V ")]
+    fs = [ln.split() for ln in real.splitlines() if ln.startswith("F ")]
+    assert len(ms) >= 5 and all(m[2] == "0" for m in ms)
+    assert vs and all(v[3] == "0" for v in vs)
+    assert len(fs) == 3 and all(f[2] == "0" for f in fs)
