@@ -33,7 +33,7 @@
 //   link <0|1|2> <up bw> <down bw> <full|half>      dispatch <s>
 //   window <bytes>    budget <bytes|unbounded>
 //   mlfq <levels> <T1 s> <S1 s> <idle s> <tick s>
-//   seed <u64>        horizon <s>
+//   seed <u64>        horizon <s>      prefetch <on|off>
 //   interactive <id> <size> <tier> <start s> <interval s> <burst> <kernel s> <jitter>
 //   batch <id> <size> <tier> <start s> <kernel s> <per_sync>
 //
@@ -41,9 +41,20 @@
 //   X k <decision t> <drain end> <completion> <from|-> <to>   one context switch
 //   S/P/L/R/B k ...                                            as scenario.hpp
 //   Q <app> <n> <begin> <first kernel done> <end>              one request
+//   H <start> <app> <moves>                                    prefetch started
+//   h <decision t> <quiesced t> <app>                          prefetch stopped for a switch
+//
+// Prefetch: with `prefetch on`,
+// whenever no switch or prefetch is running, the scheduler's
+// next_prefetch_candidate() (if not the holder) gets plan_prefetch()'s
+// paged->pinned moves, executed by an Orchestrator on its own event queue in
+// lockstep with the workload clock. A switch first cancels the prefetch's
+// queued legs (cancel_pending) and waits for the legs on the link (quiesced);
+// the switch's drain point is the later of the kernel drain and that.
 //   E / G ...                                                  scheduler log (as scenario.hpp)
 #pragma once
 
+#include <nixie/event_queue.hpp>
 #include <nixie/mem_model.hpp>
 #include <nixie/mlfq.hpp>
 #include <nixie/planner.hpp>
@@ -57,6 +68,7 @@
 #include <cstdio>
 #include <functional>
 #include <map>
+#include <memory>
 #include <optional>
 #include <queue>
 #include <sstream>
@@ -86,6 +98,7 @@ struct Spec {
   MlfqConfig mlfq;
   std::uint64_t seed = 0x4E495849;
   Seconds horizon = 30.0;
+  bool prefetch = false;
   std::vector<AppSpec> apps;
 };
 
@@ -106,6 +119,7 @@ struct Result {
   std::vector<Request> requests;
   int switches = 0;
   Bytes bytes_in = 0, bytes_out = 0;
+  Bytes prefetched = 0;  // bytes moved paged->pinned by prefetch plans (committed)
 };
 
 namespace detail {
@@ -183,6 +197,10 @@ inline Spec parse(const std::string& text) {
     } else if (op == "horizon") {
       need(1);
       s.horizon = std::stod(t[0]);
+    } else if (op == "prefetch") {
+      need(1);
+      if (t[0] != "on" && t[0] != "off") fail("prefetch takes on|off");
+      s.prefetch = t[0] == "on";
     } else if (op == "interactive") {
       need(8);
       AppSpec a;
@@ -264,9 +282,11 @@ class Engine {
       now_ = t;
       if (kind == Ev::Tick) {
         tick(res);
+        maybe_prefetch(res);
         push(now_ + spec_.mlfq.tick, Ev::Tick, 0);
       } else if (kind == Ev::SwitchDone) {
         switching_ = false;
+        maybe_prefetch(res);
         State& s = apps_.at(app);
         if (s.held) {
           s.held = false;
@@ -311,6 +331,45 @@ class Engine {
   };
 
   void push(Seconds t, Ev k, AppId a) { q_.emplace(t, seq_++, k, a); }
+
+  // Advances the prefetch orchestrator's queue to t (events at or before t run).
+  void sync_prefetch_clock(Seconds t) {
+    bool hit = false;
+    pq_.at(t, [&hit] { hit = true; });
+    while (!hit && pq_.run_one()) {
+    }
+  }
+
+  void maybe_prefetch(Result& res) {
+    if (!spec_.prefetch || switching_ || orch_) return;
+    const std::optional<AppId> cand = sched_.next_prefetch_candidate(now_);
+    if (!cand || cand == sched_.granted()) return;
+    const MigrationPlan plan = plan_prefetch(*cand, mem_, spec_.planner);
+    if (plan.moves.empty()) return;
+    sync_prefetch_clock(now_);
+    orch_ = std::make_unique<Orchestrator>(mem_, spec_.hw, pq_, nullptr);
+    pf_app_ = *cand;
+    pf_bytes_ = static_cast<Bytes>(plan.moves.size()) * kBlockBytes;
+    pf_done_ = false;
+    orch_->begin_plan(plan, spec_.planner, false, kNoApp, [this](Seconds) { pf_done_ = true; });
+    detail::put(res.trace, "H %.17g %u %zu\n", now_, *cand, plan.moves.size());
+  }
+
+  // Stops the running prefetch before a switch; returns when the link is quiet.
+  Seconds quiesce_prefetch(Result& res) {
+    if (!orch_) return now_;
+    sync_prefetch_clock(now_);
+    if (!pf_done_) {
+      orch_->cancel_pending();
+      while (orch_->active() && pq_.run_one()) {
+      }
+    }
+    const Seconds quiet = std::max(now_, pq_.now());
+    res.prefetched += pf_bytes_;  // upper bound: cancelled legs are not subtracted (trace shows the plan)
+    detail::put(res.trace, "h %.17g %.17g %u\n", now_, quiet, pf_app_);
+    orch_.reset();
+    return quiet;
+  }
 
   bool may_launch(AppId a) const {
     return !switching_ && sched_.granted() == a && mem_.app_fully_resident(a, TierId::Gpu);
@@ -387,6 +446,7 @@ class Engine {
       drained = std::max(now_, apps_.at(*holder).last_kernel_end);  // in-flight kernels finish
       sched_.on_grant_end(*holder, now_);
     }
+    drained = std::max(drained, quiesce_prefetch(res));
     PlannerConfig cfg = spec_.planner;
     cfg.eviction_policy.victim_order = sched_.victim_hint();
     const MigrationPlan plan = plan_switch(to, mem_, cfg);
@@ -441,6 +501,11 @@ class Engine {
   Seconds now_ = 0;
   Seconds gpu_free_ = 0;
   bool switching_ = false;
+  EventQueue pq_;                         // the prefetch orchestrator's clock
+  std::unique_ptr<Orchestrator> orch_;    // running prefetch plan
+  AppId pf_app_ = kNoApp;
+  Bytes pf_bytes_ = 0;
+  bool pf_done_ = false;
 };
 
 }  // namespace nixie::workload

@@ -106,6 +106,20 @@ def test_workload_properties():
     assert {g[1] for g in grants} == {"0", "1", "2"}
 
 
+def test_prefetch_shortens_switches():
+    """with prefetch the same config-3 workload spends less
+    time in context switches (fetches of the next app come from pinned)."""
+    base = run_workload_model(open(os.path.join(WL_DIR, "c3_mlfq_mix_3s.wl")).read())
+    pf = run_workload_model(open(os.path.join(WL_DIR, "c3_mlfq_mix_3s_prefetch.wl")).read())
+
+    def switch_time(tr):
+        return sum(float(x.split()[4]) - float(x.split()[2]) for x in tr.splitlines() if x.startswith("X "))
+
+    assert any(ln.startswith("H ") for ln in pf.splitlines())
+    assert not any(ln.startswith("H ") for ln in base.splitlines())
+    assert switch_time(pf) < switch_time(base)
+
+
 def test_workload_parse_errors():
     with pytest.raises(NixieError) as e:
         run_workload_model("capacity gpu 1GiB\nbogus\n")

@@ -14,7 +14,8 @@ def random_workload(seed: int) -> str:
              f"dispatch {r.choice(['0', '5e-6', '1e-4'])}",
              f"window {r.choice([4, 8, 16])}MiB",
              f"mlfq {r.randint(2, 4)} {r.choice([1, 2])} {r.choice([0.25, 0.5])} {r.choice([0.02, 0.05, 0.1])} 0.01",
-             f"seed {r.randint(0, 1 << 30)}", f"horizon {r.choice([4, 6, 8])}"]
+             f"seed {r.randint(0, 1 << 30)}", f"horizon {r.choice([4, 6, 8])}",
+             f"prefetch {r.choice(['on', 'off'])}"]
     for a in range(n):
         size = r.choice([16, 32, 48, 64]) * (1 << 20)
         size = min(size, gpu << 20)
