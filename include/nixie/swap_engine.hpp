@@ -165,6 +165,18 @@ class SwapEngine {
   // plan_switch + execute.
   ExecResult switch_to(AppId incoming, const PlannerConfig& cfg, cudaStream_t drain = nullptr);
 
+  // Prefetch: runs a plan_prefetch() plan (paged -> pinned)
+  // on the host copy pool in the background. The caller's thread owns the
+  // registry: prefetch_pump() commits finished legs and starts queued ones
+  // (call it periodically; true while active). prefetch_quiesce() is the
+  // reference's cancel_pending + wait-until-quiesced (transfer.cpp:89-113):
+  // queued legs are dropped, legs on the pool land. execute() quiesces first.
+  void prefetch_begin(const MigrationPlan& plan);
+  bool prefetch_pump();
+  void prefetch_quiesce();
+  bool prefetch_active() const;
+  Bytes prefetched_bytes() const;  // committed since construction
+
   const SwitchStats& last_stats() const;
   const std::array<std::vector<LegTrace>, 6>& lane_trace() const;  // per lane, start order, last execute
   std::uint64_t total_launches() const;  // kernels this engine has launched (all kinds)
@@ -247,6 +259,12 @@ class LaunchGate {
   std::optional<AppId> select_next(Seconds now);
   std::optional<AppId> granted();
   std::uint64_t switches() const;
+  // MLFQ prefetch: when on, every tick that does not switch
+  // pumps the engine's prefetch and, when none runs, starts plan_prefetch()
+  // for next_prefetch_candidate() (if it is not the holder). A switch
+  // quiesces it first.
+  void set_prefetch(bool on);
+  Bytes prefetched_bytes() const;
 
  private:
   struct Impl;

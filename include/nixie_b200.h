@@ -154,6 +154,14 @@ int nx_plan(nx_engine* e, uint32_t incoming, const nx_planner_config* cfg, char*
  * and host memcpy legs. drain_stream (cudaStream_t, may be NULL) is the
  * incumbent's stream; evictions wait for its queued kernels on the device. */
 int nx_switch(nx_engine* e, uint32_t incoming, const nx_planner_config* cfg, void* drain_stream, nx_switch_stats* out);
+/* Prefetch: plan_prefetch(app) (planner.cpp:218-242) started
+ * in the background on the host copy pool (*moves = its size, 0 = nothing to
+ * do); pump commits finished legs and starts queued ones (*active = 0 when
+ * done); quiesce = Orchestrator::cancel_pending + wait until quiesced
+ * (transfer.cpp:89-113). nx_switch quiesces first. */
+int nx_prefetch_begin(nx_engine* e, uint32_t app, const nx_planner_config* cfg, uint64_t* moves);
+int nx_prefetch_pump(nx_engine* e, int* active);
+int nx_prefetch_quiesce(nx_engine* e, uint64_t* committed_bytes);
 /* Per-lane leg sequence of the last switch (lane = 2*link + (up ? 0 : 1),
  * transfer.cpp:39-45), in start order. */
 int nx_lane_trace(nx_engine* e, int lane, uint64_t* blocks, uint8_t* src, uint8_t* dst, size_t cap, size_t* n);
@@ -202,6 +210,12 @@ int nx_gate_api_event(nx_gate* g, uint32_t app, double now, int kind);
  * UINT32_MAX when nothing switched. */
 int nx_gate_tick(nx_gate* g, double now, uint32_t* switched_to);
 uint64_t nx_gate_switches(nx_gate* g);
+/* MLFQ prefetch (plan_prefetch planner.cpp:218-242,
+ * next_prefetch_candidate mlfq.cpp:164-166, cancel_pending transfer.cpp:89-113):
+ * ticks that do not switch move the next candidate's pageable blocks to the
+ * pinned tier on the host copy pool; a switch quiesces it first. */
+int nx_gate_set_prefetch(nx_gate* g, int on);
+uint64_t nx_gate_prefetched_bytes(nx_gate* g);
 /* Synthetic application kernel: occupies one warp for ~ns on `stream`. */
 int nx_launch_busy_kernel(void* stream, uint64_t ns);
 /* MlfqScheduler::select_next (mlfq.cpp:144-162); *app = UINT32_MAX if none. */

@@ -113,6 +113,9 @@ _SIGNATURES = [
     ("nx_plan", c_int, [c_void_p, c_uint32, POINTER(PlannerConfigC), POINTER(c_char), c_size_t, POINTER(c_size_t),
                         POINTER(c_uint64), POINTER(c_uint64)]),
     ("nx_switch", c_int, [c_void_p, c_uint32, POINTER(PlannerConfigC), c_void_p, POINTER(SwitchStatsC)]),
+    ("nx_prefetch_begin", c_int, [c_void_p, c_uint32, POINTER(PlannerConfigC), POINTER(c_uint64)]),
+    ("nx_prefetch_pump", c_int, [c_void_p, POINTER(c_int)]),
+    ("nx_prefetch_quiesce", c_int, [c_void_p, POINTER(c_uint64)]),
     ("nx_lane_trace", c_int, [c_void_p, c_int, POINTER(c_uint64), POINTER(c_uint8), POINTER(c_uint8), c_size_t,
                               POINTER(c_size_t)]),
     ("nx_total_launches", c_uint64, [c_void_p]),
@@ -133,6 +136,8 @@ _SIGNATURES = [
     ("nx_gate_api_event", c_int, [c_void_p, c_uint32, c_double, c_int]),
     ("nx_gate_tick", c_int, [c_void_p, c_double, POINTER(c_uint32)]),
     ("nx_gate_switches", c_uint64, [c_void_p]),
+    ("nx_gate_set_prefetch", c_int, [c_void_p, c_int]),
+    ("nx_gate_prefetched_bytes", c_uint64, [c_void_p]),
     ("nx_launch_busy_kernel", c_int, [c_void_p, c_uint64]),
     ("nx_gate_select_next", c_int, [c_void_p, c_double, POINTER(c_uint32)]),
     ("nx_gate_switch", c_int, [c_void_p, c_uint32, c_double, POINTER(SwitchStatsC)]),

@@ -344,6 +344,31 @@ int nx_switch(nx_engine* e, uint32_t incoming, const nx_planner_config* cfg, voi
   });
 }
 
+int nx_prefetch_begin(nx_engine* e, uint32_t app, const nx_planner_config* cfg, uint64_t* moves) {
+  return guard([&] {
+    need(e, "engine");
+    const MigrationPlan plan = plan_prefetch(app, e->eng->mem(), to_cpp(cfg));
+    if (moves) *moves = plan.moves.size();
+    if (!plan.moves.empty()) e->eng->prefetch_begin(plan);
+  });
+}
+
+int nx_prefetch_pump(nx_engine* e, int* active) {
+  return guard([&] {
+    need(e, "engine");
+    const bool a = e->eng->prefetch_pump();
+    if (active) *active = a ? 1 : 0;
+  });
+}
+
+int nx_prefetch_quiesce(nx_engine* e, uint64_t* committed_bytes) {
+  return guard([&] {
+    need(e, "engine");
+    e->eng->prefetch_quiesce();
+    if (committed_bytes) *committed_bytes = e->eng->prefetched_bytes();
+  });
+}
+
 int nx_lane_trace(nx_engine* e, int lane, uint64_t* blocks, uint8_t* src, uint8_t* dst, size_t cap, size_t* n) {
   return guard([&] {
     need(e, "engine");
@@ -520,6 +545,15 @@ int nx_gate_tick(nx_gate* g, double now, uint32_t* switched_to) {
 }
 
 uint64_t nx_gate_switches(nx_gate* g) { return g ? g->gate->switches() : 0; }
+
+int nx_gate_set_prefetch(nx_gate* g, int on) {
+  return guard([&] {
+    need(g, "gate");
+    g->gate->set_prefetch(on != 0);
+  });
+}
+
+uint64_t nx_gate_prefetched_bytes(nx_gate* g) { return g ? g->gate->prefetched_bytes() : 0; }
 
 int nx_launch_busy_kernel(void* stream, uint64_t ns) {
   return guard([&] {

@@ -638,7 +638,73 @@ struct SwapEngine::Impl final : detail::LaneSink {
     return progress;
   }
 
+  // ---- prefetch (reference plan_prefetch, planner.cpp:218-242,
+  // run by an Orchestrator and preempted with cancel_pending,
+  // transfer.cpp:89-113): paged -> pinned host legs on the copy pool while
+  // the current app computes. The owning thread pumps it; commits happen in
+  // the pump, so the registry stays single-writer.
+  static constexpr std::uint64_t kPrefetchTag = 1ull << 62;
+  struct PfLeg {
+    BlockId block;
+    std::uint32_t src_u, dst_u;
+    bool done;
+  };
+  std::deque<BlockId> pf_queue;   // not started
+  std::deque<PfLeg> pf_inflight;  // started, FIFO
+  Bytes pf_committed = 0;
+
+  void prefetch_begin(const MigrationPlan& plan) {
+    if (!pf_queue.empty() || !pf_inflight.empty()) throw SimError(Err::InvalidState, "a prefetch is already running");
+    for (const Move& m : plan.moves)
+      if (m.kind != MoveKind::PrefetchToPinned || m.src != TierId::PagedHost || m.dst != TierId::PinnedHost)
+        throw SimError(Err::InvalidState, "prefetch plans move paged -> pinned only");
+    for (const Move& m : plan.moves) pf_queue.push_back(m.block);
+    prefetch_pump();
+  }
+
+  bool prefetch_pump() {
+    static thread_local std::vector<std::uint64_t> toks;
+    toks.clear();
+    if (pool.drain(toks))
+      for (auto t : toks) {
+        if (!(t & kPrefetchTag)) throw InvariantViolation("host copy completion outside a switch");
+        for (PfLeg& L : pf_inflight)
+          if (L.block == (t & ~kPrefetchTag)) L.done = true;
+      }
+    while (!pf_inflight.empty() && pf_inflight.front().done) {
+      const PfLeg L = pf_inflight.front();
+      pf_inflight.pop_front();
+      mem.commit_move(L.block, TierId::PinnedHost);
+      give_unit(TierId::PagedHost, L.block, L.src_u);
+      unit[L.block] = L.dst_u;
+      pf_committed += kBlockBytes;
+    }
+    while (!pf_queue.empty() && static_cast<int>(pf_inflight.size()) < cfg.host_legs_in_flight) {
+      const BlockId b = pf_queue.front();
+      pf_queue.pop_front();
+      const Location& loc = mem.block(b).loc;
+      if (!loc.is_resident() || loc.tier != TierId::PagedHost) continue;  // moved since planned
+      if (mem.tier(TierId::PinnedHost).free_bytes() < kBlockBytes) {  // room went to a switch: stop here
+        pf_queue.clear();
+        break;
+      }
+      mem.begin_move(b, TierId::PinnedHost, false);
+      const std::uint32_t dst = take_unit(TierId::PinnedHost, b);
+      pf_inflight.push_back(PfLeg{b, unit[b], dst, false});
+      pool.submit(pinned.host(dst), paged.unit(unit[b]), kBlockBytes, kPrefetchTag | b);
+    }
+    return !pf_queue.empty() || !pf_inflight.empty();
+  }
+
+  // cancel_pending + wait until quiesced: queued legs are dropped (their
+  // blocks stay where they are), legs on the copy pool land and commit.
+  void prefetch_quiesce() {
+    pf_queue.clear();
+    while (prefetch_pump()) std::this_thread::yield();
+  }
+
   ExecResult execute(const MigrationPlan& plan, const PlannerConfig& pcfg, const ExecOptions& o) {
+    if (!pf_queue.empty() || !pf_inflight.empty()) prefetch_quiesce();  // plan_switch needs a quiescent registry
     for (const Move& m : plan.moves)
       if (m.src == TierId::Disk || m.dst == TierId::Disk)
         throw SimError(Err::InvalidState, "plan touches the disk tier, which the CUDA swap engine does not back");
@@ -851,6 +917,11 @@ std::int64_t SwapEngine::frame_index(BlockId b) const {
 
 std::uint32_t SwapEngine::arena_frames() const { return impl_->arena.ring.units(); }
 void SwapEngine::set_frame_placer(FramePlacer* placer) { impl_->placer = placer; }
+void SwapEngine::prefetch_begin(const MigrationPlan& plan) { impl_->prefetch_begin(plan); }
+bool SwapEngine::prefetch_pump() { return impl_->prefetch_pump(); }
+void SwapEngine::prefetch_quiesce() { impl_->prefetch_quiesce(); }
+bool SwapEngine::prefetch_active() const { return !impl_->pf_queue.empty() || !impl_->pf_inflight.empty(); }
+Bytes SwapEngine::prefetched_bytes() const { return impl_->pf_committed; }
 void SwapEngine::set_progress_hook(std::function<void()> hook) { impl_->progress = std::move(hook); }
 
 int SwapEngine::arena_export_fd(std::uint32_t slab) const {

@@ -46,6 +46,7 @@ struct LaunchGate::Impl {
   std::map<AppId, std::unique_ptr<std::mutex>> launch; // check-and-launch atomicity
   std::uint64_t switches = 0;
   AppId incoming = kNoApp;  // swap-in submitted, grant not yet recorded
+  bool prefetch = false;
 
   Impl(SwapEngine& e, MlfqScheduler& s, PlannerConfig c) : eng(e), sched(s), cfg(std::move(c)) {}
   ~Impl() {
@@ -148,6 +149,7 @@ ExecResult LaunchGate::context_switch(AppId to, Seconds now) {
   }
   {
     std::lock_guard<std::mutex> lk(g.mu);
+    g.eng.prefetch_quiesce();  // cancel_pending + quiesced: plan_switch needs a quiescent registry
     g.cfg.eviction_policy.victim_order = g.sched.victim_hint();
     plan = plan_switch(to, g.eng.mem(), g.cfg);
     rel.event = g.landed[to];
@@ -171,17 +173,37 @@ std::optional<AppId> LaunchGate::tick(Seconds now) {
   Impl& g = *impl_;
   std::optional<AppId> next;
   {
+    std::lock_guard<std::mutex> serial(g.switch_mu);
     std::lock_guard<std::mutex> lk(g.mu);
     g.sched.infer_all(now);
     next = g.sched.select_next(now);
-    if (!next) return std::nullopt;
     const std::optional<AppId> holder = g.sched.granted();
-    const bool go = !holder || g.sched.is_idle(*holder, now) || g.sched.should_preempt(*holder, now);
-    if (!go) return std::nullopt;
+    const bool go = next && (!holder || g.sched.is_idle(*holder, now) || g.sched.should_preempt(*holder, now));
+    if (!go) {
+      if (g.prefetch && !g.eng.prefetch_pump()) {
+        const std::optional<AppId> cand = g.sched.next_prefetch_candidate(now);
+        if (cand && cand != holder) {
+          const MigrationPlan pf = plan_prefetch(*cand, g.eng.mem(), g.cfg);
+          if (!pf.moves.empty()) g.eng.prefetch_begin(pf);
+        }
+      }
+      return std::nullopt;
+    }
   }
   context_switch(*next, now);
   return next;
 }
+
+void LaunchGate::set_prefetch(bool on) {
+  std::lock_guard<std::mutex> serial(impl_->switch_mu);
+  impl_->prefetch = on;
+  if (!on) {
+    std::lock_guard<std::mutex> lk(impl_->mu);
+    impl_->eng.prefetch_quiesce();
+  }
+}
+
+Bytes LaunchGate::prefetched_bytes() const { return impl_->eng.prefetched_bytes(); }
 
 std::optional<AppId> LaunchGate::select_next(Seconds now) {
   std::lock_guard<std::mutex> lk(impl_->mu);

@@ -172,6 +172,25 @@ class SwapEngine:
         del keep
         return st.as_dict()
 
+    def prefetch_begin(self, app: int, planner: Optional[PlannerConfig] = None) -> int:
+        """Starts plan_prefetch(app) in the background; returns its move count."""
+        pc, keep = (planner or PlannerConfig()).to_c()
+        n = c_uint64()
+        check(lib.nx_prefetch_begin(self._h, app, byref(pc), byref(n)))
+        del keep
+        return n.value
+
+    def prefetch_pump(self) -> bool:
+        a = c_int()
+        check(lib.nx_prefetch_pump(self._h, byref(a)))
+        return bool(a.value)
+
+    def prefetch_quiesce(self) -> int:
+        """cancel_pending + quiesced; returns bytes committed by prefetch so far."""
+        b = c_uint64()
+        check(lib.nx_prefetch_quiesce(self._h, byref(b)))
+        return b.value
+
     def lane_trace(self, lane: int) -> List[Tuple[int, str, str]]:
         n = c_size_t()
         check(lib.nx_lane_trace(self._h, lane, None, None, None, 0, byref(n)))
@@ -285,6 +304,13 @@ class LaunchGate:
 
     def switches(self) -> int:
         return int(lib.nx_gate_switches(self._h))
+
+    def set_prefetch(self, on: bool) -> None:
+        """MLFQ prefetch of the next candidate's pageable blocks."""
+        check(lib.nx_gate_set_prefetch(self._h, 1 if on else 0))
+
+    def prefetched_bytes(self) -> int:
+        return int(lib.nx_gate_prefetched_bytes(self._h))
 
     def select_next(self, now: float) -> Optional[int]:
         a = c_uint32()

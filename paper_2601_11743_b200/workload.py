@@ -58,7 +58,7 @@ def _pct(xs: List[float], q: float) -> Optional[float]:
 
 
 def run_workload(apps: List[AppSpec], horizon_s: float = 30.0, gpu_gib: int = 32, pinned_gib: int = 16,
-                 paged_gib: int = 64, seed: int = 0x4E495849, tick_s: float = 0.01) -> Dict:
+                 paged_gib: int = 64, seed: int = 0x4E495849, tick_s: float = 0.01, prefetch: bool = False) -> Dict:
     eng = E.SwapEngine(gpu_capacity=gpu_gib * GIB, pinned_capacity=pinned_gib * GIB, paged_capacity=paged_gib * GIB)
     gate = None
     streams = {}
@@ -73,6 +73,7 @@ def run_workload(apps: List[AppSpec], horizon_s: float = 30.0, gpu_gib: int = 32
             eng.allocate(a.app, size, tier)
             eng.fill_pattern(a.app, seed)
         gate = E.LaunchGate(eng, E.PlannerConfig(pinned_budget=pinned_gib * GIB))
+        gate.set_prefetch(prefetch)
         for a in apps:
             streams[a.app] = E.stream_create()
             gate.attach(a.app, streams[a.app], 0.0)
@@ -144,7 +145,8 @@ def run_workload(apps: List[AppSpec], horizon_s: float = 30.0, gpu_gib: int = 32
                 "request_ms": {"p50": _ms(_pct(d, 0.5)), "p99": _ms(_pct(d, 0.99)), "mean": _ms(statistics.mean(d) if d else None)},
             }
         return {"horizon_s": horizon_s, "switches": gate.switches(), "per_app": per_app, "byte_exact": bad == 0,
-                "errors": errors, "apps": [a.__dict__ for a in apps]}
+                "errors": errors, "apps": [a.__dict__ for a in apps], "prefetch": prefetch,
+                "prefetched_bytes": gate.prefetched_bytes(), "pinned_gib": pinned_gib}
     finally:
         if gate is not None:
             gate.close()

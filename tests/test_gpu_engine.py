@@ -162,3 +162,36 @@ def test_calibration_and_probe(gpu):
             assert p[k] > 5.0, p
         c = e.calibrate(64 * MIB)
         assert len(c["legs"]) == 8 and all(x > 1.0 for x in c["ce_gbps"] + c["sm_gbps"])
+
+
+def test_prefetch_then_switch_is_byte_exact(gpu):
+    """Prefetch: the next app's pageable blocks move to the
+    pinned tier in the background (host copy pool) while the incumbent owns the
+    GPU; the later switch fetches them from pinned, byte-exact. A prefetch
+    still running when the switch comes is quiesced first (cancel_pending)."""
+    with SwapEngine(gpu_capacity=64 * MIB, pinned_capacity=96 * MIB, paged_capacity=256 * MIB) as e:
+        e.allocate(0, 64 * MIB, TIER_GPU)
+        e.allocate(1, 48 * MIB, TIER_PAGED)
+        e.allocate(2, 48 * MIB, TIER_PAGED)
+        for a in (0, 1, 2):
+            e.fill_pattern(a, SEED)
+        pc = PlannerConfig(streaming_window=8 * MIB, victim_order=[0])
+        assert e.prefetch_begin(1, pc) == 24
+        while e.prefetch_pump():
+            pass
+        assert e.prefetch_quiesce() == 48 * MIB
+        assert e.app_bytes_resident(1)[1] == 48 * MIB  # all of app 1 now in pinned
+        e.audit()
+        st = e.switch_to(1, pc)
+        assert st["bytes_in"] == 48 * MIB
+        app1 = set(e.app_blocks(1))
+        assert not [b for b, src, dst in e.lane_trace(2) if b in app1]  # nothing of app 1 came up from paged
+        assert e.verify_pattern(1, SEED) == 0
+        # cancelled mid-way: the switch quiesces the prefetch first
+        pc2 = PlannerConfig(streaming_window=8 * MIB, victim_order=[1, 0])
+        n = e.prefetch_begin(2, pc2)
+        assert n > 0
+        st = e.switch_to(2, pc2)
+        e.audit()
+        for a in (0, 1, 2):
+            assert e.verify_pattern(a, SEED) == 0
