@@ -69,6 +69,7 @@ struct Options {
   double ack_timeout_s = 60.0;
   int exit_after_apps = 0;         // exit once this many apps have come and gone (tests)
   int phys_slack_slabs = 16;       // physical slabs beyond the budget (partly resident slabs)
+  bool prefetch = false;           // MLFQ prefetch of the next candidate
 };
 
 Bytes parse_size(const char* s) {
@@ -87,7 +88,7 @@ void usage() {
                "usage: nixied [--socket PATH] [--device N] [--gpu SIZE] [--pinned SIZE] [--paged SIZE]\n"
                "              [--window SIZE] [--min-bytes SIZE] [--path auto|ce|sm] [--host-threads N]\n"
                "              [--tick-ms X] [--idle-ms X] [--allot-s X] [--preempt-s X] [--log FILE]\n"
-               "              [--phys-slack SLABS] [--exit-after-apps N]\n"
+               "              [--phys-slack SLABS] [--prefetch] [--exit-after-apps N]\n"
                "sizes take a K/M/G suffix (GiB when bare). The daemon serves LD_PRELOAD=libnixie_shim.so apps\n"
                "that set NIXIE_SOCKET=PATH.\n");
 }
@@ -119,6 +120,7 @@ bool parse_args(int argc, char** argv, Options& o) {
     else if (a == "--log") o.log_path = val();
     else if (a == "--exit-after-apps") o.exit_after_apps = std::atoi(val());
     else if (a == "--phys-slack") o.phys_slack_slabs = std::atoi(val());
+    else if (a == "--prefetch") o.prefetch = true;
     else if (a == "--path") {
       const std::string p = val();
       o.eng.path = p == "sm" ? CopyPath::SmKernel : p == "auto" ? CopyPath::Auto : CopyPath::CopyEngine;
@@ -440,6 +442,7 @@ class Daemon {
       if (a.alive || a.rpc < 0) continue;
       if (sched_.granted() == id) sched_.on_grant_end(id, now());
       sched_.clear_request(id);
+      eng_.prefetch_quiesce();
       const std::vector<ChunkId> chunks = eng_.mem().chunks_of(id);
       for (ChunkId c : chunks) eng_.free_chunk(id, c);
       placer_.take_released();  // its slabs return to the pool; nobody to unmap them
@@ -464,6 +467,7 @@ class Daemon {
   // ---- requests --------------------------------------------------------------
   void rpc(App& a, ipc::Msg type, const std::vector<std::uint8_t>& body) {
     ipc::Reader r{body};
+    if (type == ipc::Msg::Alloc || type == ipc::Msg::Free) eng_.prefetch_quiesce();  // registry changes: no legs in flight
     switch (type) {
       case ipc::Msg::Alloc: {
         const auto req = r.get<ipc::AllocReq>();
@@ -591,10 +595,22 @@ class Daemon {
     poll_activity(t, 0.0);
     sched_.infer_all(t);
     const std::optional<AppId> next = sched_.select_next(t);
-    if (!next) return;
     const std::optional<AppId> holder = sched_.granted();
-    const bool go = !holder || sched_.is_idle(*holder, t) || sched_.should_preempt(*holder, t);
-    if (go) context_switch(*next, t);
+    const bool go = next && (!holder || sched_.is_idle(*holder, t) || sched_.should_preempt(*holder, t));
+    if (go) {
+      context_switch(*next, t);
+      return;
+    }
+    if (opt_.prefetch && !eng_.prefetch_pump()) {  // the queue head is likely next
+      const std::optional<AppId> cand = sched_.next_prefetch_candidate(t);
+      if (cand && cand != holder) {
+        const MigrationPlan pf = plan_prefetch(*cand, eng_.mem(), opt_.planner);
+        if (!pf.moves.empty()) {
+          eng_.prefetch_begin(pf);
+          note("{\"t\": %.6f, \"event\": \"prefetch\", \"app\": %u, \"moves\": %zu}", t, *cand, pf.moves.size());
+        }
+      }
+    }
   }
 
   // ---- acks on the event socket ------------------------------------------------
@@ -662,6 +678,7 @@ class Daemon {
   void fetch_in_place(AppId app) {
     PlannerConfig cfg = opt_.planner;
     cfg.eviction_policy.victim_order = sched_.victim_hint();
+    eng_.prefetch_quiesce();
     const MigrationPlan plan = plan_switch(app, eng_.mem(), cfg);
     const ExecResult r = eng_.execute(plan, cfg);
     send_maps();
@@ -690,6 +707,7 @@ class Daemon {
     // (4) plan + real copies, victims unmapping concurrently.
     PlannerConfig cfg = opt_.planner;
     cfg.eviction_policy.victim_order = sched_.victim_hint();
+    eng_.prefetch_quiesce();  // cancel_pending + quiesced (transfer.cpp:89-113)
     const MigrationPlan plan = plan_switch(to, eng_.mem(), cfg);
     const std::uint64_t t_planned = ipc::mono_ns();
     const ExecResult r = eng_.execute(plan, cfg);

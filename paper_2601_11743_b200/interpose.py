@@ -32,7 +32,7 @@ class Daemon:
     def __init__(self, gpu: str = "32G", pinned: str = "16G", paged: str = "96G", window: Optional[str] = None,
                  path: str = "ce", idle_ms: Optional[float] = None, tick_ms: Optional[float] = None,
                  allot_s: Optional[float] = None, preempt_s: Optional[float] = None, host_threads: Optional[int] = None,
-                 log: Optional[str] = None, extra: Sequence[str] = ()):
+                 log: Optional[str] = None, prefetch: bool = False, extra: Sequence[str] = ()):
         for f in (NIXIED, SHIM):
             if not os.path.exists(f):
                 raise RuntimeError(f"{f} is not built (python -c 'import __graft_entry__ as g; g.build()')")
@@ -45,7 +45,7 @@ class Daemon:
                         ("--preempt-s", preempt_s), ("--host-threads", host_threads)):
             if v is not None:
                 args += [flag, str(v)]
-        self.args = args + list(extra)
+        self.args = args + (["--prefetch"] if prefetch else []) + list(extra)
         self.proc: Optional[subprocess.Popen] = None
         self.stderr_path = os.path.join(self.tmp, "daemon.err")
 

@@ -81,6 +81,22 @@ def test_driver_api_launches_are_gated():
         assert r["out"]["device_errors"] == 0 and r["out"]["host_mismatch"] == 0
 
 
+def test_prefetch_under_the_daemon():
+    """Three apps on a small pinned budget with the daemon's MLFQ prefetch on:
+    pageable blocks of the next candidate move to pinned between switches;
+    every app still finishes byte-exact."""
+    with Daemon(gpu="4G", pinned="2G", paged="16G", prefetch=True) as d:
+        res = run_apps(d, [_vec(2048, 5, 300, 41, "a"), _vec(2048, 5, 300, 42, "b"), _vec(2048, 5, 300, 43, "c")],
+                       timeout=600)
+        _save("prefetch", d, res)
+        _check(res, d)
+        recs = d.records()
+    for r in res:
+        assert r["out"]["device_errors"] == 0 and r["out"]["host_mismatch"] == 0
+    assert any(r.get("event") == "prefetch" for r in recs)
+    assert all(r["mismatches"] == 0 for r in recs if r.get("event") == "switch")
+
+
 def test_memgetinfo_reports_budget():
     with Daemon(gpu="6G", pinned="2G", paged="8G") as d:
         res = run_apps(d, [_vec(1024, 1, 0, 3, "m")], timeout=300)
