@@ -889,6 +889,7 @@ ExecResult SwapEngine::execute(const MigrationPlan& plan, const PlannerConfig& c
 }
 
 ExecResult SwapEngine::switch_to(AppId incoming, const PlannerConfig& cfg, cudaStream_t drain) {
+  impl_->prefetch_quiesce();  // plan_switch needs a quiescent registry (planner.cpp:132-133)
   const auto t = Clock::now();
   MigrationPlan plan = plan_switch(incoming, impl_->mem, cfg);
   const double plan_s = secs_since(t);
