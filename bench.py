@@ -280,7 +280,8 @@ def run_product(args, dist: Dist):
     peaks = measured_peaks()
     path = parse_path(args.path)
     check_host_memory(dist)
-    eng = SwapEngine(device=device, gpu_capacity=32 * GIB, pinned_capacity=16 * GIB, paged_capacity=2 * GIB, path=path)
+    extra = {"legs_per_launch": args.legs_per_launch} if args.legs_per_launch else {}
+    eng = SwapEngine(device=device, gpu_capacity=32 * GIB, pinned_capacity=16 * GIB, paged_capacity=2 * GIB, path=path, **extra)
     probe = eng.probe_pcie(1 * GIB, 64 * MIB)
     calib = eng.calibrate(256 * MIB) if path == 0 else None
     # Steady state only involves the GPU and the pinned ring, so the apps are
@@ -409,6 +410,7 @@ def main():
     ap.add_argument("--impl", choices=["product", "reference"], default="product")
     ap.add_argument("--path", choices=["auto", "sm", "ce"], default="auto")
     ap.add_argument("--no-x16", dest="x16", action="store_false")
+    ap.add_argument("--legs-per-launch", type=int, default=0, help="CE batch / K3 launch size (0: engine default)")
     args = ap.parse_args()
     dist = Dist()
     try:

@@ -53,6 +53,7 @@ struct EngineConfig {
   bool numa_bind = true;              // pinned ring + workers on the GPU's NUMA node
   int first_batch_legs = 8;           // batch-size ramp start (doubles per batch up to legs_per_launch)
   bool k3_tma = true;                 // CE-path checksum pass on the TMA pipeline (else the LDG loop)
+  bool k3_one_stream = true;          // both lanes' K3 launches on one stream (no SM contention between them)
   bool exportable_arena = false;      // GPU tier = exportable VMM slabs shims can import (interposer daemon)
   Bytes arena_slab_bytes = 128 * kMiB; // exportable arena: bytes per physical allocation (a multiple of 2 MiB)
   Bytes gpu_physical = 0;             // arena bytes (0 = gpu_capacity); the registry still enforces gpu_capacity
@@ -219,7 +220,8 @@ class SwapEngine {
   // faster one per size for CopyPath::Auto.
   Calibration calibrate(Bytes bytes_per_direction);
   // K3 launch duration (us) for 1, 2, 4 ... 128 legs: [0] TMA pipeline, [1] LDG loop.
-  std::vector<std::array<double, 2>> probe_checksum_launch();
+  // under_pcie_load: while both PCIe directions carry copy-engine traffic.
+  std::vector<std::array<double, 2>> probe_checksum_launch(bool under_pcie_load = false);
 
  private:
   struct Impl;

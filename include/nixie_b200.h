@@ -62,6 +62,7 @@ typedef struct nx_engine_config {
   int numa_bind;
   int first_batch_legs;
   int k3_tma;
+  int k3_one_stream; /* both lanes' K3 launches on one stream */
 } nx_engine_config;
 
 /* PlannerConfig (proj/include/nixie/planner.hpp:39-43). victim_order may be
@@ -185,6 +186,8 @@ int nx_set_auto_table(nx_engine* e, const int* sm_faster, size_t n);
 int nx_calibrate(nx_engine* e, uint64_t bytes_per_direction, double sm_gbps[8], double ce_gbps[8], int sm_faster[8]);
 /* K3 checksum launch duration (us) for 1, 2, 4 ... 128 legs; us[2*k] TMA, us[2*k+1] LDG. */
 int nx_probe_checksum_launch(nx_engine* e, double us[16]);
+/* Same, optionally while both PCIe directions carry copy-engine traffic. */
+int nx_probe_checksum_launch_ex(nx_engine* e, int under_pcie_load, double us[16]);
 
 /* ---- scheduler + launch gate (§3, §6) ---------------------------- */
 /* MlfqConfig defaults (proj/include/nixie/mlfq.hpp:13-23). */

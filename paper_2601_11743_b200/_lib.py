@@ -53,7 +53,7 @@ class EngineConfigC(Structure):
         ("device", c_int), ("gpu_capacity", c_uint64), ("pinned_capacity", c_uint64), ("paged_capacity", c_uint64),
         ("path", c_int), ("pcie_legs_in_flight", c_int), ("legs_per_launch", c_int), ("host_threads", c_int),
         ("host_legs_in_flight", c_int), ("max_ctas", c_int), ("fused_launch", c_int), ("verify", c_int),
-        ("numa_bind", c_int), ("first_batch_legs", c_int), ("k3_tma", c_int),
+        ("numa_bind", c_int), ("first_batch_legs", c_int), ("k3_tma", c_int), ("k3_one_stream", c_int),
     ]
 
 
@@ -127,6 +127,7 @@ _SIGNATURES = [
     ("nx_set_auto_table", c_int, [c_void_p, POINTER(c_int), c_size_t]),
     ("nx_calibrate", c_int, [c_void_p, c_uint64, POINTER(c_double), POINTER(c_double), POINTER(c_int)]),
     ("nx_probe_checksum_launch", c_int, [c_void_p, POINTER(c_double)]),
+    ("nx_probe_checksum_launch_ex", c_int, [c_void_p, c_int, POINTER(c_double)]),
     ("nx_mlfq_config_default", None, [POINTER(MlfqConfigC)]),
     ("nx_gate_create", c_int, [c_void_p, POINTER(MlfqConfigC), POINTER(PlannerConfigC), POINTER(c_void_p)]),
     ("nx_gate_destroy", None, [c_void_p]),

@@ -89,6 +89,7 @@ EngineConfig to_cpp(const nx_engine_config& c) {
   o.numa_bind = c.numa_bind != 0;
   o.first_batch_legs = c.first_batch_legs;
   o.k3_tma = c.k3_tma != 0;
+  o.k3_one_stream = c.k3_one_stream != 0;
   return o;
 }
 
@@ -194,6 +195,7 @@ void nx_engine_config_default(nx_engine_config* c) {
   c->numa_bind = d.numa_bind;
   c->first_batch_legs = d.first_batch_legs;
   c->k3_tma = d.k3_tma;
+  c->k3_one_stream = d.k3_one_stream;
 }
 
 void nx_planner_config_default(nx_planner_config* c) {
@@ -440,11 +442,13 @@ int nx_calibrate(nx_engine* e, uint64_t bytes, double sm_gbps[8], double ce_gbps
   });
 }
 
-int nx_probe_checksum_launch(nx_engine* e, double us[16]) {
+int nx_probe_checksum_launch(nx_engine* e, double us[16]) { return nx_probe_checksum_launch_ex(e, 0, us); }
+
+int nx_probe_checksum_launch_ex(nx_engine* e, int under_pcie_load, double us[16]) {
   return guard([&] {
     need(e, "engine");
     need(us, "us");
-    const auto r = e->eng->probe_checksum_launch();
+    const auto r = e->eng->probe_checksum_launch(under_pcie_load != 0);
     for (std::size_t k = 0; k < r.size() && k < 8; ++k) {
       us[2 * k] = r[k][0];
       us[2 * k + 1] = r[k][1];

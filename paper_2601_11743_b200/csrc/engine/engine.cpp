@@ -172,7 +172,14 @@ struct SwapEngine::Impl final : detail::LaneSink {
     pool.start(cfg.host_threads, numa.cpus);
     for (auto& s : st) NX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     NX_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
-    for (auto& s : cks) NX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    // K3 checksum launches of both lanes share one stream by default, so they
+    // never compete for the SMs (each is a full-GPU TMA pipeline). This
+    // cannot deadlock: a fetch is submitted only after the eviction batch that
+    // frees its frames has ended (record included), so a verify never waits
+    // on a copy that waits on a record queued behind it.
+    NX_CUDA(cudaStreamCreateWithFlags(&cks[0], cudaStreamNonBlocking));
+    if (cfg.k3_one_stream) cks[1] = cks[0];
+    else NX_CUDA(cudaStreamCreateWithFlags(&cks[1], cudaStreamNonBlocking));
     NX_CUDA(cudaMalloc(&ck.status, sizeof(NxDevStatus)));
     NX_CUDA(cudaMalloc(&ck.kstart, sizeof(unsigned long long) * kClockSlots));
     NX_CUDA(cudaMalloc(&ck.kend, sizeof(unsigned long long) * kClockSlots));
@@ -222,7 +229,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
     if (bounce) cudaFreeHost(bounce);
     for (auto& s : st) cudaStreamDestroy(s);
     cudaStreamDestroy(aux);
-    for (auto& s : cks) cudaStreamDestroy(s);
+    cudaStreamDestroy(cks[0]);
+    if (cks[1] != cks[0]) cudaStreamDestroy(cks[1]);
   }
 
   // ---- per-block tables -------------------------------------------------
@@ -548,6 +556,14 @@ struct SwapEngine::Impl final : detail::LaneSink {
     const std::size_t n = mem.block_count();
     std::memcpy(h_frames_stage, h_frames, sizeof(std::uint64_t) * n);
     NX_CUDA(cudaMemcpyAsync(d_frames, h_frames_stage, sizeof(std::uint64_t) * n, cudaMemcpyHostToDevice, st[kH2D]));
+    if (cfg.verify) {
+      // The arrival checks of the CE path run on the K3 stream: the app may
+      // start only after they have read the restored frames (its kernels
+      // may overwrite them).
+      cudaEvent_t checked = take_event();
+      NX_CUDA(cudaEventRecord(checked, cks[kH2D]));
+      NX_CUDA(cudaStreamWaitEvent(st[kH2D], checked, 0));
+    }
     if (opts->gate_event != nullptr) NX_CUDA(cudaEventRecord(opts->gate_event, st[kH2D]));
     if (opts->gate_callback != nullptr) opts->gate_callback(opts->gate_ctx);
   }
@@ -1159,12 +1175,26 @@ namespace nixie::b200 {
 // engines (both directions running, the swap's operating point).
 // K3 launch timing for 1, 2, 4 ... 128 legs over a scratch HBM buffer
 // (CUDA events, median of 9): microseconds per launch, [0] TMA, [1] LDG.
-std::vector<std::array<double, 2>> SwapEngine::probe_checksum_launch() {
+std::vector<std::array<double, 2>> SwapEngine::probe_checksum_launch(bool under_pcie_load) {
   Impl& m = *impl_;
   constexpr int kMax = 128;
   std::uint8_t* buf = nullptr;
   NX_CUDA(cudaMalloc(&buf, kMax * kBlockBytes));
   NX_CUDA(cudaMemset(buf, 7, kMax * kBlockBytes));
+  // Optional background load: both PCIe directions busy on the copy
+  // engines (as during a switch) while the K3 launches are timed.
+  constexpr std::size_t kLoad = std::size_t{1} << 30;
+  std::uint8_t *hload = nullptr, *dload = nullptr;
+  if (under_pcie_load) {
+    void* h = nullptr;
+    NX_CUDA(cudaHostAlloc(&h, 2 * kLoad, cudaHostAllocPortable));
+    hload = static_cast<std::uint8_t*>(h);
+    NX_CUDA(cudaMalloc(&dload, 2 * kLoad));
+    for (int r = 0; r < 16; ++r) {
+      NX_CUDA(cudaMemcpyAsync(dload, hload, kLoad, cudaMemcpyHostToDevice, m.st[0]));
+      NX_CUDA(cudaMemcpyAsync(hload + kLoad, dload + kLoad, kLoad, cudaMemcpyDeviceToHost, m.st[1]));
+    }
+  }
   cudaEvent_t a, z;
   NX_CUDA(cudaEventCreate(&a));
   NX_CUDA(cudaEventCreate(&z));
@@ -1173,16 +1203,35 @@ std::vector<std::array<double, 2>> SwapEngine::probe_checksum_launch() {
     std::vector<NxLeg> legs;
     for (int i = 0; i < n; ++i) legs.push_back(NxLeg{buf + static_cast<std::size_t>(i) * kBlockBytes, nullptr, static_cast<std::uint32_t>(i), 0});
     std::array<double, 2> r{};
+    // Under load, column 1 is the TMA launch issued as a CUDA graph (event,
+    // kernel, event captured once): is the extra latency the launch's trip
+    // through host memory?
+    cudaGraphExec_t gexec = nullptr;
+    if (under_pcie_load) {
+      cudaGraph_t graph = nullptr;
+      NX_CUDA(cudaStreamBeginCapture(m.aux, cudaStreamCaptureModeThreadLocal));
+      NX_CUDA(cudaEventRecord(a, m.aux));
+      NX_CUDA(launch_checksum_tma(legs.data(), n, false, 0, m.ck, m.scratch[2], m.sm_count, m.aux));
+      NX_CUDA(cudaEventRecord(z, m.aux));
+      NX_CUDA(cudaStreamEndCapture(m.aux, &graph));
+      NX_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
+      NX_CUDA(cudaGraphUpload(gexec, m.aux));
+      cudaGraphDestroy(graph);
+    }
     for (int variant = 0; variant < 2; ++variant) {
       std::vector<double> t;
       for (int rep = 0; rep < 10; ++rep) {
         NX_CUDA(launch_spin(200000, m.aux));  // host finishes enqueueing before the GPU reaches `a`
-        NX_CUDA(cudaEventRecord(a, m.aux));
-        if (variant == 0)
-          NX_CUDA(launch_checksum_tma(legs.data(), n, false, 0, m.ck, m.scratch[2], m.sm_count, m.aux));
-        else
-          NX_CUDA(launch_swap(legs.data(), n, 0, 0, m.ck, m.scratch[2], m.k3_ctas, m.aux));
-        NX_CUDA(cudaEventRecord(z, m.aux));
+        if (variant == 1 && gexec) {
+          NX_CUDA(cudaGraphLaunch(gexec, m.aux));
+        } else {
+          NX_CUDA(cudaEventRecord(a, m.aux));
+          if (variant == 0)
+            NX_CUDA(launch_checksum_tma(legs.data(), n, false, 0, m.ck, m.scratch[2], m.sm_count, m.aux));
+          else
+            NX_CUDA(launch_swap(legs.data(), n, 0, 0, m.ck, m.scratch[2], m.k3_ctas, m.aux));
+          NX_CUDA(cudaEventRecord(z, m.aux));
+        }
         NX_CUDA(cudaEventSynchronize(z));
         float ms = 0;
         NX_CUDA(cudaEventElapsedTime(&ms, a, z));
@@ -1192,11 +1241,18 @@ std::vector<std::array<double, 2>> SwapEngine::probe_checksum_launch() {
       std::sort(t.begin(), t.end());
       r[variant] = t[t.size() / 2];
     }
+    if (gexec) cudaGraphExecDestroy(gexec);
     out.push_back(r);
   }
   cudaEventDestroy(a);
   cudaEventDestroy(z);
   cudaFree(buf);
+  if (under_pcie_load) {
+    NX_CUDA(cudaStreamSynchronize(m.st[0]));
+    NX_CUDA(cudaStreamSynchronize(m.st[1]));
+    cudaFree(dload);
+    cudaFreeHost(hload);
+  }
   return out;
 }
 

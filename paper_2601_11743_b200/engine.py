@@ -38,6 +38,7 @@ class EngineConfig:
     numa_bind: bool = True
     first_batch_legs: int = 8
     k3_tma: bool = True
+    k3_one_stream: bool = True
 
     def to_c(self) -> L.EngineConfigC:
         c = L.EngineConfigC()
