@@ -54,6 +54,8 @@ struct EngineConfig {
   int first_batch_legs = 8;           // batch-size ramp start (doubles per batch up to legs_per_launch)
   bool k3_tma = true;                 // CE-path checksum pass on the TMA pipeline (else the LDG loop)
   bool k3_one_stream = true;          // both lanes' K3 launches on one stream (no SM contention between them)
+  bool k3_grouped = true;             // CE path: one record launch per switch, arrival checks per group
+  int k3_verify_group = 1024;         // legs per grouped arrival check (the last group is flushed at the end)
   bool exportable_arena = false;      // GPU tier = exportable VMM slabs shims can import (interposer daemon)
   Bytes arena_slab_bytes = 128 * kMiB; // exportable arena: bytes per physical allocation (a multiple of 2 MiB)
   Bytes gpu_physical = 0;             // arena bytes (0 = gpu_capacity); the registry still enforces gpu_capacity

@@ -63,6 +63,8 @@ typedef struct nx_engine_config {
   int first_batch_legs;
   int k3_tma;
   int k3_one_stream; /* both lanes' K3 launches on one stream */
+  int k3_grouped;    /* CE path: one switch-wide record launch, grouped arrival checks */
+  int k3_verify_group; /* legs per grouped arrival check */
 } nx_engine_config;
 
 /* PlannerConfig (proj/include/nixie/planner.hpp:39-43). victim_order may be

@@ -54,6 +54,7 @@ class EngineConfigC(Structure):
         ("path", c_int), ("pcie_legs_in_flight", c_int), ("legs_per_launch", c_int), ("host_threads", c_int),
         ("host_legs_in_flight", c_int), ("max_ctas", c_int), ("fused_launch", c_int), ("verify", c_int),
         ("numa_bind", c_int), ("first_batch_legs", c_int), ("k3_tma", c_int), ("k3_one_stream", c_int),
+        ("k3_grouped", c_int), ("k3_verify_group", c_int),
     ]
 
 

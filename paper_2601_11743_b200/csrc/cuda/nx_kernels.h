@@ -73,6 +73,15 @@ cudaError_t launch_checksum_tma(const NxLeg* legs, int n, bool arriving, std::ui
                                 const NxScratch& scratch, int ctas, cudaStream_t stream,
                                 std::uint32_t clock_slot = kNoClockSlot);
 
+// Same pass over a DEVICE-resident leg table of any length (d_legs[0..n)).
+// `scratch` must hold n entries (part_count and leg_acc zero at rest). One
+// launch covers a whole switch's departures or a group of arrival batches:
+// under PCIe load every launch pays a fixed ~30 us on the GPU's launch path
+// (tools/k3_probe.py), so fewer, larger launches run closer to HBM speed.
+cudaError_t launch_checksum_tma_table(const NxLeg* d_legs, int n, bool arriving, std::uint32_t flags, const NxCkTables& ck,
+                                      const NxScratch& scratch, int ctas, cudaStream_t stream,
+                                      std::uint32_t clock_slot = kNoClockSlot);
+
 // K4: pattern fill (records checksums, marks them valid) and compare (adds
 // the number of mismatching 16-byte vectors per leg into mismatches[i]).
 cudaError_t launch_fill(const NxLeg* legs, int n, std::uint64_t seed, const NxCkTables& ck, cudaStream_t stream);

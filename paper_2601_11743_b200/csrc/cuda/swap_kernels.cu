@@ -35,6 +35,19 @@ namespace nixie::b200 {
 
 namespace {
 
+// K3 over a device-resident leg table (any number of legs): one launch can
+// cover a whole switch's departures or a group of arrival batches.
+struct SwapParamsTable {
+  NxCkTables ck;
+  NxScratch scratch;
+  std::uint32_t n_d2h;
+  std::uint32_t n_h2d;
+  std::uint32_t parts_log2;
+  std::uint32_t flags;
+  std::uint32_t clock_slot;
+  const NxLeg* legs;  // device memory
+};
+
 // Kernel parameter block sized for up to N legs. Launches pick the smallest
 // N that fits: the block is copied into every launch, so a 6 KB block for a
 // 1-leg launch is pure overhead.
@@ -449,6 +462,32 @@ cudaError_t launch_checksum_tma(const NxLeg* legs, int n, bool arriving, std::ui
   if (n <= 32) return launch_checksum_tma_n<32>(legs, n, arriving, flags, ck, scratch, ctas, stream, slot);
   if (n <= 128) return launch_checksum_tma_n<128>(legs, n, arriving, flags, ck, scratch, ctas, stream, slot);
   return launch_checksum_tma_n<kMaxLegsPerLaunch>(legs, n, arriving, flags, ck, scratch, ctas, stream, slot);
+}
+
+cudaError_t launch_checksum_tma_table(const NxLeg* d_legs, int n, bool arriving, std::uint32_t flags, const NxCkTables& ck,
+                                      const NxScratch& scratch, int ctas, cudaStream_t stream, std::uint32_t clock_slot) {
+  if (n <= 0) return cudaSuccess;
+  static bool configured = false;
+  constexpr int kSmem = kTmaStages * kTmaChunk;
+  if (!configured) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(nx_checksum_tma_kernel<SwapParamsTable>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  SwapParamsTable p;
+  p.legs = d_legs;
+  p.ck = ck;
+  p.scratch = scratch;
+  p.n_d2h = arriving ? 0u : static_cast<std::uint32_t>(n);
+  p.n_h2d = arriving ? static_cast<std::uint32_t>(n) : 0u;
+  p.parts_log2 = 0;
+  p.clock_slot = (ck.kstart != nullptr && ck.kend != nullptr) ? clock_slot : kNoClockSlot;
+  p.flags = flags;
+  const long long chunks = static_cast<long long>(n) * kTmaChunksPerLeg;
+  if (ctas > chunks) ctas = static_cast<int>(chunks);
+  nx_checksum_tma_kernel<SwapParamsTable><<<ctas, kTmaConsumers + 32, kSmem, stream>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fill(const NxLeg* legs, int n, std::uint64_t seed, const NxCkTables& ck, cudaStream_t stream) {

@@ -90,6 +90,8 @@ EngineConfig to_cpp(const nx_engine_config& c) {
   o.first_batch_legs = c.first_batch_legs;
   o.k3_tma = c.k3_tma != 0;
   o.k3_one_stream = c.k3_one_stream != 0;
+  o.k3_grouped = c.k3_grouped != 0;
+  o.k3_verify_group = c.k3_verify_group;
   return o;
 }
 
@@ -196,6 +198,8 @@ void nx_engine_config_default(nx_engine_config* c) {
   c->first_batch_legs = d.first_batch_legs;
   c->k3_tma = d.k3_tma;
   c->k3_one_stream = d.k3_one_stream;
+  c->k3_grouped = d.k3_grouped;
+  c->k3_verify_group = d.k3_verify_group;
 }
 
 void nx_planner_config_default(nx_planner_config* c) {

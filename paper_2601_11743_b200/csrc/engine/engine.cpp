@@ -104,13 +104,95 @@ struct SwapEngine::Impl final : detail::LaneSink {
     int stream;
     bool ce;
     bool end_on_side = false;                        // CE batch: ends on the checksum side stream
+    cudaEvent_t dep_done = nullptr;                  // grouped K3: the record launch covering its departures
     std::vector<std::array<cudaEvent_t, 2>> k3ev;    // CE batch: K3 launch start/end
     std::vector<std::uint32_t> k3slot;               // device-clock slot per K3 launch
     Bytes k3_bytes = 0;
   };
   std::array<int, 2> batches_sent{};  // per PCIe lane this execute (batch-size ramp)
+
+  // Grouped K3 (CE path, one K3 stream): one table launch records every
+  // departing block of the switch at its start; arrival checks run per group
+  // of landed batches. Descriptors live in a device table (uploaded from a
+  // pinned stage) so a launch covers any number of legs.
+  struct GroupK3 {
+    cudaEvent_t a, z;
+    int legs;
+    int lane;
+    std::uint32_t slot;
+  };
+  bool grouped = false;
+  NxLeg* d_ktab = nullptr;
+  NxLeg* h_ktab = nullptr;
+  std::size_t ktab_cap = 0, ktab_used = 0;
+  NxScratch tscratch{};
+  std::size_t tscratch_cap = 0;
+  std::vector<GroupK3> gk3;
+  std::vector<NxLeg> vgroup;          // landed-or-landing arrivals not yet checked
+  std::vector<std::uint32_t> dep_pos;  // block -> position in the switch's departure order (grouped K3)
+  std::size_t dep_head = 0;            // departures covered by the first record launch
+  cudaEvent_t rec_head = nullptr, rec_all = nullptr;
+  cudaEvent_t vgroup_copied = nullptr;
   std::vector<K3Launch> k3_trace;     // last execute's K3 launches (device times)
   std::uint32_t k3_slots_used = 0;    // device-clock slots handed out this execute
+
+  // Capacity for `n` table legs this execute (grown before any work is queued).
+  void reserve_table(std::size_t n) {
+    if (n > ktab_cap) {
+      NX_CUDA(cudaDeviceSynchronize());
+      if (d_ktab) cudaFree(d_ktab);
+      if (h_ktab) cudaFreeHost(h_ktab);
+      const std::size_t cap = std::max<std::size_t>(n, 2 * ktab_cap);
+      NX_CUDA(cudaMalloc(&d_ktab, sizeof(NxLeg) * cap));
+      void* h = nullptr;
+      NX_CUDA(cudaHostAlloc(&h, sizeof(NxLeg) * cap, cudaHostAllocPortable));
+      h_ktab = static_cast<NxLeg*>(h);
+      ktab_cap = cap;
+    }
+    if (n > tscratch_cap) {
+      NX_CUDA(cudaDeviceSynchronize());
+      cudaFree(tscratch.part_sums);
+      cudaFree(tscratch.part_count);
+      cudaFree(tscratch.leg_acc);
+      const std::size_t cap = std::max<std::size_t>(n, 2 * tscratch_cap);
+      NX_CUDA(cudaMalloc(&tscratch.part_sums, sizeof(unsigned long long)));
+      NX_CUDA(cudaMalloc(&tscratch.part_count, sizeof(unsigned int) * cap));
+      NX_CUDA(cudaMemset(tscratch.part_count, 0, sizeof(unsigned int) * cap));
+      NX_CUDA(cudaMalloc(&tscratch.leg_acc, sizeof(unsigned long long) * cap));
+      NX_CUDA(cudaMemset(tscratch.leg_acc, 0, sizeof(unsigned long long) * cap));
+      tscratch_cap = cap;
+    }
+  }
+
+  // One K3 table launch on the (single) K3 stream over `l`.
+  void k3_table_launch(const std::vector<NxLeg>& l, bool arriving, int lane) {
+    const std::size_t n = l.size();
+    if (ktab_used + n > ktab_cap) throw InvariantViolation("K3 descriptor table overflow");
+    std::memcpy(h_ktab + ktab_used, l.data(), sizeof(NxLeg) * n);
+    cudaStream_t cs = cks[0];
+    NX_CUDA(cudaMemcpyAsync(d_ktab + ktab_used, h_ktab + ktab_used, sizeof(NxLeg) * n, cudaMemcpyHostToDevice, cs));
+    GroupK3 g{take_event(), take_event(), static_cast<int>(n), lane,
+              k3_slots_used < kClockSlots ? k3_slots_used++ : kNoClockSlot};
+    NX_CUDA(cudaEventRecord(g.a, cs));
+    NX_CUDA(launch_checksum_tma_table(d_ktab + ktab_used, static_cast<int>(n), arriving, cfg.verify ? kNxVerify : 0u, ck,
+                                      tscratch, sm_count, cs, g.slot));
+    NX_CUDA(cudaEventRecord(g.z, cs));
+    ktab_used += n;
+    gk3.push_back(g);
+    ++stats.launches[lane == 0 ? kH2D : kD2H];
+    ++launches_total;
+  }
+
+  // Checks the arrivals collected so far (after their copies landed). Nothing
+  // in the switch waits on it: an arrived block belongs to the incoming app,
+  // which cannot run before the gate release (which waits for this stream),
+  // and the status is read once every launch has finished.
+  void flush_verify() {
+    if (vgroup.empty()) return;
+    NX_CUDA(cudaStreamWaitEvent(cks[0], vgroup_copied, 0));  // copies land in order on the H2D stream
+    k3_table_launch(vgroup, true, 0);
+    vgroup.clear();
+  }
 
   // K3 checksum-only launch of a CE batch (record on departure, verify on arrival).
   void k3_launch(Batch& B, const std::vector<NxLeg>& l, bool arriving, cudaStream_t cs, std::uint32_t flags) {
@@ -154,6 +236,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
       throw SimError(Err::ValidationError, "tier budgets must be multiples of 2 MiB");
     if (cfg.legs_per_launch < 1 || cfg.legs_per_launch > kMaxLegsPerLaunch)
       throw SimError(Err::ValidationError, "legs_per_launch must be in [1, 256]");
+    if (cfg.k3_verify_group < 1) throw SimError(Err::ValidationError, "k3_verify_group must be >= 1");
     NX_CUDA(cudaSetDevice(cfg.device));
     sm_count = device_sm_count(cfg.device);
     max_ctas = cfg.max_ctas > 0 ? cfg.max_ctas : 2 * std::max(sm_count, 1);
@@ -227,6 +310,11 @@ struct SwapEngine::Impl final : detail::LaneSink {
       cudaFree(s.leg_acc);
     }
     if (bounce) cudaFreeHost(bounce);
+    if (d_ktab) cudaFree(d_ktab);
+    if (h_ktab) cudaFreeHost(h_ktab);
+    cudaFree(tscratch.part_sums);
+    cudaFree(tscratch.part_count);
+    cudaFree(tscratch.leg_acc);
     for (auto& s : st) cudaStreamDestroy(s);
     cudaStreamDestroy(aux);
     cudaStreamDestroy(cks[0]);
@@ -497,20 +585,34 @@ struct SwapEngine::Impl final : detail::LaneSink {
       // DMA reads them, the arrival check runs after the batch landed. The
       // batch ends (and may commit) only when both are done.
       cudaStream_t cs = cks[s];
-      NX_CUDA(cudaStreamWaitEvent(cs, B.ev_start, 0));
       std::vector<NxLeg> ckl;
-      for (auto i : d2h) ckl.push_back(NxLeg{dev_addr(legs[i].from, legs[i].src_u), nullptr, static_cast<std::uint32_t>(legs[i].block), 0});
-      if (!ckl.empty()) k3_launch(B, ckl, false, cs, flags);
+      if (grouped && !d2h.empty()) {
+        std::uint32_t last = 0;
+        for (auto i : d2h) last = std::max(last, dep_pos[legs[i].block]);
+        B.dep_done = last < dep_head ? rec_head : rec_all;
+      }
+      if (!grouped) {
+        NX_CUDA(cudaStreamWaitEvent(cs, B.ev_start, 0));
+        for (auto i : d2h) ckl.push_back(NxLeg{dev_addr(legs[i].from, legs[i].src_u), nullptr, static_cast<std::uint32_t>(legs[i].block), 0});
+        if (!ckl.empty()) k3_launch(B, ckl, false, cs, flags);
+      }  // grouped: the switch-wide record launch already covers these departures
       copy_runs(d2h, s, cudaMemcpyDeviceToHost);
       copy_runs(h2d, s, cudaMemcpyHostToDevice);
       cudaEvent_t copied = take_event();
       NX_CUDA(cudaEventRecord(copied, st[s]));
-      NX_CUDA(cudaStreamWaitEvent(cs, copied, 0));
-      ckl.clear();
-      for (auto i : h2d) ckl.push_back(NxLeg{dev_addr(legs[i].to, legs[i].dst_u), nullptr, static_cast<std::uint32_t>(legs[i].block), 0});
-      if (!ckl.empty()) k3_launch(B, ckl, true, cs, flags);
+      const bool group_check = grouped && !h2d.empty() && d2h.empty();
+      const bool record_covered = grouped && h2d.empty();  // departures only: ends on the copy stream
+      if (group_check) {
+        for (auto i : h2d) vgroup.push_back(NxLeg{dev_addr(legs[i].to, legs[i].dst_u), nullptr, static_cast<std::uint32_t>(legs[i].block), 0});
+        vgroup_copied = copied;  // the batch commits when its copy lands; a group launch checks it
+      } else if (!record_covered) {
+        NX_CUDA(cudaStreamWaitEvent(cs, copied, 0));
+        ckl.clear();
+        for (auto i : h2d) ckl.push_back(NxLeg{dev_addr(legs[i].to, legs[i].dst_u), nullptr, static_cast<std::uint32_t>(legs[i].block), 0});
+        if (!ckl.empty()) k3_launch(B, ckl, true, cs, flags);
+      }
       ++stats.ce_batches[s];
-      B.end_on_side = true;
+      B.end_on_side = !group_check && !record_covered;
     }
     NX_CUDA(cudaEventRecord(B.ev_end, B.end_on_side ? cks[s] : st[s]));
     stats.pcie_d2h_bytes += d2h.size() * kBlockBytes;
@@ -521,6 +623,11 @@ struct SwapEngine::Impl final : detail::LaneSink {
       if (lanes->move(L.mi).dst == TierId::Gpu) ++fetches_submitted;
     }
     inflight[s].push_back(std::move(B));
+    // Group arrival checks; in the tail (fewer fetches left than a group) check
+    // each batch as it is submitted so the last check after the last copy is short.
+    if (!vgroup.empty() && (static_cast<int>(vgroup.size()) >= cfg.k3_verify_group ||
+                            fetches_total - fetches_submitted < static_cast<std::size_t>(cfg.k3_verify_group)))
+      flush_verify();
     maybe_release_gate();
   }
 
@@ -548,6 +655,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   void maybe_release_gate() {
     if (gate_done || opts == nullptr || fetches_submitted < fetches_total) return;
     gate_done = true;
+    flush_verify();
     for (ChunkId c : mem.chunks_of(incoming))
       for (BlockId b : mem.chunk(c).blocks) {
         const Location& loc = mem.block(b).loc;
@@ -627,6 +735,11 @@ struct SwapEngine::Impl final : detail::LaneSink {
     bool progress = false;
     for (int s = 0; s < 2; ++s) {
       while (!inflight[s].empty()) {
+        if (inflight[s].front().dep_done != nullptr) {  // its departures must be recorded before its frames are reused
+          const cudaError_t r = cudaEventQuery(inflight[s].front().dep_done);
+          if (r == cudaErrorNotReady) break;
+          NX_CUDA(r);
+        }
         const cudaError_t e = cudaEventQuery(inflight[s].front().ev_end);
         if (e == cudaErrorNotReady) break;
         NX_CUDA(e);
@@ -745,6 +858,19 @@ struct SwapEngine::Impl final : detail::LaneSink {
     fetches_submitted = 0;
     for (const Move& m : plan.moves)
       if (m.dst == TierId::Gpu) ++fetches_total;
+    grouped = cfg.k3_grouped && cfg.k3_tma && cks[0] == cks[1] && cfg.path != CopyPath::SmKernel;
+    gk3.clear();
+    vgroup.clear();
+    ktab_used = 0;
+    rec_head = rec_all = nullptr;
+    dep_head = 0;
+    std::vector<NxLeg> departing;
+    if (grouped) {
+      for (const Move& m : plan.moves)
+        if (m.src == TierId::Gpu)
+          departing.push_back(NxLeg{arena.frame(unit[m.block]), nullptr, static_cast<std::uint32_t>(m.block), 0});
+      reserve_table(departing.size() + fetches_total);
+    }
 
     detail::LaneSet ls(mem, hw);
     ls.set_limit(kH2D, cfg.pcie_legs_in_flight);
@@ -761,6 +887,30 @@ struct SwapEngine::Impl final : detail::LaneSink {
       NX_CUDA(cudaEventRecord(d, o.drain));
       NX_CUDA(cudaStreamWaitEvent(st[kD2H], d, 0));
       if (cfg.fused_launch) NX_CUDA(cudaStreamWaitEvent(st[kH2D], d, 0));
+    }
+    if (!departing.empty()) {
+      // Record every departing block's checksum once, after the incumbent's
+      // drain (everything queued on the D2H stream so far), concurrently with
+      // the DMA reading the same frames; D2H batches end on this stream after
+      // it, so no frame is reused before it is recorded.
+      cudaEvent_t drained = take_event();
+      NX_CUDA(cudaEventRecord(drained, st[kD2H]));
+      NX_CUDA(cudaStreamWaitEvent(cks[0], drained, 0));
+      // The D2H lane starts its legs in plan order: a small first launch
+      // covers the first (ramp) batches so they can end early, one launch
+      // the rest of the switch.
+      const std::size_t head = std::min<std::size_t>(departing.size(), 4 * static_cast<std::size_t>(cfg.first_batch_legs) +
+                                                                           static_cast<std::size_t>(cfg.legs_per_launch));
+      k3_table_launch(std::vector<NxLeg>(departing.begin(), departing.begin() + head), false, 1);
+      rec_head = gk3.back().z;
+      rec_all = rec_head;
+      if (head < departing.size()) {
+        k3_table_launch(std::vector<NxLeg>(departing.begin() + head, departing.end()), false, 1);
+        rec_all = gk3.back().z;
+      }
+      dep_head = head;
+      if (dep_pos.size() < mem.block_count()) dep_pos.resize(mem.block_count());
+      for (std::size_t i = 0; i < departing.size(); ++i) dep_pos[departing[i].block] = static_cast<std::uint32_t>(i);
     }
     AppId owner = kNoApp;
     for (const Move& m : plan.moves)
@@ -793,6 +943,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
       throw;
     }
     lanes = nullptr;
+    if (grouped) NX_CUDA(cudaStreamSynchronize(cks[0]));  // the last arrival check (the switch is verified)
     stats.wall_s = secs_since(t0);
     res.completion = stats.wall_s;
     finalize_timing(res);
@@ -833,6 +984,16 @@ struct SwapEngine::Impl final : detail::LaneSink {
         r.start = s0;
         r.end = s1;
       }
+    }
+    for (const GroupK3& g : gk3) {
+      float a0 = 0, a1 = 0;
+      NX_CUDA(cudaEventElapsedTime(&a0, ev0, g.a));
+      NX_CUDA(cudaEventElapsedTime(&a1, ev0, g.z));
+      stats.k3_s += (a1 - a0) * 1e-3;
+      k3_spans.emplace_back(a0 * 1e-3, a1 * 1e-3);
+      k3_trace.push_back(K3Launch{a0 * 1e-3, a1 * 1e-3, g.legs, g.lane});
+      stats.k3_bytes += static_cast<Bytes>(g.legs) * kBlockBytes;
+      ++stats.k3_launches;
     }
     stats.device_span_s = landed.empty() ? 0.0 : last - first;
     // K3 launches of the two lanes overlap on the device; their busy time is

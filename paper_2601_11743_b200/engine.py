@@ -39,6 +39,8 @@ class EngineConfig:
     first_batch_legs: int = 8
     k3_tma: bool = True
     k3_one_stream: bool = True
+    k3_grouped: bool = True
+    k3_verify_group: int = 1024
 
     def to_c(self) -> L.EngineConfigC:
         c = L.EngineConfigC()

@@ -3,8 +3,9 @@ sys.path.insert(0, ".")
 from paper_2601_11743_b200 import GIB, PlannerConfig, SwapEngine
 from paper_2601_11743_b200._lib import TIER_GPU, TIER_PINNED
 one = (sys.argv[1] != "0") if len(sys.argv) > 1 else True
-print("k3_one_stream", one)
-e = SwapEngine(gpu_capacity=32 * GIB, pinned_capacity=16 * GIB, paged_capacity=2 * GIB, k3_one_stream=one)
+grp = (sys.argv[2] != "0") if len(sys.argv) > 2 else True
+print("k3_one_stream", one, "k3_grouped", grp)
+e = SwapEngine(gpu_capacity=32 * GIB, pinned_capacity=16 * GIB, paged_capacity=2 * GIB, k3_one_stream=one, k3_grouped=grp)
 e.allocate(0, 16 * GIB, TIER_GPU); e.allocate(1, 16 * GIB, TIER_GPU); e.allocate(1, 8 * GIB, TIER_PINNED)
 e.fill_pattern(0, 5); e.fill_pattern(1, 5)
 pc = PlannerConfig(pinned_budget=16 * GIB); nxt = 0
