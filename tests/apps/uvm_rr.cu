@@ -1,0 +1,109 @@
+// nx_uvm_rr — the UVM comparator on real hardware (the
+// reference models it in proj/src/uvm.cpp, PAPER.md:93 explains why it is
+// slow: fault-driven, half-duplex evict-then-fetch). Two "apps" share one GPU
+// through cudaMallocManaged, round-robin, like nvshare: a device balloon
+// (cudaMalloc) leaves only --cap-gib of device memory for managed pages, and
+// each app's kernel touches its whole --ws-gib working set, so every switch
+// evicts the other app and faults this one back in.
+//
+//   nx_uvm_rr --cap-gib C --ws-gib W --rounds R [--prefetch 0|1]
+//
+// --prefetch 1 issues cudaMemPrefetchAsync of the app's buffer before its
+// kernel (bulk migration instead of demand faults: UVM's best case).
+// Per switch: kernel time with the data elsewhere minus the same kernel's
+// time when resident = the switch cost. Prints one JSON line.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) {                                                                    \
+      std::fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+      std::exit(2);                                                                             \
+    }                                                                                           \
+  } while (0)
+
+__global__ void touch(std::uint64_t* p, std::uint64_t n, std::uint64_t add, unsigned long long* sum) {
+  unsigned long long acc = 0;
+  for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    const std::uint64_t v = p[i] + add;
+    p[i] = v;
+    acc += v;
+  }
+  atomicAdd(sum, acc);
+}
+
+static double ms_since(std::chrono::steady_clock::time_point t) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+}
+
+int main(int argc, char** argv) {
+  double cap_gib = 17, ws_gib = 16;
+  int rounds = 3, prefetch = 0;
+  for (int i = 1; i + 1 < argc; i += 2) {
+    const std::string a = argv[i];
+    if (a == "--cap-gib") cap_gib = std::atof(argv[i + 1]);
+    else if (a == "--ws-gib") ws_gib = std::atof(argv[i + 1]);
+    else if (a == "--rounds") rounds = std::atoi(argv[i + 1]);
+    else if (a == "--prefetch") prefetch = std::atoi(argv[i + 1]);
+  }
+  int dev = 0;
+  CK(cudaSetDevice(dev));
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const std::size_t cap = static_cast<std::size_t>(cap_gib * (1ull << 30));
+  void* balloon = nullptr;
+  if (free_b > cap) CK(cudaMalloc(&balloon, free_b - cap));
+  const std::size_t ws = static_cast<std::size_t>(ws_gib * (1ull << 30));
+  const std::uint64_t n = ws / 8;
+  std::uint64_t* app[2];
+  for (auto& p : app) {
+    CK(cudaMallocManaged(&p, ws));
+    CK(cudaMemAdvise(p, ws, cudaMemAdviseSetPreferredLocation, dev));
+  }
+  unsigned long long* sum = nullptr;
+  CK(cudaMalloc(&sum, sizeof(unsigned long long)));
+  cudaStream_t s;
+  CK(cudaStreamCreate(&s));
+  auto run = [&](int a, std::uint64_t add) {
+    const auto t = std::chrono::steady_clock::now();
+    if (prefetch) {
+      cudaMemLocation loc{};
+      loc.type = cudaMemLocationTypeDevice;
+      loc.id = dev;
+      CK(cudaMemPrefetchAsync(app[a], ws, loc, 0, s));
+    }
+    touch<<<148 * 8, 512, 0, s>>>(app[a], n, add, sum);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    return ms_since(t);
+  };
+  // populate both (first touch on the GPU), then round-robin
+  run(0, 1);
+  run(1, 1);
+  std::vector<double> sw, res;
+  for (int r = 0; r < rounds; ++r)
+    for (int a = 0; a < 2; ++a) {
+      sw.push_back(run(a, 1));   // the other app's pages occupy the GPU
+      res.push_back(run(a, 1));  // resident now: compute only
+    }
+  std::vector<double> cost;
+  for (std::size_t i = 0; i < sw.size(); ++i) cost.push_back(sw[i] - res[i]);
+  std::sort(cost.begin(), cost.end());
+  const double med = cost[cost.size() / 2];
+  std::printf("{\"mode\": \"%s\", \"cap_gib\": %.2f, \"ws_gib\": %.2f, \"switch_cost_ms\": [", prefetch ? "uvm+prefetch" : "uvm",
+              cap_gib, ws_gib);
+  for (std::size_t i = 0; i < cost.size(); ++i) std::printf("%s%.2f", i ? ", " : "", cost[i]);
+  std::printf("], \"median_ms\": %.2f, \"resident_kernel_ms\": %.2f, \"bidir_equiv_gbps\": %.2f}\n", med, res.back(),
+              2.0 * ws / (med * 1e-3) / 1e9);
+  return 0;
+}
