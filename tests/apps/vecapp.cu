@@ -5,6 +5,7 @@
 // `-cudart shared` so LD_PRELOAD can interpose the runtime.
 //
 //   nx_vecapp --mib N --buffers K --iters I --think-ms T --seed S [--name X] [--host-check 0|1] [--driver 0|1]
+//             [--passes P]   (P step kernels over the working set per iteration)
 //
 // Every word of every buffer holds hash(seed, buffer, index) + iteration; each
 // iteration's kernel checks the expected value and increments it, so a byte
@@ -15,6 +16,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <numeric>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -67,6 +69,7 @@ int main(int argc, char** argv) {
   std::string name = "vecapp";
   int host_check = 1;
   int driver = 0;  // 1: launch `step` through the driver API (cuLaunchKernel from cudaGetDriverEntryPoint)
+  int passes = 1;  // step kernels over the whole working set per iteration (compute per request)
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string a = argv[i];
     if (a == "--mib") mib = std::atof(argv[i + 1]);
@@ -77,6 +80,7 @@ int main(int argc, char** argv) {
     else if (a == "--name") name = argv[i + 1];
     else if (a == "--host-check") host_check = std::atoi(argv[i + 1]);
     else if (a == "--driver") driver = std::atoi(argv[i + 1]);
+    else if (a == "--passes") passes = std::atoi(argv[i + 1]);
   }
   const auto t_start = std::chrono::steady_clock::now();
   const std::uint64_t bytes_each = static_cast<std::uint64_t>(mib * 1048576.0 / buffers) / 4 * 4;
@@ -105,21 +109,23 @@ int main(int argc, char** argv) {
     step_fn = reinterpret_cast<CUfunction>(f);
   }
   std::vector<double> lat;
+  std::uint32_t k = 0;  // passes done so far: every word holds expect() + k
   for (int it = 0; it < iters; ++it) {
     const auto t0 = std::chrono::steady_clock::now();
+    for (int pass = 0; pass < passes; ++pass, ++k)
     for (int b = 0; b < buffers; ++b) {
       if (driver) {
         std::uint32_t* pb = buf[b];
         std::uint64_t nn = n, sd = seed;
         int bb = b;
-        std::uint32_t itv = static_cast<std::uint32_t>(it);
+        std::uint32_t itv = k;
         void* args[] = {&pb, &nn, &sd, &bb, &itv, &d_err};
         if (cu_launch(step_fn, 1184, 1, 1, 256, 1, 1, 0, nullptr, args, nullptr) != CUDA_SUCCESS) {
           std::fprintf(stderr, "cuLaunchKernel failed\n");
           return 2;
         }
       } else {
-        step<<<1184, 256>>>(buf[b], n, seed, b, static_cast<std::uint32_t>(it), d_err);
+        step<<<1184, 256>>>(buf[b], n, seed, b, k, d_err);
       }
     }
     CK(cudaGetLastError());
@@ -133,7 +139,7 @@ int main(int argc, char** argv) {
   std::vector<std::uint32_t> h(host_check ? n : 0);
   for (int b = 0; b < buffers && host_check; ++b) {
     CK(cudaMemcpy(h.data(), buf[b], bytes_each, cudaMemcpyDeviceToHost));
-    for (std::uint64_t i = 0; i < n; ++i) host_mismatch += h[i] != expect(seed, b, i) + static_cast<std::uint32_t>(iters);
+    for (std::uint64_t i = 0; i < n; ++i) host_mismatch += h[i] != expect(seed, b, i) + k;
   }
   for (auto p : buf) CK(cudaFree(p));
   CK(cudaFree(d_err));
@@ -142,8 +148,9 @@ int main(int argc, char** argv) {
   auto q = [&](double f) { return s.empty() ? 0.0 : s[std::min(s.size() - 1, static_cast<std::size_t>(f * s.size()))]; };
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   std::printf("{\"name\": \"%s\", \"bytes\": %llu, \"iters\": %d, \"device_errors\": %llu, \"host_mismatch\": %llu, "
-              "\"host_checked\": %d, \"memgetinfo\": [%zu, %zu], \"iter_ms\": {\"p50\": %.3f, \"p99\": %.3f, \"max\": %.3f}, \"wall_s\": %.3f}\n",
+              "\"host_checked\": %d, \"memgetinfo\": [%zu, %zu], \"iter_ms\": {\"p50\": %.3f, \"p99\": %.3f, \"max\": %.3f, \"mean\": %.3f}, \"wall_s\": %.3f}\n",
               name.c_str(), static_cast<unsigned long long>(bytes_each * buffers), iters, dev_errors,
-              static_cast<unsigned long long>(host_mismatch), host_check, free_b, total_b, q(0.5), q(0.99), s.empty() ? 0.0 : s.back(), wall);
+              static_cast<unsigned long long>(host_mismatch), host_check, free_b, total_b, q(0.5), q(0.99), s.empty() ? 0.0 : s.back(),
+              s.empty() ? 0.0 : std::accumulate(s.begin(), s.end(), 0.0) / s.size(), wall);
   return dev_errors == 0 && host_mismatch == 0 ? 0 : 1;
 }
