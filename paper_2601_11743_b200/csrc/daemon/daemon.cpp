@@ -68,7 +68,8 @@ struct Options {
   Bytes min_bytes = kBlockBytes;  // smaller allocations pass through
   double ack_timeout_s = 60.0;
   int exit_after_apps = 0;         // exit once this many apps have come and gone (tests)
-  int phys_slack_slabs = 16;       // physical slabs beyond the budget (partly resident slabs)
+  int phys_slack_slabs = -1;       // physical slabs beyond the budget (partly resident slabs); -1: max(4, 2 GiB worth)
+  std::uint32_t slab_blocks = ipc::kDefaultSlabBlocks;
   bool prefetch = false;           // MLFQ prefetch of the next candidate
 };
 
@@ -88,7 +89,7 @@ void usage() {
                "usage: nixied [--socket PATH] [--device N] [--gpu SIZE] [--pinned SIZE] [--paged SIZE]\n"
                "              [--window SIZE] [--min-bytes SIZE] [--path auto|ce|sm] [--host-threads N]\n"
                "              [--tick-ms X] [--idle-ms X] [--allot-s X] [--preempt-s X] [--log FILE]\n"
-               "              [--phys-slack SLABS] [--prefetch] [--exit-after-apps N]\n"
+               "              [--phys-slack SLABS] [--slab-mib 128|256|512|1024] [--prefetch] [--exit-after-apps N]\n"
                "sizes take a K/M/G suffix (GiB when bare). The daemon serves LD_PRELOAD=libnixie_shim.so apps\n"
                "that set NIXIE_SOCKET=PATH.\n");
 }
@@ -120,6 +121,7 @@ bool parse_args(int argc, char** argv, Options& o) {
     else if (a == "--log") o.log_path = val();
     else if (a == "--exit-after-apps") o.exit_after_apps = std::atoi(val());
     else if (a == "--phys-slack") o.phys_slack_slabs = std::atoi(val());
+    else if (a == "--slab-mib") o.slab_blocks = static_cast<std::uint32_t>(std::atoi(val()) / 2);
     else if (a == "--prefetch") o.prefetch = true;
     else if (a == "--path") {
       const std::string p = val();
@@ -133,14 +135,17 @@ bool parse_args(int argc, char** argv, Options& o) {
     }
   }
   o.mlfq.validate();
-  const Bytes slab = static_cast<Bytes>(ipc::kSlabBlocks) * kBlockBytes;
+  if (o.slab_blocks < 1 || (o.slab_blocks & (o.slab_blocks - 1)) != 0 || o.slab_blocks > 512)
+    throw SimError(Err::ValidationError, "--slab-mib must be a power of two between 2 and 1024");
+  const Bytes slab = static_cast<Bytes>(o.slab_blocks) * kBlockBytes;
+  if (o.phys_slack_slabs < 0) o.phys_slack_slabs = static_cast<int>(std::max<Bytes>(4, 2 * kGiB / slab));
   o.eng.arena_slab_bytes = slab;
   o.eng.gpu_physical = (o.eng.gpu_capacity + slab - 1) / slab * slab + static_cast<Bytes>(std::max(o.phys_slack_slabs, 0)) * slab;
   return true;
 }
 
 // GPU frame placement for the interposer: each application's 128 MiB virtual
-// slab (ipc::kSlabBlocks blocks of its shim's range) is backed by one whole
+// slab (slab_blocks blocks of its shim's range) is backed by one whole
 // physical slab while any of its blocks is on the GPU, at the block's slot.
 // The registry still charges 2 MiB per resident block against the budget;
 // the arena holds `slack` extra slabs for slabs that are partly resident
@@ -149,7 +154,7 @@ class SlabPlacer final : public FramePlacer {
  public:
   using Key = std::pair<AppId, std::uint32_t>;  // (app, vslab)
 
-  explicit SlabPlacer(std::uint32_t slabs) {
+  SlabPlacer(std::uint32_t slabs, std::uint32_t slab_blocks) : sb_(slab_blocks), is_free_(slabs, 1), nfree_(slabs) {
     for (std::uint32_t p = 0; p < slabs; ++p) free_.push_back(p);
   }
 
@@ -170,22 +175,34 @@ class SlabPlacer final : public FramePlacer {
     if (b >= app_.size()) throw InvariantViolation("slab placer: block " + std::to_string(b) + " has no virtual placement");
     Slab& s = slabs_[key(b)];
     if (s.phys == ipc::kNoFrame) {
-      if (free_.empty())
+      if (nfree_ == 0)
         throw InvariantViolation("slab placer: every physical slab is in use (raise --phys-slack; partly resident slabs: " +
                                  std::to_string(partial()) + ")");
-      s.phys = free_.front();
-      free_.pop_front();
+      // Affinity: the slab this vslab had last time, if it is free, is still
+      // mapped in the app (stale mappings are kept), so no remap is needed.
+      if (s.pref != ipc::kNoFrame && is_free_[s.pref]) {
+        s.phys = s.pref;
+      } else {
+        while (!is_free_[free_.front()]) free_.pop_front();  // lazily deleted entries
+        s.phys = free_.front();
+        free_.pop_front();
+      }
+      is_free_[s.phys] = 0;
+      --nfree_;
+      s.pref = s.phys;
     }
     if (s.count++ == 0) assigned_.push_back(key(b));
-    return s.phys * ipc::kSlabBlocks + static_cast<std::uint32_t>(vpos_[b] % ipc::kSlabBlocks);
+    return s.phys * sb_ + static_cast<std::uint32_t>(vpos_[b] % sb_);
   }
 
   void release(BlockId b, std::uint32_t frame) override {
     const Key k = key(b);
     Slab& s = slabs_[k];
-    if (s.count == 0 || frame / ipc::kSlabBlocks != s.phys) throw InvariantViolation("slab placer: release of an unplaced block");
+    if (s.count == 0 || frame / sb_ != s.phys) throw InvariantViolation("slab placer: release of an unplaced block");
     if (--s.count == 0) {
       free_.push_back(s.phys);
+      is_free_[s.phys] = 1;
+      ++nfree_;
       s.phys = ipc::kNoFrame;
       released_.push_back(k);
     }
@@ -212,22 +229,40 @@ class SlabPlacer final : public FramePlacer {
 
   std::uint64_t partial() const {
     std::uint64_t n = 0;
-    for (const auto& kv : slabs_) n += kv.second.phys != ipc::kNoFrame && kv.second.count < ipc::kSlabBlocks;
+    for (const auto& kv : slabs_) n += kv.second.phys != ipc::kNoFrame && kv.second.count < sb_;
     return n;
   }
-  std::size_t free_slabs() const { return free_.size(); }
+  std::size_t free_slabs() const { return nfree_; }
+
+  // What the app's shim has mapped at a vslab (as far as the daemon told it).
+  std::uint32_t mapped(const Key& k) const {
+    auto it = slabs_.find(k);
+    return it == slabs_.end() ? ipc::kNoFrame : it->second.mapped;
+  }
+  void set_mapped(const Key& k, std::uint32_t phys) { slabs_[k].mapped = phys; }
+  // After a Grant: the shim maps exactly the backed vslabs and unmaps the rest.
+  void granted(AppId app) {
+    for (auto it = slabs_.lower_bound(Key{app, 0}); it != slabs_.end() && it->first.first == app; ++it)
+      it->second.mapped = it->second.phys;
+  }
 
  private:
   struct Slab {
     std::uint32_t phys = ipc::kNoFrame;
-    std::uint32_t count = 0;  // blocks placed in it
+    std::uint32_t count = 0;               // blocks placed in it
+    std::uint32_t pref = ipc::kNoFrame;    // the physical slab it had last
+    std::uint32_t mapped = ipc::kNoFrame;  // what the shim maps there now
   };
-  Key key(BlockId b) const { return Key{app_[b], static_cast<std::uint32_t>(vpos_[b] / ipc::kSlabBlocks)}; }
+  Key key(BlockId b) const { return Key{app_[b], static_cast<std::uint32_t>(vpos_[b] / sb_)}; }
+
+  std::uint32_t sb_;  // blocks per slab
 
   std::vector<AppId> app_;
   std::vector<std::uint64_t> vpos_;
   std::map<Key, Slab> slabs_;
-  std::deque<std::uint32_t> free_;
+  std::deque<std::uint32_t> free_;  // FIFO with lazily deleted entries (is_free_)
+  std::vector<char> is_free_;
+  std::size_t nfree_ = 0;
   std::vector<Key> released_;
   std::vector<Key> assigned_;
 };
@@ -235,7 +270,7 @@ class SlabPlacer final : public FramePlacer {
 class Daemon {
  public:
   explicit Daemon(const Options& o)
-      : opt_(o), eng_(o.eng), sched_(o.mlfq), placer_(eng_.arena_frames() / ipc::kSlabBlocks) {
+      : opt_(o), eng_(o.eng), sched_(o.mlfq), placer_(eng_.arena_frames() / o.slab_blocks, o.slab_blocks) {
     eng_.set_frame_placer(&placer_);
     eng_.set_progress_hook([this] { send_maps(); });
     sched_.set_logging(true);
@@ -394,9 +429,9 @@ class Daemon {
     rep.block_bytes = kBlockBytes;
     rep.min_bytes = opt_.min_bytes;
     rep.device = opt_.eng.device;
-    const std::uint32_t slabs = eng_.arena_frames() / ipc::kSlabBlocks;
+    const std::uint32_t slabs = eng_.arena_frames() / opt_.slab_blocks;
     rep.slabs = slabs;
-    rep.slab_bytes = static_cast<std::uint64_t>(ipc::kSlabBlocks) * kBlockBytes;
+    rep.slab_bytes = static_cast<std::uint64_t>(opt_.slab_blocks) * kBlockBytes;
     rep.arena_bytes = rep.slabs * rep.slab_bytes;
     bool ok = ipc::send_msg(fd, ipc::Msg::Hello, &rep, sizeof(rep)) && ipc::send_fds(fd, &a.ctl_fd, 1);
     std::vector<int> batch;
@@ -488,8 +523,9 @@ class Daemon {
         // Slabs the free emptied: the shim unmaps them (its reply carries them).
         std::vector<std::uint32_t> mine;
         for (const auto& k : placer_.take_released()) {
-          if (k.first == a.id) mine.push_back(k.second);
-          else throw InvariantViolation("free released another app's slab");
+          if (k.first != a.id) throw InvariantViolation("free released another app's slab");
+          mine.push_back(k.second);
+          placer_.set_mapped(k, ipc::kNoFrame);
         }
         ipc::FreeRep rep{status, static_cast<std::uint32_t>(mine.size()), ++epoch_};
         ipc::Writer w;
@@ -549,8 +585,10 @@ class Daemon {
     std::vector<std::uint32_t> ids;
     for (ChunkId c : chunks) ids.push_back(static_cast<std::uint32_t>(c));
     std::vector<ipc::SlabMap> slabs;
-    for (std::uint64_t v = va_block / ipc::kSlabBlocks; v <= (va_block + nblk - 1) / ipc::kSlabBlocks; ++v)
+    for (std::uint64_t v = va_block / opt_.slab_blocks; v <= (va_block + nblk - 1) / opt_.slab_blocks; ++v) {
       slabs.push_back(placer_.map_of(a.id, static_cast<std::uint32_t>(v)));
+      placer_.set_mapped({a.id, static_cast<std::uint32_t>(v)}, slabs.back().phys);
+    }
     rep.n_chunks = static_cast<std::uint32_t>(ids.size());
     rep.n_slabs = static_cast<std::uint32_t>(slabs.size());
     rep.footprint = fp;
@@ -634,7 +672,17 @@ class Daemon {
   // every message to one shim is ordered on its event socket.
   void send_maps() {
     std::map<AppId, std::vector<ipc::SlabMap>> per_app;
-    for (const auto& k : placer_.take_assigned()) per_app[k.first].push_back(placer_.map_of(k.first, k.second));
+    for (const auto& k : placer_.take_assigned()) {
+      const ipc::SlabMap m = placer_.map_of(k.first, k.second);
+      if (m.phys == ipc::kNoFrame || placer_.mapped(k) == m.phys) continue;  // already mapped there (affinity)
+      placer_.set_mapped(k, m.phys);
+      per_app[k.first].push_back(m);
+    }
+    // A vslab that lost its slab keeps its (stale) mapping: its owner cannot
+    // run until its next Grant, which remaps what changed and unmaps what is
+    // no longer backed. Mapping only on change lets a slab that returns to
+    // the same vslab cost nothing.
+    placer_.take_released();
     for (auto& [app, ms] : per_app) {
       auto it = apps_.find(app);
       if (it == apps_.end() || !it->second.alive || it->second.ev < 0) continue;
@@ -642,25 +690,6 @@ class Daemon {
       w.put(ipc::SlabsMsg{++epoch_, static_cast<std::uint32_t>(ms.size()), 0});
       for (const auto& m : ms) w.put(m);
       if (!ipc::send_msg(it->second.ev, ipc::Msg::Map, w.buf)) it->second.alive = false;
-    }
-    send_unmaps();
-  }
-
-  // After a plan ran: owners of vslabs whose physical slab was released unmap
-  // them. No ack is needed: only applications that cannot launch (paused
-  // or waiting) lose slabs, and the next Grant to them follows on the same
-  // socket.
-  void send_unmaps() {
-    std::map<AppId, std::vector<std::uint32_t>> per_app;
-    for (const auto& k : placer_.take_released()) per_app[k.first].push_back(k.second);
-    for (auto& [app, vs] : per_app) {
-      auto it = apps_.find(app);
-      if (it == apps_.end() || !it->second.alive || it->second.ev < 0) continue;
-      if (sched_.granted() == app) throw InvariantViolation("the grant holder lost a physical slab");
-      ipc::Writer w;
-      w.put(ipc::SlabsMsg{++epoch_, static_cast<std::uint32_t>(vs.size()), 0});
-      w.put_u32s(vs);
-      if (!ipc::send_msg(it->second.ev, ipc::Msg::Unmap, w.buf)) it->second.alive = false;
     }
   }
 
@@ -717,6 +746,7 @@ class Daemon {
     const std::uint64_t t_unmapped = ipc::mono_ns();
     // (5) grant: the incoming shim maps its slabs and sets its flag.
     const std::vector<ipc::SlabMap> slabs = placer_.backed(to);
+    placer_.granted(to);
     ipc::Writer w;
     w.put(ipc::SlabsMsg{++epoch_, static_cast<std::uint32_t>(slabs.size()), 0});
     for (const auto& m : slabs) w.put(m);

@@ -58,12 +58,13 @@ enum class Msg : std::uint32_t {
 
 // Virtual slabs: a shim reserves one large virtual range and places its
 // managed allocations in it at 2 MiB granularity; vslab k is the 128 MiB
-// (kSlabBlocks frames) window k of that range. The daemon backs every vslab
+// (slab_blocks frames, announced in HelloRep) window k of that range. The daemon backs every vslab
 // that holds a GPU-resident block with one physical slab of its arena, so the
 // shim maps whole slabs (one mapping per 64 blocks), and block j of an
-// allocation placed at range block v lives in frame phys * kSlabBlocks +
-// (v + j) % kSlabBlocks.
-constexpr std::uint32_t kSlabBlocks = 64;
+// allocation placed at range block v lives in frame phys * slab_blocks +
+// (v + j) % slab_blocks. The daemon picks the slab size (--slab-mib); every
+// mapping costs the same whatever its size (profiles/r01_vmm_probe*.txt).
+constexpr std::uint32_t kDefaultSlabBlocks = 256;  // 512 MiB
 
 struct SlabMap {
   std::uint32_t vslab;

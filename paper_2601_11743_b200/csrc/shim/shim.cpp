@@ -157,7 +157,7 @@ void die(const char* what, CUresult r = CUDA_SUCCESS) {
 }
 
 // ---- state ----------------------------------------------------------------------
-// A virtual slab (ipc::kSlabBlocks x 2 MiB window of the shim's range) and
+// A virtual slab (slab_blocks x 2 MiB window of the shim's range) and
 // the physical arena slab mapped under it.
 struct VSlab {
   std::uint32_t want = ipc::kNoFrame;  // physical slab the daemon placed it on (kNoFrame: none)
@@ -174,7 +174,7 @@ struct Shim {
   bool active = false;
   int device = 0;
   std::uint32_t app = 0;
-  std::uint64_t budget = 0, min_bytes = kBlock, slab_bytes = 0;
+  std::uint64_t budget = 0, min_bytes = kBlock, slab_bytes = 0, slab_blocks = 0;
   int rpc = -1, ev = -1;
   ipc::CtlPage* ctl = nullptr;
   std::vector<CUmemGenericAllocationHandle> slabs;  // imported arena slabs
@@ -267,7 +267,8 @@ void init_once() {
   g.budget = rep.gpu_budget;
   g.min_bytes = rep.min_bytes;
   g.slab_bytes = rep.slab_bytes;
-  if (g.slab_bytes != ipc::kSlabBlocks * kBlock) die("the daemon's slab size differs from this shim's");
+  if (g.slab_bytes == 0 || g.slab_bytes % kBlock != 0) die("bad slab size from the daemon");
+  g.slab_blocks = g.slab_bytes / kBlock;
   g.slabs.resize(rep.slabs, 0);
   std::vector<int> fds(ipc::kFdBatch);
   for (std::uint64_t f = 0; f < rep.slabs; f += ipc::kFdBatch) {
@@ -529,7 +530,7 @@ struct Blocking {
 // First fit in the range (caller holds g.mu); allocations of 64 MiB or more
 // start on a slab boundary so they do not straddle more slabs than needed.
 bool take_range(std::uint64_t n, std::uint64_t& start) {
-  const std::uint64_t align = n >= ipc::kSlabBlocks / 2 ? ipc::kSlabBlocks : 1;
+  const std::uint64_t align = n >= g.slab_blocks / 2 ? g.slab_blocks : 1;
   for (auto it = g.free_runs.begin(); it != g.free_runs.end(); ++it) {
     const std::uint64_t s0 = (it->first + align - 1) / align * align;
     if (s0 + n > it->first + it->second) continue;

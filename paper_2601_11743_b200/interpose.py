@@ -32,7 +32,8 @@ class Daemon:
     def __init__(self, gpu: str = "32G", pinned: str = "16G", paged: str = "96G", window: Optional[str] = None,
                  path: str = "ce", idle_ms: Optional[float] = None, tick_ms: Optional[float] = None,
                  allot_s: Optional[float] = None, preempt_s: Optional[float] = None, host_threads: Optional[int] = None,
-                 log: Optional[str] = None, prefetch: bool = False, extra: Sequence[str] = ()):
+                 log: Optional[str] = None, prefetch: bool = False, slab_mib: Optional[int] = None,
+                 extra: Sequence[str] = ()):
         for f in (NIXIED, SHIM):
             if not os.path.exists(f):
                 raise RuntimeError(f"{f} is not built (python -c 'import __graft_entry__ as g; g.build()')")
@@ -42,7 +43,7 @@ class Daemon:
         args = [NIXIED, "--socket", self.sock, "--gpu", gpu, "--pinned", pinned, "--paged", paged, "--path", path,
                 "--log", self.log]
         for flag, v in (("--window", window), ("--idle-ms", idle_ms), ("--tick-ms", tick_ms), ("--allot-s", allot_s),
-                        ("--preempt-s", preempt_s), ("--host-threads", host_threads)):
+                        ("--preempt-s", preempt_s), ("--host-threads", host_threads), ("--slab-mib", slab_mib)):
             if v is not None:
                 args += [flag, str(v)]
         self.args = args + (["--prefetch"] if prefetch else []) + list(extra)

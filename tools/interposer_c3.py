@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--horizon", type=float, default=60.0)
     ap.add_argument("--prefetch", action="store_true")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--slab-mib", type=int, default=None)
     a = ap.parse_args()
     h = a.horizon
     apps = [
@@ -34,10 +35,12 @@ def main():
     cmds = [[VECAPP, "--mib", str(mib), "--buffers", str(bufs), "--passes", str(passes), "--think-ms", str(think * 1e3),
              "--iters", str(iters), "--seed", str(i + 3), "--name", name, "--host-check", "0"]
             for i, (name, mib, bufs, passes, think, iters) in enumerate(apps)]
-    with Daemon(gpu="32G", pinned="16G", paged="96G", log=a.out, prefetch=a.prefetch) as d:
+    with Daemon(gpu="32G", pinned="16G", paged="96G", log=a.out, prefetch=a.prefetch, slab_mib=a.slab_mib) as d:
         res = run_apps(d, cmds, timeout=h * 4 + 300, stagger_s=0.2)
         sw = d.switches()
-    out = {"interval_s": a.interval, "horizon_s": h, "prefetch": a.prefetch, "switches": len(sw),
+    grants = sorted(s["grant_ms"] for s in sw)
+    out = {"interval_s": a.interval, "horizon_s": h, "prefetch": a.prefetch, "slab_mib": a.slab_mib or 128, "switches": len(sw),
+           "grant_ms": {"p50": grants[len(grants) // 2] if grants else None, "max": grants[-1] if grants else None},
            "apps_ok": all(r["rc"] == 0 for r in res),
            "mismatches": sum(s["mismatches"] for s in sw), "verified": sum(s["verified"] for s in sw),
            "switch_ms": {"p50": statistics.median([s["total_ms"] for s in sw]) if sw else None,
