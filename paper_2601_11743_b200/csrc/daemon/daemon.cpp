@@ -69,7 +69,7 @@ struct Options {
   double ack_timeout_s = 60.0;
   int exit_after_apps = 0;         // exit once this many apps have come and gone (tests)
   int phys_slack_slabs = -1;       // physical slabs beyond the budget (partly resident slabs); -1: max(4, 2 GiB worth)
-  std::uint32_t slab_blocks = ipc::kDefaultSlabBlocks;
+  std::uint32_t slab_blocks = 0;   // 0: 512 MiB for budgets >= 16 GiB, else 128 MiB
   bool prefetch = false;           // MLFQ prefetch of the next candidate
 };
 
@@ -89,7 +89,7 @@ void usage() {
                "usage: nixied [--socket PATH] [--device N] [--gpu SIZE] [--pinned SIZE] [--paged SIZE]\n"
                "              [--window SIZE] [--min-bytes SIZE] [--path auto|ce|sm] [--host-threads N]\n"
                "              [--tick-ms X] [--idle-ms X] [--allot-s X] [--preempt-s X] [--log FILE]\n"
-               "              [--phys-slack SLABS] [--slab-mib 128|256|512|1024] [--prefetch] [--exit-after-apps N]\n"
+               "              [--phys-slack SLABS] [--slab-mib 2..1024, power of 2] [--prefetch] [--exit-after-apps N]\n"
                "sizes take a K/M/G suffix (GiB when bare). The daemon serves LD_PRELOAD=libnixie_shim.so apps\n"
                "that set NIXIE_SOCKET=PATH.\n");
 }
@@ -135,10 +135,14 @@ bool parse_args(int argc, char** argv, Options& o) {
     }
   }
   o.mlfq.validate();
+  // Larger slabs mean fewer driver mappings per switch (each costs ~1 ms
+  // whatever its size); smaller ones waste less physical memory on partly
+  // resident slabs, which matters on small budgets.
+  if (o.slab_blocks == 0) o.slab_blocks = o.eng.gpu_capacity >= 16 * kGiB ? ipc::kDefaultSlabBlocks : 64;
   if (o.slab_blocks < 1 || (o.slab_blocks & (o.slab_blocks - 1)) != 0 || o.slab_blocks > 512)
     throw SimError(Err::ValidationError, "--slab-mib must be a power of two between 2 and 1024");
   const Bytes slab = static_cast<Bytes>(o.slab_blocks) * kBlockBytes;
-  if (o.phys_slack_slabs < 0) o.phys_slack_slabs = static_cast<int>(std::max<Bytes>(4, 2 * kGiB / slab));
+  if (o.phys_slack_slabs < 0) o.phys_slack_slabs = static_cast<int>(std::max<Bytes>(4, 2 * kGiB / slab));  // 2 GiB
   o.eng.arena_slab_bytes = slab;
   o.eng.gpu_physical = (o.eng.gpu_capacity + slab - 1) / slab * slab + static_cast<Bytes>(std::max(o.phys_slack_slabs, 0)) * slab;
   return true;

@@ -64,7 +64,7 @@ enum class Msg : std::uint32_t {
 // allocation placed at range block v lives in frame phys * slab_blocks +
 // (v + j) % slab_blocks. The daemon picks the slab size (--slab-mib); every
 // mapping costs the same whatever its size (profiles/r01_vmm_probe*.txt).
-constexpr std::uint32_t kDefaultSlabBlocks = 256;  // 512 MiB
+constexpr std::uint32_t kDefaultSlabBlocks = 256;  // 512 MiB (budgets >= 16 GiB; 128 MiB below)
 
 struct SlabMap {
   std::uint32_t vslab;
