@@ -682,11 +682,12 @@ class Daemon {
       placer_.set_mapped(k, m.phys);
       per_app[k.first].push_back(m);
     }
-    // A vslab that lost its slab keeps its (stale) mapping: its owner cannot
-    // run until its next Grant, which remaps what changed and unmaps what is
-    // no longer backed. Mapping only on change lets a slab that returns to
-    // the same vslab cost nothing.
-    placer_.take_released();
+    // A vslab that lost its slab keeps its (stale) mapping for now: its owner
+    // cannot run before its next Grant. cuMemUnmap while the copy engines
+    // move data costs up to ~80 ms per slab on these hosts (it waits on the
+    // GPU), so the owners drop their stale mappings after the switch, when
+    // the link is quiet (flush_unmaps).
+    for (const auto& k : placer_.take_released()) stale_.push_back(k);
     for (auto& [app, ms] : per_app) {
       auto it = apps_.find(app);
       if (it == apps_.end() || !it->second.alive || it->second.ev < 0) continue;
@@ -694,6 +695,27 @@ class Daemon {
       w.put(ipc::SlabsMsg{++epoch_, static_cast<std::uint32_t>(ms.size()), 0});
       for (const auto& m : ms) w.put(m);
       if (!ipc::send_msg(it->second.ev, ipc::Msg::Map, w.buf)) it->second.alive = false;
+    }
+  }
+
+  // After a switch: victims unmap the slabs they lost, off the critical path.
+  // A vslab that got a slab back meanwhile is skipped (mapped there again).
+  void flush_unmaps() {
+    std::map<AppId, std::vector<std::uint32_t>> per_app;
+    for (const auto& k : stale_) {
+      if (placer_.map_of(k.first, k.second).phys != ipc::kNoFrame) continue;  // backed again
+      if (placer_.mapped(k) == ipc::kNoFrame) continue;
+      placer_.set_mapped(k, ipc::kNoFrame);
+      per_app[k.first].push_back(k.second);
+    }
+    stale_.clear();
+    for (auto& [app, vs] : per_app) {
+      auto it = apps_.find(app);
+      if (it == apps_.end() || !it->second.alive || it->second.ev < 0 || sched_.granted() == app) continue;
+      ipc::Writer w;
+      w.put(ipc::SlabsMsg{++epoch_, static_cast<std::uint32_t>(vs.size()), 0});
+      w.put_u32s(vs);
+      if (!ipc::send_msg(it->second.ev, ipc::Msg::Unmap, w.buf)) it->second.alive = false;
     }
   }
 
@@ -716,6 +738,7 @@ class Daemon {
     const ExecResult r = eng_.execute(plan, cfg);
     send_maps();
     account(r);
+    flush_unmaps();
     note("{\"t\": %.6f, \"event\": \"fetch_in_place\", \"app\": %u, \"bytes_in\": %" PRIu64 ", \"bytes_out\": %" PRIu64 "}",
          now(), app, plan.bytes_in, plan.bytes_out);
   }
@@ -757,6 +780,7 @@ class Daemon {
     if (!eng_.mem().app_fully_resident(to, TierId::Gpu))
       throw InvariantViolation("grant: app " + std::to_string(to) + " is not GPU-resident after its switch");
     ipc::GrantedMsg gm{};
+    const std::uint64_t t_grant_sent = ipc::mono_ns();
     if (ipc::send_msg(in.ev, ipc::Msg::Grant, w.buf) && wait_ack(in, ipc::Msg::Granted, body) && body.size() >= sizeof(gm))
       std::memcpy(&gm, body.data(), sizeof(gm));
     const std::uint64_t t_end = ipc::mono_ns();
@@ -764,18 +788,23 @@ class Daemon {
     const Seconds granted_at = t + static_cast<double>(t_end - t_start) * 1e-9;
     sched_.on_grant_start(to, granted_at);
     sched_.on_api_event(to, granted_at, ApiEventKind::NonBlockingReturn);  // its held launch resumes now
+    flush_unmaps();
     ++switches_;
     const SwitchStats& s = eng_.last_stats();
     auto ms = [](std::uint64_t a, std::uint64_t b) { return static_cast<double>(b - a) * 1e-6; };
     note("{\"t\": %.6f, \"event\": \"switch\", \"from\": %d, \"to\": %u, \"bytes_in\": %" PRIu64 ", \"bytes_out\": %" PRIu64
          ", \"pcie_h2d\": %" PRIu64 ", \"pcie_d2h\": %" PRIu64 ", \"host_bytes\": %" PRIu64
          ", \"pause_ms\": %.3f, \"plan_ms\": %.3f, \"copy_ms\": %.3f, \"unmap_wait_ms\": %.3f, \"grant_ms\": %.3f"
-         ", \"map_ms\": %.3f, \"map_calls\": %" PRIu64 ", \"unmap_calls\": %" PRIu64 ", \"total_ms\": %.3f, \"device_span_ms\": %.3f"
+         ", \"map_ms\": %.3f, \"map_calls\": %" PRIu64 ", \"unmap_calls\": %" PRIu64 ", \"grant_recv_ms\": %.3f"
+         ", \"premap_ms\": %.3f, \"premap_calls\": %" PRIu64 ", \"premap_unmap_ms\": %.3f, \"total_ms\": %.3f"
+         ", \"device_span_ms\": %.3f"
          ", \"verified\": %" PRIu64 ", \"unverified\": %" PRIu64 ", \"mismatches\": %" PRIu64
          ", \"partial_slabs\": %" PRIu64 ", \"free_slabs\": %zu}",
          t, holder ? static_cast<int>(*holder) : -1, to, plan.bytes_in, plan.bytes_out, s.pcie_h2d_bytes, s.pcie_d2h_bytes,
          s.host_bytes, ms(t_start, t_drained), ms(t_drained, t_planned), ms(t_planned, t_copied), ms(t_copied, t_unmapped),
-         ms(t_unmapped, t_end), static_cast<double>(gm.map_ns) * 1e-6, gm.map_calls, gm.unmap_calls, ms(t_start, t_end),
+         ms(t_unmapped, t_end), static_cast<double>(gm.map_ns) * 1e-6, gm.map_calls, gm.unmap_calls,
+         gm.recv_ns > t_grant_sent ? ms(t_grant_sent, gm.recv_ns) : 0.0, static_cast<double>(gm.premap_ns) * 1e-6, gm.premap_calls,
+         static_cast<double>(gm.premap_unmap_ns) * 1e-6, ms(t_start, t_end),
          s.device_span_s * 1e3, s.verified, s.unverified, s.mismatches, placer_.partial(), placer_.free_slabs());
   }
 
@@ -802,6 +831,7 @@ class Daemon {
   SlabPlacer placer_;
   int listen_fd_ = -1;
   std::vector<int> pending_;
+  std::vector<SlabPlacer::Key> stale_;  // released vslabs whose owners still map their old slab
   std::map<AppId, App> apps_;
   AppId next_app_ = 0;
   int gone_ = 0;

@@ -133,6 +133,10 @@ struct GrantedMsg {
   std::uint64_t map_ns;       // shim-side mapping time
   std::uint64_t map_calls;    // cuMemMap calls made
   std::uint64_t unmap_calls;  // cuMemUnmap calls made
+  std::uint64_t recv_ns;      // CLOCK_MONOTONIC when the listener took the Grant off the socket
+  std::uint64_t premap_ns;    // time spent on Map messages since the previous Grant
+  std::uint64_t premap_calls; // cuMemMap calls they made
+  std::uint64_t premap_unmap_ns;  // of premap_ns: cuMemUnmap of the slabs' previous mappings
 };
 struct StatsRep {
   std::uint64_t switches;

@@ -379,18 +379,28 @@ void on_unmap(const std::vector<std::uint8_t>& body) {
   for (std::uint32_t i = 0; i < m.n && r.ok; ++i) place(r.get<std::uint32_t>(), ipc::kNoFrame, m.epoch, maps, unmaps);
 }
 
+std::uint64_t g_premap_ns = 0, g_premap_calls = 0, g_premap_unmap_ns = 0;  // listener thread only
+
 void on_map(const std::vector<std::uint8_t>& body) {
+  const std::uint64_t t0 = ipc::mono_ns();
+  const std::uint64_t u0 = g.ctl ? g.ctl->unmap_ns.load() : 0;
   ipc::Reader r{body};
   const auto m = r.get<ipc::SlabsMsg>();
   std::uint64_t maps = 0, unmaps = 0;
-  std::lock_guard<std::mutex> lk(g.mu);
-  for (std::uint32_t i = 0; i < m.n && r.ok; ++i) {
-    const auto sm = r.get<ipc::SlabMap>();
-    place(sm.vslab, sm.phys, m.epoch, maps, unmaps);
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    for (std::uint32_t i = 0; i < m.n && r.ok; ++i) {
+      const auto sm = r.get<ipc::SlabMap>();
+      place(sm.vslab, sm.phys, m.epoch, maps, unmaps);
+    }
   }
+  g_premap_ns += ipc::mono_ns() - t0;
+  g_premap_calls += maps;
+  if (g.ctl) g_premap_unmap_ns += g.ctl->unmap_ns.load() - u0;
 }
 
 void on_grant(const std::vector<std::uint8_t>& body) {
+  const std::uint64_t recv = ipc::mono_ns();
   ipc::Reader r{body};
   const auto m = r.get<ipc::SlabsMsg>();
   const std::uint64_t t0 = ipc::mono_ns();
@@ -410,7 +420,8 @@ void on_grant(const std::vector<std::uint8_t>& body) {
     if (g.ctl) g.ctl->granted.store(1);
   }
   g.cv.notify_all();
-  ipc::GrantedMsg ack{m.epoch, ipc::mono_ns() - t0, maps, unmaps};
+  ipc::GrantedMsg ack{m.epoch, ipc::mono_ns() - t0, maps, unmaps, recv, g_premap_ns, g_premap_calls, g_premap_unmap_ns};
+  g_premap_ns = g_premap_calls = g_premap_unmap_ns = 0;
   ipc::send_msg(g.ev, ipc::Msg::Granted, &ack, sizeof(ack));
 }
 
