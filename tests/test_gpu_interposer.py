@@ -118,3 +118,28 @@ def test_three_apps_with_torch():
     assert res[1]["out"]["mismatch"] == 0 and res[1]["out"]["matmul_mismatch"] == 0
     assert res[1]["out"]["memgetinfo"][1] == 5 << 30
     assert len(sw) >= 3 and all(s["mismatches"] == 0 for s in sw)
+
+
+def test_app_killed_mid_run_does_not_stall_the_others():
+    """An application killed while it holds or waits for the GPU: the daemon
+    reaps it (its chunks return to the registry, its slabs to the pool) and
+    the other applications finish byte-exact."""
+    import signal
+    import time
+    with Daemon(gpu="4G", pinned="4G", paged="16G") as d:
+        victim = d.spawn(_vec(2048, 1000, 100, 51, "victim"))
+        others = [d.spawn(_vec(2048, 6, 200, 52 + i, f"o{i}")) for i in range(2)]
+        time.sleep(6.0)
+        victim.send_signal(signal.SIGKILL)
+        victim.wait(30)
+        outs = [p.communicate(timeout=600) for p in others]
+        recs = d.records()
+        alive = d.proc.poll() is None
+    assert alive, d.stderr()
+    for p, (out, err) in zip(others, outs):
+        assert p.returncode == 0, err
+        r = json.loads(out.strip().splitlines()[-1])
+        assert r["device_errors"] == 0 and r["host_mismatch"] == 0
+    byes = [r for r in recs if r.get("event") == "bye"]
+    assert len(byes) == 3
+    assert all(r["mismatches"] == 0 for r in recs if r.get("event") == "switch")
