@@ -273,6 +273,23 @@ def x16_exchange(path: int, switches: int = 4) -> dict:
             "byte_exact": bad == 0}
 
 
+def interposer_c2(timeout_s: float = 240.0) -> dict:
+    """The same workload (config 2) through the deployment path: two unmodified
+    CUDA programs (16 + 24 GiB vecapps) under nixied + LD_PRELOAD shim on the
+    32 GiB budget (tools/interposer_bench.py). Steady switches exchange 8 GiB
+    each way; GB/s = both directions' bytes over the daemon's copy time."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "interposer_bench.py"), "--iters", "10"],
+                       capture_output=True, text=True, timeout=timeout_s)
+    try:
+        d = json.loads(p.stdout.strip().splitlines()[-1])
+    except (ValueError, IndexError):
+        return {"error": (p.stderr or p.stdout)[-300:]}
+    return {"value": d.get("copy_bidir_gbps_median"), "unit": "GB/s", "switch_ms": d.get("switch_total_ms"),
+            "grant_ms_median": d.get("grant_ms_median"), "steady_switches": d.get("steady_switches"),
+            "verified": d.get("verified"), "mismatches": d.get("mismatches"), "apps_ok": d.get("apps_ok"),
+            "apps": "2 unmodified CUDA programs (tests/apps/vecapp.cu) under lib/nixied + LD_PRELOAD lib/libnixie_shim.so"}
+
+
 def run_product(args, dist: Dist):
     from paper_2601_11743_b200 import PlannerConfig, SwapEngine, load_scenario, parse_path
     from paper_2601_11743_b200._lib import TIER_GPU, TIER_PINNED
@@ -329,6 +346,12 @@ def run_product(args, dist: Dist):
     wall_max = dist.reduce(wall, "max")
     bad_all = dist.reduce(bad, "sum")
     x16 = x16_exchange(path) if (args.x16 and dist.rank == 0) else None
+    ip = None
+    if args.interposer and args.gpus == 1 and dist.rank == 0:
+        try:
+            ip = interposer_c2()
+        except Exception as e:  # noqa: BLE001  (reported, never fatal to the bench line)
+            ip = {"error": str(e)[-300:]}
     if dist.rank != 0:
         return 0
 
@@ -403,6 +426,7 @@ def run_product(args, dist: Dist):
         "byte_exact": bad_all == 0,
         "verified_restores": sum(s["verified"] for s in stats),
         "x16_exchange": x16,
+        "interposer": ip,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -417,6 +441,8 @@ def main():
     ap.add_argument("--path", choices=["auto", "sm", "ce"], default="auto")
     ap.add_argument("--no-x16", dest="x16", action="store_false")
     ap.add_argument("--legs-per-launch", type=int, default=0, help="CE batch / K3 launch size (0: engine default)")
+    ap.add_argument("--no-interposer", dest="interposer", action="store_false",
+                    help="skip the config-2 run through nixied + the LD_PRELOAD shim")
     args = ap.parse_args()
     dist = Dist()
     try:
