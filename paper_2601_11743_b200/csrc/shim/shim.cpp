@@ -55,6 +55,7 @@
 #include <vector>
 
 #include "nixie_ipc.hpp"
+#include "range_alloc.hpp"
 
 // Per-thread-default-stream variants (declared by cuda_runtime_api.h only
 // when that mode is compiled in; libcudart exports them regardless).
@@ -185,7 +186,7 @@ struct Shim {
   std::mutex rpc_mu;            // one request in flight on the rpc socket
   std::mutex mu;                // everything below (slow paths only)
   std::condition_variable cv;
-  std::map<std::uint64_t, std::uint64_t> free_runs;  // range blocks: start -> length
+  nixie::shim::RangeAlloc ranges;  // managed allocations in the range, 2 MiB blocks
   std::map<CUdeviceptr, Region> regions;
   std::unordered_map<std::uint32_t, VSlab> vslabs;
   std::map<void*, std::size_t> small;  // passthrough allocations (for cudaMemGetInfo)
@@ -285,7 +286,7 @@ void init_once() {
     const CUresult r = drv().addr_reserve(&g.range, kRangeBytes, g.slab_bytes, 0, 0);
     if (r != CUDA_SUCCESS) die("cuMemAddressReserve(range)", r);
     g.range_blocks = kRangeBytes / kBlock;
-    g.free_runs[0] = g.range_blocks;
+    g.ranges.reset(g.range_blocks);
   }
   void* p = ::mmap(nullptr, 4096, PROT_READ | PROT_WRITE, MAP_SHARED, ctl_fd, 0);
   if (p == MAP_FAILED) die("mmap control page");
@@ -538,45 +539,12 @@ struct Blocking {
 };
 
 // ---- allocation -------------------------------------------------------------------------
-// First fit in the range (caller holds g.mu); allocations of 64 MiB or more
-// start on a slab boundary so they do not straddle more slabs than needed.
-bool take_range(std::uint64_t n, std::uint64_t& start) {
-  const std::uint64_t align = n >= g.slab_blocks / 2 ? g.slab_blocks : 1;
-  for (auto it = g.free_runs.begin(); it != g.free_runs.end(); ++it) {
-    const std::uint64_t s0 = (it->first + align - 1) / align * align;
-    if (s0 + n > it->first + it->second) continue;
-    const std::uint64_t run_start = it->first, run_len = it->second;
-    g.free_runs.erase(it);
-    if (s0 > run_start) g.free_runs[run_start] = s0 - run_start;
-    if (s0 + n < run_start + run_len) g.free_runs[s0 + n] = run_start + run_len - (s0 + n);
-    start = s0;
-    return true;
-  }
-  return false;
-}
-
-void give_range(std::uint64_t start, std::uint64_t n) {
-  auto next = g.free_runs.lower_bound(start);
-  if (next != g.free_runs.end() && start + n == next->first) {
-    n += next->second;
-    next = g.free_runs.erase(next);
-  }
-  if (next != g.free_runs.begin()) {
-    auto prev = std::prev(next);
-    if (prev->first + prev->second == start) {
-      prev->second += n;
-      return;
-    }
-  }
-  g.free_runs[start] = n;
-}
-
 int managed_alloc(void** out, std::size_t bytes) {
   const std::uint64_t n = (bytes + kBlock - 1) / kBlock;
   std::uint64_t first = 0;
   {
     std::lock_guard<std::mutex> lk(g.mu);
-    if (!take_range(n, first)) return 2;
+    if (!g.ranges.take(n, g.slab_blocks, first)) return 2;
   }
   ipc::AllocReq req{bytes, first};
   ipc::Msg rt;
@@ -587,7 +555,7 @@ int managed_alloc(void** out, std::size_t bytes) {
   const auto rep = r.get<ipc::AllocRep>();
   std::lock_guard<std::mutex> lk(g.mu);
   if (rep.status != 0) {
-    give_range(first, n);
+    g.ranges.give(first, n);
     return 2;
   }
   Region reg{first, n, {}};
@@ -633,7 +601,7 @@ bool managed_free(void* p) {
   std::lock_guard<std::mutex> lk(g.mu);
   std::uint64_t maps = 0, unmaps = 0;
   for (std::uint32_t k = 0; k < rep.n && r.ok; ++k) place(r.get<std::uint32_t>(), ipc::kNoFrame, rep.epoch, maps, unmaps);
-  give_range(reg.first, reg.blocks);
+  g.ranges.give(reg.first, reg.blocks);
   g.managed_bytes -= reg.blocks * kBlock;
   return true;
 }

@@ -1,0 +1,100 @@
+// Host-only unit tests of the interposer's placement logic (no GPU):
+//   SlabPlacer (csrc/daemon/slab_placer.hpp): slot arithmetic, sharing of a
+//     slab by the blocks of one vslab, release, affinity, exhaustion,
+//     mapping bookkeeping;
+//   RangeAlloc (csrc/shim/range_alloc.hpp): first fit, slab alignment,
+//     coalescing on free.
+// Built by paper_2601_11743_b200/Makefile (lib/nx_unit_tests); run by
+// tests/test_interposer_host.py.
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "range_alloc.hpp"
+#include "slab_placer.hpp"
+
+using namespace nixie;
+using namespace nixie::b200;
+
+static int failures = 0, checks = 0;
+#define CHECK(c)                                                       \
+  do {                                                                 \
+    ++checks;                                                          \
+    if (!(c)) {                                                        \
+      ++failures;                                                      \
+      std::fprintf(stderr, "%s:%d CHECK(%s) failed\n", __FILE__, __LINE__, #c); \
+    }                                                                  \
+  } while (0)
+
+static void slab_placer() {
+  const std::uint32_t sb = 4;      // blocks per slab
+  SlabPlacer p(3, sb);             // 3 physical slabs
+  // app 7: blocks 0..5 at range blocks 2..7 (vslab 0: slots 2,3; vslab 1: slots 0..3)
+  p.expect(0, 6, 7, 2);
+  const std::uint32_t f0 = p.acquire(0), f1 = p.acquire(1), f2 = p.acquire(2);
+  CHECK(f0 / sb == f1 / sb);            // same vslab -> same physical slab
+  CHECK(f0 % sb == 2 && f1 % sb == 3);  // at the blocks' slots
+  CHECK(f2 / sb != f0 / sb && f2 % sb == 0);
+  CHECK(p.free_slabs() == 1);
+  auto as = p.take_assigned();
+  CHECK(as.size() == 2);                // two vslabs got slabs
+  CHECK(p.take_assigned().empty());
+  p.release(0, f0);
+  CHECK(p.take_released().empty());     // vslab 0 still holds block 1
+  p.release(1, f1);
+  auto rel = p.take_released();
+  CHECK(rel.size() == 1 && rel[0].first == 7 && rel[0].second == 0);
+  CHECK(p.free_slabs() == 2);
+  // affinity: vslab 0 gets its old slab back while it is free
+  const std::uint32_t g0 = p.acquire(0);
+  CHECK(g0 / sb == f0 / sb);
+  // ... but not once another vslab took it
+  p.release(0, g0);
+  p.expect(6, 4, 9, 0);                 // app 9, vslab 0
+  const std::uint32_t h = p.acquire(6);
+  const std::uint32_t h2 = p.acquire(7);  // app 9 takes another free slab for the same vslab? no: same vslab
+  CHECK(h / sb == h2 / sb);
+  const std::uint32_t again = p.acquire(0);
+  CHECK(again / sb != h / sb);
+  // exhaustion
+  p.expect(10, 4, 11, 0);
+  bool threw = false;
+  try {
+    p.acquire(10);
+  } catch (const InvariantViolation&) {
+    threw = true;
+  }
+  CHECK(threw);
+  // mapping bookkeeping
+  const SlabPlacer::Key k{7, 1};
+  CHECK(p.mapped(k) == ipc::kNoFrame);
+  p.set_mapped(k, 2);
+  CHECK(p.mapped(k) == 2);
+  p.granted(7);
+  CHECK(p.mapped(k) == p.map_of(7, 1).phys);
+  CHECK(p.backed(7).size() == 2);
+  CHECK(p.backed(9).size() == 1);
+}
+
+static void range_alloc() {
+  nixie::shim::RangeAlloc r;
+  r.reset(1024);
+  std::uint64_t a = 0, b = 0, c = 0, d = 0;
+  CHECK(r.take(3, 64, a) && a == 0);     // small: first fit
+  CHECK(r.take(40, 64, b) && b == 64);   // >= half a slab: slab aligned
+  CHECK(r.take(10, 64, c) && c == 3);    // fills the hole
+  CHECK(!r.take(2000, 64, d));
+  r.give(b, 40);
+  r.give(a, 3);
+  r.give(c, 10);
+  CHECK(r.runs().size() == 1 && r.runs().begin()->first == 0 && r.runs().begin()->second == 1024);  // coalesced
+  CHECK(r.take(1024, 64, d) && d == 0);
+  CHECK(!r.take(1, 64, d));
+}
+
+int main() {
+  slab_placer();
+  range_alloc();
+  std::printf("nx_unit_tests: %d checks, %d failures\n", checks, failures);
+  return failures ? 1 : 0;
+}

@@ -58,3 +58,11 @@ def test_test_app_links_the_shared_runtime():
     """LD_PRELOAD can only interpose a dynamically linked CUDA runtime."""
     out = subprocess.run(["readelf", "-d", VECAPP], capture_output=True, text=True, check=True).stdout
     assert "libcudart.so" in out
+
+
+def test_placement_unit_tests():
+    """SlabPlacer (daemon) and RangeAlloc (shim) host-only unit tests."""
+    exe = os.path.join(ROOT, "paper_2601_11743_b200", "lib", "nx_unit_tests")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout
