@@ -28,7 +28,7 @@ class EngineConfig:
     pinned_capacity: int = 16 * GIB
     paged_capacity: int = 96 * GIB
     path: int = L.PATH_AUTO
-    pcie_legs_in_flight: int = 512
+    pcie_legs_in_flight: int = 1024
     legs_per_launch: int = 128
     host_threads: int = 8
     host_legs_in_flight: int = 64
