@@ -195,7 +195,8 @@ struct Shim {
   std::atomic<bool> granted{false};
   std::atomic<bool> exiting{false};  // the process is exiting: the driver may be torn down
   std::atomic<int> inflight{0};
-  std::atomic<int> capturing{0};
+  std::atomic<int> capturing{0};         // stream captures in progress (any mode)
+  std::atomic<int> capturing_global{0};  // ... in global mode: no other thread may call unsafe APIs
 };
 
 constexpr std::uint64_t kRangeBytes = 1ull << 40;  // 1 TiB of virtual space per process
@@ -205,6 +206,7 @@ Shim& g = *new Shim;
 bool exiting() { return g.exiting.load(); }
 std::once_flag g_once;
 thread_local int t_capturing = 0;  // this thread began a stream capture
+thread_local std::vector<bool> t_capture_global;  // mode of each open capture of this thread
 thread_local int t_gate_depth = 0; // this thread holds a gate slot (nested gated calls pass)
 thread_local int t_in_shim = 0;    // re-entrancy guard
 
@@ -355,6 +357,12 @@ void place(std::uint32_t v, std::uint32_t phys, std::uint64_t epoch, std::uint64
   sync_vslab(v, s, maps, unmaps);
 }
 
+// A global-mode capture forbids other threads' unsafe CUDA calls (they would
+// invalidate it): the listener's VMM calls wait until it ends.
+void wait_for_global_captures() {
+  while (g.capturing_global.load() != 0) std::this_thread::sleep_for(std::chrono::microseconds(50));
+}
+
 // ---- event socket: Pause / Unmap / Grant ----------------------------------------------
 void on_pause(const std::vector<std::uint8_t>& body) {
   ipc::EpochMsg m{};
@@ -373,6 +381,7 @@ void on_pause(const std::vector<std::uint8_t>& body) {
 }
 
 void on_unmap(const std::vector<std::uint8_t>& body) {
+  wait_for_global_captures();
   ipc::Reader r{body};
   const auto m = r.get<ipc::SlabsMsg>();
   std::uint64_t maps = 0, unmaps = 0;
@@ -383,6 +392,7 @@ void on_unmap(const std::vector<std::uint8_t>& body) {
 std::uint64_t g_premap_ns = 0, g_premap_calls = 0, g_premap_unmap_ns = 0;  // listener thread only
 
 void on_map(const std::vector<std::uint8_t>& body) {
+  wait_for_global_captures();
   const std::uint64_t t0 = ipc::mono_ns();
   const std::uint64_t u0 = g.ctl ? g.ctl->unmap_ns.load() : 0;
   ipc::Reader r{body};
@@ -402,6 +412,7 @@ void on_map(const std::vector<std::uint8_t>& body) {
 
 void on_grant(const std::vector<std::uint8_t>& body) {
   const std::uint64_t recv = ipc::mono_ns();
+  wait_for_global_captures();
   ipc::Reader r{body};
   const auto m = r.get<ipc::SlabsMsg>();
   const std::uint64_t t0 = ipc::mono_ns();
@@ -864,6 +875,8 @@ cudaError_t cudaStreamBeginCapture(cudaStream_t st, cudaStreamCaptureMode mode) 
   if (e == cudaSuccess && !t_in_shim) {
     ++t_capturing;
     g.capturing.fetch_add(1);
+    t_capture_global.push_back(mode == cudaStreamCaptureModeGlobal);
+    if (mode == cudaStreamCaptureModeGlobal) g.capturing_global.fetch_add(1);
   }
   return e;
 }
@@ -874,6 +887,10 @@ cudaError_t cudaStreamEndCapture(cudaStream_t st, cudaGraph_t* graph) {
   if (!t_in_shim && t_capturing > 0) {
     --t_capturing;
     g.capturing.fetch_sub(1);
+    if (!t_capture_global.empty()) {
+      if (t_capture_global.back()) g.capturing_global.fetch_sub(1);
+      t_capture_global.pop_back();
+    }
   }
   return e;
 }

@@ -6,6 +6,8 @@
 //
 //   nx_vecapp --mib N --buffers K --iters I --think-ms T --seed S [--name X] [--host-check 0|1] [--driver 0|1]
 //             [--passes P]   (P step kernels over the working set per iteration)
+//             [--graph 0|1|2] (iterations as launches of one captured CUDA graph;
+//                              2: captured in global mode)
 //
 // Every word of every buffer holds hash(seed, buffer, index) + iteration; each
 // iteration's kernel checks the expected value and increments it, so a byte
@@ -52,6 +54,21 @@ __global__ void step(std::uint32_t* p, std::uint64_t n, std::uint64_t seed, int 
   if (bad) atomicAdd(errors, bad);
 }
 
+__global__ void step_dev(std::uint32_t* p, std::uint64_t n, std::uint64_t seed, int buf, const std::uint32_t* iter,
+                         unsigned long long* errors) {
+  const std::uint32_t it = *iter;
+  unsigned long long bad = 0;
+  for (std::uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const std::uint32_t want = expect(seed, buf, i) + it;
+    const std::uint32_t v = p[i];
+    bad += v != want;
+    p[i] = v + 1;
+  }
+  if (bad) atomicAdd(errors, bad);
+}
+
+__global__ void bump(std::uint32_t* k) { *k += 1; }
+
 #define CK(x)                                                                                   \
   do {                                                                                          \
     cudaError_t e_ = (x);                                                                       \
@@ -70,6 +87,7 @@ int main(int argc, char** argv) {
   int host_check = 1;
   int driver = 0;  // 1: launch `step` through the driver API (cuLaunchKernel from cudaGetDriverEntryPoint)
   int passes = 1;  // step kernels over the whole working set per iteration (compute per request)
+  int graph = 0;   // 1: each iteration is one cudaGraphLaunch of a graph captured once (per pass offset)
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string a = argv[i];
     if (a == "--mib") mib = std::atof(argv[i + 1]);
@@ -81,6 +99,7 @@ int main(int argc, char** argv) {
     else if (a == "--host-check") host_check = std::atoi(argv[i + 1]);
     else if (a == "--driver") driver = std::atoi(argv[i + 1]);
     else if (a == "--passes") passes = std::atoi(argv[i + 1]);
+    else if (a == "--graph") graph = std::atoi(argv[i + 1]);
   }
   const auto t_start = std::chrono::steady_clock::now();
   const std::uint64_t bytes_each = static_cast<std::uint64_t>(mib * 1048576.0 / buffers) / 4 * 4;
@@ -110,7 +129,34 @@ int main(int argc, char** argv) {
   }
   std::vector<double> lat;
   std::uint32_t k = 0;  // passes done so far: every word holds expect() + k
-  for (int it = 0; it < iters; ++it) {
+  // --graph: the step kernels read the pass counter from device memory, so one
+  // captured graph (steps + counter increment) serves every iteration.
+  std::uint32_t* d_k = nullptr;
+  cudaStream_t gs = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  if (graph) {
+    CK(cudaMalloc(&d_k, sizeof(std::uint32_t)));
+    CK(cudaMemset(d_k, 0, sizeof(std::uint32_t)));
+    CK(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(gs, graph == 2 ? cudaStreamCaptureModeGlobal : cudaStreamCaptureModeThreadLocal));
+    for (int pass = 0; pass < passes; ++pass) {
+      for (int b = 0; b < buffers; ++b) step_dev<<<1184, 256, 0, gs>>>(buf[b], n, seed, b, d_k, d_err);
+      bump<<<1, 1, 0, gs>>>(d_k);
+    }
+    CK(cudaStreamEndCapture(gs, &g));
+    CK(cudaGraphInstantiate(&gexec, g, 0));
+    CK(cudaGraphDestroy(g));
+  }
+  for (int it = 0; it < iters && graph; ++it) {
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaGraphLaunch(gexec, gs));
+    CK(cudaStreamSynchronize(gs));
+    k += passes;
+    lat.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    if (think_ms > 0) std::this_thread::sleep_for(std::chrono::duration<double, std::milli>(think_ms));
+  }
+  for (int it = 0; it < iters && !graph; ++it) {
     const auto t0 = std::chrono::steady_clock::now();
     for (int pass = 0; pass < passes; ++pass, ++k)
     for (int b = 0; b < buffers; ++b) {

@@ -97,6 +97,22 @@ def test_prefetch_under_the_daemon():
     assert all(r["mismatches"] == 0 for r in recs if r.get("event") == "switch")
 
 
+def test_cuda_graph_apps():
+    """Apps that capture their iteration into a CUDA graph (thread-local and
+    global capture mode) and launch it every iteration: the capture guard
+     keeps the shim's own CUDA calls out of the capture, and
+    graph launches are gated like kernel launches."""
+    with Daemon(gpu="4G", pinned="4G", paged="16G") as d:
+        res = run_apps(d, [_vec(3072, 5, 250, 61, "g1") + ["--graph", "1", "--passes", "2"],
+                           _vec(3072, 5, 250, 62, "g2") + ["--graph", "2", "--passes", "2"]], timeout=600)
+        _save("graphs", d, res)
+        _check(res, d)
+        sw = d.switches()
+    for r in res:
+        assert r["out"]["device_errors"] == 0 and r["out"]["host_mismatch"] == 0
+    assert len(sw) >= 3 and all(s["mismatches"] == 0 for s in sw)
+
+
 def test_memgetinfo_reports_budget():
     with Daemon(gpu="6G", pinned="2G", paged="8G") as d:
         res = run_apps(d, [_vec(1024, 1, 0, 3, "m")], timeout=300)
