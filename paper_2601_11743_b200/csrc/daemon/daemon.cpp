@@ -347,9 +347,24 @@ class Daemon {
     } catch (const InvariantViolation&) {
       throw;
     } catch (const std::exception& e) {
+      // The request failed (e.g. a tier is full): answer with the reply type
+      // the shim waits for, carrying an error status (cudaMalloc then
+      // returns cudaErrorMemoryAllocation).
       std::fprintf(stderr, "[nixied] app %u: %s\n", a->id, e.what());
-      ipc::StatusRep st{100, 0};
-      ipc::send_msg(a->rpc, ipc::Msg::Status, &st, sizeof(st));
+      const auto* se = dynamic_cast<const SimError*>(&e);
+      const std::int32_t code = 100 + (se ? static_cast<std::int32_t>(se->code()) : 0);
+      if (type == ipc::Msg::Alloc) {
+        ipc::AllocRep rep{};
+        rep.status = code;
+        rep.epoch = ++epoch_;
+        ipc::send_msg(a->rpc, ipc::Msg::Alloc, &rep, sizeof(rep));
+      } else if (type == ipc::Msg::Free) {
+        ipc::FreeRep rep{code, 0, ++epoch_};
+        ipc::send_msg(a->rpc, ipc::Msg::Free, &rep, sizeof(rep));
+      } else {
+        ipc::StatusRep st{code, 0};
+        ipc::send_msg(a->rpc, type == ipc::Msg::Stats ? ipc::Msg::Stats : ipc::Msg::Status, &st, sizeof(st));
+      }
     }
   }
 
