@@ -177,6 +177,7 @@ class SwapEngine {
   void prefetch_begin(const MigrationPlan& plan);
   bool prefetch_pump();
   void prefetch_quiesce();
+  void prefetch_wait();  // runs every queued leg to completion
   bool prefetch_active() const;
   Bytes prefetched_bytes() const;  // committed since construction
 

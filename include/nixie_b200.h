@@ -258,8 +258,10 @@ int nx_scenario_real(const char* spec, const nx_engine_config* cfg, uint64_t see
  * (SPEC.md:455); its reference twin is oracle/_ref/ref_workload. */
 int nx_workload_model(const char* spec, char** trace, size_t* len);
 /* Same workload with every planned switch executed by the CUDA engine (real
- * bytes; decisions keep the virtual clock). Adds `M k differing-blocks`,
- * `V k app bad ...` and final `F app bad` lines. */
+ * bytes; decisions keep the virtual clock; with `prefetch on` the engine also
+ * performs the prefetch moves the model committed before each switch). Adds
+ * `H k moves`, `M k differing-blocks`, `V k app bad ...` and final
+ * `F app bad` lines. */
 int nx_workload_real(const char* spec, const nx_engine_config* cfg, uint64_t seed, char** trace, size_t* len);
 void nx_free(void* p);
 

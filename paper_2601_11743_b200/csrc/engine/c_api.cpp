@@ -737,20 +737,38 @@ int nx_workload_real(const char* spec, const nx_engine_config* cfg, uint64_t see
     ec.pinned_capacity = ws.hw.tier_capacity[1];
     ec.paged_capacity = ws.hw.tier_capacity[2];
     SwapEngine eng(ec);
+    // The workload engine runs on its own model registry (its prefetch
+    // Orchestrator commits there, on the virtual clock); the CUDA engine
+    // mirrors it: before each switch it performs, for real, the prefetch
+    // moves the model committed, then executes the same plan.
+    MemState model_mem;
+    ws.hw.apply_to(model_mem);
     std::string extra;
     std::size_t k = 0;
     workload::Runner runner = [&](const MigrationPlan& plan, MemState& mem, const HardwareConfig& hw, const PlannerConfig& pc,
                                   Seconds now, std::array<std::vector<std::array<std::uint64_t, 3>>, 6>& lanes) {
-      MemState model = mem;
-      const ExecResult m = execute(plan, model, hw, pc, now);
-      eng.execute(plan, pc);
+      MigrationPlan pf;
+      for (std::size_t b = 0; b < mem.block_count(); ++b) {
+        const Block& mb = mem.block(b);
+        const Block& eb = eng.mem().block(b);
+        if (mb.alive && mb.loc.is_resident() && eb.loc.is_resident() && mb.loc.tier == TierId::PinnedHost &&
+            eb.loc.tier == TierId::PagedHost)
+          pf.moves.push_back(Move{b, TierId::PagedHost, TierId::PinnedHost, MoveKind::PrefetchToPinned});
+      }
+      if (!pf.moves.empty()) {
+        eng.prefetch_begin(pf);
+        eng.prefetch_wait();
+        extra += "H " + std::to_string(k) + " " + std::to_string(pf.moves.size()) + "\n";
+      }
+      const ExecResult m = execute(plan, mem, hw, pc, now);  // the model (decisions, virtual clock)
+      eng.execute(plan, pc);                                  // the bytes
       const auto& t = eng.lane_trace();
       for (int l = 0; l < 6; ++l)
         for (const LegTrace& x : t[l])
           lanes[l].push_back({x.block, static_cast<std::uint64_t>(x.src), static_cast<std::uint64_t>(x.dst)});
       std::uint64_t differ = 0;
       for (std::size_t b = 0; b < mem.block_count(); ++b)
-        if (mem.block(b).alive && mem.block(b).loc.tier != model.block(b).loc.tier) ++differ;
+        if (mem.block(b).alive && mem.block(b).loc.tier != eng.mem().block(b).loc.tier) ++differ;
       const SwitchStats& s = eng.last_stats();
       AppId incoming = kNoApp;
       for (const Move& mv : plan.moves)
@@ -765,8 +783,9 @@ int nx_workload_real(const char* spec, const nx_engine_config* cfg, uint64_t see
       ++k;
       return m.completion;
     };
-    workload::Engine we(ws, eng.mem(), runner);
+    workload::Engine we(ws, model_mem, runner);
     const workload::Result r = we.run([&](AppId a, Bytes size, TierId tier) {
+      model_mem.allocate(a, size, tier);
       eng.allocate(a, size, tier);
       eng.fill_pattern(a, seed);
     });

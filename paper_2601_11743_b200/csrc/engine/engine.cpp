@@ -832,6 +832,10 @@ struct SwapEngine::Impl final : detail::LaneSink {
     while (prefetch_pump()) std::this_thread::yield();
   }
 
+  void prefetch_wait() {  // every queued leg, to the end
+    while (prefetch_pump()) std::this_thread::yield();
+  }
+
   ExecResult execute(const MigrationPlan& plan, const PlannerConfig& pcfg, const ExecOptions& o) {
     if (!pf_queue.empty() || !pf_inflight.empty()) prefetch_quiesce();  // plan_switch needs a quiescent registry
     for (const Move& m : plan.moves)
@@ -1098,6 +1102,7 @@ void SwapEngine::set_frame_placer(FramePlacer* placer) { impl_->placer = placer;
 void SwapEngine::prefetch_begin(const MigrationPlan& plan) { impl_->prefetch_begin(plan); }
 bool SwapEngine::prefetch_pump() { return impl_->prefetch_pump(); }
 void SwapEngine::prefetch_quiesce() { impl_->prefetch_quiesce(); }
+void SwapEngine::prefetch_wait() { impl_->prefetch_wait(); }
 bool SwapEngine::prefetch_active() const { return !impl_->pf_queue.empty() || !impl_->pf_inflight.empty(); }
 Bytes SwapEngine::prefetched_bytes() const { return impl_->pf_committed; }
 void SwapEngine::set_progress_hook(std::function<void()> hook) { impl_->progress = std::move(hook); }

@@ -49,7 +49,7 @@ def test_mlfq_workload_real_bytes_follow_reference_decisions(gpu):
     from paper_2601_11743_b200 import run_workload_model, run_workload_real
     model = run_workload_model(C3_SMALL)
     real = run_workload_real(C3_SMALL)
-    core = [ln for ln in real.splitlines() if ln[0] not in "MVF"]
+    core = [ln for ln in real.splitlines() if not (ln[0] in "MVF" or (ln.startswith("H ") and len(ln.split()) == 3))]
     assert core == model.splitlines()
     ms = [ln.split() for ln in real.splitlines() if ln.startswith("M ")]
     vs = [ln.split() for ln in real.splitlines() if ln.startswith("V ")]
@@ -57,3 +57,19 @@ def test_mlfq_workload_real_bytes_follow_reference_decisions(gpu):
     assert len(ms) >= 5 and all(m[2] == "0" for m in ms)
     assert vs and all(v[3] == "0" for v in vs)
     assert len(fs) == 3 and all(f[2] == "0" for f in fs)
+
+
+def test_mlfq_workload_with_prefetch_real_bytes(gpu):
+    """Prefetch on: the model's committed prefetch moves are mirrored by the
+    engine's real prefetch before each switch; placement equals the model's
+    and every restore is byte-exact."""
+    from paper_2601_11743_b200 import run_workload_model, run_workload_real
+    spec = C3_SMALL.replace("horizon 40", "horizon 40\nprefetch on")
+    model = run_workload_model(spec)
+    real = run_workload_real(spec)
+    core = [ln for ln in real.splitlines() if not (ln[0] in "MVF" or (ln.startswith("H ") and len(ln.split()) == 3))]
+    assert core == model.splitlines()
+    assert any(ln.startswith("H ") and len(ln.split()) == 3 for ln in real.splitlines())  # real prefetch happened
+    assert all(ln.split()[2] == "0" for ln in real.splitlines() if ln.startswith("M "))
+    assert all(ln.split()[3] == "0" for ln in real.splitlines() if ln.startswith("V "))
+    assert all(ln.split()[2] == "0" for ln in real.splitlines() if ln.startswith("F "))
