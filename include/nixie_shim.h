@@ -12,7 +12,7 @@
  * (proj/src/mem_model.cpp:48-116); the grant it enforces,
  * MlfqScheduler::on_grant_start / on_grant_end (proj/src/mlfq.cpp:188-194).
  *
- *   allocation   cudaMalloc, cudaFree, cuMemAlloc_v2, cuMemFree_v2
+ *   allocation   cudaMalloc, cudaFree, cudaMallocAsync, cudaFreeAsync, cuMemAlloc_v2, cuMemFree_v2
  *   memory info  cudaMemGetInfo
  *   launch gate  cudaLaunchKernel, cudaLaunchKernelExC, cudaLaunchCooperativeKernel,
  *                cudaGraphLaunch, cuLaunchKernel, cudaMemcpy, cudaMemcpyAsync,

@@ -4,7 +4,7 @@
 //
 // Interposed ("memory allocation and free ... kernel/graph
 // launches ... APIs that implicitly allocate memory ... memory usage"):
-//   cudaMalloc / cudaFree, cuMemAlloc_v2 / cuMemFree_v2
+//   cudaMalloc / cudaFree, cudaMallocAsync / cudaFreeAsync, cuMemAlloc_v2 / cuMemFree_v2
 //       allocations >= min_bytes (2 MiB) become daemon chunks: the shim
 //       are placed in a virtual range the shim reserved once (stable
 //       addresses); every 128 MiB virtual slab of it that holds GPU-resident
@@ -807,6 +807,34 @@ cudaError_t cudaFree(void* devPtr) {
     }
   }
   return real_cudaFree(devPtr);
+}
+
+// Stream-ordered allocation (cudaMallocAsync / cudaFreeAsync, e.g. PyTorch's
+// cudaMallocAsync backend): managed sizes take the cudaMalloc path (memory
+// usable on return is valid stream-ordered semantics); a managed free waits
+// for the stream's queued work first, then frees.
+cudaError_t cudaMallocAsync(void** devPtr, size_t size, cudaStream_t stream) {
+  REAL(cudaMallocAsync);
+  if (t_in_shim || !active() || size < g.min_bytes) return real_cudaMallocAsync(devPtr, size, stream);
+  return managed_alloc(devPtr, size) == 0 ? cudaSuccess : cudaErrorMemoryAllocation;
+}
+
+cudaError_t cudaFreeAsync(void* devPtr, cudaStream_t stream) {
+  REAL(cudaFreeAsync);
+  if (t_in_shim || !devPtr || !active()) return real_cudaFreeAsync(devPtr, stream);
+  bool managed = false;
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    managed = g.regions.count(reinterpret_cast<CUdeviceptr>(devPtr)) != 0;
+  }
+  if (!managed) return real_cudaFreeAsync(devPtr, stream);
+  REAL(cudaStreamSynchronize);
+  t_in_shim++;
+  const cudaError_t e = real_cudaStreamSynchronize(stream);
+  t_in_shim--;
+  if (e != cudaSuccess) return e;
+  managed_free(devPtr);
+  return cudaSuccess;
 }
 
 cudaError_t cudaMemGetInfo(size_t* free_b, size_t* total_b) {

@@ -113,6 +113,21 @@ def test_cuda_graph_apps():
     assert len(sw) >= 3 and all(s["mismatches"] == 0 for s in sw)
 
 
+def test_torch_stream_ordered_allocator():
+    """PyTorch with its cudaMallocAsync backend (cudaMallocAsync /
+    cudaFreeAsync interposed) beside a CUDA program on a 5 GiB budget."""
+    torch_cmd = ["env", "PYTORCH_CUDA_ALLOC_CONF=backend:cudaMallocAsync", sys.executable,
+                 os.path.join(ROOT, "tests", "apps", "torch_app.py"), "2048", "12", "0.3"]
+    with Daemon(gpu="5G", pinned="4G", paged="16G") as d:
+        res = run_apps(d, [torch_cmd, _vec(3072, 16, 300, 71, "a")], timeout=900, stagger_s=2.0)
+        _save("torch_async", d, res)
+        _check(res, d)
+        sw = d.switches()
+        byes = {r["app"]: r for r in d.records() if r.get("event") == "bye"}
+    assert res[0]["out"]["mismatch"] == 0 and res[0]["out"]["matmul_mismatch"] == 0
+    assert len(sw) >= 2 and all(s["mismatches"] == 0 for s in sw)
+
+
 def test_memgetinfo_reports_budget():
     with Daemon(gpu="6G", pinned="2G", paged="8G") as d:
         res = run_apps(d, [_vec(1024, 1, 0, 3, "m")], timeout=300)

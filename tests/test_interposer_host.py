@@ -13,7 +13,7 @@ sys.path.insert(0, ROOT)
 from paper_2601_11743_b200.interpose import NIXIED, SHIM, VECAPP  # noqa: E402
 
 INTERPOSED = {
-    "cudaMalloc", "cudaFree", "cuMemAlloc_v2", "cuMemFree_v2", "cudaMemGetInfo",
+    "cudaMalloc", "cudaFree", "cudaMallocAsync", "cudaFreeAsync", "cuMemAlloc_v2", "cuMemFree_v2", "cudaMemGetInfo",
     "cudaLaunchKernel", "cudaLaunchKernel_ptsz", "cudaLaunchKernelExC", "cudaLaunchKernelExC_ptsz",
     "cudaLaunchCooperativeKernel", "cudaLaunchCooperativeKernel_ptsz", "cudaGraphLaunch", "cudaGraphLaunch_ptsz",
     "cuLaunchKernel", "cudaMemcpy", "cudaMemcpyAsync", "cudaMemcpyAsync_ptsz", "cudaMemcpy2D", "cudaMemcpy2DAsync",
