@@ -16,6 +16,15 @@ def test_three_app_mix_under_mlfq(gpu):
     assert cc["requests"] >= 2 and cc["request_ms"]["p50"] is not None
 
 
+def test_three_app_mix_with_prefetch(gpu):
+    """The gate's ticks prefetch the next candidate's pageable blocks into the
+    pinned tier between switches (small pinned budget); still byte-exact."""
+    r = run_workload(config3_mix(1.0), horizon_s=8.0, pinned_gib=8, prefetch=True)
+    assert r["errors"] == [] and r["byte_exact"]
+    assert r["switches"] >= 3
+    assert r["prefetched_bytes"] > 0
+
+
 def test_small_mix_fast_switches(gpu):
     """Small working sets that do not all fit the 1 GiB GPU: frequent real swaps."""
     apps = [AppSpec(0, "a", 0.5, burst=2, kernel_ms=5, think_s=0.2), AppSpec(1, "b", 0.5, burst=2, kernel_ms=5, think_s=0.2),
