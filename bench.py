@@ -293,7 +293,13 @@ def interposer_c2(timeout_s: float = 240.0) -> dict:
 def run_product(args, dist: Dist):
     from paper_2601_11743_b200 import PlannerConfig, SwapEngine, load_scenario, parse_path
     from paper_2601_11743_b200._lib import TIER_GPU, TIER_PINNED
-    device = dist.local if args.gpus > 1 else 0
+    from paper_2601_11743_b200 import cuda_device_count
+    ndev = max(1, cuda_device_count())
+    # One GPU per rank. With fewer visible GPUs than ranks (a functional check
+    # of the multi-rank path on a 1-GPU box) ranks share devices and the line
+    # says so: its numbers are then not a scaling result.
+    device = (dist.local % ndev) if args.gpus > 1 else 0
+    shared_device = args.gpus > ndev
     peaks = measured_peaks()
     path = parse_path(args.path)
     check_host_memory(dist)
@@ -427,6 +433,7 @@ def run_product(args, dist: Dist):
         "verified_restores": sum(s["verified"] for s in stats),
         "x16_exchange": x16,
         "interposer": ip,
+        "shared_device": shared_device,
     }
     print(json.dumps(line), flush=True)
     return 0
