@@ -18,6 +18,8 @@
  *                cudaGraphLaunch, cuLaunchKernel, cudaMemcpy, cudaMemcpyAsync,
  *                cudaMemcpy2D, cudaMemcpy2DAsync, cudaMemset, cudaMemsetAsync
  *                (and the _ptsz per-thread-stream variants of each runtime call)
+ *                cublasLtMatmul, cublasGemmEx, cublasGemmStridedBatchedEx, cublasSgemm_v2,
+ *                cublasSgemmStridedBatched (cuBLAS launches through a private driver table)
  *   blocking     cudaDeviceSynchronize, cudaStreamSynchronize, cudaEventSynchronize
  *   capture      cudaStreamBeginCapture, cudaStreamEndCapture
  */

@@ -378,10 +378,11 @@ class Daemon {
       const std::vector<ChunkId> chunks = eng_.mem().chunks_of(id);
       for (ChunkId c : chunks) eng_.free_chunk(id, c);
       placer_.take_released();  // its slabs return to the pool; nobody to unmap them
-      std::uint64_t launches = 0, table = 0, waits = 0, wait_ns = 0, drain_ns = 0, map_ns = 0;
+      std::uint64_t launches = 0, table = 0, blas = 0, waits = 0, wait_ns = 0, drain_ns = 0, map_ns = 0;
       if (a.ctl) {
         launches = a.ctl->launches.load();
         table = a.ctl->table_launches.load();
+        blas = a.ctl->blas_calls.load();
         waits = a.ctl->gate_waits.load();
         wait_ns = a.ctl->gate_wait_ns.load();
         drain_ns = a.ctl->drain_ns.load();
@@ -390,9 +391,9 @@ class Daemon {
       close_app(a);
       ++gone_;
       note("{\"t\": %.6f, \"event\": \"bye\", \"app\": %u, \"chunks_freed\": %zu, \"gated_calls\": %" PRIu64
-           ", \"table_launches\": %" PRIu64 ", \"gate_waits\": %" PRIu64 ", \"gate_wait_ms\": %.3f, \"drain_ms\": %.3f"
+           ", \"table_launches\": %" PRIu64 ", \"blas_calls\": %" PRIu64 ", \"gate_waits\": %" PRIu64 ", \"gate_wait_ms\": %.3f, \"drain_ms\": %.3f"
            ", \"map_ms\": %.3f}",
-           now(), id, chunks.size(), launches, table, waits, wait_ns * 1e-6, drain_ns * 1e-6, map_ns * 1e-6);
+           now(), id, chunks.size(), launches, table, blas, waits, wait_ns * 1e-6, drain_ns * 1e-6, map_ns * 1e-6);
     }
   }
 

@@ -19,6 +19,10 @@
 //       the launch gate (PAPER.md:116 steps 1-2 and 6): pass while the
 //       execution flag is set; otherwise ask the daemon (Acquire) and hold
 //       the calling thread until a Grant has mapped the app's slabs.
+//   cublasLtMatmul, cublasGemmEx, cublasGemmStridedBatchedEx, cublasSgemm_v2,
+//   cublasSgemmStridedBatched
+//       gated too: cuBLAS launches through its static runtime's private driver
+//       table, which no public hook sees.
 //   cudaDeviceSynchronize, cudaStreamSynchronize, cudaEventSynchronize,
 //   cudaMemcpy (sync)
 //       blocking-call brackets for the MLFQ's idleness test (§6.1).
@@ -33,6 +37,8 @@
 // The shim never copies application data: the daemon's swap engine moves
 // every byte (both PCIe directions at once) through its own mapping of the
 // same physical slabs; the shim only maps, unmaps and gates.
+#include <cublasLt.h>
+#include <cublas_api.h>
 #include <cuda.h>
 #include <cuda_runtime_api.h>
 #include <dlfcn.h>
@@ -87,6 +93,10 @@ void* cudart_handle() {
 void* real_sym(const char* name) {
   void* p = dlsym(RTLD_NEXT, name);
   if (!p && cudart_handle()) p = dlsym(cudart_handle(), name);
+  for (const char* lib : {"libcublasLt.so.12", "libcublas.so.12"}) {  // loaded RTLD_LOCAL by the app
+    if (p) break;
+    if (void* h = dlopen(lib, RTLD_NOW | RTLD_NOLOAD)) p = dlsym(h, name);
+  }
   if (!p) {
     static void* cuda = dlopen("libcuda.so.1", RTLD_NOW);
     if (cuda) p = dlsym(cuda, name);
@@ -869,6 +879,43 @@ GATED(cudaError_t, cudaMemsetAsync, (void* d, int v, size_t n, cudaStream_t st),
 GATED(cudaError_t, cudaMemsetAsync_ptsz, (void* d, int v, size_t n, cudaStream_t st), (d, v, n, st))
 GATED(cudaError_t, cudaMemset, (void* d, int v, size_t n), (d, v, n))
 GATED(cudaError_t, cudaMemcpy2D, (void* d, size_t dp, const void* s, size_t sp, size_t w, size_t h, cudaMemcpyKind k), (d, dp, s, sp, w, h, k))
+
+// Like GATED, for names the C++ headers overload (the real symbol is the C one).
+#define GATED_C(ret, name, params, args)                                               \
+  ret name params {                                                                    \
+    static auto real_##name = reinterpret_cast<ret(*) params>(real_sym(#name));       \
+    Gate gate_;                                                                        \
+    if (gate_.held) g.ctl->blas_calls.fetch_add(1, std::memory_order_relaxed);        \
+    return real_##name args;                                                           \
+  }
+
+// cuBLAS / cuBLASLt GEMM entry points. cuBLAS links a static CUDA runtime
+// and launches through its private driver table, which no public hook sees;
+// gating its API calls holds the app's GEMMs at the gate like its own kernels
+// (their internal launches happen inside the call, on the held slot).
+GATED_C(cublasStatus_t, cublasLtMatmul,
+      (cublasLtHandle_t h, cublasLtMatmulDesc_t cd, const void* al, const void* A, cublasLtMatrixLayout_t Ad, const void* B,
+       cublasLtMatrixLayout_t Bd, const void* be, const void* C, cublasLtMatrixLayout_t Cd, void* D, cublasLtMatrixLayout_t Dd,
+       const cublasLtMatmulAlgo_t* algo, void* ws, size_t wss, cudaStream_t st),
+      (h, cd, al, A, Ad, B, Bd, be, C, Cd, D, Dd, algo, ws, wss, st))
+GATED_C(cublasStatus_t, cublasGemmEx,
+      (cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, const void* al, const void* A,
+       cudaDataType At, int lda, const void* B, cudaDataType Bt, int ldb, const void* be, void* C, cudaDataType Ct, int ldc,
+       cublasComputeType_t ct, cublasGemmAlgo_t algo),
+      (h, ta, tb, m, n, k, al, A, At, lda, B, Bt, ldb, be, C, Ct, ldc, ct, algo))
+GATED_C(cublasStatus_t, cublasGemmStridedBatchedEx,
+      (cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, const void* al, const void* A,
+       cudaDataType At, int lda, long long sa, const void* B, cudaDataType Bt, int ldb, long long sb, const void* be, void* C,
+       cudaDataType Ct, int ldc, long long sc, int bc, cublasComputeType_t ct, cublasGemmAlgo_t algo),
+      (h, ta, tb, m, n, k, al, A, At, lda, sa, B, Bt, ldb, sb, be, C, Ct, ldc, sc, bc, ct, algo))
+GATED_C(cublasStatus_t, cublasSgemm_v2,
+      (cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, const float* al, const float* A,
+       int lda, const float* B, int ldb, const float* be, float* C, int ldc),
+      (h, ta, tb, m, n, k, al, A, lda, B, ldb, be, C, ldc))
+GATED_C(cublasStatus_t, cublasSgemmStridedBatched,
+      (cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, const float* al, const float* A,
+       int lda, long long sa, const float* B, int ldb, long long sb, const float* be, float* C, int ldc, long long sc, int bc),
+      (h, ta, tb, m, n, k, al, A, lda, sa, B, ldb, sb, be, C, ldc, sc, bc))
 
 cudaError_t cudaMemcpy(void* d, const void* s, size_t n, cudaMemcpyKind k) {
   REAL(cudaMemcpy);

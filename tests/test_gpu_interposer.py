@@ -148,6 +148,9 @@ def test_three_apps_with_torch():
         sw = d.switches()
     assert res[1]["out"]["mismatch"] == 0 and res[1]["out"]["matmul_mismatch"] == 0
     assert res[1]["out"]["memgetinfo"][1] == 5 << 30
+    byes = {r["app"]: r for r in d.records() if r.get("event") == "bye"}
+    py = [r["app"] for r in d.records() if r.get("event") == "hello" and r["name"].startswith("python")][0]
+    assert byes[py]["blas_calls"] > 0  # the matmuls were held at the gate
     assert len(sw) >= 3 and all(s["mismatches"] == 0 for s in sw)
 
 

@@ -20,6 +20,7 @@ INTERPOSED = {
     "cudaMemset", "cudaMemsetAsync", "cudaMemsetAsync_ptsz",
     "cudaDeviceSynchronize", "cudaStreamSynchronize", "cudaEventSynchronize",
     "cudaStreamBeginCapture", "cudaStreamEndCapture",
+    "cublasLtMatmul", "cublasGemmEx", "cublasGemmStridedBatchedEx", "cublasSgemm_v2", "cublasSgemmStridedBatched",
 }
 
 
