@@ -19,7 +19,8 @@
  *                cudaMemcpy2D, cudaMemcpy2DAsync, cudaMemset, cudaMemsetAsync
  *                (and the _ptsz per-thread-stream variants of each runtime call)
  *                cublasLtMatmul, cublasGemmEx, cublasGemmStridedBatchedEx, cublasSgemm_v2,
- *                cublasSgemmStridedBatched (cuBLAS launches through a private driver table)
+ *                cublasSgemmStridedBatched, cudnnBackendExecute (cuBLAS and cuDNN launch
+ *                through their static runtimes' private driver tables)
  *   blocking     cudaDeviceSynchronize, cudaStreamSynchronize, cudaEventSynchronize
  *   capture      cudaStreamBeginCapture, cudaStreamEndCapture
  */

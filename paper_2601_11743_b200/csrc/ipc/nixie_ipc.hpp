@@ -157,7 +157,7 @@ struct alignas(64) CtlPage {
   std::atomic<std::uint64_t> map_ns;          // total mapping time
   std::atomic<std::uint64_t> unmap_ns;        // total unmapping time
   std::atomic<std::uint64_t> drain_ns;        // total pause-drain time
-  std::atomic<std::uint64_t> blas_calls;      // gated cuBLAS / cuBLASLt GEMM calls
+  std::atomic<std::uint64_t> blas_calls;      // gated library calls (cuBLAS / cuBLASLt GEMMs, cuDNN executes)
   std::atomic<std::uint64_t> table_launches;  // gated calls that came through cuGetProcAddress entry
                                               // points directly (not via an interposed runtime call)
 };

@@ -20,9 +20,9 @@
 //       execution flag is set; otherwise ask the daemon (Acquire) and hold
 //       the calling thread until a Grant has mapped the app's slabs.
 //   cublasLtMatmul, cublasGemmEx, cublasGemmStridedBatchedEx, cublasSgemm_v2,
-//   cublasSgemmStridedBatched
-//       gated too: cuBLAS launches through its static runtime's private driver
-//       table, which no public hook sees.
+//   cublasSgemmStridedBatched, cudnnBackendExecute
+//       gated too: cuBLAS and cuDNN launch through their static runtimes'
+//       private driver tables, which no public hook sees.
 //   cudaDeviceSynchronize, cudaStreamSynchronize, cudaEventSynchronize,
 //   cudaMemcpy (sync)
 //       blocking-call brackets for the MLFQ's idleness test (§6.1).
@@ -93,7 +93,7 @@ void* cudart_handle() {
 void* real_sym(const char* name) {
   void* p = dlsym(RTLD_NEXT, name);
   if (!p && cudart_handle()) p = dlsym(cudart_handle(), name);
-  for (const char* lib : {"libcublasLt.so.12", "libcublas.so.12"}) {  // loaded RTLD_LOCAL by the app
+  for (const char* lib : {"libcublasLt.so.12", "libcublas.so.12", "libcudnn.so.9"}) {  // loaded RTLD_LOCAL by the app
     if (p) break;
     if (void* h = dlopen(lib, RTLD_NOW | RTLD_NOLOAD)) p = dlsym(h, name);
   }
@@ -916,6 +916,11 @@ GATED_C(cublasStatus_t, cublasSgemmStridedBatched,
       (cublasHandle_t h, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, const float* al, const float* A,
        int lda, long long sa, const float* B, int ldb, long long sb, const float* be, float* C, int ldc, long long sc, int bc),
       (h, ta, tb, m, n, k, al, A, lda, sa, B, ldb, sb, be, C, ldc, sc, bc))
+
+// cuDNN 9 executes every backend (graph API) plan through one entry point;
+// PyTorch's convolutions go through it. Handles are opaque pointers and the
+// status an enum, so no cuDNN header is needed.
+GATED_C(int, cudnnBackendExecute, (void* handle, void* plan, void* variant_pack), (handle, plan, variant_pack))
 
 cudaError_t cudaMemcpy(void* d, const void* s, size_t n, cudaMemcpyKind k) {
   REAL(cudaMemcpy);

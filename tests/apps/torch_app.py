@@ -23,6 +23,10 @@ def main():
     a = torch.randn(2048, 2048, device="cuda", generator=g)
     b = torch.randn(2048, 2048, device="cuda", generator=g)
     ref = (a @ b).double().sum().item()
+    # cuDNN work (convolution through cudnnBackendExecute)
+    img = torch.randn(8, 16, 64, 64, device="cuda", generator=g)
+    wgt = torch.randn(32, 16, 3, 3, device="cuda", generator=g)
+    conv_ref = torch.nn.functional.conv2d(img, wgt, padding=1).double().sum().item()
     mm_bad = 0
     lat = []
     for it in range(iters):
@@ -30,8 +34,10 @@ def main():
         for x in xs:
             x.add_(1)
         c = a @ b
+        y = torch.nn.functional.conv2d(img, wgt, padding=1)
         torch.cuda.synchronize()
         mm_bad += int(abs(c.double().sum().item() - ref) > 1e-6 * max(1.0, abs(ref)))
+        mm_bad += int(abs(y.double().sum().item() - conv_ref) > 1e-6 * max(1.0, abs(conv_ref)))
         lat.append((time.perf_counter() - t0) * 1e3)
         time.sleep(think)
     bad = 0

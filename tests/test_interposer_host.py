@@ -21,6 +21,7 @@ INTERPOSED = {
     "cudaDeviceSynchronize", "cudaStreamSynchronize", "cudaEventSynchronize",
     "cudaStreamBeginCapture", "cudaStreamEndCapture",
     "cublasLtMatmul", "cublasGemmEx", "cublasGemmStridedBatchedEx", "cublasSgemm_v2", "cublasSgemmStridedBatched",
+    "cudnnBackendExecute",
 }
 
 
