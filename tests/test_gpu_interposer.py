@@ -128,6 +128,22 @@ def test_torch_stream_ordered_allocator():
     assert len(sw) >= 2 and all(s["mismatches"] == 0 for s in sw)
 
 
+def test_two_llm_inference_apps():
+    """Two unmodified PyTorch LLM-inference programs (Llama architecture,
+    ~0.8B parameters, bf16) that do not fit the budget together: every
+    request's logits equal the first request's bit for bit."""
+    llm = os.path.join(ROOT, "tests", "apps", "llm_app.py")
+    with Daemon(gpu="3G", pinned="4G", paged="16G") as d:
+        res = run_apps(d, [[sys.executable, llm, "8", "0.3", "1"], [sys.executable, llm, "8", "0.3", "2"]], timeout=900)
+        _save("llm", d, res)
+        _check(res, d)
+        sw = d.switches()
+    for r in res:
+        assert r["out"]["logit_mismatch"] == 0
+    assert len(sw) >= 3 and all(s["mismatches"] == 0 for s in sw)
+    assert sum(s["pcie_h2d"] for s in sw) > (1 << 30)
+
+
 def test_memgetinfo_reports_budget():
     with Daemon(gpu="6G", pinned="2G", paged="8G") as d:
         res = run_apps(d, [_vec(1024, 1, 0, 3, "m")], timeout=300)
