@@ -59,6 +59,7 @@ struct EngineConfig {
   bool exportable_arena = false;      // GPU tier = exportable VMM slabs shims can import (interposer daemon)
   Bytes arena_slab_bytes = 128 * kMiB; // exportable arena: bytes per physical allocation (a multiple of 2 MiB)
   Bytes gpu_physical = 0;             // arena bytes (0 = gpu_capacity); the registry still enforces gpu_capacity
+  Bytes gpu_physical_max = 0;         // exportable arena: virtual space reserved for growth (0 = gpu_physical)
 };
 
 // Physical placement of blocks arriving on the GPU tier. Default (no placer):
@@ -199,6 +200,8 @@ class SwapEngine {
   std::int64_t frame_index(BlockId block) const;
   int arena_export_fd(std::uint32_t slab) const;
   std::uint32_t arena_frames() const;  // physical 2 MiB frames in the arena
+  // Exportable arena: one more physical slab (up to gpu_physical_max); returns its index.
+  std::uint32_t arena_grow_slab();
   // Not owned; nullptr restores the default. Install before any GPU allocation.
   void set_frame_placer(FramePlacer* placer);
   // Called on the thread running execute() whenever legs have committed (the

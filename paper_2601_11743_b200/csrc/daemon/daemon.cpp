@@ -146,6 +146,7 @@ bool parse_args(int argc, char** argv, Options& o) {
   if (o.phys_slack_slabs < 0) o.phys_slack_slabs = static_cast<int>(std::max<Bytes>(4, 2 * kGiB / slab));  // 2 GiB
   o.eng.arena_slab_bytes = slab;
   o.eng.gpu_physical = (o.eng.gpu_capacity + slab - 1) / slab * slab + static_cast<Bytes>(std::max(o.phys_slack_slabs, 0)) * slab;
+  o.eng.gpu_physical_max = 2 * o.eng.gpu_physical;  // room to grow when partly resident slabs use up the slack
   return true;
 }
 
@@ -154,6 +155,7 @@ class Daemon {
   explicit Daemon(const Options& o)
       : opt_(o), eng_(o.eng), sched_(o.mlfq), placer_(eng_.arena_frames() / o.slab_blocks, o.slab_blocks) {
     eng_.set_frame_placer(&placer_);
+    placer_.set_grow([this] { return grow_arena(); });
     eng_.set_progress_hook([this] { send_maps(); });
     sched_.set_logging(true);
     t0_ = ipc::mono_ns();
@@ -236,6 +238,7 @@ class Daemon {
     std::uint64_t seen_launches = 0;
     bool seen_blocking = false;
     std::uint64_t active_launch_mark = 0;
+    std::uint32_t slabs_rpc = 0, slabs_ev = 0;  // slab descriptors sent on each socket
   };
 
   Seconds now() const { return static_cast<double>(ipc::mono_ns() - t0_) * 1e-9; }
@@ -311,7 +314,7 @@ class Daemon {
     rep.block_bytes = kBlockBytes;
     rep.min_bytes = opt_.min_bytes;
     rep.device = opt_.eng.device;
-    const std::uint32_t slabs = eng_.arena_frames() / opt_.slab_blocks;
+    const std::uint32_t slabs = static_cast<std::uint32_t>(placer_.slabs());
     rep.slabs = slabs;
     rep.slab_bytes = static_cast<std::uint64_t>(opt_.slab_blocks) * kBlockBytes;
     rep.arena_bytes = rep.slabs * rep.slab_bytes;
@@ -324,6 +327,7 @@ class Daemon {
       ok = ipc::send_fds(fd, batch.data(), static_cast<int>(n));
       for (int x : batch) ::close(x);
     }
+    a.slabs_rpc = a.slabs_ev = slabs;  // imported at start-up, before the listener runs
     apps_[a.id] = a;
     if (!ok) apps_[a.id].alive = false;
     note("{\"t\": %.6f, \"event\": \"hello\", \"app\": %u, \"pid\": %d, \"name\": \"%s\"}", now(), a.id, a.pid, a.name.c_str());
@@ -490,6 +494,7 @@ class Daemon {
     rep.n_chunks = static_cast<std::uint32_t>(ids.size());
     rep.n_slabs = static_cast<std::uint32_t>(slabs.size());
     rep.footprint = fp;
+    send_new_slabs(a, true);
     rep.epoch = ++epoch_;
     ipc::Writer w;
     w.put(rep);
@@ -585,10 +590,34 @@ class Daemon {
     for (auto& [app, ms] : per_app) {
       auto it = apps_.find(app);
       if (it == apps_.end() || !it->second.alive || it->second.ev < 0) continue;
+      send_new_slabs(it->second, false);
       ipc::Writer w;
       w.put(ipc::SlabsMsg{++epoch_, static_cast<std::uint32_t>(ms.size()), 0});
       for (const auto& m : ms) w.put(m);
       if (!ipc::send_msg(it->second.ev, ipc::Msg::Map, w.buf)) it->second.alive = false;
+    }
+  }
+
+  // A new physical slab when partly resident slabs used up the slack. Shims
+  // learn about it lazily: before any message on a socket that may name it
+  // (send_new_slabs), so each socket delivers the descriptor first.
+  std::uint32_t grow_arena() {
+    const std::uint32_t s = eng_.arena_grow_slab();
+    note("{\"t\": %.6f, \"event\": \"slab_grow\", \"slab\": %u, \"partial_slabs\": %" PRIu64 "}", now(), s, placer_.partial());
+    return s;
+  }
+
+  // Sends the app every slab it has not received on this socket yet
+  // (Slab message + descriptor each).
+  void send_new_slabs(App& a, bool on_rpc) {
+    std::uint32_t& known = on_rpc ? a.slabs_rpc : a.slabs_ev;
+    const int sock = on_rpc ? a.rpc : a.ev;
+    for (; known < placer_.slabs() && a.alive && sock >= 0; ++known) {
+      const int fd = eng_.arena_export_fd(known);
+      ipc::SlabFdMsg m{known, 0};
+      const bool ok = ipc::send_msg(sock, ipc::Msg::Slab, &m, sizeof(m)) && ipc::send_fds(sock, &fd, 1);
+      ::close(fd);
+      if (!ok) a.alive = false;
     }
   }
 
@@ -674,6 +703,7 @@ class Daemon {
     if (!eng_.mem().app_fully_resident(to, TierId::Gpu))
       throw InvariantViolation("grant: app " + std::to_string(to) + " is not GPU-resident after its switch");
     ipc::GrantedMsg gm{};
+    send_new_slabs(in, false);
     const std::uint64_t t_grant_sent = ipc::mono_ns();
     if (ipc::send_msg(in.ev, ipc::Msg::Grant, w.buf) && wait_ack(in, ipc::Msg::Granted, body) && body.size() >= sizeof(gm))
       std::memcpy(&gm, body.data(), sizeof(gm));

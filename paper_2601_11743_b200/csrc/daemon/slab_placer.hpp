@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <deque>
+#include <functional>
 #include <map>
 #include <string>
 #include <utility>
@@ -45,9 +46,19 @@ class SlabPlacer final : public FramePlacer {
     if (b >= app_.size()) throw InvariantViolation("slab placer: block " + std::to_string(b) + " has no virtual placement");
     Slab& s = slabs_[key(b)];
     if (s.phys == ipc::kNoFrame) {
-      if (nfree_ == 0)
-        throw InvariantViolation("slab placer: every physical slab is in use (raise --phys-slack; partly resident slabs: " +
-                                 std::to_string(partial()) + ")");
+      if (nfree_ == 0) {
+        // Partly resident slabs (eviction boundaries, allocations sharing a
+        // slab) can use up the slack: the arena grows by one slab.
+        if (!grow_)
+          throw InvariantViolation("slab placer: every physical slab is in use (partly resident slabs: " +
+                                   std::to_string(partial()) + ")");
+        const std::uint32_t p = grow_();
+        if (is_free_.size() <= p) is_free_.resize(p + 1, 0);
+        is_free_[p] = 1;
+        free_.push_back(p);
+        ++nfree_;
+        ++grown_;
+      }
       // Affinity: the slab this vslab had last time, if it is free, is still
       // mapped in the app (stale mappings are kept), so no remap is needed.
       if (s.pref != ipc::kNoFrame && is_free_[s.pref]) {
@@ -103,6 +114,10 @@ class SlabPlacer final : public FramePlacer {
     return n;
   }
   std::size_t free_slabs() const { return nfree_; }
+  std::size_t slabs() const { return is_free_.size(); }
+  std::uint32_t grown() const { return grown_; }
+  // Called when no slab is free; returns the index of a new one.
+  void set_grow(std::function<std::uint32_t()> g) { grow_ = std::move(g); }
 
   // What the app's shim has mapped at a vslab (as far as the daemon told it).
   std::uint32_t mapped(const Key& k) const {
@@ -133,6 +148,8 @@ class SlabPlacer final : public FramePlacer {
   std::deque<std::uint32_t> free_;  // FIFO with lazily deleted entries (is_free_)
   std::vector<char> is_free_;
   std::size_t nfree_ = 0;
+  std::function<std::uint32_t()> grow_;
+  std::uint32_t grown_ = 0;
   std::vector<Key> released_;
   std::vector<Key> assigned_;
 };

@@ -249,7 +249,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
     hw.tier_capacity[3] = 0;
     hw.apply_to(mem);
 
-    arena.init(cfg.gpu_physical ? cfg.gpu_physical : cfg.gpu_capacity, cfg.exportable_arena, cfg.device, cfg.arena_slab_bytes);
+    arena.init(cfg.gpu_physical ? cfg.gpu_physical : cfg.gpu_capacity, cfg.exportable_arena, cfg.device, cfg.arena_slab_bytes,
+               cfg.gpu_physical_max);
     pinned.init(cfg.pinned_capacity, numa.node);
     paged.init(cfg.paged_capacity);
     pool.start(cfg.host_threads, numa.cpus);
@@ -1098,6 +1099,7 @@ std::int64_t SwapEngine::frame_index(BlockId b) const {
 }
 
 std::uint32_t SwapEngine::arena_frames() const { return impl_->arena.ring.units(); }
+std::uint32_t SwapEngine::arena_grow_slab() { return impl_->arena.grow_slab(); }
 void SwapEngine::set_frame_placer(FramePlacer* placer) { impl_->placer = placer; }
 void SwapEngine::prefetch_begin(const MigrationPlan& plan) { impl_->prefetch_begin(plan); }
 bool SwapEngine::prefetch_pump() { return impl_->prefetch_pump(); }

@@ -99,12 +99,12 @@ void pin_thread_to(const std::vector<int>& cpus) {
   pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
 }
 
-void DeviceArena::init(Bytes capacity, bool exportable, int device, Bytes slab_bytes) {
+void DeviceArena::init(Bytes capacity, bool exportable, int device, Bytes slab_bytes, Bytes reserve) {
   const auto units = static_cast<std::uint32_t>(capacity / kBlockBytes);
   if (units > 0) {
     if (exportable) {
       vmm_ = new ExportableArena();
-      vmm_->init(device, static_cast<Bytes>(units) * kBlockBytes, slab_bytes ? slab_bytes : kBlockBytes);
+      vmm_->init(device, static_cast<Bytes>(units) * kBlockBytes, slab_bytes ? slab_bytes : kBlockBytes, reserve);
       base_ = vmm_->base();
     } else {
       NX_CUDA(cudaMalloc(&base_, static_cast<std::size_t>(units) * kBlockBytes));
@@ -122,6 +122,14 @@ DeviceArena::~DeviceArena() {
 }
 
 int DeviceArena::export_fd(std::uint32_t slab) const { return vmm_ ? vmm_->export_fd(slab) : -1; }
+
+std::uint32_t DeviceArena::grow_slab() {
+  if (!vmm_) throw SimError(Err::InvalidState, "only an exportable arena grows");
+  const std::uint32_t s = vmm_->grow();
+  const auto per = static_cast<std::uint32_t>(vmm_->slab_bytes() / kBlockBytes);
+  ring.reset(static_cast<std::uint32_t>(ring.units() + per));  // the frame count (the placer owns the frames)
+  return s;
+}
 
 void PinnedRing::init(Bytes capacity, int numa_node) {
   const auto units = static_cast<std::uint32_t>(capacity / kBlockBytes);

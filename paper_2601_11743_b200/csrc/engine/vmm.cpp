@@ -47,14 +47,22 @@ const VmmApi& vmm_api() {
   return api;
 }
 
-void ExportableArena::init(int device, Bytes bytes, Bytes slab_bytes) {
-  const VmmApi& v = vmm_api();
-  NX_CUDA(cudaFree(nullptr));  // the primary context is current on this thread
+namespace {
+CUmemAllocationProp slab_prop(int device) {
   CUmemAllocationProp prop{};
   prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   prop.location.id = device;
   prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  return prop;
+}
+}  // namespace
+
+void ExportableArena::init(int device, Bytes bytes, Bytes slab_bytes, Bytes reserve_bytes) {
+  const VmmApi& v = vmm_api();
+  NX_CUDA(cudaFree(nullptr));  // the primary context is current on this thread
+  device_ = device;
+  const CUmemAllocationProp prop = slab_prop(device);
   size_t gran = 0;
   check(v.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM), "cuMemGetAllocationGranularity");
   if (gran == 0 || kBlockBytes % gran != 0)
@@ -62,20 +70,35 @@ void ExportableArena::init(int device, Bytes bytes, Bytes slab_bytes) {
   if (slab_bytes == 0 || slab_bytes % kBlockBytes || bytes % slab_bytes)
     throw SimError(Err::ValidationError, "exportable arena: bytes must be a multiple of the slab, the slab of 2 MiB");
   slab_ = slab_bytes;
-  bytes_ = bytes;
-  const auto n = static_cast<std::uint32_t>(bytes_ / slab_);
-  check(v.addr_reserve(&va_, bytes_, slab_, 0, 0), "cuMemAddressReserve(arena)");
-  handles_.resize(n, 0);
-  for (std::uint32_t f = 0; f < n; ++f) {
-    check(v.mem_create(&handles_[f], slab_, &prop, 0), "cuMemCreate(exportable slab)");
-    check(v.map(va_ + static_cast<CUdeviceptr>(f) * slab_, slab_, 0, handles_[f], 0), "cuMemMap(slab)");
-    mapped_ = f + 1;
-  }
+  reserved_ = std::max(bytes, reserve_bytes) / slab_ * slab_;
+  check(v.addr_reserve(&va_, reserved_, slab_, 0, 0), "cuMemAddressReserve(arena)");
+  const auto n = static_cast<std::uint32_t>(bytes / slab_);
+  for (std::uint32_t f = 0; f < n; ++f) add_slab();
+}
+
+void ExportableArena::add_slab() {
+  const VmmApi& v = vmm_api();
+  const CUmemAllocationProp prop = slab_prop(device_);
+  const std::uint32_t f = mapped_;
+  CUmemGenericAllocationHandle h = 0;
+  check(v.mem_create(&h, slab_, &prop, 0), "cuMemCreate(exportable slab)");
+  handles_.push_back(h);
+  const CUdeviceptr at = va_ + static_cast<CUdeviceptr>(f) * slab_;
+  check(v.map(at, slab_, 0, h, 0), "cuMemMap(slab)");
+  mapped_ = f + 1;
   CUmemAccessDesc acc{};
   acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-  acc.location.id = device;
+  acc.location.id = device_;
   acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  check(v.set_access(va_, bytes_, &acc, 1), "cuMemSetAccess(arena)");
+  check(v.set_access(at, slab_, &acc, 1), "cuMemSetAccess(slab)");
+  bytes_ = static_cast<Bytes>(mapped_) * slab_;
+}
+
+std::uint32_t ExportableArena::grow() {
+  if (static_cast<Bytes>(mapped_ + 1) * slab_ > reserved_)
+    throw InvariantViolation("exportable arena: the reserved range is full (" + std::to_string(mapped_) + " slabs)");
+  add_slab();
+  return mapped_ - 1;
 }
 
 ExportableArena::~ExportableArena() {
@@ -84,7 +107,7 @@ ExportableArena::~ExportableArena() {
   for (std::uint32_t f = 0; f < mapped_; ++f) v.unmap(va_ + static_cast<CUdeviceptr>(f) * slab_, slab_);
   for (CUmemGenericAllocationHandle h : handles_)
     if (h) v.mem_release(h);
-  v.addr_free(va_, bytes_);
+  v.addr_free(va_, reserved_);
 }
 
 int ExportableArena::export_fd(std::uint32_t f) const {

@@ -50,8 +50,13 @@ const VmmApi& vmm_api();
 // profiles/r01_vmm_probe.txt), so slabs are large (128 MiB = 64 frames).
 class ExportableArena {
  public:
-  void init(int device, Bytes bytes, Bytes slab_bytes);
+  // `reserve_bytes` (>= bytes) of virtual space is reserved up front so
+  // grow() can append slabs at contiguous addresses later.
+  void init(int device, Bytes bytes, Bytes slab_bytes, Bytes reserve_bytes = 0);
   ~ExportableArena();
+  // Creates, maps and opens one more slab after the last; returns its index.
+  // Throws when the reserved range is full.
+  std::uint32_t grow();
   std::uint8_t* base() const { return reinterpret_cast<std::uint8_t*>(va_); }
   Bytes bytes() const { return bytes_; }
   std::uint32_t slabs() const { return static_cast<std::uint32_t>(handles_.size()); }
@@ -64,8 +69,11 @@ class ExportableArena {
   std::vector<CUmemGenericAllocationHandle> handles_;
   CUdeviceptr va_ = 0;
   Bytes bytes_ = 0;
+  Bytes reserved_ = 0;
   Bytes slab_ = 0;
+  int device_ = 0;
   std::uint32_t mapped_ = 0;
+  void add_slab();
 };
 
 }  // namespace nixie::b200

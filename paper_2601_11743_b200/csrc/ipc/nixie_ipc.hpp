@@ -54,6 +54,12 @@ enum class Msg : std::uint32_t {
   Granted,       // event shim->d: GrantedMsg
   Stats,         // rpc  shim->d : (empty)    reply StatsRep
   Map,           // event d->shim: SlabsMsg + SlabMap[n] (slabs placed while the switch runs; no ack)
+  Slab,          // event d->shim: SlabFdMsg, then 1 fd: the arena grew by one slab (import it; no ack)
+};
+
+struct SlabFdMsg {
+  std::uint32_t slab;
+  std::uint32_t pad;
 };
 
 // Virtual slabs: a shim reserves one large virtual range and places its

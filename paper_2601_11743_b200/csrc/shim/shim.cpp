@@ -447,6 +447,30 @@ void on_grant(const std::vector<std::uint8_t>& body) {
   ipc::send_msg(g.ev, ipc::Msg::Granted, &ack, sizeof(ack));
 }
 
+// The daemon's arena grew: import the new slab (its fd follows the message).
+// Arrives on whichever socket the daemon is about to name the slab on.
+void on_slab(int sock, const std::vector<std::uint8_t>& body) {
+  ipc::SlabFdMsg m{};
+  std::memcpy(&m, body.data(), std::min(body.size(), sizeof(m)));
+  int fd = -1;
+  if (!ipc::recv_fds(sock, &fd, 1)) die("receiving a new slab's descriptor");
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    if (m.slab < g.slabs.size() && g.slabs[m.slab] != 0) {  // already imported through the other socket
+      ::close(fd);
+      return;
+    }
+  }
+  CUmemGenericAllocationHandle h = 0;
+  ensure_ctx();
+  const CUresult r = drv().import_handle(&h, reinterpret_cast<void*>(static_cast<std::uintptr_t>(fd)), CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+  ::close(fd);
+  if (r != CUDA_SUCCESS) die("cuMemImportFromShareableHandle(new slab)", r);
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.slabs.size() <= m.slab) g.slabs.resize(m.slab + 1, 0);
+  if (g.slabs[m.slab] == 0) g.slabs[m.slab] = h;
+}
+
 void listener() {
   t_listener = true;
   t_in_shim++;
@@ -463,6 +487,7 @@ void listener() {
       case ipc::Msg::Unmap: on_unmap(body); break;
       case ipc::Msg::Grant: on_grant(body); break;
       case ipc::Msg::Map: on_map(body); break;
+      case ipc::Msg::Slab: on_slab(g.ev, body); break;
       default:
         std::fprintf(stderr, "[nixie-shim] unexpected event %u\n", static_cast<unsigned>(type));
     }
@@ -476,7 +501,14 @@ void listener() {
 // ---- rpc ----------------------------------------------------------------------------
 bool rpc(ipc::Msg type, const void* p, std::size_t n, ipc::Msg& rtype, std::vector<std::uint8_t>& body) {
   std::lock_guard<std::mutex> lk(g.rpc_mu);
-  return ipc::send_msg(g.rpc, type, p, n) && ipc::recv_msg(g.rpc, rtype, body);
+  if (!ipc::send_msg(g.rpc, type, p, n)) return false;
+  for (;;) {  // new slabs the reply may name come first
+    if (!ipc::recv_msg(g.rpc, rtype, body)) return false;
+    if (rtype != ipc::Msg::Slab) return true;
+    t_in_shim++;
+    on_slab(g.rpc, body);
+    t_in_shim--;
+  }
 }
 
 // ---- the gate -------------------------------------------------------------------------

@@ -76,6 +76,18 @@ static void slab_placer() {
   CHECK(p.backed(9).size() == 1);
 }
 
+static void slab_growth() {
+  SlabPlacer p(1, 2);
+  std::uint32_t next = 1;
+  p.set_grow([&] { return next++; });
+  p.expect(0, 6, 3, 0);  // 3 vslabs of 2 blocks
+  const std::uint32_t a = p.acquire(0), b = p.acquire(2), c = p.acquire(4);
+  CHECK(a / 2 == 0 && b / 2 == 1 && c / 2 == 2);  // slabs 1 and 2 were created on demand
+  CHECK(p.grown() == 2 && p.slabs() == 3 && p.free_slabs() == 0);
+  p.release(2, b);
+  CHECK(p.free_slabs() == 1);
+}
+
 static void range_alloc() {
   nixie::shim::RangeAlloc r;
   r.reset(1024);
@@ -94,6 +106,7 @@ static void range_alloc() {
 
 int main() {
   slab_placer();
+  slab_growth();
   range_alloc();
   std::printf("nx_unit_tests: %d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;

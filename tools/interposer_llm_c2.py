@@ -22,6 +22,7 @@ with Daemon(gpu="32G", pinned="16G", paged="96G", log=out) as d:
                        [sys.executable, LLM, str(reqs), "1.5", "2", "flux-12b", "1", "1024"]], timeout=1800, stagger_s=1.0)
     sw = d.switches()
     err = d.stderr()
+    daemon_rc = d.proc.poll()
 steady = [s for s in sw if s["pcie_h2d"] > (1 << 30) and s["pcie_d2h"] > (1 << 30)]
 summary = {"apps_ok": all(r["rc"] == 0 for r in res), "apps": [r["out"] for r in res], "switches": len(sw),
            "steady_switches": len(steady),
@@ -30,5 +31,6 @@ summary = {"apps_ok": all(r["rc"] == 0 for r in res), "apps": [r["out"] for r in
            "switch_ms": {"p50": statistics.median([s["total_ms"] for s in steady]), "max": max(s["total_ms"] for s in steady)} if steady else None,
            "verified": sum(s["verified"] for s in sw), "mismatches": sum(s["mismatches"] for s in sw)}
 if not summary["apps_ok"]:
-    summary["errors"] = [r["stderr"][-500:] for r in res] + [err[-500:]]
+    summary["errors"] = [r["stderr"][-500:] for r in res] + [d.stderr()[-2000:]]  # after the daemon exited
+    summary["daemon_rc"] = daemon_rc
 print(json.dumps(summary))
