@@ -202,6 +202,9 @@ class SwapEngine {
   std::uint32_t arena_frames() const;  // physical 2 MiB frames in the arena
   // Exportable arena: one more physical slab (up to gpu_physical_max); returns its index.
   std::uint32_t arena_grow_slab();
+  // Exportable arena: unmaps and releases a slab no block uses (its slot is
+  // refilled by the next grow).
+  void arena_drop_slab(std::uint32_t slab);
   // Not owned; nullptr restores the default. Install before any GPU allocation.
   void set_frame_placer(FramePlacer* placer);
   // Called on the thread running execute() whenever legs have committed (the

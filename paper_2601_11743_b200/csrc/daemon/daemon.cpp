@@ -238,7 +238,7 @@ class Daemon {
     std::uint64_t seen_launches = 0;
     bool seen_blocking = false;
     std::uint64_t active_launch_mark = 0;
-    std::uint32_t slabs_rpc = 0, slabs_ev = 0;  // slab descriptors sent on each socket
+    std::vector<std::uint32_t> gen_rpc, gen_ev;  // slab generation whose descriptor each socket carried (0: none)
   };
 
   Seconds now() const { return static_cast<double>(ipc::mono_ns() - t0_) * 1e-9; }
@@ -314,7 +314,7 @@ class Daemon {
     rep.block_bytes = kBlockBytes;
     rep.min_bytes = opt_.min_bytes;
     rep.device = opt_.eng.device;
-    const std::uint32_t slabs = static_cast<std::uint32_t>(placer_.slabs());
+    const std::uint32_t slabs = placer_.base();  // grown slabs follow lazily (send_new_slabs)
     rep.slabs = slabs;
     rep.slab_bytes = static_cast<std::uint64_t>(opt_.slab_blocks) * kBlockBytes;
     rep.arena_bytes = rep.slabs * rep.slab_bytes;
@@ -327,7 +327,8 @@ class Daemon {
       ok = ipc::send_fds(fd, batch.data(), static_cast<int>(n));
       for (int x : batch) ::close(x);
     }
-    a.slabs_rpc = a.slabs_ev = slabs;  // imported at start-up, before the listener runs
+    a.gen_rpc.assign(slabs, 1);  // imported at start-up, before the listener runs
+    a.gen_ev = a.gen_rpc;
     apps_[a.id] = a;
     if (!ok) apps_[a.id].alive = false;
     note("{\"t\": %.6f, \"event\": \"hello\", \"app\": %u, \"pid\": %d, \"name\": \"%s\"}", now(), a.id, a.pid, a.name.c_str());
@@ -603,21 +604,45 @@ class Daemon {
   // (send_new_slabs), so each socket delivers the descriptor first.
   std::uint32_t grow_arena() {
     const std::uint32_t s = eng_.arena_grow_slab();
+    placer_.revive(s);
     note("{\"t\": %.6f, \"event\": \"slab_grow\", \"slab\": %u, \"partial_slabs\": %" PRIu64 "}", now(), s, placer_.partial());
     return s;
   }
 
-  // Sends the app every slab it has not received on this socket yet
-  // (Slab message + descriptor each).
+  // Sends the app every live slab generation it has not received on this
+  // socket yet (Slab message + descriptor each).
   void send_new_slabs(App& a, bool on_rpc) {
-    std::uint32_t& known = on_rpc ? a.slabs_rpc : a.slabs_ev;
+    std::vector<std::uint32_t>& known = on_rpc ? a.gen_rpc : a.gen_ev;
     const int sock = on_rpc ? a.rpc : a.ev;
-    for (; known < placer_.slabs() && a.alive && sock >= 0; ++known) {
-      const int fd = eng_.arena_export_fd(known);
-      ipc::SlabFdMsg m{known, 0};
+    if (known.size() < placer_.slabs()) known.resize(placer_.slabs(), 0);
+    for (std::uint32_t f = 0; f < placer_.slabs() && a.alive && sock >= 0; ++f) {
+      if (placer_.dropped(f) || known[f] == placer_.gen(f)) continue;
+      const int fd = eng_.arena_export_fd(f);
+      ipc::SlabFdMsg m{f, placer_.gen(f)};
       const bool ok = ipc::send_msg(sock, ipc::Msg::Slab, &m, sizeof(m)) && ipc::send_fds(sock, &fd, 1);
       ::close(fd);
       if (!ok) a.alive = false;
+      known[f] = placer_.gen(f);
+    }
+  }
+
+  // Between switches: grown slabs beyond the slack that no block uses are
+  // released again, in the daemon and in every shim that imported them, so
+  // physical use returns to budget + slack (growth is only transient).
+  void shrink_arena() {
+    const std::vector<std::uint32_t> drop = placer_.take_droppable(static_cast<std::size_t>(opt_.phys_slack_slabs));
+    for (std::uint32_t f : drop) {
+      const std::uint32_t gen = placer_.gen(f);
+      eng_.arena_drop_slab(f);
+      for (auto& [id, a] : apps_) {
+        const bool has = (f < a.gen_ev.size() && a.gen_ev[f] == gen) || (f < a.gen_rpc.size() && a.gen_rpc[f] == gen);
+        if (f < a.gen_ev.size()) a.gen_ev[f] = 0;
+        if (f < a.gen_rpc.size()) a.gen_rpc[f] = 0;
+        if (!has || !a.alive || a.ev < 0) continue;
+        ipc::DropMsg m{++epoch_, f, gen};
+        if (!ipc::send_msg(a.ev, ipc::Msg::Drop, &m, sizeof(m))) a.alive = false;
+      }
+      note("{\"t\": %.6f, \"event\": \"slab_drop\", \"slab\": %u}", now(), f);
     }
   }
 
@@ -662,6 +687,7 @@ class Daemon {
     send_maps();
     account(r);
     flush_unmaps();
+    shrink_arena();
     note("{\"t\": %.6f, \"event\": \"fetch_in_place\", \"app\": %u, \"bytes_in\": %" PRIu64 ", \"bytes_out\": %" PRIu64 "}",
          now(), app, plan.bytes_in, plan.bytes_out);
   }
@@ -713,6 +739,7 @@ class Daemon {
     sched_.on_grant_start(to, granted_at);
     sched_.on_api_event(to, granted_at, ApiEventKind::NonBlockingReturn);  // its held launch resumes now
     flush_unmaps();
+    shrink_arena();
     ++switches_;
     const SwitchStats& s = eng_.last_stats();
     auto ms = [](std::uint64_t a, std::uint64_t b) { return static_cast<double>(b - a) * 1e-6; };
@@ -723,13 +750,14 @@ class Daemon {
          ", \"premap_ms\": %.3f, \"premap_calls\": %" PRIu64 ", \"premap_unmap_ms\": %.3f, \"total_ms\": %.3f"
          ", \"device_span_ms\": %.3f"
          ", \"verified\": %" PRIu64 ", \"unverified\": %" PRIu64 ", \"mismatches\": %" PRIu64
-         ", \"partial_slabs\": %" PRIu64 ", \"free_slabs\": %zu}",
+         ", \"partial_slabs\": %" PRIu64 ", \"free_slabs\": %zu, \"live_slabs\": %zu}",
          t, holder ? static_cast<int>(*holder) : -1, to, plan.bytes_in, plan.bytes_out, s.pcie_h2d_bytes, s.pcie_d2h_bytes,
          s.host_bytes, ms(t_start, t_drained), ms(t_drained, t_planned), ms(t_planned, t_copied), ms(t_copied, t_unmapped),
          ms(t_unmapped, t_end), static_cast<double>(gm.map_ns) * 1e-6, gm.map_calls, gm.unmap_calls,
          gm.recv_ns > t_grant_sent ? ms(t_grant_sent, gm.recv_ns) : 0.0, static_cast<double>(gm.premap_ns) * 1e-6, gm.premap_calls,
          static_cast<double>(gm.premap_unmap_ns) * 1e-6, ms(t_start, t_end),
-         s.device_span_s * 1e3, s.verified, s.unverified, s.mismatches, placer_.partial(), placer_.free_slabs());
+         s.device_span_s * 1e3, s.verified, s.unverified, s.mismatches, placer_.partial(), placer_.free_slabs(),
+         placer_.live_slabs());
   }
 
   template <typename... A>

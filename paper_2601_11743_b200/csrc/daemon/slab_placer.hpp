@@ -6,6 +6,7 @@
 #include <deque>
 #include <functional>
 #include <map>
+#include <set>
 #include <string>
 #include <utility>
 #include <vector>
@@ -25,7 +26,8 @@ class SlabPlacer final : public FramePlacer {
  public:
   using Key = std::pair<AppId, std::uint32_t>;  // (app, vslab)
 
-  SlabPlacer(std::uint32_t slabs, std::uint32_t slab_blocks) : sb_(slab_blocks), is_free_(slabs, 1), nfree_(slabs) {
+  SlabPlacer(std::uint32_t slabs, std::uint32_t slab_blocks)
+      : sb_(slab_blocks), base_(slabs), is_free_(slabs, 1), gen_(slabs, 1), nfree_(slabs) {
     for (std::uint32_t p = 0; p < slabs; ++p) free_.push_back(p);
   }
 
@@ -53,7 +55,12 @@ class SlabPlacer final : public FramePlacer {
           throw InvariantViolation("slab placer: every physical slab is in use (partly resident slabs: " +
                                    std::to_string(partial()) + ")");
         const std::uint32_t p = grow_();
-        if (is_free_.size() <= p) is_free_.resize(p + 1, 0);
+        if (is_free_.size() <= p) {
+          is_free_.resize(p + 1, 0);
+          gen_.resize(p + 1, 0);
+        }
+        ++gen_[p];
+        dropped_.erase(p);
         is_free_[p] = 1;
         free_.push_back(p);
         ++nfree_;
@@ -114,7 +121,32 @@ class SlabPlacer final : public FramePlacer {
     return n;
   }
   std::size_t free_slabs() const { return nfree_; }
-  std::size_t slabs() const { return is_free_.size(); }
+  std::size_t slabs() const { return is_free_.size(); }  // slots (dropped ones included)
+  std::uint32_t gen(std::uint32_t p) const { return gen_[p]; }
+  std::uint32_t base() const { return base_; }  // slabs created at start, never dropped
+  std::size_t live_slabs() const { return is_free_.size() - dropped_.size(); }
+  bool dropped(std::uint32_t p) const { return gen_[p] == 0 || dropped_.count(p) != 0; }
+
+  // Free grown slabs beyond `keep_free` free ones, taken out of the pool to
+  // be dropped (highest index first); vslabs still (stale-)mapped to them are
+  // marked unmapped (the shims unmap them on Drop).
+  std::vector<std::uint32_t> take_droppable(std::size_t keep_free) {
+    std::vector<std::uint32_t> out;
+    for (std::uint32_t p = static_cast<std::uint32_t>(is_free_.size()); p-- > base_ && nfree_ > keep_free;) {
+      if (!is_free_[p]) continue;
+      is_free_[p] = 0;
+      --nfree_;
+      dropped_.insert(p);
+      out.push_back(p);
+    }
+    if (!out.empty())
+      for (auto& kv : slabs_)
+        for (std::uint32_t p : out)
+          if (kv.second.mapped == p) kv.second.mapped = ipc::kNoFrame;
+    return out;
+  }
+  // A dropped slot handed out again by grow() is live again.
+  void revive(std::uint32_t p) { dropped_.erase(p); }
   std::uint32_t grown() const { return grown_; }
   // Called when no slab is free; returns the index of a new one.
   void set_grow(std::function<std::uint32_t()> g) { grow_ = std::move(g); }
@@ -146,7 +178,10 @@ class SlabPlacer final : public FramePlacer {
   std::vector<std::uint64_t> vpos_;
   std::map<Key, Slab> slabs_;
   std::deque<std::uint32_t> free_;  // FIFO with lazily deleted entries (is_free_)
+  std::uint32_t base_;           // slabs created at start (never dropped)
   std::vector<char> is_free_;
+  std::vector<std::uint32_t> gen_;
+  std::set<std::uint32_t> dropped_;
   std::size_t nfree_ = 0;
   std::function<std::uint32_t()> grow_;
   std::uint32_t grown_ = 0;

@@ -1100,6 +1100,7 @@ std::int64_t SwapEngine::frame_index(BlockId b) const {
 
 std::uint32_t SwapEngine::arena_frames() const { return impl_->arena.ring.units(); }
 std::uint32_t SwapEngine::arena_grow_slab() { return impl_->arena.grow_slab(); }
+void SwapEngine::arena_drop_slab(std::uint32_t slab) { impl_->arena.drop_slab(slab); }
 void SwapEngine::set_frame_placer(FramePlacer* placer) { impl_->placer = placer; }
 void SwapEngine::prefetch_begin(const MigrationPlan& plan) { impl_->prefetch_begin(plan); }
 bool SwapEngine::prefetch_pump() { return impl_->prefetch_pump(); }

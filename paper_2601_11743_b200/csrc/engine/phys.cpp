@@ -127,8 +127,14 @@ std::uint32_t DeviceArena::grow_slab() {
   if (!vmm_) throw SimError(Err::InvalidState, "only an exportable arena grows");
   const std::uint32_t s = vmm_->grow();
   const auto per = static_cast<std::uint32_t>(vmm_->slab_bytes() / kBlockBytes);
-  ring.reset(static_cast<std::uint32_t>(ring.units() + per));  // the frame count (the placer owns the frames)
+  const auto frames = static_cast<std::uint32_t>((s + 1) * per);
+  if (frames > ring.units()) ring.reset(frames);  // the frame count (the placer owns the frames)
   return s;
+}
+
+void DeviceArena::drop_slab(std::uint32_t slab) {
+  if (!vmm_) throw SimError(Err::InvalidState, "only an exportable arena shrinks");
+  vmm_->drop(slab);
 }
 
 void PinnedRing::init(Bytes capacity, int numa_node) {

@@ -76,6 +76,7 @@ class DeviceArena {
   void init(Bytes capacity, bool exportable = false, int device = 0, Bytes slab_bytes = 0, Bytes reserve = 0);
   // Exportable arenas only: one more slab at the end (frames grow with it).
   std::uint32_t grow_slab();
+  void drop_slab(std::uint32_t slab);
   ~DeviceArena();
   std::uint8_t* frame(std::uint32_t u) const { return base_ + static_cast<std::size_t>(u) * kBlockBytes; }
   std::uint8_t* base() const { return base_; }

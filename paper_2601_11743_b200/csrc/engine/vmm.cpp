@@ -76,42 +76,64 @@ void ExportableArena::init(int device, Bytes bytes, Bytes slab_bytes, Bytes rese
   for (std::uint32_t f = 0; f < n; ++f) add_slab();
 }
 
-void ExportableArena::add_slab() {
+// Creates slab `f`'s physical allocation and maps it at its slot.
+void ExportableArena::create_at(std::uint32_t f) {
   const VmmApi& v = vmm_api();
   const CUmemAllocationProp prop = slab_prop(device_);
-  const std::uint32_t f = mapped_;
   CUmemGenericAllocationHandle h = 0;
   check(v.mem_create(&h, slab_, &prop, 0), "cuMemCreate(exportable slab)");
-  handles_.push_back(h);
+  if (handles_.size() <= f) handles_.resize(f + 1, 0);
+  handles_[f] = h;
   const CUdeviceptr at = va_ + static_cast<CUdeviceptr>(f) * slab_;
   check(v.map(at, slab_, 0, h, 0), "cuMemMap(slab)");
-  mapped_ = f + 1;
   CUmemAccessDesc acc{};
   acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   acc.location.id = device_;
   acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
   check(v.set_access(at, slab_, &acc, 1), "cuMemSetAccess(slab)");
+}
+
+void ExportableArena::add_slab() {
+  create_at(mapped_);
+  ++mapped_;
   bytes_ = static_cast<Bytes>(mapped_) * slab_;
 }
 
 std::uint32_t ExportableArena::grow() {
+  for (std::uint32_t f = 0; f < mapped_; ++f)
+    if (handles_[f] == 0) {  // a dropped slot comes back first
+      create_at(f);
+      bytes_ += slab_;
+      return f;
+    }
   if (static_cast<Bytes>(mapped_ + 1) * slab_ > reserved_)
     throw InvariantViolation("exportable arena: the reserved range is full (" + std::to_string(mapped_) + " slabs)");
   add_slab();
   return mapped_ - 1;
 }
 
+void ExportableArena::drop(std::uint32_t f) {
+  if (f >= mapped_ || handles_[f] == 0) throw InvariantViolation("exportable arena: drop of a missing slab");
+  const VmmApi& v = vmm_api();
+  NX_CUDA(cudaDeviceSynchronize());  // nothing of ours may still touch it
+  check(v.unmap(va_ + static_cast<CUdeviceptr>(f) * slab_, slab_), "cuMemUnmap(slab)");
+  check(v.mem_release(handles_[f]), "cuMemRelease(slab)");
+  handles_[f] = 0;
+  bytes_ -= slab_;
+}
+
 ExportableArena::~ExportableArena() {
   if (!va_) return;
   const VmmApi& v = vmm_api();
-  for (std::uint32_t f = 0; f < mapped_; ++f) v.unmap(va_ + static_cast<CUdeviceptr>(f) * slab_, slab_);
+  for (std::uint32_t f = 0; f < mapped_; ++f)
+    if (handles_[f]) v.unmap(va_ + static_cast<CUdeviceptr>(f) * slab_, slab_);
   for (CUmemGenericAllocationHandle h : handles_)
     if (h) v.mem_release(h);
   v.addr_free(va_, reserved_);
 }
 
 int ExportableArena::export_fd(std::uint32_t f) const {
-  if (f >= handles_.size()) throw SimError(Err::InvalidState, "export of slab " + std::to_string(f) + " out of range");
+  if (f >= handles_.size() || handles_[f] == 0) throw SimError(Err::InvalidState, "export of slab " + std::to_string(f) + ": none");
   int fd = -1;
   check(vmm_api().export_handle(&fd, handles_[f], CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0), "cuMemExportToShareableHandle");
   return fd;

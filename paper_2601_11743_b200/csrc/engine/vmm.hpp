@@ -54,9 +54,13 @@ class ExportableArena {
   // grow() can append slabs at contiguous addresses later.
   void init(int device, Bytes bytes, Bytes slab_bytes, Bytes reserve_bytes = 0);
   ~ExportableArena();
-  // Creates, maps and opens one more slab after the last; returns its index.
-  // Throws when the reserved range is full.
+  // Creates, maps and opens one more slab (a dropped slot first, else after
+  // the last); returns its index. Throws when the reserved range is full.
   std::uint32_t grow();
+  // Unmaps and releases slab `f` (its slot stays reserved; grow() refills it).
+  // Shims holding an imported handle keep the memory alive until they
+  // release it too.
+  void drop(std::uint32_t f);
   std::uint8_t* base() const { return reinterpret_cast<std::uint8_t*>(va_); }
   Bytes bytes() const { return bytes_; }
   std::uint32_t slabs() const { return static_cast<std::uint32_t>(handles_.size()); }
@@ -72,8 +76,9 @@ class ExportableArena {
   Bytes reserved_ = 0;
   Bytes slab_ = 0;
   int device_ = 0;
-  std::uint32_t mapped_ = 0;
+  std::uint32_t mapped_ = 0;  // slots in use (dropped ones included)
   void add_slab();
+  void create_at(std::uint32_t f);
 };
 
 }  // namespace nixie::b200

@@ -54,12 +54,18 @@ enum class Msg : std::uint32_t {
   Granted,       // event shim->d: GrantedMsg
   Stats,         // rpc  shim->d : (empty)    reply StatsRep
   Map,           // event d->shim: SlabsMsg + SlabMap[n] (slabs placed while the switch runs; no ack)
-  Slab,          // event d->shim: SlabFdMsg, then 1 fd: the arena grew by one slab (import it; no ack)
+  Slab,          // rpc or event d->shim: SlabFdMsg, then 1 fd: a (re)created slab to import (no ack)
+  Drop,          // event d->shim: DropMsg: the daemon released a grown slab; unmap and release it (no ack)
 };
 
 struct SlabFdMsg {
   std::uint32_t slab;
-  std::uint32_t pad;
+  std::uint32_t gen;  // creation count of that slot (a dropped slot can be created again)
+};
+struct DropMsg {
+  std::uint64_t epoch;
+  std::uint32_t slab;
+  std::uint32_t gen;
 };
 
 // Virtual slabs: a shim reserves one large virtual range and places its

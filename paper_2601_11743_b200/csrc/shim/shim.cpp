@@ -121,6 +121,7 @@ struct Drv {
   CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
   CUresult (*ctx_get_current)(CUcontext*);
   CUresult (*ctx_set_current)(CUcontext);
+  CUresult (*release)(CUmemGenericAllocationHandle);
 };
 
 Drv& drv() {
@@ -147,6 +148,7 @@ Drv& drv() {
     x.set_access = reinterpret_cast<decltype(x.set_access)>(get("cuMemSetAccess"));
     x.ctx_get_current = reinterpret_cast<decltype(x.ctx_get_current)>(get("cuCtxGetCurrent"));
     x.ctx_set_current = reinterpret_cast<decltype(x.ctx_set_current)>(get("cuCtxSetCurrent"));
+    x.release = reinterpret_cast<decltype(x.release)>(get("cuMemRelease"));
     return x;
   }();
   return d;
@@ -188,7 +190,10 @@ struct Shim {
   std::uint64_t budget = 0, min_bytes = kBlock, slab_bytes = 0, slab_blocks = 0;
   int rpc = -1, ev = -1;
   ipc::CtlPage* ctl = nullptr;
-  std::vector<CUmemGenericAllocationHandle> slabs;  // imported arena slabs
+  std::vector<CUmemGenericAllocationHandle> slabs;  // imported arena slabs (0: none)
+  std::vector<std::uint32_t> slab_gen;             // generation of each imported slab
+  std::vector<std::uint32_t> slab_gone_gen;        // highest dropped generation per slot
+  std::vector<std::uint64_t> slab_drop_epoch;      // epoch of the last Drop per slot
   CUcontext ctx = nullptr;
   CUdeviceptr range = 0;          // reserved once; managed allocations live here
   std::uint64_t range_blocks = 0;
@@ -283,6 +288,7 @@ void init_once() {
   if (g.slab_bytes == 0 || g.slab_bytes % kBlock != 0) die("bad slab size from the daemon");
   g.slab_blocks = g.slab_bytes / kBlock;
   g.slabs.resize(rep.slabs, 0);
+  g.slab_gen.assign(rep.slabs, 1);
   std::vector<int> fds(ipc::kFdBatch);
   for (std::uint64_t f = 0; f < rep.slabs; f += ipc::kFdBatch) {
     const int n = static_cast<int>(std::min<std::uint64_t>(ipc::kFdBatch, rep.slabs - f));
@@ -342,7 +348,7 @@ void sync_vslab(std::uint32_t v, VSlab& s, std::uint64_t& maps, std::uint64_t& u
   }
   const std::uint64_t t1 = ipc::mono_ns();
   if (s.want != ipc::kNoFrame) {
-    if (s.want >= g.slabs.size()) die("the daemon named a slab outside the arena");
+    if (s.want >= g.slabs.size() || g.slabs[s.want] == 0) die("the daemon named a slab this shim has no handle for");
     CUresult e = drv().map(va, g.slab_bytes, 0, g.slabs[s.want], 0);
     if (e != CUDA_SUCCESS) die("cuMemMap", e);
     const CUmemAccessDesc acc = access_desc();
@@ -362,6 +368,9 @@ void sync_vslab(std::uint32_t v, VSlab& s, std::uint64_t& maps, std::uint64_t& u
 void place(std::uint32_t v, std::uint32_t phys, std::uint64_t epoch, std::uint64_t& maps, std::uint64_t& unmaps) {
   VSlab& s = g.vslabs[v];
   if (epoch <= s.epoch) return;
+  // A placement older than a Drop of its slab is stale: the slab was freed
+  // (the vslab evicted) after it was sent; a later message places the vslab.
+  if (phys != ipc::kNoFrame && phys < g.slab_drop_epoch.size() && epoch < g.slab_drop_epoch[phys]) phys = ipc::kNoFrame;
   s.want = phys;
   s.epoch = epoch;
   sync_vslab(v, s, maps, unmaps);
@@ -448,7 +457,25 @@ void on_grant(const std::vector<std::uint8_t>& body) {
 }
 
 // The daemon's arena grew: import the new slab (its fd follows the message).
-// Arrives on whichever socket the daemon is about to name the slab on.
+// Unmaps every vslab currently mapped to physical slab `p` (caller holds g.mu).
+void unmap_slab_users(std::uint32_t p, std::uint64_t epoch) {
+  std::uint64_t maps = 0, unmaps = 0;
+  for (auto& [v, st] : g.vslabs)
+    if (st.have == p) {
+      st.want = ipc::kNoFrame;
+      st.epoch = std::max(st.epoch, epoch);
+      sync_vslab(v, st, maps, unmaps);
+    }
+}
+
+void grow_slot_tables(std::uint32_t p) {
+  if (g.slabs.size() <= p) g.slabs.resize(p + 1, 0);
+  if (g.slab_gen.size() <= p) g.slab_gen.resize(p + 1, 0);
+  if (g.slab_gone_gen.size() <= p) g.slab_gone_gen.resize(p + 1, 0);
+  if (g.slab_drop_epoch.size() <= p) g.slab_drop_epoch.resize(p + 1, 0);
+}
+
+// A (re)created slab, on whichever socket the daemon is about to name it on.
 void on_slab(int sock, const std::vector<std::uint8_t>& body) {
   ipc::SlabFdMsg m{};
   std::memcpy(&m, body.data(), std::min(body.size(), sizeof(m)));
@@ -456,7 +483,8 @@ void on_slab(int sock, const std::vector<std::uint8_t>& body) {
   if (!ipc::recv_fds(sock, &fd, 1)) die("receiving a new slab's descriptor");
   {
     std::lock_guard<std::mutex> lk(g.mu);
-    if (m.slab < g.slabs.size() && g.slabs[m.slab] != 0) {  // already imported through the other socket
+    grow_slot_tables(m.slab);
+    if (g.slab_gen[m.slab] >= m.gen || g.slab_gone_gen[m.slab] >= m.gen) {  // seen through the other socket, or dropped
       ::close(fd);
       return;
     }
@@ -467,8 +495,33 @@ void on_slab(int sock, const std::vector<std::uint8_t>& body) {
   ::close(fd);
   if (r != CUDA_SUCCESS) die("cuMemImportFromShareableHandle(new slab)", r);
   std::lock_guard<std::mutex> lk(g.mu);
-  if (g.slabs.size() <= m.slab) g.slabs.resize(m.slab + 1, 0);
-  if (g.slabs[m.slab] == 0) g.slabs[m.slab] = h;
+  if (g.slab_gen[m.slab] >= m.gen) {  // raced with the other socket
+    drv().release(h);
+    return;
+  }
+  if (g.slabs[m.slab] != 0) {  // an older generation of the slot: nothing may map it any more
+    unmap_slab_users(m.slab, 0);
+    drv().release(g.slabs[m.slab]);
+  }
+  g.slabs[m.slab] = h;
+  g.slab_gen[m.slab] = m.gen;
+}
+
+// The daemon released a grown slab: drop every mapping of it and the handle.
+void on_drop(const std::vector<std::uint8_t>& body) {
+  ipc::DropMsg m{};
+  std::memcpy(&m, body.data(), std::min(body.size(), sizeof(m)));
+  wait_for_global_captures();
+  std::lock_guard<std::mutex> lk(g.mu);
+  grow_slot_tables(m.slab);
+  g.slab_gone_gen[m.slab] = std::max(g.slab_gone_gen[m.slab], m.gen);
+  g.slab_drop_epoch[m.slab] = std::max(g.slab_drop_epoch[m.slab], m.epoch);
+  if (g.slab_gen[m.slab] != m.gen || g.slabs[m.slab] == 0) return;  // superseded already
+  ensure_ctx();
+  unmap_slab_users(m.slab, m.epoch);
+  drv().release(g.slabs[m.slab]);
+  g.slabs[m.slab] = 0;
+  g.slab_gen[m.slab] = 0;
 }
 
 void listener() {
@@ -488,6 +541,7 @@ void listener() {
       case ipc::Msg::Grant: on_grant(body); break;
       case ipc::Msg::Map: on_map(body); break;
       case ipc::Msg::Slab: on_slab(g.ev, body); break;
+      case ipc::Msg::Drop: on_drop(body); break;
       default:
         std::fprintf(stderr, "[nixie-shim] unexpected event %u\n", static_cast<unsigned>(type));
     }

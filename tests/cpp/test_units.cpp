@@ -86,6 +86,16 @@ static void slab_growth() {
   CHECK(p.grown() == 2 && p.slabs() == 3 && p.free_slabs() == 0);
   p.release(2, b);
   CHECK(p.free_slabs() == 1);
+  p.release(4, c);
+  // shrink: grown free slabs beyond the kept slack leave the pool
+  auto drop = p.take_droppable(0);
+  CHECK(drop.size() == 2 && p.free_slabs() == 0);
+  CHECK(p.dropped(1) && p.dropped(2) && !p.dropped(0));
+  // the next growth refills a dropped slot with a new generation
+  next = 2;
+  const std::uint32_t gen_before = p.gen(2);
+  const std::uint32_t d = p.acquire(2);
+  CHECK(d / 2 == 2 && p.gen(2) == gen_before + 1 && !p.dropped(2));
 }
 
 static void range_alloc() {

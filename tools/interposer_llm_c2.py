@@ -23,6 +23,7 @@ with Daemon(gpu="32G", pinned="16G", paged="96G", log=out, slab_mib=slab) as d:
                        [sys.executable, LLM, str(reqs), "1.5", "2", "flux-12b", "1", "1024"]], timeout=1800, stagger_s=1.0)
     sw = d.switches()
     grows = sum(1 for r in d.records() if r.get("event") == "slab_grow")
+    drops = sum(1 for r in d.records() if r.get("event") == "slab_drop")
     err = d.stderr()
     daemon_rc = d.proc.poll()
 steady = [s for s in sw if s["pcie_h2d"] > (1 << 30) and s["pcie_d2h"] > (1 << 30)]
@@ -32,7 +33,8 @@ summary = {"apps_ok": all(r["rc"] == 0 for r in res), "apps": [r["out"] for r in
            "copy_bidir_gbps_median": round(statistics.median([(s["pcie_h2d"] + s["pcie_d2h"]) / (s["copy_ms"] * 1e-3) / 1e9 for s in steady]), 1) if steady else None,
            "switch_ms": {"p50": statistics.median([s["total_ms"] for s in steady]), "max": max(s["total_ms"] for s in steady)} if steady else None,
            "verified": sum(s["verified"] for s in sw), "mismatches": sum(s["mismatches"] for s in sw),
-           "slab_mib": slab or 512, "slabs_grown": grows,
+           "slab_mib": slab or 512, "slabs_grown": grows, "slabs_dropped": drops,
+           "live_slabs_after_switches": [s["live_slabs"] for s in sw][-6:],
            "grant_ms_p50": statistics.median([s["grant_ms"] for s in steady]) if steady else None}
 if not summary["apps_ok"]:
     summary["errors"] = [r["stderr"][-500:] for r in res] + [d.stderr()[-2000:]]  # after the daemon exited
