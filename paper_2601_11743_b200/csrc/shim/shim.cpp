@@ -304,7 +304,8 @@ void init_once() {
     const CUresult r = drv().addr_reserve(&g.range, kRangeBytes, g.slab_bytes, 0, 0);
     if (r != CUDA_SUCCESS) die("cuMemAddressReserve(range)", r);
     g.range_blocks = kRangeBytes / kBlock;
-    g.ranges.reset(g.range_blocks);
+    const char* ff = std::getenv("NIXIE_SHIM_FIRST_FIT");  // reuse freed ranges (scatters eviction order)
+    g.ranges.reset(g.range_blocks, ff && *ff == '1');
   }
   void* p = ::mmap(nullptr, 4096, PROT_READ | PROT_WRITE, MAP_SHARED, ctl_fd, 0);
   if (p == MAP_FAILED) die("mmap control page");

@@ -99,8 +99,18 @@ static void slab_growth() {
 }
 
 static void range_alloc() {
+  {  // bump (default): allocation order = range order, no reuse
+    nixie::shim::RangeAlloc b;
+    b.reset(1024);
+    std::uint64_t x = 0, y = 0, z = 0;
+    CHECK(b.take(3, 64, x) && x == 0);
+    CHECK(b.take(10, 64, y) && y == 3);
+    b.give(x, 3);
+    CHECK(b.take(2, 64, z) && z == 13);  // not the freed hole
+    CHECK(b.take(40, 64, z) && z == 64);  // slab aligned
+  }
   nixie::shim::RangeAlloc r;
-  r.reset(1024);
+  r.reset(1024, true);
   std::uint64_t a = 0, b = 0, c = 0, d = 0;
   CHECK(r.take(3, 64, a) && a == 0);     // small: first fit
   CHECK(r.take(40, 64, b) && b == 64);   // >= half a slab: slab aligned
