@@ -2,8 +2,8 @@
 //   SlabPlacer (csrc/daemon/slab_placer.hpp): slot arithmetic, sharing of a
 //     slab by the blocks of one vslab, release, affinity, exhaustion,
 //     mapping bookkeeping;
-//   RangeAlloc (csrc/shim/range_alloc.hpp): first fit, slab alignment,
-//     coalescing on free.
+//   RangeAlloc (csrc/shim/range_alloc.hpp): per-size lanes, common bump,
+//     first fit, slab alignment, coalescing on free.
 // Built by paper_2601_11743_b200/Makefile (lib/nx_unit_tests); run by
 // tests/test_interposer_host.py.
 #include <cstdio>
@@ -100,14 +100,22 @@ static void slab_growth() {
 
 static void range_alloc() {
   {  // bump (default): allocation order = range order, no reuse
-    nixie::shim::RangeAlloc b;
-    b.reset(1024);
-    std::uint64_t x = 0, y = 0, z = 0;
-    CHECK(b.take(3, 64, x) && x == 0);
-    CHECK(b.take(10, 64, y) && y == 3);
+    nixie::shim::RangeAlloc b;  // lanes (default)
+    b.reset(4096);                // 64 slabs of 64 blocks; lanes span 8 slabs
+    std::uint64_t x = 0, y = 0, z = 0, w = 0;
+    CHECK(b.take(3, 64, x) && x == 0);       // lane for size 3
+    CHECK(b.take(10, 64, y) && y == 512);    // lane for size 10, slab aligned
+    CHECK(b.take(3, 64, z) && z == 3);       // same size: next in its lane
     b.give(x, 3);
-    CHECK(b.take(2, 64, z) && z == 13);  // not the freed hole
-    CHECK(b.take(40, 64, z) && z == 64);  // slab aligned
+    CHECK(b.take(3, 64, z) && z == 6);       // freed ranges are not reused
+    CHECK(b.take(1, 64, w) && w == 1024);    // single block: common bump
+    CHECK(b.take(40, 64, w) && w == 1088);   // under a slab: its own lane
+    CHECK(b.take(64, 64, w) && w == 1600);   // a slab: common, slab aligned
+    CHECK(b.lanes() == 3);
+    for (int i = 0; i < 167; ++i) CHECK(b.take(3, 64, z));  // lane 3 full (9 + 167 * 3 = 510)
+    CHECK(b.take(3, 64, z) && z == 1664);    // a second span for size 3
+    CHECK(b.take(5, 64, w) && w == 2176);    // another lane: tail 1920 - 512 >= 1024
+    CHECK(b.take(7, 64, w) && w == 2688);    // tail 1408 - 512 < 1024: common bump
   }
   nixie::shim::RangeAlloc r;
   r.reset(1024, true);
