@@ -72,6 +72,7 @@ struct Options {
   int phys_slack_slabs = -1;       // physical slabs beyond the budget (partly resident slabs); -1: max(4, 2 GiB worth)
   std::uint32_t slab_blocks = 0;   // 0: 512 MiB for budgets >= 16 GiB, else 128 MiB
   bool prefetch = false;           // MLFQ prefetch of the next candidate
+  bool reference_victims = false;  // the planner's own victim blocks instead of slab-aligned ones
 };
 
 Bytes parse_size(const char* s) {
@@ -90,7 +91,7 @@ void usage() {
                "usage: nixied [--socket PATH] [--device N] [--gpu SIZE] [--pinned SIZE] [--paged SIZE]\n"
                "              [--window SIZE] [--min-bytes SIZE] [--path auto|ce|sm] [--host-threads N]\n"
                "              [--tick-ms X] [--idle-ms X] [--allot-s X] [--preempt-s X] [--log FILE]\n"
-               "              [--phys-slack SLABS] [--slab-mib 2..1024, power of 2] [--prefetch] [--exit-after-apps N]\n"
+               "              [--phys-slack SLABS] [--slab-mib 2..1024, power of 2] [--prefetch] [--exit-after-apps N]\n              [--reference-victims]\n"
                "sizes take a K/M/G suffix (GiB when bare). The daemon serves LD_PRELOAD=libnixie_shim.so apps\n"
                "that set NIXIE_SOCKET=PATH.\n");
 }
@@ -124,6 +125,7 @@ bool parse_args(int argc, char** argv, Options& o) {
     else if (a == "--phys-slack") o.phys_slack_slabs = std::atoi(val());
     else if (a == "--slab-mib") o.slab_blocks = static_cast<std::uint32_t>(std::atoi(val()) / 2);
     else if (a == "--prefetch") o.prefetch = true;
+    else if (a == "--reference-victims") o.reference_victims = true;
     else if (a == "--path") {
       const std::string p = val();
       o.eng.path = p == "sm" ? CopyPath::SmKernel : p == "auto" ? CopyPath::Auto : CopyPath::CopyEngine;
@@ -156,6 +158,10 @@ class Daemon {
       : opt_(o), eng_(o.eng), sched_(o.mlfq), placer_(eng_.arena_frames() / o.slab_blocks, o.slab_blocks) {
     eng_.set_frame_placer(&placer_);
     placer_.set_grow([this] { return grow_arena(); });
+    if (!o.reference_victims)
+      victims_ = [this](const MemState& st, const std::vector<AppId>& order, Bytes want) {
+        return placer_.slab_victims(st, order, want);
+      };
     eng_.set_progress_hook([this] { send_maps(); });
     sched_.set_logging(true);
     t0_ = ipc::mono_ns();
@@ -681,6 +687,7 @@ class Daemon {
   void fetch_in_place(AppId app) {
     PlannerConfig cfg = opt_.planner;
     cfg.eviction_policy.victim_order = sched_.victim_hint();
+    cfg.gpu_victims = victims_;
     eng_.prefetch_quiesce();
     const MigrationPlan plan = plan_switch(app, eng_.mem(), cfg);
     const ExecResult r = eng_.execute(plan, cfg);
@@ -712,6 +719,7 @@ class Daemon {
     // (4) plan + real copies, victims unmapping concurrently.
     PlannerConfig cfg = opt_.planner;
     cfg.eviction_policy.victim_order = sched_.victim_hint();
+    cfg.gpu_victims = victims_;
     eng_.prefetch_quiesce();  // cancel_pending + quiesced (transfer.cpp:89-113)
     const MigrationPlan plan = plan_switch(to, eng_.mem(), cfg);
     const std::uint64_t t_planned = ipc::mono_ns();
@@ -781,6 +789,7 @@ class Daemon {
   SwapEngine eng_;
   MlfqScheduler sched_;
   SlabPlacer placer_;
+  std::function<std::vector<BlockId>(const MemState&, const std::vector<AppId>&, Bytes)> victims_;
   int listen_fd_ = -1;
   std::vector<int> pending_;
   std::vector<SlabPlacer::Key> stale_;  // released vslabs whose owners still map their old slab

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <algorithm>
 #include <deque>
 #include <functional>
 #include <map>
@@ -157,6 +158,38 @@ class SlabPlacer final : public FramePlacer {
     return it == slabs_.end() ? ipc::kNoFrame : it->second.mapped;
   }
   void set_mapped(const Key& k, std::uint32_t phys) { slabs_[k].mapped = phys; }
+  // Slab-aligned victim choice (PlannerConfig::gpu_victims): per victim app,
+  // in the planner's app order, its GPU-resident blocks grouped by virtual
+  // slab, fewest resident first, whole groups until `want` bytes are covered;
+  // only the last group is split. Same bytes and app order as the reference
+  // planner, but an eviction frees whole physical slabs instead of leaving
+  // every slab the largest chunks touch partly resident.
+  std::vector<BlockId> slab_victims(const MemState& st, const std::vector<AppId>& order, Bytes want) const {
+    std::vector<BlockId> out;
+    const std::uint64_t need = block_count_for(want);
+    for (AppId app : order) {
+      std::map<std::uint32_t, std::vector<BlockId>> by_vslab;
+      for (ChunkId c : st.chunks_of(app))
+        for (BlockId b : st.chunk(c).blocks) {
+          const Location& loc = st.block(b).loc;
+          if (!loc.is_resident() || loc.tier != TierId::Gpu) continue;
+          if (b >= app_.size()) throw InvariantViolation("slab placer: block " + std::to_string(b) + " has no virtual placement");
+          by_vslab[key(b).second].push_back(b);
+        }
+      std::vector<std::vector<BlockId>*> groups;
+      for (auto& kv : by_vslab) groups.push_back(&kv.second);
+      std::stable_sort(groups.begin(), groups.end(), [](auto* a, auto* b) { return a->size() < b->size(); });
+      for (auto* g : groups) {
+        std::sort(g->begin(), g->end(), [&](BlockId a, BlockId b) { return vpos_[a] < vpos_[b]; });
+        for (BlockId b : *g) {
+          out.push_back(b);
+          if (out.size() >= need) return out;
+        }
+      }
+    }
+    return out;
+  }
+
   // After a Grant: the shim maps exactly the backed vslabs and unmaps the rest.
   void granted(AppId app) {
     for (auto it = slabs_.lower_bound(Key{app, 0}); it != slabs_.end() && it->first.first == app; ++it)

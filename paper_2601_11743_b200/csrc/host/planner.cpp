@@ -193,7 +193,10 @@ class SwitchPlanner {
 
   void assign_victims() {
     Bytes placed = 0;
-    for (BlockId b : victims_on(st_, order_, TierId::Gpu, plan_.bytes_out)) {
+    const std::vector<BlockId> picked = cfg_.gpu_victims && plan_.bytes_out
+                                            ? cfg_.gpu_victims(st_, order_, plan_.bytes_out)
+                                            : victims_on(st_, order_, TierId::Gpu, plan_.bytes_out);
+    for (BlockId b : picked) {
       TierId dst = TierId::Disk;
       if (placed < keep_pinned_)
         dst = TierId::PinnedHost;

@@ -2,14 +2,17 @@
 //   SlabPlacer (csrc/daemon/slab_placer.hpp): slot arithmetic, sharing of a
 //     slab by the blocks of one vslab, release, affinity, exhaustion,
 //     mapping bookkeeping;
-//   RangeAlloc (csrc/shim/range_alloc.hpp): per-size lanes, common bump,
-//     first fit, slab alignment, coalescing on free.
+//   RangeAlloc (csrc/shim/range_alloc.hpp): first fit, slab alignment,
+//     coalescing on free.
 // Built by paper_2601_11743_b200/Makefile (lib/nx_unit_tests); run by
 // tests/test_interposer_host.py.
 #include <cstdio>
 #include <cstdlib>
+#include <set>
 #include <string>
+#include <algorithm>
 
+#include "nixie/planner.hpp"
 #include "range_alloc.hpp"
 #include "slab_placer.hpp"
 
@@ -98,24 +101,55 @@ static void slab_growth() {
   CHECK(d / 2 == 2 && p.gen(2) == gen_before + 1 && !p.dropped(2));
 }
 
+// Slab-aligned victims: same bytes as the reference planner, whole vslabs
+// first (fewest resident blocks first), one split group at most.
+static void slab_victims() {
+  MemState st;
+  st.set_capacity(TierId::Gpu, 16 * kBlockBytes);
+  st.set_capacity(TierId::PinnedHost, 64 * kBlockBytes);
+  SlabPlacer p(4, 4);
+  // app 1: chunks of 3, 2, 3, 2 blocks -> blocks 0..9 at range blocks 0..9
+  // (vslabs {0..3} {4..7} {8,9}); app 2: 8 blocks in pinned memory
+  for (Bytes sz : {3, 2, 3, 2}) st.allocate(1, sz * kBlockBytes, TierId::Gpu);
+  p.expect(0, 10, 1, 0);
+  for (BlockId b = 0; b < 10; ++b) p.acquire(b);
+  st.allocate(2, 8 * kBlockBytes, TierId::PinnedHost);
+  PlannerConfig cfg;
+  auto evicted = [](const MigrationPlan& plan) {
+    std::vector<BlockId> v;
+    for (const Move& m : plan.moves)
+      if (m.kind == MoveKind::EvictFromGpu) v.push_back(m.block);
+    std::sort(v.begin(), v.end());
+    return v;
+  };
+  const MigrationPlan ref = plan_switch(2, st, cfg);
+  CHECK(ref.bytes_out == 2 * kBlockBytes);  // 8 in, 6 free
+  CHECK((evicted(ref) == std::vector<BlockId>{0, 1}));  // largest chunk first
+  st.allocate(1, 2 * kBlockBytes, TierId::Gpu);  // blocks 18, 19 at range blocks 10, 11: vslab 2 full; 4 free
+  p.expect(18, 2, 1, 10);
+  const MigrationPlan ref2 = plan_switch(2, st, cfg);
+  CHECK((evicted(ref2) == std::vector<BlockId>{0, 1, 2, 5}));  // both 3-block chunks: vslabs 0 and 1 split
+  cfg.gpu_victims = [&](const MemState& s, const std::vector<AppId>& order, Bytes want) {
+    return p.slab_victims(s, order, want);
+  };
+  const MigrationPlan ours = plan_switch(2, st, cfg);
+  CHECK(ours.bytes_out == ref2.bytes_out && ours.bytes_in == ref2.bytes_in);
+  CHECK(evicted(ours).size() == 4);
+  std::set<std::uint32_t> touched;
+  for (BlockId b : evicted(ours)) touched.insert(static_cast<std::uint32_t>((b < 10 ? b : b - 8) / 4));
+  CHECK(touched.size() == 1);  // one whole vslab
+}
+
 static void range_alloc() {
   {  // bump (default): allocation order = range order, no reuse
-    nixie::shim::RangeAlloc b;  // lanes (default)
-    b.reset(4096);                // 64 slabs of 64 blocks; lanes span 8 slabs
-    std::uint64_t x = 0, y = 0, z = 0, w = 0;
-    CHECK(b.take(3, 64, x) && x == 0);       // lane for size 3
-    CHECK(b.take(10, 64, y) && y == 512);    // lane for size 10, slab aligned
-    CHECK(b.take(3, 64, z) && z == 3);       // same size: next in its lane
+    nixie::shim::RangeAlloc b;
+    b.reset(1024);
+    std::uint64_t x = 0, y = 0, z = 0;
+    CHECK(b.take(3, 64, x) && x == 0);
+    CHECK(b.take(10, 64, y) && y == 3);
     b.give(x, 3);
-    CHECK(b.take(3, 64, z) && z == 6);       // freed ranges are not reused
-    CHECK(b.take(1, 64, w) && w == 1024);    // single block: common bump
-    CHECK(b.take(40, 64, w) && w == 1088);   // under a slab: its own lane
-    CHECK(b.take(64, 64, w) && w == 1600);   // a slab: common, slab aligned
-    CHECK(b.lanes() == 3);
-    for (int i = 0; i < 167; ++i) CHECK(b.take(3, 64, z));  // lane 3 full (9 + 167 * 3 = 510)
-    CHECK(b.take(3, 64, z) && z == 1664);    // a second span for size 3
-    CHECK(b.take(5, 64, w) && w == 2176);    // another lane: tail 1920 - 512 >= 1024
-    CHECK(b.take(7, 64, w) && w == 2688);    // tail 1408 - 512 < 1024: common bump
+    CHECK(b.take(2, 64, z) && z == 13);  // not the freed hole
+    CHECK(b.take(40, 64, z) && z == 64);  // slab aligned
   }
   nixie::shim::RangeAlloc r;
   r.reset(1024, true);
@@ -136,6 +170,7 @@ int main() {
   slab_placer();
   slab_growth();
   range_alloc();
+  slab_victims();
   std::printf("nx_unit_tests: %d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;
 }
