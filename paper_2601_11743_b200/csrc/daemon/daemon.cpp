@@ -673,27 +673,6 @@ class Daemon {
     }
   }
 
-  // plan_switch, then (slab-aligned victims) each run of evictions in
-  // descending block order. The engine starts legs in plan order and fetches
-  // run ascending, so the victim's last chosen vslab is emptied first and its
-  // slab goes to the incoming app's first vslab that needs one beyond the free
-  // pool. Two apps switching back and forth then hand the same slabs to the
-  // same vslabs every time (slab affinity holds, no remaps); in plan order the
-  // pairing shifted every switch (13-17 remaps per switch, measured).
-  MigrationPlan plan_moves(AppId app, const PlannerConfig& cfg) {
-    MigrationPlan plan = plan_switch(app, eng_.mem(), cfg);
-    if (!victims_) return plan;
-    auto& mv = plan.moves;
-    for (std::size_t i = 0; i < mv.size();) {
-      std::size_t j = i + 1;
-      if (mv[i].kind == MoveKind::EvictFromGpu)
-        while (j < mv.size() && mv[j].kind == MoveKind::EvictFromGpu && mv[j].dst == mv[i].dst) ++j;
-      std::reverse(mv.begin() + static_cast<std::ptrdiff_t>(i), mv.begin() + static_cast<std::ptrdiff_t>(j));
-      i = j;
-    }
-    return plan;
-  }
-
   void account(const ExecResult&) {
     const SwitchStats& s = eng_.last_stats();
     bytes_in_ += s.pcie_h2d_bytes;
@@ -710,7 +689,7 @@ class Daemon {
     cfg.eviction_policy.victim_order = sched_.victim_hint();
     cfg.gpu_victims = victims_;
     eng_.prefetch_quiesce();
-    const MigrationPlan plan = plan_moves(app, cfg);
+    const MigrationPlan plan = plan_switch(app, eng_.mem(), cfg);
     const ExecResult r = eng_.execute(plan, cfg);
     send_maps();
     account(r);
@@ -742,7 +721,7 @@ class Daemon {
     cfg.eviction_policy.victim_order = sched_.victim_hint();
     cfg.gpu_victims = victims_;
     eng_.prefetch_quiesce();  // cancel_pending + quiesced (transfer.cpp:89-113)
-    const MigrationPlan plan = plan_moves(to, cfg);
+    const MigrationPlan plan = plan_switch(to, eng_.mem(), cfg);
     const std::uint64_t t_planned = ipc::mono_ns();
     const ExecResult r = eng_.execute(plan, cfg);
     const std::uint64_t t_copied = ipc::mono_ns();
