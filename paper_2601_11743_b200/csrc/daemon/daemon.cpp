@@ -73,6 +73,7 @@ struct Options {
   std::uint32_t slab_blocks = 0;   // 0: 512 MiB for budgets >= 16 GiB, else 128 MiB
   bool prefetch = false;           // MLFQ prefetch of the next candidate
   bool reference_victims = false;  // the planner's own victim blocks instead of slab-aligned ones
+  bool keep_stale_maps = false;    // victims keep mappings of lost slabs until their next Grant
 };
 
 Bytes parse_size(const char* s) {
@@ -91,7 +92,7 @@ void usage() {
                "usage: nixied [--socket PATH] [--device N] [--gpu SIZE] [--pinned SIZE] [--paged SIZE]\n"
                "              [--window SIZE] [--min-bytes SIZE] [--path auto|ce|sm] [--host-threads N]\n"
                "              [--tick-ms X] [--idle-ms X] [--allot-s X] [--preempt-s X] [--log FILE]\n"
-               "              [--phys-slack SLABS] [--slab-mib 2..1024, power of 2] [--prefetch] [--exit-after-apps N]\n              [--reference-victims]\n"
+               "              [--phys-slack SLABS] [--slab-mib 2..1024, power of 2] [--prefetch] [--exit-after-apps N]\n              [--reference-victims] [--keep-stale-maps]\n"
                "sizes take a K/M/G suffix (GiB when bare). The daemon serves LD_PRELOAD=libnixie_shim.so apps\n"
                "that set NIXIE_SOCKET=PATH.\n");
 }
@@ -126,6 +127,7 @@ bool parse_args(int argc, char** argv, Options& o) {
     else if (a == "--slab-mib") o.slab_blocks = static_cast<std::uint32_t>(std::atoi(val()) / 2);
     else if (a == "--prefetch") o.prefetch = true;
     else if (a == "--reference-victims") o.reference_victims = true;
+    else if (a == "--keep-stale-maps") o.keep_stale_maps = true;
     else if (a == "--path") {
       const std::string p = val();
       o.eng.path = p == "sm" ? CopyPath::SmKernel : p == "auto" ? CopyPath::Auto : CopyPath::CopyEngine;
@@ -654,7 +656,14 @@ class Daemon {
 
   // After a switch: victims unmap the slabs they lost, off the critical path.
   // A vslab that got a slab back meanwhile is skipped (mapped there again).
+  // --keep-stale-maps: a paused victim keeps mapping slabs another app now
+  // uses (no isolation while paused; its next Grant remaps what changed), so
+  // a vslab that gets its old slab back costs no driver call.
   void flush_unmaps() {
+    if (opt_.keep_stale_maps) {
+      stale_.clear();
+      return;
+    }
     std::map<AppId, std::vector<std::uint32_t>> per_app;
     for (const auto& k : stale_) {
       if (placer_.map_of(k.first, k.second).phys != ipc::kNoFrame) continue;  // backed again
@@ -673,6 +682,26 @@ class Daemon {
     }
   }
 
+  // plan_switch; with --keep-stale-maps and slab-aligned victims, each run of
+  // evictions in descending block order. The engine starts legs in plan order
+  // and fetches run ascending, so a victim's vslab empties before the
+  // incoming vslab that had its slab asks for one, and the same slabs go to
+  // the same vslabs at every switch (tools/slab_sim.cpp: 13-18 remaps per
+  // switch in plan order, 0 descending).
+  MigrationPlan plan_moves(AppId app, const PlannerConfig& cfg) {
+    MigrationPlan plan = plan_switch(app, eng_.mem(), cfg);
+    if (!victims_ || !opt_.keep_stale_maps) return plan;
+    auto& mv = plan.moves;
+    for (std::size_t i = 0; i < mv.size();) {
+      std::size_t j = i + 1;
+      if (mv[i].kind == MoveKind::EvictFromGpu)
+        while (j < mv.size() && mv[j].kind == MoveKind::EvictFromGpu && mv[j].dst == mv[i].dst) ++j;
+      std::reverse(mv.begin() + static_cast<std::ptrdiff_t>(i), mv.begin() + static_cast<std::ptrdiff_t>(j));
+      i = j;
+    }
+    return plan;
+  }
+
   void account(const ExecResult&) {
     const SwitchStats& s = eng_.last_stats();
     bytes_in_ += s.pcie_h2d_bytes;
@@ -689,7 +718,7 @@ class Daemon {
     cfg.eviction_policy.victim_order = sched_.victim_hint();
     cfg.gpu_victims = victims_;
     eng_.prefetch_quiesce();
-    const MigrationPlan plan = plan_switch(app, eng_.mem(), cfg);
+    const MigrationPlan plan = plan_moves(app, cfg);
     const ExecResult r = eng_.execute(plan, cfg);
     send_maps();
     account(r);
@@ -721,7 +750,7 @@ class Daemon {
     cfg.eviction_policy.victim_order = sched_.victim_hint();
     cfg.gpu_victims = victims_;
     eng_.prefetch_quiesce();  // cancel_pending + quiesced (transfer.cpp:89-113)
-    const MigrationPlan plan = plan_switch(to, eng_.mem(), cfg);
+    const MigrationPlan plan = plan_moves(to, cfg);
     const std::uint64_t t_planned = ipc::mono_ns();
     const ExecResult r = eng_.execute(plan, cfg);
     const std::uint64_t t_copied = ipc::mono_ns();

@@ -44,12 +44,16 @@ def _check(res, d):
         assert r["out"] is not None, r["stdout"]
 
 
-def test_two_vecapps_oversubscribed():
+@pytest.mark.parametrize("mode", ["default", "keep_stale_maps", "reference_victims"])
+def test_two_vecapps_oversubscribed(mode):
     """2 x 3 GiB on a 4 GiB budget: every iteration after a think gap needs a
-    switch. Byte-exact (device + host checks), every restore verified."""
-    with Daemon(gpu="4G", pinned="4G", paged="16G") as d:
+    switch. Byte-exact (device + host checks), every restore verified. Also
+    with victims keeping stale mappings (descending evictions) and with the
+    reference planner's victim blocks."""
+    extra = {"default": [], "keep_stale_maps": ["--keep-stale-maps"], "reference_victims": ["--reference-victims"]}[mode]
+    with Daemon(gpu="4G", pinned="4G", paged="16G", extra=extra) as d:
         res = run_apps(d, [_vec(3072, 6, 250, 11, "a"), _vec(3072, 6, 250, 22, "b")], timeout=600)
-        _save("two_vecapps", d, res)
+        _save("two_vecapps" + ("" if mode == "default" else "_" + mode), d, res)
         _check(res, d)
         sw = d.switches()
     d.stop()
