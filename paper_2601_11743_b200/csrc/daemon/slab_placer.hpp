@@ -190,6 +190,8 @@ class SlabPlacer final : public FramePlacer {
     return out;
   }
 
+  std::uint32_t vslab_of(BlockId b) const { return key(b).second; }
+
   // After a Grant: the shim maps exactly the backed vslabs and unmaps the rest.
   void granted(AppId app) {
     for (auto it = slabs_.lower_bound(Key{app, 0}); it != slabs_.end() && it->first.first == app; ++it)

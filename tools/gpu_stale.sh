@@ -1,7 +1,7 @@
 # LLM config 2 through the interposer: slab-aligned victims with
 # --keep-stale-maps (descending evictions), then the default.
 mkdir -p gpurun_out
-for v in stale def; do
+for v in ${VARIANTS:-stale def}; do
   f=""; [ "$v" = stale ] && f="slab,stale"
   timeout 900 python tools/interposer_llm_c2.py 12 gpurun_out/llm_c2_$v.jsonl 0 $f > gpurun_out/llm_c2_$v.out 2>&1
   tail -1 gpurun_out/llm_c2_$v.out | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', {k: d.get(k) for k in ('apps_ok','slabs_grown','live_slabs_after_switches','steady_switches','copy_bidir_gbps_median','switch_ms','grant_ms_p50','mismatches','errors')})"

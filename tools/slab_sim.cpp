@@ -6,7 +6,7 @@
 // ends). Prints, per switch, the slabs the incoming app must remap, the
 // partly resident slabs and growth. Used to study victim/affinity policies
 // (DESIGN.md §10). `slab_sim ref` uses the planner's own victims; SIM_DESC=1
-// evicts each run in descending block order. The model ignores the victims'
+// evicts each run in descending virtual-slab order. The model ignores the victims'
 // post-switch unmaps (every returning vslab then needs a map on hardware).
 //   g++ -std=c++20 -O2 -Iinclude -Ipaper_2601_11743_b200/csrc/daemon -Ipaper_2601_11743_b200/csrc/ipc
 //       tools/slab_sim.cpp paper_2601_11743_b200/lib/libnixie_host.a -o /tmp/slab_sim
@@ -80,7 +80,8 @@ int main(int argc, char** argv) {
         std::size_t j = i + 1;
         if (mv[i].kind == MoveKind::EvictFromGpu)
           while (j < mv.size() && mv[j].kind == MoveKind::EvictFromGpu && mv[j].dst == mv[i].dst) ++j;
-        std::reverse(mv.begin() + i, mv.begin() + j);
+        std::stable_sort(mv.begin() + i, mv.begin() + j,
+                         [&](const Move& a, const Move& b) { return p.vslab_of(a.block) > p.vslab_of(b.block); });
         i = j;
       }
     }
