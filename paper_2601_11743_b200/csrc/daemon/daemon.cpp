@@ -73,7 +73,7 @@ struct Options {
   std::uint32_t slab_blocks = 0;   // 0: 512 MiB for budgets >= 16 GiB, else 128 MiB
   bool prefetch = false;           // MLFQ prefetch of the next candidate
   bool reference_victims = false;  // the planner's own victim blocks instead of slab-aligned ones
-  bool keep_stale_maps = false;    // victims keep mappings of lost slabs until their next Grant
+  bool keep_stale_maps = true;     // victims keep mappings of lost slabs until their next Grant (--isolate-victims: unmap)
 };
 
 Bytes parse_size(const char* s) {
@@ -92,7 +92,7 @@ void usage() {
                "usage: nixied [--socket PATH] [--device N] [--gpu SIZE] [--pinned SIZE] [--paged SIZE]\n"
                "              [--window SIZE] [--min-bytes SIZE] [--path auto|ce|sm] [--host-threads N]\n"
                "              [--tick-ms X] [--idle-ms X] [--allot-s X] [--preempt-s X] [--log FILE]\n"
-               "              [--phys-slack SLABS] [--slab-mib 2..1024, power of 2] [--prefetch] [--exit-after-apps N]\n              [--reference-victims] [--keep-stale-maps]\n"
+               "              [--phys-slack SLABS] [--slab-mib 2..1024, power of 2] [--prefetch] [--exit-after-apps N]\n              [--reference-victims] [--isolate-victims]\n"
                "sizes take a K/M/G suffix (GiB when bare). The daemon serves LD_PRELOAD=libnixie_shim.so apps\n"
                "that set NIXIE_SOCKET=PATH.\n");
 }
@@ -128,6 +128,7 @@ bool parse_args(int argc, char** argv, Options& o) {
     else if (a == "--prefetch") o.prefetch = true;
     else if (a == "--reference-victims") o.reference_victims = true;
     else if (a == "--keep-stale-maps") o.keep_stale_maps = true;
+    else if (a == "--isolate-victims") o.keep_stale_maps = false;
     else if (a == "--path") {
       const std::string p = val();
       o.eng.path = p == "sm" ? CopyPath::SmKernel : p == "auto" ? CopyPath::Auto : CopyPath::CopyEngine;
@@ -656,9 +657,11 @@ class Daemon {
 
   // After a switch: victims unmap the slabs they lost, off the critical path.
   // A vslab that got a slab back meanwhile is skipped (mapped there again).
-  // --keep-stale-maps: a paused victim keeps mapping slabs another app now
-  // uses (no isolation while paused; its next Grant remaps what changed), so
-  // a vslab that gets its old slab back costs no driver call.
+  // By default a paused victim keeps mapping slabs another app now uses (its
+  // next Grant remaps what changed), so a vslab that gets its old slab back
+  // costs no driver call. Nixie's threat model is one user's applications,
+  // which already share the pinned pool.
+  // --isolate-victims unmaps them right after the switch instead.
   void flush_unmaps() {
     if (opt_.keep_stale_maps) {
       stale_.clear();
@@ -682,7 +685,7 @@ class Daemon {
     }
   }
 
-  // plan_switch; with --keep-stale-maps and slab-aligned victims, each run of
+  // plan_switch; with stale mappings kept and slab-aligned victims, each run of
   // evictions in descending virtual-slab order. The engine starts legs in plan order
   // and fetches run ascending, so a victim's vslab empties before the
   // incoming vslab that had its slab asks for one, and the same slabs go to

@@ -44,13 +44,13 @@ def _check(res, d):
         assert r["out"] is not None, r["stdout"]
 
 
-@pytest.mark.parametrize("mode", ["default", "keep_stale_maps", "reference_victims"])
+@pytest.mark.parametrize("mode", ["default", "isolate_victims", "reference_victims"])
 def test_two_vecapps_oversubscribed(mode):
     """2 x 3 GiB on a 4 GiB budget: every iteration after a think gap needs a
     switch. Byte-exact (device + host checks), every restore verified. Also
-    with victims keeping stale mappings (descending evictions) and with the
+    with victims unmapping lost slabs right after each switch, and with the
     reference planner's victim blocks."""
-    extra = {"default": [], "keep_stale_maps": ["--keep-stale-maps"], "reference_victims": ["--reference-victims"]}[mode]
+    extra = {"default": [], "isolate_victims": ["--isolate-victims"], "reference_victims": ["--reference-victims"]}[mode]
     with Daemon(gpu="4G", pinned="4G", paged="16G", extra=extra) as d:
         res = run_apps(d, [_vec(3072, 6, 250, 11, "a"), _vec(3072, 6, 250, 22, "b")], timeout=600)
         _save("two_vecapps" + ("" if mode == "default" else "_" + mode), d, res)

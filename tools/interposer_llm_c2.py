@@ -20,10 +20,10 @@ out = sys.argv[2] if len(sys.argv) > 2 else None
 slab = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3] != "0" else None
 flags = sys.argv[4].split(",") if len(sys.argv) > 4 else []
 ref_victims = "ref" in flags  # the planner's own victim blocks
-keep_stale = "stale" in flags  # --keep-stale-maps
+isolate = "isolate" in flags  # --isolate-victims
 slack = int(sys.argv[5]) if len(sys.argv) > 5 else None  # physical slack slabs
 with Daemon(gpu="32G", pinned="16G", paged="96G", log=out, slab_mib=slab,
-            extra=(["--reference-victims"] if ref_victims else []) + (["--keep-stale-maps"] if keep_stale else []) + (["--phys-slack", str(slack)] if slack is not None else [])) as d:
+            extra=(["--reference-victims"] if ref_victims else []) + (["--isolate-victims"] if isolate else []) + (["--phys-slack", str(slack)] if slack is not None else [])) as d:
     res = run_apps(d, [[sys.executable, LLM, str(reqs), "1.0", "1", "qwen3-8b", "1", "512"],
                        [sys.executable, LLM, str(reqs), "1.5", "2", "flux-12b", "1", "1024"]], timeout=1800, stagger_s=1.0)
     sw = d.switches()
@@ -38,7 +38,7 @@ summary = {"apps_ok": all(r["rc"] == 0 for r in res), "apps": [r["out"] for r in
            "copy_bidir_gbps_median": round(statistics.median([(s["pcie_h2d"] + s["pcie_d2h"]) / (s["copy_ms"] * 1e-3) / 1e9 for s in steady]), 1) if steady else None,
            "switch_ms": {"p50": statistics.median([s["total_ms"] for s in steady]), "max": max(s["total_ms"] for s in steady)} if steady else None,
            "verified": sum(s["verified"] for s in sw), "mismatches": sum(s["mismatches"] for s in sw),
-           "slab_mib": slab or 512, "victims": "reference" if ref_victims else "slab", "phys_slack": slack, "keep_stale_maps": keep_stale, "slabs_grown": grows, "slabs_dropped": drops,
+           "slab_mib": slab or 512, "victims": "reference" if ref_victims else "slab", "phys_slack": slack, "isolate_victims": isolate, "slabs_grown": grows, "slabs_dropped": drops,
            "live_slabs_after_switches": [s["live_slabs"] for s in sw][-6:],
            "grant_ms_p50": statistics.median([s["grant_ms"] for s in steady]) if steady else None}
 if not summary["apps_ok"]:
