@@ -39,7 +39,8 @@ def main():
         res = run_apps(d, cmds, timeout=h * 4 + 300, stagger_s=0.2)
         sw = d.switches()
     grants = sorted(s["grant_ms"] for s in sw)
-    out = {"interval_s": a.interval, "horizon_s": h, "prefetch": a.prefetch, "slab_mib": a.slab_mib or 128, "switches": len(sw),
+    out = {"interval_s": a.interval, "horizon_s": h, "prefetch": a.prefetch, "slab_mib": a.slab_mib or 512,  # the daemon default for a 32 GiB budget
+           "switches": len(sw),
            "grant_ms": {"p50": grants[len(grants) // 2] if grants else None, "max": grants[-1] if grants else None},
            "apps_ok": all(r["rc"] == 0 for r in res),
            "mismatches": sum(s["mismatches"] for s in sw), "verified": sum(s["verified"] for s in sw),
