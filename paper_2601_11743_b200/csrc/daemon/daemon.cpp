@@ -73,7 +73,8 @@ struct Options {
   std::uint32_t slab_blocks = 0;   // 0: 512 MiB for budgets >= 16 GiB, else 128 MiB
   bool prefetch = false;           // MLFQ prefetch of the next candidate
   bool reference_victims = false;  // the planner's own victim blocks instead of slab-aligned ones
-  bool keep_stale_maps = true;     // victims keep mappings of lost slabs until their next Grant (--isolate-victims: unmap)
+  int keep_stale_maps = -1;        // victims keep mappings of lost slabs until their next Grant: 1 always, 0 never
+                                   // (--isolate-victims), -1 while exactly two apps hold memory
 };
 
 Bytes parse_size(const char* s) {
@@ -92,7 +93,7 @@ void usage() {
                "usage: nixied [--socket PATH] [--device N] [--gpu SIZE] [--pinned SIZE] [--paged SIZE]\n"
                "              [--window SIZE] [--min-bytes SIZE] [--path auto|ce|sm] [--host-threads N]\n"
                "              [--tick-ms X] [--idle-ms X] [--allot-s X] [--preempt-s X] [--log FILE]\n"
-               "              [--phys-slack SLABS] [--slab-mib 2..1024, power of 2] [--prefetch] [--exit-after-apps N]\n              [--reference-victims] [--isolate-victims]\n"
+               "              [--phys-slack SLABS] [--slab-mib 2..1024, power of 2] [--prefetch] [--exit-after-apps N]\n              [--reference-victims] [--keep-stale-maps | --isolate-victims]\n"
                "sizes take a K/M/G suffix (GiB when bare). The daemon serves LD_PRELOAD=libnixie_shim.so apps\n"
                "that set NIXIE_SOCKET=PATH.\n");
 }
@@ -127,8 +128,8 @@ bool parse_args(int argc, char** argv, Options& o) {
     else if (a == "--slab-mib") o.slab_blocks = static_cast<std::uint32_t>(std::atoi(val()) / 2);
     else if (a == "--prefetch") o.prefetch = true;
     else if (a == "--reference-victims") o.reference_victims = true;
-    else if (a == "--keep-stale-maps") o.keep_stale_maps = true;
-    else if (a == "--isolate-victims") o.keep_stale_maps = false;
+    else if (a == "--keep-stale-maps") o.keep_stale_maps = 1;
+    else if (a == "--isolate-victims") o.keep_stale_maps = 0;
     else if (a == "--path") {
       const std::string p = val();
       o.eng.path = p == "sm" ? CopyPath::SmKernel : p == "auto" ? CopyPath::Auto : CopyPath::CopyEngine;
@@ -596,7 +597,7 @@ class Daemon {
     // move data costs up to ~80 ms per slab on these hosts (it waits on the
     // GPU), so the owners drop their stale mappings after the switch, when
     // the link is quiet (flush_unmaps).
-    for (const auto& k : placer_.take_released()) stale_.push_back(k);
+    for (const auto& k : placer_.take_released()) stale_.insert(k);
     for (auto& [app, ms] : per_app) {
       auto it = apps_.find(app);
       if (it == apps_.end() || !it->second.alive || it->second.ev < 0) continue;
@@ -657,16 +658,21 @@ class Daemon {
 
   // After a switch: victims unmap the slabs they lost, off the critical path.
   // A vslab that got a slab back meanwhile is skipped (mapped there again).
-  // By default a paused victim keeps mapping slabs another app now uses (its
-  // next Grant remaps what changed), so a vslab that gets its old slab back
-  // costs no driver call. Nixie's threat model is one user's applications,
-  // which already share the pinned pool.
-  // --isolate-victims unmaps them right after the switch instead.
+  // A paused victim may keep mapping slabs another app now uses (its next
+  // Grant remaps what changed), so a vslab that gets its old slab back costs
+  // no driver call. Nixie's threat model is one user's applications, which
+  // already share the pinned pool. That pays off when two
+  // apps alternate: the descending eviction order (plan_moves) hands every
+  // vslab its old slab back. With more apps the slabs rotate, a kept mapping
+  // must be unmapped during a later switch, and cuMemUnmap then waits on the
+  // copies (up to 600 ms per switch in config 3, measured), so by default
+  // stale mappings are kept only while exactly two apps hold memory.
+  bool keep_stale() const {
+    return opt_.keep_stale_maps > 0 || (opt_.keep_stale_maps < 0 && eng_.mem().apps().size() == 2);
+  }
+
   void flush_unmaps() {
-    if (opt_.keep_stale_maps) {
-      stale_.clear();
-      return;
-    }
+    if (keep_stale()) return;  // kept in stale_: unmapped if a third app arrives
     std::map<AppId, std::vector<std::uint32_t>> per_app;
     for (const auto& k : stale_) {
       if (placer_.map_of(k.first, k.second).phys != ipc::kNoFrame) continue;  // backed again
@@ -693,7 +699,7 @@ class Daemon {
   // switch in plan order, 0 descending).
   MigrationPlan plan_moves(AppId app, const PlannerConfig& cfg) {
     MigrationPlan plan = plan_switch(app, eng_.mem(), cfg);
-    if (!victims_ || !opt_.keep_stale_maps) return plan;
+    if (!victims_ || !keep_stale()) return plan;
     auto& mv = plan.moves;
     for (std::size_t i = 0; i < mv.size();) {
       std::size_t j = i + 1;
@@ -828,7 +834,7 @@ class Daemon {
   std::function<std::vector<BlockId>(const MemState&, const std::vector<AppId>&, Bytes)> victims_;
   int listen_fd_ = -1;
   std::vector<int> pending_;
-  std::vector<SlabPlacer::Key> stale_;  // released vslabs whose owners still map their old slab
+  std::set<SlabPlacer::Key> stale_;  // released vslabs whose owners may still map their old slab
   std::map<AppId, App> apps_;
   AppId next_app_ = 0;
   int gone_ = 0;
