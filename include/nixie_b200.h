@@ -263,6 +263,23 @@ int nx_workload_model(const char* spec, char** trace, size_t* len);
  * `H k moves`, `M k differing-blocks`, `V k app bad ...` and final
  * `F app bad` lines. */
 int nx_workload_real(const char* spec, const nx_engine_config* cfg, uint64_t seed, char** trace, size_t* len);
+/* ---- UVM demand-paging model (the comparator; include/nixie/uvm.hpp) ------
+ * UvmSim (proj/include/nixie/uvm.hpp:40-80) behind a handle,
+ * for policy comparisons in the CLI (uvm_rr_<W>: round-robin time slices
+ * over demand paging, as nvshare does). No GPU. */
+typedef struct nx_uvm nx_uvm;
+/* UvmSim(gpu_capacity, pcie link, UvmConfig{fault_latency, prefetch_pages}) (uvm.hpp:42-44). */
+int nx_uvm_create(uint64_t gpu_capacity, double pcie_up_bw, double pcie_down_bw, int half_duplex,
+                  double fault_latency, int prefetch_pages, nx_uvm** out);
+/* register_alloc(app, size) (uvm.hpp:46). */
+int nx_uvm_register(nx_uvm* h, uint32_t app, uint64_t size);
+/* touch_kernel(app, every chunk of app, base, now) (uvm.hpp:55): the kernel's
+ * duration including the fault service time. */
+int nx_uvm_touch(nx_uvm* h, uint32_t app, double base_duration, double now, double* duration);
+/* fault_count, faulted_bytes_total, pinned_mirror_peak (uvm.hpp:58-63); any pointer may be NULL. */
+int nx_uvm_stats(const nx_uvm* h, uint64_t* faults, uint64_t* faulted_bytes, uint64_t* mirror_peak);
+void nx_uvm_destroy(nx_uvm* h);
+
 void nx_free(void* p);
 
 #ifdef __cplusplus

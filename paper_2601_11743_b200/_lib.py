@@ -156,6 +156,11 @@ _SIGNATURES = [
     ("nx_scenario_real", c_int, [c_char_p, POINTER(EngineConfigC), c_uint64, POINTER(c_void_p), POINTER(c_size_t)]),
     ("nx_workload_model", c_int, [c_char_p, POINTER(c_void_p), POINTER(c_size_t)]),
     ("nx_workload_real", c_int, [c_char_p, POINTER(EngineConfigC), c_uint64, POINTER(c_void_p), POINTER(c_size_t)]),
+    ("nx_uvm_create", c_int, [c_uint64, c_double, c_double, c_int, c_double, c_int, POINTER(c_void_p)]),
+    ("nx_uvm_register", c_int, [c_void_p, c_uint32, c_uint64]),
+    ("nx_uvm_touch", c_int, [c_void_p, c_uint32, c_double, c_double, POINTER(c_double)]),
+    ("nx_uvm_stats", c_int, [c_void_p, POINTER(c_uint64), POINTER(c_uint64), POINTER(c_uint64)]),
+    ("nx_uvm_destroy", None, [c_void_p]),
     ("nx_free", None, [c_void_p]),
 ]
 

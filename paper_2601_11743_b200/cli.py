@@ -1,7 +1,7 @@
 """nixie command line: scenarios in, reports out (module cli).
 
     python -m paper_2601_11743_b200.cli run --scenario s.json --out r.json [--format json|csv|text]
-    python -m paper_2601_11743_b200.cli compare --scenario s.json --policies nixie,nixie_prefetch
+    python -m paper_2601_11743_b200.cli compare --scenario s.json --policies nixie,nixie_prefetch,uvm_rr_4,uvm_rr_30
     python -m paper_2601_11743_b200.cli sweep --scenario s.json --sweep pinned=16G,24G,32G
     python -m paper_2601_11743_b200.cli validate --scenario s.json
 
@@ -284,9 +284,97 @@ def metrics(trace: str, sc: Dict[str, Any]) -> Dict[str, Any]:
     }
 
 
+def simulate_uvm_rr(sc: Dict[str, Any], window_s: float) -> str:
+    """The nvshare-style baseline: apps take the GPU in
+    round-robin time slices of `window_s` seconds (a holder keeps it while no
+    other app has work) and their memory is demand-paged by the UVM model
+    (UvmSim through the C ABI: LRU, sequential evict-then-fetch, 2 MiB pages
+    with adjacent-page prefetch). Every kernel touches its app's whole
+    footprint, as the Nixie workload model assumes. Same app generators as the
+    workload engine (workload_sim.hpp:16-20); jitter draws from Python's
+    random seeded by (seed, app). Emits the workload trace's X and Q lines
+    plus `U faults faulted_bytes mirror_peak`."""
+    from ctypes import byref, c_double, c_uint64, c_void_p
+    import random
+    from ._lib import check, lib
+    hw = sc["hardware"]
+    gib = float(1 << 30)
+    h = c_void_p()
+    check(lib.nx_uvm_create(parse_size(hw["gpu"], "gpu"), hw["pcie_gbs"][0] * gib, hw["pcie_gbs"][1] * gib, 1,
+                            30e-6, 15, byref(h)))
+    try:
+        apps = sorted(sc["apps"], key=lambda a: int(a["id"]))
+        st = {}
+        for a in apps:
+            check(lib.nx_uvm_register(h, int(a["id"]), parse_size(a["size"], "size")))
+            st[a["id"]] = {"rng": random.Random(int(sc["seed"]) * 1000003 + int(a["id"])), "next": float(a["start"]),
+                           "queue": [], "done": 0, "first": None, "n": 0}
+        horizon = float(sc["horizon"])
+        out: List[str] = []
+        dur = c_double()
+
+        def arrive(a, t):  # interactive arrivals up to t join the queue
+            s_ = st[a["id"]]
+            while a["kind"] == "interactive" and s_["next"] <= t:
+                s_["queue"].append(s_["next"])
+                j = float(a["jitter"])
+                s_["next"] += float(a["interval"]) * (1 + (s_["rng"].uniform(-j, j) if j else 0.0))
+
+        def has_work(a, t):
+            arrive(a, t)
+            return bool(st[a["id"]]["queue"]) if a["kind"] == "interactive" else t >= float(a["start"])
+
+        t, holder, slice_start, k = 0.0, None, 0.0, 0
+        while t < horizon:
+            order = apps if holder is None else apps[apps.index(holder) + 1:] + apps[:apps.index(holder) + 1]
+            want = [a for a in order if has_work(a, t)]
+            if holder is not None and holder in want and (t - slice_start < window_s or want == [holder]):
+                cur = holder
+            elif want:
+                cur = next(a for a in want if a is not holder) if any(a is not holder for a in want) else want[0]
+            else:  # idle until the next arrival or batch start
+                nxt = [st[a["id"]]["next"] if a["kind"] == "interactive" else float(a["start"]) for a in apps]
+                t = min(x for x in nxt if x > t) if any(x > t for x in nxt) else horizon
+                continue
+            if cur is not holder:
+                out.append(f"X {k} {t!r} {t!r} {t!r} {'-' if holder is None else int(holder['id'])} {int(cur['id'])}")
+                k += 1
+                holder, slice_start = cur, t
+            check(lib.nx_uvm_touch(h, int(cur["id"]), float(cur["kernel"]), t, byref(dur)))
+            t += dur.value
+            if cur["kind"] == "interactive":
+                s_ = st[cur["id"]]
+                s_["done"] += 1
+                if s_["first"] is None:
+                    s_["first"] = t
+                if s_["done"] == int(cur["burst"]) and t <= horizon:
+                    out.append(f"Q {int(cur['id'])} {s_['n']} {s_['queue'][0]!r} {s_['first']!r} {t!r}")
+                if s_["done"] == int(cur["burst"]):
+                    s_["queue"].pop(0)
+                    s_["n"] += 1
+                    s_["done"], s_["first"] = 0, None
+        f, fb, mp = c_uint64(), c_uint64(), c_uint64()
+        check(lib.nx_uvm_stats(h, byref(f), byref(fb), byref(mp)))
+        out.append(f"U {f.value} {fb.value} {mp.value}")
+        return "\n".join(out) + "\n"
+    finally:
+        lib.nx_uvm_destroy(h)
+
+
 def run_policy(sc: Dict[str, Any], policy: str, real: bool = False) -> Dict[str, Any]:
+    if policy.startswith("uvm_rr_"):
+        try:
+            w = float(policy[len("uvm_rr_"):])
+        except ValueError:
+            raise ScenarioError(f"policies: bad time slice in '{policy}'") from None
+        if w <= 0 or real:
+            raise ScenarioError(f"policies: '{policy}' needs a positive slice and runs on the model only")
+        trace = simulate_uvm_rr(sc, w)
+        u = [l.split() for l in trace.splitlines() if l.startswith("U ")][0]
+        return {"policy": policy, "mode": "model", **metrics(trace, sc),
+                "uvm": {"faults": int(u[1]), "faulted_bytes": int(u[2]), "pinned_mirror_peak_bytes": int(u[3])}}
     if policy not in POLICIES:
-        raise ScenarioError(f"policies: unknown policy '{policy}' (known: {', '.join(POLICIES)})")
+        raise ScenarioError(f"policies: unknown policy '{policy}' (known: {', '.join(POLICIES)}, uvm_rr_<seconds>)")
     prefetch = {"nixie": None, "nixie_prefetch": True, "nixie_noprefetch": False}[policy]
     spec = to_spec(sc, prefetch)
     from . import engine  # loads lib/libnixie_b200.so: no fallback

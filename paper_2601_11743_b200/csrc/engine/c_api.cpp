@@ -11,9 +11,11 @@
 #include <string>
 
 #include "nixie/scenario.hpp"
+#include "nixie/uvm.hpp"
 #include "nixie/workload.hpp"
 #include <nixie_workload/workload_sim.hpp>
 #include "nixie/swap_engine.hpp"
+#include "nixie/uvm.hpp"
 #include "nx_kernels.h"
 #include "phys.hpp"
 
@@ -795,6 +797,51 @@ int nx_workload_real(const char* spec, const nx_engine_config* cfg, uint64_t see
     *trace = dup_out(out, len);
   });
 }
+
+// ---- UVM model (include/nixie/uvm.hpp; reference proj/include/nixie/uvm.hpp) ----
+struct nx_uvm {
+  std::unique_ptr<UvmSim> sim;
+};
+
+int nx_uvm_create(uint64_t gpu_capacity, double pcie_up_bw, double pcie_down_bw, int half_duplex,
+                  double fault_latency, int prefetch_pages, nx_uvm** out) {
+  return guard([&] {
+    need(out, "out");
+    LinkConfig pcie{pcie_up_bw, pcie_down_bw, half_duplex ? Duplex::HalfDuplex : Duplex::FullDuplex};
+    UvmConfig cfg;
+    cfg.fault_latency = fault_latency;
+    cfg.prefetch_pages = prefetch_pages;
+    auto h = std::make_unique<nx_uvm>();
+    h->sim = std::make_unique<UvmSim>(gpu_capacity, pcie, cfg);
+    *out = h.release();
+  });
+}
+
+int nx_uvm_register(nx_uvm* h, uint32_t app, uint64_t size) {
+  return guard([&] {
+    need(h, "uvm");
+    h->sim->register_alloc(app, size);
+  });
+}
+
+int nx_uvm_touch(nx_uvm* h, uint32_t app, double base_duration, double now, double* duration) {
+  return guard([&] {
+    need(h, "uvm");
+    need(duration, "duration");
+    *duration = h->sim->touch_kernel(app, h->sim->chunks_of(app), base_duration, now);
+  });
+}
+
+int nx_uvm_stats(const nx_uvm* h, uint64_t* faults, uint64_t* faulted_bytes, uint64_t* mirror_peak) {
+  return guard([&] {
+    need(h, "uvm");
+    if (faults) *faults = h->sim->fault_count();
+    if (faulted_bytes) *faulted_bytes = h->sim->faulted_bytes_total();
+    if (mirror_peak) *mirror_peak = h->sim->pinned_mirror_peak();
+  });
+}
+
+void nx_uvm_destroy(nx_uvm* h) { delete h; }
 
 void nx_free(void* p) { std::free(p); }
 

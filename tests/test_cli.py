@@ -156,3 +156,34 @@ def test_real_run_matches_the_model_and_is_byte_exact(tmp_path):
     model = cli.run_policy(cli.load_scenario(path), "nixie")
     assert real["mode"] == "real" and real["byte_check_failures"] == 0
     assert {k: v for k, v in real.items() if k != "mode"} == {k: v for k, v in model.items() if k != "mode"}
+
+
+def test_uvm_round_robin_baselines():
+    """uvm_rr_<W>: nvshare-style time slices over the UVM demand-paging model
+    (PAPER.md:462). Deterministic; every oversubscribed slice faults; on
+    BASELINE config 3 the interactive app waits far longer than under Nixie
+    (the paper's comparison)."""
+    sc = cli.load_scenario(SCEN)
+    a, b = cli.run_policy(sc, "uvm_rr_4"), cli.run_policy(sc, "uvm_rr_4")
+    assert a == b
+    assert a["uvm"]["faults"] > 0 and a["uvm"]["faulted_bytes"] > 0 and a["uvm"]["pinned_mirror_peak_bytes"] > 0
+    assert a["context_switches"]["count"] > 0 and a["apps"]["0"]["requests"] > 0
+    nixie = cli.run_policy(sc, "nixie")
+    assert nixie["apps"]["0"]["request_latency"]["mean_ms"] < a["apps"]["0"]["request_latency"]["mean_ms"]
+    w30 = cli.run_policy(sc, "uvm_rr_30")
+    assert w30["context_switches"]["count"] < a["context_switches"]["count"]  # longer slices, fewer handoffs
+    for bad in ("uvm_rr_x", "uvm_rr_0", "uvm_rr_-1"):
+        with pytest.raises(cli.ScenarioError):
+            cli.run_policy(sc, bad)
+
+
+def test_uvm_fits_without_faults_after_first_touch(tmp_path):
+    """Two apps that fit the GPU together fault each page once (first touch)
+    and never again: faulted bytes equal the footprints."""
+    sc = cli.load_scenario(_write(tmp_path, {
+        "hardware": {"gpu": "1G"}, "horizon": 5.0,
+        "apps": [{"id": 0, "kind": "interactive", "size": "256M", "interval": 0.5, "burst": 2, "kernel": 0.01},
+                 {"id": 1, "kind": "interactive", "size": "256M", "start": 0.1, "interval": 0.5, "burst": 2,
+                  "kernel": 0.01}]}))
+    r = cli.run_policy(sc, "uvm_rr_4")
+    assert r["uvm"]["faulted_bytes"] == 512 << 20
