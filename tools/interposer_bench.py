@@ -29,8 +29,9 @@ def main():
     ap.add_argument("--think-ms", type=float, default=300)
     ap.add_argument("--host-check", type=int, default=0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--daemon-arg", action="append", default=[], help="extra nixied flag (repeatable)")
     a = ap.parse_args()
-    with Daemon(gpu=a.gpu, pinned=a.pinned, paged="96G", log=a.out) as d:
+    with Daemon(gpu=a.gpu, pinned=a.pinned, paged="96G", log=a.out, extra=a.daemon_arg) as d:
         cmds = [[VECAPP, "--mib", str(a.a_mib), "--buffers", "8", "--iters", str(a.iters), "--think-ms", str(a.think_ms),
                  "--seed", "7", "--name", "interactive", "--host-check", str(a.host_check)],
                 [VECAPP, "--mib", str(a.b_mib), "--buffers", "12", "--iters", str(a.iters), "--think-ms", str(a.think_ms),
