@@ -278,12 +278,17 @@ def interposer_c2(timeout_s: float = 240.0) -> dict:
     CUDA programs (16 + 24 GiB vecapps) under nixied + LD_PRELOAD shim on the
     32 GiB budget (tools/interposer_bench.py). Steady switches exchange 8 GiB
     each way; GB/s = both directions' bytes over the daemon's copy time."""
-    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "interposer_bench.py"), "--iters", "10"],
-                       capture_output=True, text=True, timeout=timeout_s)
-    try:
-        d = json.loads(p.stdout.strip().splitlines()[-1])
-    except (ValueError, IndexError):
-        return {"error": (p.stderr or p.stdout)[-300:]}
+    for attempt in range(2):
+        p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "interposer_bench.py"), "--iters", "10"],
+                           capture_output=True, text=True, timeout=timeout_s)
+        try:
+            d = json.loads(p.stdout.strip().splitlines()[-1])
+        except (ValueError, IndexError):
+            return {"error": (p.stderr or p.stdout)[-300:]}
+        # The scheduler decides when the apps alternate; a run where one app
+        # finished before the other started competing has no steady switches.
+        if (d.get("steady_switches") or 0) >= 3:
+            break
     return {"value": d.get("copy_bidir_gbps_median"), "unit": "GB/s", "switch_ms": d.get("switch_total_ms"),
             "grant_ms_median": d.get("grant_ms_median"), "steady_switches": d.get("steady_switches"),
             "verified": d.get("verified"), "mismatches": d.get("mismatches"), "apps_ok": d.get("apps_ok"),
