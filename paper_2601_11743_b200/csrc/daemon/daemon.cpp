@@ -4,9 +4,10 @@
 //
 // One daemon per GPU. It owns:
 //   * the allocation registry (MemState, proj/src/mem_model.cpp) and the GPU
-//     tier as ONE exportable VMM allocation (csrc/engine/vmm.hpp); every
-//     application's shim imports it and maps 2 MiB frames under the stable
-//     virtual range it reserved at cudaMalloc time;
+//     tier as a row of exportable VMM slabs (csrc/engine/vmm.hpp); each
+//     application's shim imports the slabs it is handed and maps them under
+//     the stable virtual range it reserved, one physical slab
+//     per virtual slab that holds resident blocks (SlabPlacer);
 //   * the MLFQ scheduler (proj/src/mlfq.cpp) fed from the shims' control
 //     pages (launch counts, blocking calls: PAPER.md §6.1);
 //   * the swap engine (csrc/engine/engine.cpp): a context switch is
@@ -17,12 +18,16 @@
 //   Pause(incumbent)   its shim clears the execution flag, waits for
 //                      launches in progress, synchronises its context,
 //                      acks Drained
-//   plan_switch        victim order = the scheduler's hint
-//   Unmap(victims)     owners of evicted blocks drop those mappings (acked
-//                      before any frame is handed to another application)
-//   execute            the swap engine: evictions and fetches at once
-//   Grant(incoming)    frame list for every chunk; the shim maps what moved,
+//   plan_switch        victim order = the scheduler's hint; victim blocks
+//                      slab by slab (SlabPlacer::slab_victims)
+//   execute            the swap engine: evictions and fetches at once; slabs
+//                      newly assigned to the incoming app are mapped in its
+//                      shim while the copies run (Map, from the progress hook)
+//   Grant(incoming)    the remaining mapping changes; the shim applies them,
 //                      sets the execution flag, acks Granted
+//   after the grant    victims unmap the slabs they lost, unless stale
+//                      mappings are kept (two apps, or --keep-stale-maps);
+//                      grown slabs beyond the slack are dropped
 // The daemon loop is single-threaded: every decision and
 // registry mutation happens here, in arrival order.
 #include <fcntl.h>

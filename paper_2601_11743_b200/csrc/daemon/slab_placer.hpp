@@ -1,5 +1,5 @@
 // SlabPlacer: GPU frame placement of the interposer daemon (internal header,
-// unit-tested by tests/cpp/test_slab_placer.cpp).
+// unit-tested by tests/cpp/test_units.cpp).
 #pragma once
 
 #include <cstdint>
