@@ -4,6 +4,7 @@
     python -m paper_2601_11743_b200.cli compare --scenario s.json --policies nixie,nixie_prefetch,uvm_rr_4,uvm_rr_30
     python -m paper_2601_11743_b200.cli sweep --scenario s.json --sweep pinned=16G,24G,32G
     python -m paper_2601_11743_b200.cli validate --scenario s.json
+    (run / compare / sweep also take --seed, --real and --log transfers|sched|faults)
 
 The reference ships this module as a spec only. A scenario is a JSON file
 (schema below). It is translated into the workload engine's text grammar
@@ -361,7 +362,23 @@ def simulate_uvm_rr(sc: Dict[str, Any], window_s: float) -> str:
         lib.nx_uvm_destroy(h)
 
 
-def run_policy(sc: Dict[str, Any], policy: str, real: bool = False) -> Dict[str, Any]:
+LOG_KINDS = {  # --log: trace lines kept in the report (workload_sim.hpp / scenario.hpp trace formats)
+    "transfers": ("S", "P", "L", "R", "H", "h"),  # switch headers, plans, per-lane legs, residency, prefetch
+    "sched": ("X", "E", "G", "Q"),                 # switches, scheduler log rows, requests
+    "faults": ("U",),                              # UVM policies: fault count, faulted bytes, mirror peak
+}
+
+
+def _with_log(run: Dict[str, Any], trace: str, log: Optional[str]) -> Dict[str, Any]:
+    if log:
+        keep = LOG_KINDS[log]
+        run["log"] = [l for l in trace.splitlines() if l.split(" ", 1)[0] in keep]
+    return run
+
+
+def run_policy(sc: Dict[str, Any], policy: str, real: bool = False, log: Optional[str] = None) -> Dict[str, Any]:
+    if log is not None and log not in LOG_KINDS:
+        raise ScenarioError(f"--log: expected one of {', '.join(LOG_KINDS)}, got {log!r}")
     if policy.startswith("uvm_rr_"):
         try:
             w = float(policy[len("uvm_rr_"):])
@@ -371,15 +388,16 @@ def run_policy(sc: Dict[str, Any], policy: str, real: bool = False) -> Dict[str,
             raise ScenarioError(f"policies: '{policy}' needs a positive slice and runs on the model only")
         trace = simulate_uvm_rr(sc, w)
         u = [l.split() for l in trace.splitlines() if l.startswith("U ")][0]
-        return {"policy": policy, "mode": "model", **metrics(trace, sc),
-                "uvm": {"faults": int(u[1]), "faulted_bytes": int(u[2]), "pinned_mirror_peak_bytes": int(u[3])}}
+        return _with_log({"policy": policy, "mode": "model", **metrics(trace, sc),
+                          "uvm": {"faults": int(u[1]), "faulted_bytes": int(u[2]), "pinned_mirror_peak_bytes": int(u[3])}},
+                         trace, log)
     if policy not in POLICIES:
         raise ScenarioError(f"policies: unknown policy '{policy}' (known: {', '.join(POLICIES)}, uvm_rr_<seconds>)")
     prefetch = {"nixie": None, "nixie_prefetch": True, "nixie_noprefetch": False}[policy]
     spec = to_spec(sc, prefetch)
     from . import engine  # loads lib/libnixie_b200.so: no fallback
     trace = engine.run_workload_real(spec) if real else engine.run_workload_model(spec)
-    return {"policy": policy, "mode": "real" if real else "model", **metrics(trace, sc)}
+    return _with_log({"policy": policy, "mode": "real" if real else "model", **metrics(trace, sc)}, trace, log)
 
 
 def report(sc: Dict[str, Any], runs: List[Dict[str, Any]], **extra) -> Dict[str, Any]:
@@ -461,6 +479,7 @@ def main(argv: Optional[List[str]] = None) -> int:
             p.add_argument("--out")
             p.add_argument("--format", default="json")
             p.add_argument("--real", action="store_true", help="move the bytes on the GPU (CUDA engine)")
+            p.add_argument("--log", choices=sorted(LOG_KINDS), help="keep these trace lines in each run")
         if name == "compare":
             p.add_argument("--policies", default="nixie,nixie_prefetch")
         if name == "sweep":
@@ -477,16 +496,16 @@ def main(argv: Optional[List[str]] = None) -> int:
             print(json.dumps(sc, sort_keys=True, indent=2))
             return 0
         if a.cmd == "run":
-            rep = report(sc, [run_policy(sc, "nixie", a.real)])
+            rep = report(sc, [run_policy(sc, "nixie", a.real, a.log)])
         elif a.cmd == "compare":
-            rep = report(sc, [run_policy(sc, p.strip(), a.real) for p in a.policies.split(",") if p.strip()])
+            rep = report(sc, [run_policy(sc, p.strip(), a.real, a.log) for p in a.policies.split(",") if p.strip()])
         else:
             param, _, values = a.sweep.partition("=")
             if not values:
                 raise ScenarioError("--sweep: expected param=v1,v2,...")
             runs = []
             for v in values.split(","):
-                r = run_policy(_set_path(sc, param, v), a.policy, a.real)
+                r = run_policy(_set_path(sc, param, v), a.policy, a.real, a.log)
                 r["label"] = f"{param}={v}"
                 runs.append(r)
             rep = report(sc, runs, sweep={"parameter": param, "values": values.split(",")})

@@ -187,3 +187,14 @@ def test_uvm_fits_without_faults_after_first_touch(tmp_path):
                   "kernel": 0.01}]}))
     r = cli.run_policy(sc, "uvm_rr_4")
     assert r["uvm"]["faulted_bytes"] == 512 << 20
+
+
+def test_log_keeps_the_requested_trace_lines(tmp_path):
+    path = _write(tmp_path, SMALL)
+    rep = json.loads(_cli("run", "--scenario", path, "--log", "sched").stdout)
+    log = rep["runs"][0]["log"]
+    assert log and {l.split()[0] for l in log} <= {"X", "E", "G", "Q"}
+    assert sum(1 for l in log if l.startswith("X ")) == rep["runs"][0]["context_switches"]["count"]
+    rep = json.loads(_cli("compare", "--scenario", path, "--policies", "nixie,uvm_rr_1", "--log", "transfers").stdout)
+    assert {l.split()[0] for l in rep["runs"][0]["log"]} >= {"S", "P", "L"} and rep["runs"][1]["log"] == []
+    assert _cli("run", "--scenario", path, "--log", "everything").returncode != 0
