@@ -12,6 +12,8 @@ configs = [dict(first_batch_legs=8, legs_per_launch=128, pcie_legs_in_flight=512
            dict(first_batch_legs=16, legs_per_launch=64, pcie_legs_in_flight=1024),
            dict(first_batch_legs=32, legs_per_launch=128, pcie_legs_in_flight=1024),
            dict(first_batch_legs=16, legs_per_launch=128, pcie_legs_in_flight=2048)]
+if len(sys.argv) > 1:  # a JSON list of configs replaces the default set
+    configs = json.loads(sys.argv[1])
 res = {i: [] for i in range(len(configs))}
 engines = []
 for rnd in range(4):
