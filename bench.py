@@ -290,6 +290,7 @@ def interposer_c2(timeout_s: float = 240.0) -> dict:
         if (d.get("steady_switches") or 0) >= 3:
             break
     return {"value": d.get("copy_bidir_gbps_median"), "unit": "GB/s", "switch_ms": d.get("switch_total_ms"),
+            "warmup_switch_ms": d.get("warmup_switch_ms"),
             "grant_ms_median": d.get("grant_ms_median"), "steady_switches": d.get("steady_switches"),
             "verified": d.get("verified"), "mismatches": d.get("mismatches"), "apps_ok": d.get("apps_ok"),
             "apps": "2 unmodified CUDA programs (tests/apps/vecapp.cu) under lib/nixied + LD_PRELOAD lib/libnixie_shim.so"}
