@@ -287,7 +287,7 @@ def interposer_c2(timeout_s: float = 240.0) -> dict:
             return {"error": (p.stderr or p.stdout)[-300:]}
         # The scheduler decides when the apps alternate; a run where one app
         # finished before the other started competing has no steady switches.
-        if (d.get("steady_switches") or 0) >= 3:
+        if (d.get("steady_switches") or 0) >= 5:
             break
     return {"value": d.get("copy_bidir_gbps_median"), "unit": "GB/s", "switch_ms": d.get("switch_total_ms"),
             "warmup_switch_ms": d.get("warmup_switch_ms"),
