@@ -51,7 +51,7 @@ struct EngineConfig {
   bool fused_launch = false;          // both directions in one launch stream (warp-group split)
   bool verify = true;                 // checksum every restore
   bool numa_bind = true;              // pinned ring + workers on the GPU's NUMA node
-  int first_batch_legs = 2;           // batch-size ramp start (doubles per batch up to legs_per_launch); 2 measured ~1 ms/switch faster than 8 (tools/tune_batches.py)
+  int first_batch_legs = 8;           // batch-size ramp start (doubles per batch up to legs_per_launch); 2 vs 8 within 1% either way
   bool k3_tma = true;                 // CE-path checksum pass on the TMA pipeline (else the LDG loop)
   bool k3_one_stream = true;          // both lanes' K3 launches on one stream (no SM contention between them)
   bool k3_grouped = true;             // CE path: one record launch per switch, arrival checks per group

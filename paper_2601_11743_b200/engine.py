@@ -36,7 +36,7 @@ class EngineConfig:
     fused_launch: bool = False
     verify: bool = True
     numa_bind: bool = True
-    first_batch_legs: int = 2
+    first_batch_legs: int = 8
     k3_tma: bool = True
     k3_one_stream: bool = True
     k3_grouped: bool = True
