@@ -115,6 +115,18 @@ struct K3Launch {
   int lane;  // 0 = arrivals (verify), 1 = departures (record)
 };
 
+// One PCIe batch of the last execute: device times (s, from the switch start)
+// of its start, of the end of its copies, and of its end (checks included);
+// host times (s, from the execute() call) of its submission and of the poll
+// that saw it end. The per-switch timeline (tools/timeline.py).
+struct BatchTrace {
+  int stream;  // 0 = H2D, 1 = D2H
+  int legs;
+  bool ce;
+  double start_s, copied_s, end_s;
+  double host_submit_s, host_done_s;
+};
+
 struct LegTrace {
   BlockId block;
   TierId src, dst;
@@ -186,6 +198,7 @@ class SwapEngine {
   const std::array<std::vector<LegTrace>, 6>& lane_trace() const;  // per lane, start order, last execute
   std::uint64_t total_launches() const;  // kernels this engine has launched (all kinds)
   const std::vector<K3Launch>& k3_launches() const;  // last execute
+  const std::vector<BatchTrace>& batch_trace() const;  // last execute
 
   // Device pointer of the frame holding a GPU-resident block; device table
   // of frame pointers indexed by BlockId (0 when not on the GPU), refreshed

@@ -172,6 +172,20 @@ uint64_t nx_total_launches(nx_engine* e);
 /* K3 checksum launches of the last switch: device start/end (s, from the
  * switch start), legs per launch, lane (0 arrivals, 1 departures). */
 int nx_k3_trace(nx_engine* e, double* start_s, double* end_s, int* legs, int* lane, size_t cap, size_t* n);
+/* PCIe batches of the last switch, in landing order (the switch timeline;
+ * the reference's per-leg TransferRecord log, transfer.hpp:40-47, at batch
+ * granularity): device times (s, from the switch start) of the batch start,
+ * copy end and end (checks included), and host times of its submission and
+ * of the poll that committed it. */
+typedef struct {
+  int32_t stream; /* 0 = H2D, 1 = D2H */
+  int32_t legs;
+  int32_t ce;     /* 1 = copy engines, 0 = K1 */
+  int32_t pad;
+  double start_s, copied_s, end_s;
+  double host_submit_s, host_done_s;
+} nx_batch_record;
+int nx_batch_trace(nx_engine* e, nx_batch_record* out, size_t cap, size_t* n);
 /* cudaStream_t of a PCIe lane: 0 = H2D, 1 = D2H. */
 void* nx_lane_stream(nx_engine* e, int lane);
 

@@ -85,6 +85,11 @@ class PcieProbeC(Structure):
                 ("numa_node", c_int)]
 
 
+class BatchRecordC(Structure):
+    _fields_ = [("stream", c_int), ("legs", c_int), ("ce", c_int), ("pad", c_int), ("start_s", c_double),
+                ("copied_s", c_double), ("end_s", c_double), ("host_submit_s", c_double), ("host_done_s", c_double)]
+
+
 class MlfqConfigC(Structure):
     _fields_ = [("levels", c_int), ("base_allotment", c_double), ("base_preemption", c_double),
                 ("idle_threshold", c_double), ("tick", c_double)]
@@ -122,6 +127,7 @@ _SIGNATURES = [
     ("nx_total_launches", c_uint64, [c_void_p]),
     ("nx_k3_trace", c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_int), POINTER(c_int), c_size_t,
                             POINTER(c_size_t)]),
+    ("nx_batch_trace", c_int, [c_void_p, POINTER(BatchRecordC), c_size_t, POINTER(c_size_t)]),
     ("nx_lane_stream", c_void_p, [c_void_p, c_int]),
     ("nx_probe_pcie", c_int, [c_void_p, c_uint64, c_uint64, POINTER(PcieProbeC)]),
     ("nx_probe_copy_variant", c_int, [c_void_p, c_int, c_uint64, c_int, POINTER(c_double)]),

@@ -406,6 +406,16 @@ int nx_k3_trace(nx_engine* e, double* start_s, double* end_s, int* legs, int* la
     if (n) *n = t.size();
   });
 }
+int nx_batch_trace(nx_engine* e, nx_batch_record* out, size_t cap, size_t* n) {
+  return guard([&] {
+    need(e, "engine");
+    const auto& t = e->eng->batch_trace();
+    for (size_t i = 0; i < t.size() && i < cap && out; ++i)
+      out[i] = nx_batch_record{t[i].stream, t[i].legs, t[i].ce ? 1 : 0, 0, t[i].start_s, t[i].copied_s, t[i].end_s,
+                               t[i].host_submit_s, t[i].host_done_s};
+    if (n) *n = t.size();
+  });
+}
 void* nx_lane_stream(nx_engine* e, int lane) { return e ? static_cast<void*>(e->eng->stream(lane)) : nullptr; }
 
 int nx_probe_pcie(nx_engine* e, uint64_t bytes, uint64_t chunk, nx_pcie_probe* out) {

@@ -101,6 +101,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
   struct Batch {
     std::vector<std::uint32_t> legs;
     cudaEvent_t ev_start, ev_end;
+    cudaEvent_t ev_copied = nullptr;  // CE batch: its copies landed
+    double host_submit = 0, host_done = 0;
     int stream;
     bool ce;
     bool end_on_side = false;                        // CE batch: ends on the checksum side stream
@@ -134,6 +136,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   cudaEvent_t rec_head = nullptr, rec_all = nullptr;
   cudaEvent_t vgroup_copied = nullptr;
   std::vector<K3Launch> k3_trace;     // last execute's K3 launches (device times)
+  std::vector<BatchTrace> batch_tr;   // last execute's PCIe batches (timeline)
   std::uint32_t k3_slots_used = 0;    // device-clock slots handed out this execute
 
   // Capacity for `n` table legs this execute (grown before any work is queued).
@@ -569,6 +572,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
     B.ev_start = take_event();
     B.ev_end = take_event();
     B.ce = !use_sm_kernel(static_cast<int>(B.legs.size()));
+    B.host_submit = secs_since(t0);
     const std::uint32_t flags = cfg.verify ? kNxVerify : 0u;
     NX_CUDA(cudaEventRecord(B.ev_start, st[s]));
     if (!B.ce) {
@@ -601,6 +605,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
       copy_runs(h2d, s, cudaMemcpyHostToDevice);
       cudaEvent_t copied = take_event();
       NX_CUDA(cudaEventRecord(copied, st[s]));
+      B.ev_copied = copied;
       const bool group_check = grouped && !h2d.empty() && d2h.empty();
       const bool record_covered = grouped && h2d.empty();  // departures only: ends on the copy stream
       if (group_check) {
@@ -746,6 +751,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
         NX_CUDA(e);
         Batch B = std::move(inflight[s].front());
         inflight[s].pop_front();
+        B.host_done = secs_since(t0);
         for (auto i : B.legs) complete(i);
         landed.push_back(std::move(B));
         progress = true;
@@ -961,11 +967,15 @@ struct SwapEngine::Impl final : detail::LaneSink {
     double first = 1e30, last = 0;
     std::vector<std::pair<double, double>> k3_spans;
     k3_trace.clear();
+    batch_tr.clear();
     for (const Batch& B : landed) {
-      float a = 0, b = 0;
+      float a = 0, b = 0, c = 0;
       NX_CUDA(cudaEventElapsedTime(&a, ev0, B.ev_start));
       NX_CUDA(cudaEventElapsedTime(&b, ev0, B.ev_end));
+      if (B.ev_copied != nullptr) NX_CUDA(cudaEventElapsedTime(&c, ev0, B.ev_copied));
       const double s0 = a * 1e-3, s1 = b * 1e-3;
+      batch_tr.push_back(BatchTrace{B.stream, static_cast<int>(B.legs.size()), B.ce, s0,
+                                    B.ev_copied != nullptr ? c * 1e-3 : s1, s1, B.host_submit, B.host_done});
       first = std::min(first, s0);
       last = std::max(last, s1);
       stats.kernel_s[B.stream] += s1 - s0;
@@ -1084,6 +1094,7 @@ const SwitchStats& SwapEngine::last_stats() const { return impl_->stats; }
 const std::array<std::vector<LegTrace>, 6>& SwapEngine::lane_trace() const { return impl_->trace; }
 std::uint64_t SwapEngine::total_launches() const { return impl_->launches_total; }
 const std::vector<K3Launch>& SwapEngine::k3_launches() const { return impl_->k3_trace; }
+const std::vector<BatchTrace>& SwapEngine::batch_trace() const { return impl_->batch_tr; }
 
 void* SwapEngine::frame_of(BlockId b) const {
   const Location& loc = impl_->mem.block(b).loc;

@@ -215,6 +215,15 @@ class SwapEngine:
         check(lib.nx_k3_trace(self._h, a, z, g, l, n.value, byref(n)))
         return [(a[i], z[i], g[i], l[i]) for i in range(n.value)]
 
+    def batch_trace(self) -> List[Dict]:
+        """The last switch's PCIe batches (device and host times, s)."""
+        n = c_size_t()
+        check(lib.nx_batch_trace(self._h, None, 0, byref(n)))
+        arr = (L.BatchRecordC * max(1, n.value))()
+        check(lib.nx_batch_trace(self._h, arr, n.value, byref(n)))
+        keys = ("stream", "legs", "ce", "start_s", "copied_s", "end_s", "host_submit_s", "host_done_s")
+        return [{k: getattr(arr[i], k) for k in keys} for i in range(n.value)]
+
     def lane_stream(self, lane: int) -> int:
         return lib.nx_lane_stream(self._h, lane) or 0
 

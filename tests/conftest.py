@@ -13,6 +13,21 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
 
 
+# Parity gates first, deployment-path tests last: under `pytest -x` a flaky
+# interposer test (real processes, wall-clock think times) must never stop
+# the run before the engine and full-size parity tests have run.
+_FILE_ORDER = ["test_oracle_pinned", "test_dropin", "test_parity_model", "test_parity_workload", "test_abi",
+               "test_gpu_engine", "test_gpu_scale", "test_gpu_workload", "test_gpu_uvm", "test_cli",
+               "test_multirank", "test_interposer_host", "test_gpu_daemon_parity", "test_gpu_interposer"]
+
+
+def pytest_collection_modifyitems(session, config, items):
+    def rank(item):
+        mod = os.path.splitext(os.path.basename(str(item.fspath)))[0]
+        return _FILE_ORDER.index(mod) if mod in _FILE_ORDER else len(_FILE_ORDER)
+    items.sort(key=rank)  # stable: file-internal order is kept
+
+
 @pytest.fixture(scope="session")
 def oracle_lib():
     """C restatement of the byte-level functions (oracle/swap_oracle.c)."""
