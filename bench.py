@@ -74,6 +74,13 @@ class Dist:
         self.td.all_reduce(t, op=self.td.ReduceOp.MAX if op == "max" else self.td.ReduceOp.SUM)
         return float(t.item())
 
+    def gather(self, obj) -> list:
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.td.all_gather_object(out, obj)
+        return out
+
     def close(self):
         if self.world > 1:
             self.td.destroy_process_group()
@@ -133,6 +140,101 @@ def pcie_link(device: int) -> dict:
         return {"gpu": name, "gen": int(g), "gen_max": int(gm), "width": int(w), "width_max": int(wm)}
     except Exception as e:  # noqa: BLE001
         return {"error": str(e)[:80]}
+
+
+class PcieCounters:
+    """The GPU's own PCIe byte counters (NVML field values
+    NVML_FI_DEV_PCIE_COUNT_TX_BYTES / RX_BYTES, cumulative), read around the
+    timed region: a counter-level reading of what the copy engines moved,
+    which ncu cannot see (it profiles kernels, not DMA). TX = GPU -> host
+    (evictions plus the read requests of fetches), RX = host -> GPU."""
+
+    def __init__(self, pci_bus_id: str):
+        self.h = None
+        self.err = None
+        try:
+            import pynvml
+            self.nv = pynvml
+            pynvml.nvmlInit()
+            bus = pci_bus_id.upper()
+            for cand in (bus, "0000" + bus if len(bus) == 12 else bus, bus[4:] if len(bus) == 16 else bus):
+                try:
+                    self.h = pynvml.nvmlDeviceGetHandleByPciBusId(cand)
+                    break
+                except Exception:  # noqa: BLE001
+                    continue
+            if self.h is None:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(0)
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)[:120]
+
+    def read(self):
+        if self.h is None:
+            return None
+        nv = self.nv
+        try:
+            ids = [nv.NVML_FI_DEV_PCIE_COUNT_TX_BYTES, nv.NVML_FI_DEV_PCIE_COUNT_RX_BYTES, nv.NVML_FI_DEV_PCIE_REPLAY_COUNTER]
+            vals = nv.nvmlDeviceGetFieldValues(self.h, ids)
+            out = []
+            for v in vals:
+                if v.nvmlReturn != 0:
+                    return None
+                out.append(int(v.value.ullVal))
+            return out
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)[:120]
+            return None
+
+    @staticmethod
+    def delta(a, b, seconds: float, alg_in: float, alg_out: float) -> dict:
+        if a is None or b is None:
+            return {"available": False}
+        tx, rx, rep = b[0] - a[0], b[1] - a[1], b[2] - a[2]
+        return {"available": True, "source": "NVML_FI_DEV_PCIE_COUNT_TX_BYTES/RX_BYTES (cumulative, per GPU)",
+                "tx_bytes": tx, "rx_bytes": rx, "replays": rep,
+                "tx_gbs": tx / seconds / 1e9, "rx_gbs": rx / seconds / 1e9,
+                "rx_per_algorithmic_h2d_byte": rx / alg_in if alg_in else None,
+                "tx_per_algorithmic_d2h_byte": tx / alg_out if alg_out else None}
+
+
+def link_reference(device: int, bus_id: str, link: dict) -> dict:
+    """An independent ceiling beside the same-run probe: the link's raw rate
+    from its generation and width, and the TLP-payload bound from the max
+    payload size (lspci); nvbandwidth when installed."""
+    gt = {1: 2.5, 2: 5.0, 3: 8.0, 4: 16.0, 5: 32.0, 6: 64.0}.get(link.get("gen", 0), 0.0)
+    enc = 0.8 if link.get("gen", 0) <= 2 else (242 / 256 if link.get("gen", 0) >= 6 else 128 / 130)
+    raw = gt * link.get("width", 0) * enc / 8.0
+    out = {"raw_gbs_per_direction": raw, "gen": link.get("gen"), "width": link.get("width")}
+    try:
+        txt = subprocess.run(["lspci", "-vvv", "-s", bus_id], capture_output=True, text=True, timeout=10).stdout
+        import re
+        m = re.search(r"DevCtl:.*?MaxPayload (\d+) bytes, MaxReadReq (\d+) bytes", txt, re.S)
+        if m:
+            mps, mrrs = int(m.group(1)), int(m.group(2))
+            # per TLP: 4 B framing + 2 B sequence + 16 B header (64-bit address) + 4 B LCRC
+            out.update(max_payload=mps, max_read_request=mrrs, tlp_payload_bound_gbs_per_direction=raw * mps / (mps + 26))
+    except (OSError, subprocess.SubprocessError):
+        pass
+    import shutil
+    out["nvbandwidth"] = "present" if shutil.which("nvbandwidth") else "absent from the image"
+    return out
+
+
+def topo_matrix() -> list:
+    try:
+        return subprocess.run(["nvidia-smi", "topo", "-m"], capture_output=True, text=True, timeout=20).stdout.strip().splitlines()
+    except (OSError, subprocess.SubprocessError):
+        return []
+
+
+def pct(vals, q):
+    s = sorted(vals)
+    if not s:
+        return None
+    k = (len(s) - 1) * q
+    lo = int(k)
+    hi = min(lo + 1, len(s) - 1)
+    return s[lo] + (s[hi] - s[lo]) * (k - lo)
 
 
 def settle_host_link(eng, limit_s: float = 30.0) -> dict:
@@ -248,8 +350,10 @@ def run_reference(args, dist: Dist):
 # ---------------------------------------------------------------------------------------------
 # Product arm
 # ---------------------------------------------------------------------------------------------
-def x16_exchange(path: int, switches: int = 4) -> dict:
-    """North-star latency case: 16 GiB <-> 16 GiB exchange at a 16 GiB cap."""
+def x16_exchange(path: int, probe: dict, switches: int = 20) -> dict:
+    """North-star latency case: 16 GiB <-> 16 GiB exchange at a 16 GiB cap,
+    `switches` times. Ideal = max(bytes / H2D-while-bidirectional, bytes /
+    D2H-while-bidirectional) from the same-run probe."""
     from paper_2601_11743_b200 import PlannerConfig, SwapEngine
     from paper_2601_11743_b200._lib import TIER_GPU, TIER_PINNED
     e = SwapEngine(gpu_capacity=16 * GIB, pinned_capacity=34 * GIB, paged_capacity=2 * GIB, path=path)
@@ -269,8 +373,34 @@ def x16_exchange(path: int, switches: int = 4) -> dict:
         bad = e.verify_pattern(0, 1) + e.verify_pattern(1, 1)
     finally:
         e.close()
-    return {"bytes_each_way": 16 * GIB, "latency_s": [round(x, 4) for x in lat], "device_span_s": [round(x, 4) for x in dev],
-            "byte_exact": bad == 0}
+    ideal = max(16 * GIB / (probe["ce_bidir_h2d"] * 1e9), 16 * GIB / (probe["ce_bidir_d2h"] * 1e9))
+    return {"bytes_each_way": 16 * GIB, "n": len(lat), "ideal_s": ideal,
+            "p50_s": pct(lat, 0.5), "p99_s": pct(lat, 0.99), "max_s": max(lat),
+            "p50_over_ideal": pct(lat, 0.5) / ideal, "p99_over_ideal": pct(lat, 0.99) / ideal, "target_over_ideal": 1.2,
+            "device_span_p50_s": pct(dev, 0.5), "latency_s": [round(x, 4) for x in lat], "byte_exact": bad == 0}
+
+
+def uvm_comparator(x16: dict | None, rounds: int = 2) -> dict:
+    """The UVM comparator on the same exchange (reference
+    claim Nixie/UVM ~2x): two 16 GiB
+    cudaMallocManaged working sets round-robin on 17 GiB of usable device
+    memory (tests/apps/uvm_rr.cu), fault-driven. Switch cost = kernel time
+    with the other app resident minus the resident kernel time."""
+    exe = os.path.join(ROOT, "paper_2601_11743_b200", "lib", "nx_uvm_rr")
+    p = subprocess.run([exe, "--cap-gib", "17", "--ws-gib", "16", "--rounds", str(rounds), "--prefetch", "0"],
+                       capture_output=True, text=True, timeout=600)
+    try:
+        d = json.loads(p.stdout.strip().splitlines()[-1])
+    except (ValueError, IndexError):
+        return {"error": (p.stderr or p.stdout)[-300:]}
+    out = {"what": "cudaMallocManaged round-robin, 16 GiB <-> 16 GiB, demand faults (tests/apps/uvm_rr.cu)",
+           "switch_ms_median": d["median_ms"], "switch_ms": d["switch_cost_ms"], "byte_exact": d.get("mismatches") == 0,
+           "host_peak_rss_bytes": d.get("host_peak_rss_bytes")}
+    if x16 and x16.get("p50_s"):
+        out["engine_switch_ms_p50"] = x16["p50_s"] * 1e3
+        out["engine_speedup"] = d["median_ms"] / (x16["p50_s"] * 1e3)
+        out["reference_claim"] = "~2x (SPEC.md:563, PAPER.md:313)"
+    return out
 
 
 def interposer_c2(timeout_s: float = 240.0) -> dict:
@@ -296,9 +426,27 @@ def interposer_c2(timeout_s: float = 240.0) -> dict:
             "apps": "2 unmodified CUDA programs (tests/apps/vecapp.cu) under lib/nixied + LD_PRELOAD lib/libnixie_shim.so"}
 
 
+def aggregate(ranks: list, steps: int) -> dict:
+    """Whole-job numbers from the per-rank records (rank 0, after a gather).
+    value: bytes of all ranks / device time, where the device time is the sum
+    over steps of the slowest rank's CUDA-event span of that step (at N > 1
+    every step starts on a barrier, so the ranks' switches overlap and the
+    per-step max is the concurrent time). window: bytes / the sum over steps
+    of (last rank's end - first rank's start) on the shared host clock, which
+    also counts host gaps. e2e: bytes / the slowest rank's wall time of the
+    timed public-API calls."""
+    total = sum(r["bytes"] for r in ranks)
+    dev = sum(max(r["spans"][i] for r in ranks) for i in range(steps))
+    window = sum(max(r["windows"][i][1] for r in ranks) - min(r["windows"][i][0] for r in ranks) for i in range(steps))
+    wall = max(r["wall_s"] for r in ranks)
+    return {"total_bytes": total, "dev_max_s": dev, "window_s": window, "wall_max_s": wall,
+            "value": total / dev / 1e9, "e2e": total / wall / 1e9,
+            "window_gbs": total / window / 1e9 if window > 0 else None, "bad": sum(r["bad"] for r in ranks)}
+
+
 def run_product(args, dist: Dist):
-    from paper_2601_11743_b200 import PlannerConfig, SwapEngine, load_scenario, parse_path
-    from paper_2601_11743_b200._lib import TIER_GPU, TIER_PINNED
+    from paper_2601_11743_b200 import PlannerConfig, SwapEngine, parse_path
+    from paper_2601_11743_b200._lib import TIER_GPU, TIER_PINNED, device_info
     from paper_2601_11743_b200 import cuda_device_count
     ndev = max(1, cuda_device_count())
     # One GPU per rank. With fewer visible GPUs than ranks (a functional check
@@ -309,6 +457,8 @@ def run_product(args, dist: Dist):
     peaks = measured_peaks()
     path = parse_path(args.path)
     check_host_memory(dist)
+    info = device_info(device)
+    counters = PcieCounters(info["pci_bus_id"])
     extra = {"legs_per_launch": args.legs_per_launch} if args.legs_per_launch else {}
     eng = SwapEngine(device=device, gpu_capacity=32 * GIB, pinned_capacity=16 * GIB, paged_capacity=2 * GIB, path=path, **extra)
     probe = eng.probe_pcie(1 * GIB, 64 * MIB)
@@ -339,40 +489,64 @@ def run_product(args, dist: Dist):
     sampler = ClockSampler(device)
     sampler.start()
     dist.barrier()
+    c0 = counters.read()
     t0 = time.perf_counter()
-    stats = [step() for _ in range(args.steps)]
+    stats, windows = [], []
+    for _ in range(args.steps):
+        if dist.world > 1:
+            dist.barrier()  # every rank switches at once: a common window per step
+        w0 = time.time()
+        stats.append(step())
+        windows.append((w0, time.time()))
     wall = time.perf_counter() - t0
+    c1 = counters.read()
     dist.barrier()
     clocks = sampler.stop()
     launches = eng.total_launches() - launches0
+    # Latency distribution: >= --latency-switches steady switches (the timed
+    # ones included), independent of --steps (p50/p99 over >= 100).
+    more = [step() for _ in range(max(0, args.latency_switches - args.steps))]
     probe_after = eng.probe_pcie(1 * GIB, 64 * MIB)
+    pinned_now, pinned_peak = eng.pinned_physical()
+    pinned_extra = eng.pinned_overhead()
     bad = eng.verify_pattern(0, seed) + eng.verify_pattern(1, seed)
     eng.audit()
     eng.close()
 
     bytes_rank = sum(s["bytes_in"] + s["bytes_out"] for s in stats)
     dev_rank = sum(s["device_span_s"] for s in stats)
-    lat = sorted(s["wall_s"] + s["plan_s"] for s in stats)
-    total_bytes = dist.reduce(bytes_rank, "sum")
-    dev_max = dist.reduce(dev_rank, "max")
-    wall_max = dist.reduce(wall, "max")
-    bad_all = dist.reduce(bad, "sum")
-    x16 = x16_exchange(path) if (args.x16 and dist.rank == 0) else None
+    lat = [(s["wall_s"] + s["plan_s"]) * 1e3 for s in stats + more]
+    dev_lat = [s["device_span_s"] * 1e3 for s in stats + more]
+    peak_rank = max(probe["ce_bidir_total"], probe["sm_bidir_total"], probe_after["ce_bidir_total"], probe_after["sm_bidir_total"])
+    rank_rec = {"rank": dist.rank, "device": device, **info, "gbs": bytes_rank / dev_rank / 1e9, "pcie_peak_gbs": peak_rank,
+                "pct_of_own_peak": bytes_rank / dev_rank / 1e9 / peak_rank * 100.0, "windows": windows,
+                "bytes": bytes_rank, "dev_s": dev_rank, "wall_s": wall, "bad": bad,
+                "spans": [s["device_span_s"] for s in stats]}
+    ranks = dist.gather(rank_rec)
+    x16 = x16_exchange(path, probe, args.x16_switches) if (args.x16 and dist.rank == 0) else None
     ip = None
     if args.interposer and args.gpus == 1 and dist.rank == 0:
         try:
             ip = interposer_c2()
         except Exception as e:  # noqa: BLE001  (reported, never fatal to the bench line)
             ip = {"error": str(e)[-300:]}
+    uvm = None
+    if args.uvm and dist.rank == 0 and args.gpus == 1:
+        try:
+            uvm = uvm_comparator(x16)
+        except Exception as e:  # noqa: BLE001
+            uvm = {"error": str(e)[-300:]}
     if dist.rank != 0:
         return 0
 
-    value = total_bytes / dev_max / 1e9
-    e2e = total_bytes / wall_max / 1e9
+    agg = aggregate(ranks, args.steps)
+    total_bytes, dev_max, wall_max, window = agg["total_bytes"], agg["dev_max_s"], agg["wall_max_s"], agg["window_s"]
+    bad_all = agg["bad"]
+    value = agg["value"]
+    e2e = agg["e2e"]
     # Denominator: the better of the probes right before and right after the
     # timed region (shared hosts: neighbours' DRAM/PCIe load moves both).
-    pcie_peak = max(probe["ce_bidir_total"], probe["sm_bidir_total"], probe_after["ce_bidir_total"],
-                    probe_after["sm_bidir_total"])
+    pcie_peak = peak_rank
     per_gpu = value / args.gpus
     k3_s = sum(s["k3_s"] for s in stats)
     k3_busy = sum(s["k3_busy_s"] for s in stats)
@@ -403,6 +577,7 @@ def run_product(args, dist: Dist):
                 "achieved_kernel_clock": k3_b / k3_kernel / 1e9 if k3_kernel else None,
                 "peak": hbm, "unit": "GB/s", "launches": k3_n, "bytes_per_launch": k3_b / max(1, k3_n),
                 "avg_launch_ms": k3_s / max(1, k3_n) * 1e3, "busy_ms_per_step": k3_busy / args.steps * 1e3,
+                "share_of_step": k3_busy / dev_rank if dev_rank else None,
                 # ncu --set full (profiles/ncu_summary.json): DRAM bytes per
                 # algorithmic byte of the K3 launches captured, scaled to this run's launches
                 "traffic": ratio * k3_b / max(1, k3_n) if ratio else None,
@@ -411,6 +586,10 @@ def run_product(args, dist: Dist):
     roof["frac"] = roof["achieved"] / roof["peak"] if roof["peak"] else None
     base = cpu_baseline(2)
     st0 = stats[0]
+    ideal_ms = max(st0["bytes_in"] / (probe["ce_bidir_h2d"] * 1e9), st0["bytes_out"] / (probe["ce_bidir_d2h"] * 1e9)) * 1e3
+    link = pcie_link(device)
+    alg_in = sum(s["bytes_in"] for s in stats)
+    alg_out = sum(s["bytes_out"] for s in stats)
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_max / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -420,14 +599,21 @@ def run_product(args, dist: Dist):
                    "l2": "inputs (8 GiB per direction per step) far exceed the 126 MB L2",
                    "parallelism": f"{args.gpus} independent per-GPU instances, no collectives"},
         "per_gpu_gbps": per_gpu, "pct_of_pcie_peak": per_gpu / pcie_peak * 100.0,
-        "switch_latency_ms": {"p50": statistics.median(lat) * 1e3, "p99": lat[min(len(lat) - 1, int(0.99 * len(lat)))] * 1e3,
-                              "min": lat[0] * 1e3, "max": lat[-1] * 1e3},
-        "ideal_latency_ms": max(st0["bytes_in"] / (probe["ce_bidir_h2d"] * 1e9), st0["bytes_out"] / (probe["ce_bidir_d2h"] * 1e9)) * 1e3,
-        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": sum(s["bytes_in"] for s in stats) / args.steps,
-                "d2h_bytes_per_step": sum(s["bytes_out"] for s in stats) / args.steps},
+        "switch_latency_ms": {"n": len(lat), "p50": pct(lat, 0.5), "p99": pct(lat, 0.99), "min": min(lat), "max": max(lat),
+                              "ideal": ideal_ms, "p50_over_ideal": pct(lat, 0.5) / ideal_ms,
+                              "p99_over_ideal": pct(lat, 0.99) / ideal_ms,
+                              "device_span_p50": pct(dev_lat, 0.5), "device_span_p99": pct(dev_lat, 0.99),
+                              "what": "host wall of the public call per steady switch (plan_switch + execute + commits + "
+                                      "status read-back); device span = first PCIe batch start .. last check end"},
+        "ideal_latency_ms": ideal_ms,
+        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": alg_in / args.steps,
+                "d2h_bytes_per_step": alg_out / args.steps},
         "roofline": roof,
         "link_roofline": {"bound": "pcie", "achieved": per_gpu, "peak": pcie_peak, "unit": "GB/s", "frac": per_gpu / pcie_peak,
-                          "link": pcie_link(device), "peak_source": "same-run probe, 1 GiB/direction, 64 MiB chunks, max(CE, SM)"},
+                          "link": link, "peak_source": "same-run probe, 1 GiB/direction, 64 MiB chunks, max(CE, SM), "
+                                                       "best of before/after the timed region"},
+        "link_reference": link_reference(device, info["pci_bus_id"], link),
+        "pcie_counters": {**PcieCounters.delta(c0, c1, wall, alg_in, alg_out), **({"error": counters.err} if counters.err else {})},
         "pcie_probe": {k: (round(v, 2) if isinstance(v, float) else v) for k, v in probe.items()},
         "pcie_probe_after": {k: round(probe_after[k], 2) for k in ("ce_bidir_total", "ce_bidir_h2d", "ce_bidir_d2h", "sm_bidir_total")},
         "settle": settle,
@@ -437,8 +623,18 @@ def run_product(args, dist: Dist):
         "clocks": clocks,
         "byte_exact": bad_all == 0,
         "verified_restores": sum(s["verified"] for s in stats),
+        "pinned": {"budget_bytes": 16 * GIB, "ring_bytes": 16 * GIB, "physical_peak_bytes": pinned_peak,
+                   "out_of_budget_bytes": pinned_extra,
+                   "out_of_budget_what": "128 MiB bounce buffer for pageable fills/compares (not on the swap path) + pinned "
+                                         "stages of the K3 leg table and the frame table; probes allocate and free their own"},
         "x16_exchange": x16,
+        "uvm": uvm,
         "interposer": ip,
+        "multi_gpu": {"ranks": [{k: v for k, v in r.items() if k not in ("windows", "spans")} for r in ranks],
+                      "concurrent_window_gbs": agg["window_gbs"],
+                      "concurrent_window_what": "sum of bytes over ranks / sum over steps of (last rank's end - first "
+                                                "rank's start), host clock, steps barrier-aligned at N > 1",
+                      "topo": topo_matrix() if args.gpus > 1 else None},
         "shared_device": shared_device,
     }
     print(json.dumps(line), flush=True)
@@ -453,6 +649,10 @@ def main():
     ap.add_argument("--impl", choices=["product", "reference"], default="product")
     ap.add_argument("--path", choices=["auto", "sm", "ce"], default="auto")
     ap.add_argument("--no-x16", dest="x16", action="store_false")
+    ap.add_argument("--x16-switches", type=int, default=20)
+    ap.add_argument("--latency-switches", type=int, default=100,
+                    help="steady switches sampled for p50/p99 (the timed ones included)")
+    ap.add_argument("--no-uvm", dest="uvm", action="store_false", help="skip the cudaMallocManaged comparator")
     ap.add_argument("--legs-per-launch", type=int, default=0, help="CE batch / K3 launch size (0: engine default)")
     ap.add_argument("--no-interposer", dest="interposer", action="store_false",
                     help="skip the config-2 run through nixied + the LD_PRELOAD shim")

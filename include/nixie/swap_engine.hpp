@@ -199,6 +199,9 @@ class SwapEngine {
   std::uint64_t total_launches() const;  // kernels this engine has launched (all kinds)
   const std::vector<K3Launch>& k3_launches() const;  // last execute
   const std::vector<BatchTrace>& batch_trace() const;  // last execute
+  // Pinned bytes held outside the budgeted staging ring (bounce buffer, leg
+  // and frame table stages).
+  Bytes pinned_overhead() const;
 
   // Device pointer of the frame holding a GPU-resident block; device table
   // of frame pointers indexed by BlockId (0 when not on the GPU), refreshed

@@ -131,6 +131,10 @@ int nx_audit(nx_engine* e);
 int nx_app_resident(nx_engine* e, uint32_t app, uint64_t out[4]);
 /* MemState::pinned_physical / pinned_physical_peak (mem_model.cpp:244-247, 270-272). */
 int nx_pinned_physical(nx_engine* e, uint64_t* now, uint64_t* peak);
+/* Pinned host memory the engine holds OUTSIDE the budgeted staging ring:
+ * the 128 MiB bounce buffer for pageable fills/compares (never on the swap
+ * path) and the pinned stages of the K3 leg table and the frame table. */
+int nx_pinned_overhead(nx_engine* e, uint64_t* bytes);
 
 /* ---- K4 synthetic working set ------------------------------------------- */
 int nx_fill_pattern(nx_engine* e, uint32_t app, uint64_t seed);
@@ -192,6 +196,19 @@ void* nx_lane_stream(nx_engine* e, int lane);
 /* ---- host link ------------------------------------------------------------ */
 /* CE and SM bandwidth, H2D / D2H alone and simultaneously. */
 int nx_probe_pcie(nx_engine* e, uint64_t bytes_per_direction, uint64_t chunk_bytes, nx_pcie_probe* out);
+/* Where a device sits on the host: PCI bus id, NUMA node
+ * (sysfs numa_node; when that reads -1, the node holding most of the
+ * device's local_cpulist, node_from_cpus = 1) and the local CPUs this process
+ * may use (cpulist, e.g. "0-15,32-47"). This is the placement the engine's
+ * pinned ring and host copy pool bind to. */
+typedef struct {
+  char pci_bus_id[32];
+  int32_t numa_node;
+  int32_t node_from_cpus;
+  int32_t n_cpus;
+  char cpulist[256];
+} nx_device_info;
+int nx_device_info_get(int device, nx_device_info* out);
 /* Raw SM copy variant probe: out = {H2D, D2H, bidirectional total} GB/s. */
 int nx_probe_copy_variant(nx_engine* e, int variant, uint64_t bytes, int ctas, double out[3]);
 /* CopyPath::Auto table: sm_faster[k] for launches of 2^k legs. */

@@ -90,6 +90,11 @@ class BatchRecordC(Structure):
                 ("copied_s", c_double), ("end_s", c_double), ("host_submit_s", c_double), ("host_done_s", c_double)]
 
 
+class DeviceInfoC(Structure):
+    _fields_ = [("pci_bus_id", c_char * 32), ("numa_node", c_int), ("node_from_cpus", c_int), ("n_cpus", c_int),
+                ("cpulist", c_char * 256)]
+
+
 class MlfqConfigC(Structure):
     _fields_ = [("levels", c_int), ("base_allotment", c_double), ("base_preemption", c_double),
                 ("idle_threshold", c_double), ("tick", c_double)]
@@ -100,6 +105,7 @@ _SIGNATURES = [
     ("nx_last_error", c_char_p, []),
     ("nx_version", c_char_p, []),
     ("nx_cuda_device_count", c_int, [POINTER(c_int)]),
+    ("nx_device_info_get", c_int, [c_int, POINTER(DeviceInfoC)]),
     ("nx_engine_config_default", None, [POINTER(EngineConfigC)]),
     ("nx_planner_config_default", None, [POINTER(PlannerConfigC)]),
     ("nx_engine_create", c_int, [POINTER(EngineConfigC), POINTER(c_void_p)]),
@@ -109,6 +115,7 @@ _SIGNATURES = [
     ("nx_audit", c_int, [c_void_p]),
     ("nx_app_resident", c_int, [c_void_p, c_uint32, POINTER(c_uint64)]),
     ("nx_pinned_physical", c_int, [c_void_p, POINTER(c_uint64), POINTER(c_uint64)]),
+    ("nx_pinned_overhead", c_int, [c_void_p, POINTER(c_uint64)]),
     ("nx_fill_pattern", c_int, [c_void_p, c_uint32, c_uint64]),
     ("nx_verify_pattern", c_int, [c_void_p, c_uint32, c_uint64, POINTER(c_uint64)]),
     ("nx_block_frame", c_int, [c_void_p, c_uint64, POINTER(c_void_p)]),
@@ -205,6 +212,14 @@ def cuda_device_count() -> int:
     n = c_int(0)
     check(lib.nx_cuda_device_count(byref(n)))
     return n.value
+
+
+def device_info(device: int) -> dict:
+    """PCI bus id, NUMA node and local CPUs of a CUDA device (nx_device_info_get)."""
+    d = DeviceInfoC()
+    check(lib.nx_device_info_get(device, byref(d)))
+    return {"pci_bus_id": d.pci_bus_id.decode(), "numa_node": d.numa_node, "numa_from_cpulist": bool(d.node_from_cpus),
+            "n_cpus": d.n_cpus, "cpulist": d.cpulist.decode()}
 
 
 __all__ = [

@@ -10,6 +10,7 @@
 #include <new>
 #include <string>
 
+#include "phys.hpp"
 #include "nixie/scenario.hpp"
 #include "nixie/uvm.hpp"
 #include "nixie/workload.hpp"
@@ -267,6 +268,14 @@ int nx_pinned_physical(nx_engine* e, uint64_t* now, uint64_t* peak) {
   });
 }
 
+int nx_pinned_overhead(nx_engine* e, uint64_t* bytes) {
+  return guard([&] {
+    need(e, "engine");
+    need(bytes, "bytes");
+    *bytes = e->eng->pinned_overhead();
+  });
+}
+
 int nx_fill_pattern(nx_engine* e, uint32_t app, uint64_t seed) {
   return guard([&] {
     need(e, "engine");
@@ -434,6 +443,27 @@ int nx_probe_pcie(nx_engine* e, uint64_t bytes, uint64_t chunk, nx_pcie_probe* o
     out->bytes_per_direction = p.bytes_per_direction;
     out->chunk_bytes = p.chunk_bytes;
     out->numa_node = p.numa_node;
+  });
+}
+
+int nx_device_info_get(int device, nx_device_info* out) {
+  return guard([&] {
+    need(out, "out");
+    std::memset(out, 0, sizeof(*out));
+    const nixie::b200::NumaInfo n = nixie::b200::numa_for_device(device);
+    std::snprintf(out->pci_bus_id, sizeof(out->pci_bus_id), "%s", n.pci_bus_id.c_str());
+    out->numa_node = n.node;
+    out->node_from_cpus = n.node_from_cpus ? 1 : 0;
+    out->n_cpus = static_cast<int32_t>(n.cpus.size());
+    std::string list;
+    for (std::size_t i = 0; i < n.cpus.size();) {  // compress runs: 0-15,32-47
+      std::size_t j = i;
+      while (j + 1 < n.cpus.size() && n.cpus[j + 1] == n.cpus[j] + 1) ++j;
+      if (!list.empty()) list += ",";
+      list += std::to_string(n.cpus[i]) + (j > i ? "-" + std::to_string(n.cpus[j]) : "");
+      i = j + 1;
+    }
+    std::snprintf(out->cpulist, sizeof(out->cpulist), "%s", list.c_str());
   });
 }
 

@@ -1095,6 +1095,9 @@ const std::array<std::vector<LegTrace>, 6>& SwapEngine::lane_trace() const { ret
 std::uint64_t SwapEngine::total_launches() const { return impl_->launches_total; }
 const std::vector<K3Launch>& SwapEngine::k3_launches() const { return impl_->k3_trace; }
 const std::vector<BatchTrace>& SwapEngine::batch_trace() const { return impl_->batch_tr; }
+Bytes SwapEngine::pinned_overhead() const {
+  return static_cast<Bytes>(kBounceUnits) * kBlockBytes + impl_->ktab_cap * sizeof(NxLeg) + 2 * impl_->ck_cap * sizeof(std::uint64_t);
+}
 
 void* SwapEngine::frame_of(BlockId b) const {
   const Location& loc = impl_->mem.block(b).loc;

@@ -48,6 +48,34 @@ std::vector<int> parse_cpulist(const std::string& s) {
   return cpus;
 }
 
+// The node holding most of `cpus` (sysfs node*/cpulist), or -1. Used when the
+// device's numa_node reads -1 (firmware did not describe the affinity) but
+// its local_cpulist is narrower than the machine.
+int node_of_cpus(const std::vector<int>& cpus) {
+  if (cpus.empty()) return -1;
+  int best = -1;
+  std::size_t best_n = 0, nodes = 0;
+  for (int n = 0; n < 1024; ++n) {
+    const std::string list = read_line("/sys/devices/system/node/node" + std::to_string(n) + "/cpulist");
+    if (list.empty()) {
+      if (n > 64) break;
+      continue;
+    }
+    ++nodes;
+    const std::vector<int> nc = parse_cpulist(list);
+    std::size_t hit = 0;
+    for (int c : cpus)
+      for (int d : nc) hit += (c == d);
+    if (hit > best_n) {
+      best_n = hit;
+      best = n;
+    }
+  }
+  // One node, or the local list spans several nodes evenly: nothing to bind to.
+  if (nodes <= 1 || best_n * 2 <= cpus.size()) return -1;
+  return best;
+}
+
 }  // namespace
 
 NumaInfo numa_for_device(int device) {
@@ -58,6 +86,7 @@ NumaInfo numa_for_device(int device) {
   for (char& c : id) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
   // sysfs uses a 4-digit domain; CUDA may print 8.
   if (id.size() > 12 && id.find(':') == 8) id = id.substr(4);
+  info.pci_bus_id = id;
   const std::string dir = "/sys/bus/pci/devices/" + id;
   const std::string node = read_line(dir + "/numa_node");
   try {
@@ -66,6 +95,10 @@ NumaInfo numa_for_device(int device) {
     info.node = -1;
   }
   info.cpus = parse_cpulist(read_line(dir + "/local_cpulist"));
+  if (info.node < 0) {
+    info.node = node_of_cpus(info.cpus);
+    info.node_from_cpus = info.node >= 0;
+  }
   // Keep only CPUs this process may run on.
   cpu_set_t allowed;
   CPU_ZERO(&allowed);

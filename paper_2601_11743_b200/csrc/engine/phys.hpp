@@ -59,7 +59,9 @@ class UnitRing {
 // NUMA placement of the GPU's host-side resources.
 struct NumaInfo {
   int node = -1;
-  std::vector<int> cpus;  // local CPU list
+  bool node_from_cpus = false;  // sysfs numa_node was -1; derived from local_cpulist
+  std::vector<int> cpus;        // local CPU list (allowed by this process's affinity)
+  std::string pci_bus_id;
 };
 NumaInfo numa_for_device(int device);
 // Prefer `node` for this thread's future page allocations (-1: default policy).

@@ -123,6 +123,12 @@ class SwapEngine:
         check(lib.nx_pinned_physical(self._h, byref(now), byref(peak)))
         return now.value, peak.value
 
+    def pinned_overhead(self) -> int:
+        """Pinned bytes outside the budgeted ring (bounce buffer, table stages)."""
+        v = c_uint64()
+        check(lib.nx_pinned_overhead(self._h, byref(v)))
+        return v.value
+
     def app_blocks(self, app: int) -> List[int]:
         n = c_size_t()
         check(lib.nx_app_blocks(self._h, app, None, 0, byref(n)))

@@ -42,6 +42,37 @@ __global__ void touch(std::uint64_t* p, std::uint64_t n, std::uint64_t add, unsi
   atomicAdd(sum, acc);
 }
 
+__global__ void fill(std::uint64_t* p, std::uint64_t n, std::uint64_t salt) {
+  for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
+    p[i] = (i * 0x9E3779B97F4A7C15ull) ^ salt;
+}
+
+// Counts words that differ from fill(salt) + `adds` touches: the data
+// survived every fault-driven migration.
+__global__ void check(const std::uint64_t* p, std::uint64_t n, std::uint64_t salt, std::uint64_t adds,
+                      unsigned long long* bad) {
+  unsigned long long b = 0;
+  for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
+    b += p[i] != ((i * 0x9E3779B97F4A7C15ull) ^ salt) + adds;
+  atomicAdd(bad, b);
+}
+
+// Peak resident host memory of this process (kB, /proc/self/status VmHWM):
+// with UVM, evicted managed pages live in host memory, so this is the host
+// mirror the reference models as UVM's pinned peak (proj/include/nixie/uvm.hpp:58-63).
+static long vm_hwm_kb() {
+  FILE* f = std::fopen("/proc/self/status", "r");
+  if (!f) return -1;
+  char line[256];
+  long kb = -1;
+  while (std::fgets(line, sizeof(line), f))
+    if (std::sscanf(line, "VmHWM: %ld kB", &kb) == 1) break;
+  std::fclose(f);
+  return kb;
+}
+
 static double ms_since(std::chrono::steady_clock::time_point t) {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
 }
@@ -88,6 +119,10 @@ int main(int argc, char** argv) {
     return ms_since(t);
   };
   // populate both (first touch on the GPU), then round-robin
+  for (int a = 0; a < 2; ++a) {
+    fill<<<148 * 8, 512, 0, s>>>(app[a], n, 0x5157ull + a);
+    CK(cudaStreamSynchronize(s));
+  }
   run(0, 1);
   run(1, 1);
   std::vector<double> sw, res;
@@ -96,6 +131,12 @@ int main(int argc, char** argv) {
       sw.push_back(run(a, 1));   // the other app's pages occupy the GPU
       res.push_back(run(a, 1));  // resident now: compute only
     }
+  unsigned long long* bad = nullptr;
+  CK(cudaMallocManaged(&bad, sizeof(unsigned long long)));
+  *bad = 0;
+  for (int a = 0; a < 2; ++a) check<<<148 * 8, 512, 0, s>>>(app[a], n, 0x5157ull + a, 1 + 2ull * rounds, bad);
+  CK(cudaStreamSynchronize(s));
+  const unsigned long long mismatches = *bad;
   std::vector<double> cost;
   for (std::size_t i = 0; i < sw.size(); ++i) cost.push_back(sw[i] - res[i]);
   std::sort(cost.begin(), cost.end());
@@ -103,7 +144,8 @@ int main(int argc, char** argv) {
   std::printf("{\"mode\": \"%s\", \"cap_gib\": %.2f, \"ws_gib\": %.2f, \"switch_cost_ms\": [", prefetch ? "uvm+prefetch" : "uvm",
               cap_gib, ws_gib);
   for (std::size_t i = 0; i < cost.size(); ++i) std::printf("%s%.2f", i ? ", " : "", cost[i]);
-  std::printf("], \"median_ms\": %.2f, \"resident_kernel_ms\": %.2f, \"bidir_equiv_gbps\": %.2f}\n", med, res.back(),
-              2.0 * ws / (med * 1e-3) / 1e9);
+  std::printf("], \"median_ms\": %.2f, \"resident_kernel_ms\": %.2f, \"bidir_equiv_gbps\": %.2f, \"mismatches\": %llu"
+              ", \"host_peak_rss_bytes\": %lld}\n", med, res.back(), 2.0 * ws / (med * 1e-3) / 1e9, mismatches,
+              static_cast<long long>(vm_hwm_kb()) * 1024);
   return 0;
 }
