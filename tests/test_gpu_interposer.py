@@ -150,6 +150,11 @@ def test_two_llm_inference_apps():
         assert r["out"]["weights_gib"] > 1.3  # the pair does not fit 2 GiB
     assert all(s["mismatches"] == 0 for s in sw)
     between = [s for s in sw if s["from"] >= 0 and s["from"] != s["to"]]
+    # Switches before both models are loaded may find the incoming app with
+    # nothing allocated yet; from the first switch that restores a model on,
+    # every switch must move a model's worth each way.
+    first = next(i for i, s in enumerate(between) if s["bytes_in"] > 0)
+    between = between[first:]
     assert len(between) >= 3, sw
     for s in between:  # per switch, not a timing-dependent sum
         assert s["pcie_h2d"] >= (512 << 20) and s["pcie_d2h"] >= (512 << 20), s
