@@ -12,17 +12,37 @@
  * (proj/src/mem_model.cpp:48-116); the grant it enforces,
  * MlfqScheduler::on_grant_start / on_grant_end (proj/src/mlfq.cpp:188-194).
  *
- *   allocation   cudaMalloc, cudaFree, cudaMallocAsync, cudaFreeAsync, cuMemAlloc_v2, cuMemFree_v2
- *   memory info  cudaMemGetInfo
+ *   allocation   cudaMalloc, cudaFree, cudaMallocAsync, cudaFreeAsync, cudaMallocPitch, cudaMalloc3D,
+ *                cuMemAlloc_v2, cuMemFree_v2, cuMemAllocPitch_v2, cuMemAllocAsync, cuMemFreeAsync
+ *   memory info  cudaMemGetInfo (budget as total; managed + passthrough + implicit bytes as used)
+ *   implicit     cudaStreamCreate, cudaStreamCreateWithFlags, cudaStreamCreateWithPriority,
+ *   allocations  cudaStreamDestroy, cudaGraphInstantiate, cudaGraphInstantiateWithFlags,
+ *                cudaGraphExecDestroy, cudaDeviceSetLimit, cuStreamCreate, cuStreamCreateWithPriority,
+ *                cuStreamDestroy_v2, cublasCreate_v2, cublasDestroy_v2, cublasLtCreate, cublasLtDestroy,
+ *                cudnnCreate, cudnnDestroy (the device memory each call takes is charged to the app:
+ *                PAPER.md:137, "APIs that implicitly allocate memory (e.g., cudaStreamCreate)")
  *   launch gate  cudaLaunchKernel, cudaLaunchKernelExC, cudaLaunchCooperativeKernel,
- *                cudaGraphLaunch, cuLaunchKernel, cudaMemcpy, cudaMemcpyAsync,
- *                cudaMemcpy2D, cudaMemcpy2DAsync, cudaMemset, cudaMemsetAsync
- *                (and the _ptsz per-thread-stream variants of each runtime call)
+ *                cudaGraphLaunch, cuLaunchKernel, cuLaunchKernelEx, cuLaunchCooperativeKernel,
+ *                cuGraphLaunch, cudaMemcpy, cudaMemcpyAsync, cudaMemcpy2D, cudaMemcpy2DAsync,
+ *                cudaMemcpy3D, cudaMemcpy3DAsync, cudaMemcpyPeer, cudaMemcpyPeerAsync,
+ *                cudaMemcpy3DPeer, cudaMemcpy3DPeerAsync, cudaMemcpyBatchAsync,
+ *                cudaMemcpy3DBatchAsync, cudaMemset, cudaMemsetAsync, cudaMemset2D,
+ *                cudaMemset2DAsync, cudaMemset3D, cudaMemset3DAsync
+ *                (and the _ptds / _ptsz per-thread-stream variants of each runtime call)
+ *                cuMemcpy, cuMemcpyAsync, cuMemcpyHtoD_v2, cuMemcpyDtoH_v2, cuMemcpyDtoD_v2,
+ *                cuMemcpyHtoDAsync_v2, cuMemcpyDtoHAsync_v2, cuMemcpyDtoDAsync_v2, cuMemcpy2D_v2,
+ *                cuMemcpy2DUnaligned_v2, cuMemcpy2DAsync_v2, cuMemcpy3D_v2, cuMemcpy3DAsync_v2,
+ *                cuMemcpyPeer, cuMemcpyPeerAsync, cuMemsetD8_v2, cuMemsetD16_v2, cuMemsetD32_v2,
+ *                cuMemsetD8Async, cuMemsetD16Async, cuMemsetD32Async, cuMemsetD2D8_v2,
+ *                cuMemsetD2D16_v2, cuMemsetD2D32_v2 (driver entry points; the same set, plus the
+ *                2D/3D/peer/batch async copies and 2D memsets, is wrapped in the table
+ *                cuGetProcAddress hands to cudart and libraries)
  *                cublasLtMatmul, cublasGemmEx, cublasGemmStridedBatchedEx, cublasSgemm_v2,
  *                cublasSgemmStridedBatched, cudnnBackendExecute (cuBLAS and cuDNN launch
  *                through their static runtimes' private driver tables)
  *   blocking     cudaDeviceSynchronize, cudaStreamSynchronize, cudaEventSynchronize
- *   capture      cudaStreamBeginCapture, cudaStreamEndCapture
+ *   capture      cudaStreamBeginCapture, cudaStreamEndCapture (launches recorded into a
+ *                capture are not gated but count as activity)
  */
 #ifndef NIXIE_SHIM_H
 #define NIXIE_SHIM_H

@@ -39,6 +39,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cerrno>
 #include <deque>
 #include <utility>
 #include <cinttypes>
@@ -68,6 +69,7 @@ void on_signal(int) { g_stop = 1; }
 struct Options {
   std::string socket_path = "/tmp/nixie.sock";
   std::string log_path;
+  std::string trace_path;          // registry + plan trace for the reference replay (oracle/ref_replay.cpp)
   EngineConfig eng;
   PlannerConfig planner;
   MlfqConfig mlfq;
@@ -97,7 +99,7 @@ void usage() {
   std::fprintf(stderr,
                "usage: nixied [--socket PATH] [--device N] [--gpu SIZE] [--pinned SIZE] [--paged SIZE]\n"
                "              [--window SIZE] [--min-bytes SIZE] [--path auto|ce|sm] [--host-threads N]\n"
-               "              [--tick-ms X] [--idle-ms X] [--allot-s X] [--preempt-s X] [--log FILE]\n"
+               "              [--tick-ms X] [--idle-ms X] [--allot-s X] [--preempt-s X] [--log FILE] [--trace FILE]\n"
                "              [--phys-slack SLABS] [--slab-mib 2..1024, power of 2] [--prefetch] [--exit-after-apps N]\n              [--reference-victims] [--keep-stale-maps | --isolate-victims]\n"
                "sizes take a K/M/G suffix (GiB when bare). The daemon serves LD_PRELOAD=libnixie_shim.so apps\n"
                "that set NIXIE_SOCKET=PATH.\n");
@@ -128,9 +130,18 @@ bool parse_args(int argc, char** argv, Options& o) {
     else if (a == "--allot-s") o.mlfq.base_allotment = std::atof(val());
     else if (a == "--preempt-s") o.mlfq.base_preemption = std::atof(val());
     else if (a == "--log") o.log_path = val();
+    else if (a == "--trace") o.trace_path = val();
     else if (a == "--exit-after-apps") o.exit_after_apps = std::atoi(val());
     else if (a == "--phys-slack") o.phys_slack_slabs = std::atoi(val());
-    else if (a == "--slab-mib") o.slab_blocks = static_cast<std::uint32_t>(std::atoi(val()) / 2);
+    else if (a == "--slab-mib") {
+      // Validated as given (a truncating division would turn 1 into "default" and 3 into 2).
+      char* end = nullptr;
+      const char* v = val();
+      const long mib = std::strtol(v, &end, 10);
+      if (!end || *end != 0 || mib < 2 || mib > 1024 || (mib & (mib - 1)) != 0)
+        throw SimError(Err::ValidationError, std::string("--slab-mib must be a power of two between 2 and 1024, got ") + v);
+      o.slab_blocks = static_cast<std::uint32_t>(mib / 2);
+    }
     else if (a == "--prefetch") o.prefetch = true;
     else if (a == "--reference-victims") o.reference_victims = true;
     else if (a == "--keep-stale-maps") o.keep_stale_maps = 1;
@@ -147,6 +158,8 @@ bool parse_args(int argc, char** argv, Options& o) {
     }
   }
   o.mlfq.validate();
+  if (!o.trace_path.empty() && o.prefetch)
+    throw SimError(Err::ValidationError, "--trace replays whole plans; it cannot be combined with --prefetch");
   // Larger slabs mean fewer driver mappings per switch (each costs ~1 ms
   // whatever its size); smaller ones waste less physical memory on partly
   // resident slabs, which matters on small budgets.
@@ -178,6 +191,11 @@ class Daemon {
       log_ = std::fopen(o.log_path.c_str(), "w");
       if (!log_) throw SimError(Err::IoError, "cannot open log " + o.log_path);
     }
+    if (!o.trace_path.empty()) {
+      trace_ = std::fopen(o.trace_path.c_str(), "w");
+      if (!trace_) throw SimError(Err::IoError, "cannot open trace " + o.trace_path);
+      trace_header();
+    }
   }
   ~Daemon() {
     for (auto& [id, a] : apps_) close_app(a);
@@ -185,6 +203,7 @@ class Daemon {
     if (listen_fd_ >= 0) ::close(listen_fd_);
     ::unlink(opt_.socket_path.c_str());
     if (log_) std::fclose(log_);
+    if (trace_) std::fclose(trace_);
   }
 
   void listen_on() {
@@ -362,6 +381,11 @@ class Daemon {
       a->alive = false;
       return;
     }
+    serve(*a, type, body);
+  }
+
+  void serve(App& app, ipc::Msg type, const std::vector<std::uint8_t>& body) {
+    App* a = &app;
     try {
       rpc(*a, type, body);
     } catch (const InvariantViolation&) {
@@ -396,9 +420,13 @@ class Daemon {
       sched_.clear_request(id);
       eng_.prefetch_quiesce();
       const std::vector<ChunkId> chunks = eng_.mem().chunks_of(id);
-      for (ChunkId c : chunks) eng_.free_chunk(id, c);
+      for (ChunkId c : chunks) {
+        eng_.free_chunk(id, c);
+        trace_free(id, c);
+      }
       placer_.take_released();  // its slabs return to the pool; nobody to unmap them
       std::uint64_t launches = 0, table = 0, blas = 0, waits = 0, wait_ns = 0, drain_ns = 0, map_ns = 0;
+      std::uint64_t small = 0, implicit = 0, captured = 0;
       if (a.ctl) {
         launches = a.ctl->launches.load();
         table = a.ctl->table_launches.load();
@@ -407,13 +435,17 @@ class Daemon {
         wait_ns = a.ctl->gate_wait_ns.load();
         drain_ns = a.ctl->drain_ns.load();
         map_ns = a.ctl->map_ns.load();
+        small = a.ctl->small_bytes.load();
+        implicit = a.ctl->implicit_bytes.load();
+        captured = a.ctl->captured_launches.load();
       }
       close_app(a);
       ++gone_;
       note("{\"t\": %.6f, \"event\": \"bye\", \"app\": %u, \"chunks_freed\": %zu, \"gated_calls\": %" PRIu64
            ", \"table_launches\": %" PRIu64 ", \"blas_calls\": %" PRIu64 ", \"gate_waits\": %" PRIu64 ", \"gate_wait_ms\": %.3f, \"drain_ms\": %.3f"
-           ", \"map_ms\": %.3f}",
-           now(), id, chunks.size(), launches, table, blas, waits, wait_ns * 1e-6, drain_ns * 1e-6, map_ns * 1e-6);
+           ", \"map_ms\": %.3f, \"small_bytes\": %" PRIu64 ", \"implicit_bytes\": %" PRIu64 ", \"captured_launches\": %" PRIu64 "}",
+           now(), id, chunks.size(), launches, table, blas, waits, wait_ns * 1e-6, drain_ns * 1e-6, map_ns * 1e-6, small, implicit,
+           captured);
     }
   }
 
@@ -434,6 +466,7 @@ class Daemon {
           const auto c = r.get<std::uint32_t>();
           try {
             eng_.free_chunk(a.id, c);
+            trace_free(a.id, c);
           } catch (const SimError&) {
             status = 1;
           }
@@ -471,17 +504,24 @@ class Daemon {
     }
   }
 
+  // Device memory an app holds outside the registry: passthrough allocations
+  // below min_bytes and what implicitly allocating APIs took (shim control page).
+  static Bytes unmanaged(const App& a) {
+    return a.ctl ? a.ctl->small_bytes.load(std::memory_order_relaxed) + a.ctl->implicit_bytes.load(std::memory_order_relaxed) : 0;
+  }
+
   // cudaMalloc >= min_bytes (MemState::allocate, proj/src/mem_model.cpp:48-86).
   // Placement: the GPU when it has room; otherwise the holder's allocation
   // is brought in by an in-place plan (other apps' blocks are evicted), and
   // a waiting app's allocation starts in pageable memory (its next grant
   // fetches it). An app's footprint may not exceed the GPU budget
-  // (the planner's precondition).
+  // (the planner's precondition), counting the app's
+  // unmanaged device memory too (implicit allocations count).
   void alloc(App& a, Bytes bytes, std::uint64_t va_block) {
     MemState& mem = eng_.mem();
     const Bytes fp = footprint_for(bytes);
     ipc::AllocRep rep{};
-    if (bytes == 0 || mem.app_footprint(a.id) + fp > opt_.eng.gpu_capacity) {
+    if (bytes == 0 || mem.app_footprint(a.id) + fp + unmanaged(a) > opt_.eng.gpu_capacity) {
       rep.status = 2;
       ipc::send_msg(a.rpc, ipc::Msg::Alloc, &rep, sizeof(rep));
       return;
@@ -499,6 +539,7 @@ class Daemon {
     const std::uint64_t nblk = fp / kBlockBytes;
     placer_.expect(mem.block_count(), nblk, a.id, va_block);
     const std::vector<ChunkId> chunks = eng_.allocate(a.id, bytes, tier);
+    trace_alloc(a.id, bytes, tier, chunks);
     if (holder && tier != TierId::Gpu) fetch_in_place(a.id);
     std::vector<std::uint32_t> ids;
     for (ChunkId c : chunks) ids.push_back(static_cast<std::uint32_t>(c));
@@ -571,17 +612,52 @@ class Daemon {
   }
 
   // ---- acks on the event socket ------------------------------------------------
+  // The shim acks from its listener thread while the application's own
+  // threads keep running: one of them may be inside cudaMalloc during a
+  // stream capture, which the pause waits out, so its Alloc/Free RPCs are
+  // served while the ack is awaited (otherwise both sides wait on each other
+  // until the ack timeout). An Acquire is answered and queued for after the
+  // switch (no scheduling decision inside a switch).
   bool wait_ack(App& a, ipc::Msg want, std::vector<std::uint8_t>& body) {
     if (!a.alive || a.ev < 0) return false;
-    pollfd p{a.ev, POLLIN, 0};
-    const int n = ::poll(&p, 1, static_cast<int>(opt_.ack_timeout_s * 1000));
+    const std::uint64_t deadline = ipc::mono_ns() + static_cast<std::uint64_t>(opt_.ack_timeout_s * 1e9);
     ipc::Msg type;
-    if (n <= 0 || !ipc::recv_msg(a.ev, type, body) || type != want) {
-      std::fprintf(stderr, "[nixied] app %u: no %u ack (dropping the app)\n", a.id, static_cast<unsigned>(want));
-      a.alive = false;
-      return false;
+    while (a.alive) {
+      const std::uint64_t t = ipc::mono_ns();
+      if (t >= deadline) break;
+      pollfd p[2] = {{a.ev, POLLIN, 0}, {a.rpc, POLLIN, 0}};
+      const int n = ::poll(p, 2, static_cast<int>(std::min<std::uint64_t>((deadline - t) / 1000000 + 1, 1000)));
+      if (n < 0 && errno != EINTR) break;
+      if (n <= 0) continue;
+      if (p[0].revents) {
+        if (!ipc::recv_msg(a.ev, type, body) || type != want) break;
+        return true;
+      }
+      if (p[1].revents) {
+        std::vector<std::uint8_t> req;
+        if (!ipc::recv_msg(a.rpc, type, req)) break;
+        if (type == ipc::Msg::Acquire) {
+          ipc::StatusRep st{0, 0};
+          ipc::send_msg(a.rpc, ipc::Msg::Status, &st, sizeof(st));
+          deferred_acquires_.push_back(a.id);
+        } else {
+          ++rpcs_in_switch_;
+          serve(a, type, req);
+        }
+      }
     }
-    return true;
+    std::fprintf(stderr, "[nixied] app %u: no %u ack (dropping the app)\n", a.id, static_cast<unsigned>(want));
+    a.alive = false;
+    return false;
+  }
+
+  // Acquires that arrived during a switch: queued now (decided at the next tick).
+  void take_deferred_acquires() {
+    for (AppId id : deferred_acquires_) {
+      auto it = apps_.find(id);
+      if (it != apps_.end() && it->second.alive && sched_.granted() != id) sched_.enqueue_request(id, now());
+    }
+    deferred_acquires_.clear();
   }
 
   // While a plan runs: the incoming app maps the slabs its blocks are landing
@@ -738,6 +814,7 @@ class Daemon {
     eng_.prefetch_quiesce();
     const MigrationPlan plan = plan_moves(app, cfg);
     const ExecResult r = eng_.execute(plan, cfg);
+    trace_plan("inplace", app, cfg, plan);
     send_maps();
     account(r);
     flush_unmaps();
@@ -772,6 +849,7 @@ class Daemon {
     const std::uint64_t t_planned = ipc::mono_ns();
     const ExecResult r = eng_.execute(plan, cfg);
     const std::uint64_t t_copied = ipc::mono_ns();
+    trace_plan("switch", to, cfg, plan);
     send_maps();
     account(r);
     const std::uint64_t t_unmapped = ipc::mono_ns();
@@ -795,6 +873,7 @@ class Daemon {
     sched_.on_api_event(to, granted_at, ApiEventKind::NonBlockingReturn);  // its held launch resumes now
     flush_unmaps();
     shrink_arena();
+    take_deferred_acquires();
     ++switches_;
     const SwitchStats& s = eng_.last_stats();
     auto ms = [](std::uint64_t a, std::uint64_t b) { return static_cast<double>(b - a) * 1e-6; };
@@ -815,6 +894,52 @@ class Daemon {
          placer_.live_slabs());
   }
 
+  // ---- reference replay trace (--trace) ---------------------------------------
+  // Every registry mutation and executed plan in the order this single thread
+  // performed them. oracle/ref_replay.cpp replays the allocations and frees on
+  // the unmodified reference MemState (proj/src/mem_model.cpp:48-116),
+  // recomputes plan_switch for each plan (proj/src/planner.cpp:111-216) and
+  // executes the daemon's plan on the reference Orchestrator
+  // (proj/src/transfer.cpp:250-271) for its per-lane leg sequences, so the
+  // interposer path is checked against the reference switch by switch.
+  void trace_header() {
+    std::fprintf(trace_, "capacity gpu %" PRIu64 "\ncapacity pinned %" PRIu64 "\ncapacity paged %" PRIu64 "\n",
+                 opt_.eng.gpu_capacity, opt_.eng.pinned_capacity, opt_.eng.paged_capacity);
+    std::fprintf(trace_, "window %" PRIu64 "\nbudget %" PRIu64 "\nvictims %s\n", opt_.planner.streaming_window,
+                 opt_.planner.pinned_budget, opt_.reference_victims ? "reference" : "slab");
+    std::fflush(trace_);
+  }
+  void trace_alloc(AppId app, Bytes bytes, TierId tier, const std::vector<ChunkId>& chunks) {
+    if (!trace_) return;
+    std::fprintf(trace_, "alloc %u %" PRIu64 " %s", app, bytes, tier_name(tier));
+    for (ChunkId c : chunks) std::fprintf(trace_, " %u", static_cast<unsigned>(c));
+    std::fputc('\n', trace_);
+    std::fflush(trace_);
+  }
+  void trace_free(AppId app, ChunkId c) {
+    if (!trace_) return;
+    std::fprintf(trace_, "free %u %u\n", app, static_cast<unsigned>(c));
+    std::fflush(trace_);
+  }
+  void trace_plan(const char* kind, AppId app, const PlannerConfig& cfg, const MigrationPlan& plan) {
+    if (!trace_) return;
+    const std::uint64_t k = plans_++;
+    std::fprintf(trace_, "plan %" PRIu64 " %s %u in %" PRIu64 " out %" PRIu64 " victims", k, kind, app, plan.bytes_in, plan.bytes_out);
+    for (AppId v : cfg.eviction_policy.victim_order) std::fprintf(trace_, " %u", v);
+    std::fputc('\n', trace_);
+    std::string dump = plan.dump();
+    for (std::size_t i = 0; i < dump.size();) {
+      const std::size_t j = dump.find('\n', i);
+      std::fprintf(trace_, "P %" PRIu64 " %s\n", k, dump.substr(i, j - i).c_str());
+      i = j == std::string::npos ? dump.size() : j + 1;
+    }
+    const auto& lanes = eng_.lane_trace();
+    for (int l = 0; l < 6; ++l)
+      for (const LegTrace& x : lanes[l])
+        std::fprintf(trace_, "L %" PRIu64 " %d %" PRIu64 " %s %s\n", k, l, static_cast<std::uint64_t>(x.block), tier_name(x.src), tier_name(x.dst));
+    std::fflush(trace_);
+  }
+
   template <typename... A>
   void note(const char* fmt, A... args) {
     if (!log_) return;
@@ -825,8 +950,8 @@ class Daemon {
 
   void write_summary() {
     note("{\"event\": \"summary\", \"switches\": %" PRIu64 ", \"pcie_bytes_in\": %" PRIu64 ", \"pcie_bytes_out\": %" PRIu64
-         ", \"verified\": %" PRIu64 ", \"mismatches\": %" PRIu64 ", \"apps\": %u}",
-         switches_, bytes_in_, bytes_out_, verified_, mismatches_, next_app_);
+         ", \"verified\": %" PRIu64 ", \"mismatches\": %" PRIu64 ", \"apps\": %u, \"rpcs_in_switch\": %" PRIu64 "}",
+         switches_, bytes_in_, bytes_out_, verified_, mismatches_, next_app_, rpcs_in_switch_);
     for (const SchedLogRow& row : sched_.log())
       note("{\"event\": \"sched\", \"t\": %.6f, \"app\": %u, \"what\": \"%s\", \"level\": %d}", row.time, row.app,
            row.event.c_str(), row.level);
@@ -848,6 +973,10 @@ class Daemon {
   Seconds last_tick_ = 0;
   std::uint64_t switches_ = 0, bytes_in_ = 0, bytes_out_ = 0, verified_ = 0, mismatches_ = 0;
   std::FILE* log_ = nullptr;
+  std::FILE* trace_ = nullptr;
+  std::uint64_t plans_ = 0;             // plans written to the trace
+  std::vector<AppId> deferred_acquires_;
+  std::uint64_t rpcs_in_switch_ = 0;    // requests served while awaiting an ack
 };
 
 }  // namespace

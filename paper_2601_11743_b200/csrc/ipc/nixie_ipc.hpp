@@ -172,6 +172,10 @@ struct alignas(64) CtlPage {
   std::atomic<std::uint64_t> blas_calls;      // gated library calls (cuBLAS / cuBLASLt GEMMs, cuDNN executes)
   std::atomic<std::uint64_t> table_launches;  // gated calls that came through cuGetProcAddress entry
                                               // points directly (not via an interposed runtime call)
+  std::atomic<std::uint64_t> small_bytes;     // passthrough allocations below min_bytes (live)
+  std::atomic<std::uint64_t> implicit_bytes;  // device memory taken by implicitly allocating APIs
+                                              // (stream/handle creation, limits, graph instantiation), live
+  std::atomic<std::uint64_t> captured_launches;  // launches recorded into stream captures (activity, not gated)
 };
 static_assert(sizeof(CtlPage) <= 4096, "control page fits one page");
 

@@ -4,7 +4,9 @@
 //
 // Interposed ("memory allocation and free ... kernel/graph
 // launches ... APIs that implicitly allocate memory ... memory usage"):
-//   cudaMalloc / cudaFree, cudaMallocAsync / cudaFreeAsync, cuMemAlloc_v2 / cuMemFree_v2
+//   cudaMalloc / cudaFree, cudaMallocAsync[_ptsz] / cudaFreeAsync, cudaMallocPitch,
+//   cudaMalloc3D, cuMemAlloc_v2 / cuMemFree_v2, cuMemAllocPitch_v2,
+//   cuMemAllocAsync / cuMemFreeAsync
 //       allocations >= min_bytes (2 MiB) become daemon chunks: the shim
 //       are placed in a virtual range the shim reserved once (stable
 //       addresses); every 128 MiB virtual slab of it that holds GPU-resident
@@ -15,7 +17,12 @@
 //       Chunk::logical_base (proj/include/nixie/mem_model.hpp:72).
 //   cudaLaunchKernel[_ptsz], cudaLaunchKernelExC[_ptsz],
 //   cudaLaunchCooperativeKernel[_ptsz], cudaGraphLaunch[_ptsz], cuLaunchKernel,
-//   cudaMemcpy[Async], cudaMemcpy2D[Async], cudaMemset[Async]
+//   cuLaunchKernelEx, cuLaunchCooperativeKernel, cuGraphLaunch, and every
+//   copy/memset that can touch device memory: cudaMemcpy{,2D,3D,Peer,3DPeer}
+//   [Async] and cudaMemset{,2D,3D}[Async] (with their _ptds/_ptsz
+//   per-thread-stream twins), cudaMemcpy[3D]BatchAsync; the driver's
+//   cuMemcpy*/cuMemset* (synchronous and async) through the PLT and through
+//   the cuGetProcAddress table
 //       the launch gate (PAPER.md:116 steps 1-2 and 6): pass while the
 //       execution flag is set; otherwise ask the daemon (Acquire) and hold
 //       the calling thread until a Grant has mapped the app's slabs.
@@ -32,7 +39,15 @@
 //       CUDA API.
 //   cudaMemGetInfo
 //       reports the daemon's budget as total and budget - own usage as free
-//       (PAPER.md:147).
+//       (PAPER.md:147); own usage = managed + passthrough + implicit bytes.
+//   cudaStreamCreate*, cuStreamCreate*, cudaDeviceSetLimit,
+//   cudaGraphInstantiate*, cublasCreate_v2, cublasLtCreate, cudnnCreate (and
+//   their destroys)
+//       implicitly allocating APIs: the device memory a call
+//       takes (the drop of the device's free memory across it, measured under
+//       a process lock) is charged to the app: the daemon admits managed
+//       allocations only while managed + passthrough + implicit bytes fit the
+//       budget, and cudaMemGetInfo reports it.
 //
 // The shim never copies application data: the daemon's swap engine moves
 // every byte (both PCIe directions at once) through its own mapping of the
@@ -72,6 +87,22 @@ cudaError_t cudaLaunchCooperativeKernel_ptsz(const void*, dim3, dim3, void**, si
 cudaError_t cudaGraphLaunch_ptsz(cudaGraphExec_t, cudaStream_t);
 cudaError_t cudaMemcpyAsync_ptsz(void*, const void*, size_t, cudaMemcpyKind, cudaStream_t);
 cudaError_t cudaMemsetAsync_ptsz(void*, int, size_t, cudaStream_t);
+cudaError_t cudaMallocAsync_ptsz(void**, size_t, cudaStream_t);
+cudaError_t cudaMemcpy_ptds(void*, const void*, size_t, cudaMemcpyKind);
+cudaError_t cudaMemcpy2D_ptds(void*, size_t, const void*, size_t, size_t, size_t, cudaMemcpyKind);
+cudaError_t cudaMemcpy2DAsync_ptsz(void*, size_t, const void*, size_t, size_t, size_t, cudaMemcpyKind, cudaStream_t);
+cudaError_t cudaMemcpy3D_ptds(const cudaMemcpy3DParms*);
+cudaError_t cudaMemcpy3DAsync_ptsz(const cudaMemcpy3DParms*, cudaStream_t);
+cudaError_t cudaMemcpy3DPeer_ptds(const cudaMemcpy3DPeerParms*);
+cudaError_t cudaMemcpy3DPeerAsync_ptsz(const cudaMemcpy3DPeerParms*, cudaStream_t);
+cudaError_t cudaMemset_ptds(void*, int, size_t);
+cudaError_t cudaMemset2D_ptds(void*, size_t, int, size_t, size_t);
+cudaError_t cudaMemset2DAsync_ptsz(void*, size_t, int, size_t, size_t, cudaStream_t);
+cudaError_t cudaMemset3D_ptds(cudaPitchedPtr, int, cudaExtent);
+cudaError_t cudaMemset3DAsync_ptsz(cudaPitchedPtr, int, cudaExtent, cudaStream_t);
+cudaError_t cudaMemcpyBatchAsync_ptsz(void**, void**, size_t*, size_t, cudaMemcpyAttributes*, size_t*, size_t, size_t*,
+                                      cudaStream_t);
+cudaError_t cudaMemcpy3DBatchAsync_ptsz(size_t, cudaMemcpy3DBatchOp*, size_t*, unsigned long long, cudaStream_t);
 }
 
 namespace ipc = nixie::ipc;
@@ -600,7 +631,16 @@ void acquire_slow() {
 // Entry of every gated call: returns true holding an in-flight slot (a pause
 // waits for it), false when the call need not be gated.
 bool gate_enter() {
-  if (t_in_shim || t_gate_depth || !active() || t_capturing) return false;
+  if (t_in_shim || t_gate_depth || !active()) return false;
+  if (t_capturing) {
+    // Recorded into a capture, not executed: no gate (the graph launch is
+    // gated), but it is activity, so a capturing holder is not seen as idle
+    // by the MLFQ and preempted mid-capture.
+    g.ctl->captured_launches.fetch_add(1, std::memory_order_relaxed);
+    g.ctl->launches.fetch_add(1, std::memory_order_relaxed);
+    now_api();
+    return false;
+  }
   for (;;) {
     g.inflight.fetch_add(1, std::memory_order_seq_cst);
     if (g.granted.load(std::memory_order_seq_cst)) break;
@@ -645,6 +685,92 @@ struct Blocking {
     }
   }
 };
+
+// ---- implicitly allocating APIs ---------------------------------------------
+// The device memory such a call takes is the drop of the device's free memory
+// across it, measured under a process-wide lock so this process's other
+// implicit calls cannot interleave. The charge is kept per handle and
+// returned when the handle is destroyed. While a global-mode capture is open
+// nothing is measured (cudaMemGetInfo must not run then).
+std::mutex g_implicit_mu;
+std::unordered_map<const void*, std::uint64_t> g_implicit;  // handle (or limit tag) -> bytes charged
+
+std::size_t device_free_bytes() {
+  REAL(cudaMemGetInfo);
+  std::size_t f = 0, t = 0;
+  t_in_shim++;
+  real_cudaMemGetInfo(&f, &t);
+  t_in_shim--;
+  return f;
+}
+
+struct ImplicitScope {
+  bool on;
+  std::size_t before = 0;
+  std::unique_lock<std::mutex> lk;
+  ImplicitScope() : on(!t_in_shim && active() && g.capturing_global.load() == 0) {
+    if (!on) return;
+    lk = std::unique_lock<std::mutex>(g_implicit_mu);
+    before = device_free_bytes();
+  }
+  // Free-memory change across the call: > 0 taken, < 0 returned.
+  std::int64_t delta() const {
+    const std::size_t after = device_free_bytes();
+    return static_cast<std::int64_t>(before) - static_cast<std::int64_t>(after);
+  }
+};
+
+// Caller holds g_implicit_mu (through an ImplicitScope).
+void implicit_adjust(const void* key, std::int64_t bytes) {
+  std::uint64_t& have = g_implicit[key];
+  if (bytes < 0) bytes = -static_cast<std::int64_t>(std::min<std::uint64_t>(have, static_cast<std::uint64_t>(-bytes)));
+  have += static_cast<std::uint64_t>(bytes);
+  g.ctl->implicit_bytes.fetch_add(static_cast<std::uint64_t>(bytes), std::memory_order_relaxed);
+  if (have == 0) g_implicit.erase(key);
+}
+
+void implicit_release(const void* key) {
+  if (t_in_shim || !active()) return;
+  std::lock_guard<std::mutex> lk(g_implicit_mu);
+  auto it = g_implicit.find(key);
+  if (it == g_implicit.end()) return;
+  g.ctl->implicit_bytes.fetch_sub(it->second, std::memory_order_relaxed);
+  g_implicit.erase(it);
+}
+
+// Runs a creating call and charges what it took to the handle it returns.
+template <typename R, typename H, typename Fn>
+R implicit_create(R ok, H* out, Fn&& call) {
+  ImplicitScope sc;
+  const R e = call();
+  if (sc.on && e == ok && out) {
+    const std::int64_t d = sc.delta();
+    if (d > 0) implicit_adjust(reinterpret_cast<const void*>(*out), d);
+  }
+  return e;
+}
+
+void small_add(void* p, std::size_t bytes) {
+  if (!p || !g.active || t_in_shim) return;
+  std::lock_guard<std::mutex> lk(g.mu);
+  g.small[p] = bytes;
+  g.small_bytes += bytes;
+  g.ctl->small_bytes.store(g.small_bytes, std::memory_order_relaxed);
+}
+
+void small_remove(void* p) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  auto it = g.small.find(p);
+  if (it == g.small.end()) return;
+  g.small_bytes -= it->second;
+  g.small.erase(it);
+  g.ctl->small_bytes.store(g.small_bytes, std::memory_order_relaxed);
+}
+
+// cudaMallocPitch / cudaMalloc3D / cuMemAllocPitch pitch for managed
+// allocations: rows aligned to 512 bytes (>= the texture pitch alignment).
+constexpr std::size_t kPitchAlign = 512;
+std::size_t pitch_of(std::size_t width) { return (width + kPitchAlign - 1) / kPitchAlign * kPitchAlign; }
 
 // ---- allocation -------------------------------------------------------------------------
 int managed_alloc(void** out, std::size_t bytes) {
@@ -755,6 +881,38 @@ NX_DRV(MemcpyDtoHAsync, CUresult, (void* d, CUdeviceptr s, size_t n, CUstream st
 NX_DRV(MemcpyDtoDAsync, CUresult, (CUdeviceptr d, CUdeviceptr s, size_t n, CUstream st), (d, s, n, st))
 NX_DRV(MemsetD8Async, CUresult, (CUdeviceptr d, unsigned char v, size_t n, CUstream st), (d, v, n, st))
 NX_DRV(MemsetD32Async, CUresult, (CUdeviceptr d, unsigned v, size_t n, CUstream st), (d, v, n, st))
+NX_DRV(MemsetD16Async, CUresult, (CUdeviceptr d, unsigned short v, size_t n, CUstream st), (d, v, n, st))
+NX_DRV(MemsetD2D8Async, CUresult, (CUdeviceptr d, size_t p, unsigned char v, size_t w, size_t h, CUstream st), (d, p, v, w, h, st))
+NX_DRV(MemsetD2D16Async, CUresult, (CUdeviceptr d, size_t p, unsigned short v, size_t w, size_t h, CUstream st), (d, p, v, w, h, st))
+NX_DRV(MemsetD2D32Async, CUresult, (CUdeviceptr d, size_t p, unsigned v, size_t w, size_t h, CUstream st), (d, p, v, w, h, st))
+NX_DRV(Memcpy2DAsync, CUresult, (const CUDA_MEMCPY2D* c, CUstream st), (c, st))
+NX_DRV(Memcpy3DAsync, CUresult, (const CUDA_MEMCPY3D* c, CUstream st), (c, st))
+NX_DRV(MemcpyPeerAsync, CUresult, (CUdeviceptr d, CUcontext dc, CUdeviceptr s, CUcontext sc, size_t n, CUstream st),
+       (d, dc, s, sc, n, st))
+NX_DRV(Memcpy3DPeerAsync, CUresult, (const CUDA_MEMCPY3D_PEER* c, CUstream st), (c, st))
+NX_DRV(MemcpyBatchAsync, CUresult,
+       (CUdeviceptr* d, CUdeviceptr* s, size_t* sz, size_t n, CUmemcpyAttributes* at, size_t* ai, size_t na, size_t* fi,
+        CUstream st),
+       (d, s, sz, n, at, ai, na, fi, st))
+NX_DRV(Memcpy3DBatchAsync, CUresult, (size_t n, CUDA_MEMCPY3D_BATCH_OP* ops, size_t* fi, unsigned long long fl, CUstream st),
+       (n, ops, fi, fl, st))
+// Synchronous copies and memsets: a paused app's thread must not touch device
+// memory either (its mappings may be gone or, kept stale, another app's).
+NX_DRV(Memcpy, CUresult, (CUdeviceptr d, CUdeviceptr s, size_t n), (d, s, n))
+NX_DRV(MemcpyHtoD, CUresult, (CUdeviceptr d, const void* s, size_t n), (d, s, n))
+NX_DRV(MemcpyDtoH, CUresult, (void* d, CUdeviceptr s, size_t n), (d, s, n))
+NX_DRV(MemcpyDtoD, CUresult, (CUdeviceptr d, CUdeviceptr s, size_t n), (d, s, n))
+NX_DRV(Memcpy2D, CUresult, (const CUDA_MEMCPY2D* c), (c))
+NX_DRV(Memcpy2DUnaligned, CUresult, (const CUDA_MEMCPY2D* c), (c))
+NX_DRV(Memcpy3D, CUresult, (const CUDA_MEMCPY3D* c), (c))
+NX_DRV(MemcpyPeer, CUresult, (CUdeviceptr d, CUcontext dc, CUdeviceptr s, CUcontext sc, size_t n), (d, dc, s, sc, n))
+NX_DRV(Memcpy3DPeer, CUresult, (const CUDA_MEMCPY3D_PEER* c), (c))
+NX_DRV(MemsetD8, CUresult, (CUdeviceptr d, unsigned char v, size_t n), (d, v, n))
+NX_DRV(MemsetD16, CUresult, (CUdeviceptr d, unsigned short v, size_t n), (d, v, n))
+NX_DRV(MemsetD32, CUresult, (CUdeviceptr d, unsigned v, size_t n), (d, v, n))
+NX_DRV(MemsetD2D8, CUresult, (CUdeviceptr d, size_t p, unsigned char v, size_t w, size_t h), (d, p, v, w, h))
+NX_DRV(MemsetD2D16, CUresult, (CUdeviceptr d, size_t p, unsigned short v, size_t w, size_t h), (d, p, v, w, h))
+NX_DRV(MemsetD2D32, CUresult, (CUdeviceptr d, size_t p, unsigned v, size_t w, size_t h), (d, p, v, w, h))
 
 struct DrvWrap {
   const char* name;
@@ -771,7 +929,32 @@ const DrvWrap kDrvWraps[] = {
     NX_ENTRY(MemcpyAsync, "cuMemcpyAsync"),         NX_ENTRY(MemcpyHtoDAsync, "cuMemcpyHtoDAsync"),
     NX_ENTRY(MemcpyDtoHAsync, "cuMemcpyDtoHAsync"), NX_ENTRY(MemcpyDtoDAsync, "cuMemcpyDtoDAsync"),
     NX_ENTRY(MemsetD8Async, "cuMemsetD8Async"),     NX_ENTRY(MemsetD32Async, "cuMemsetD32Async"),
+    NX_ENTRY(MemsetD16Async, "cuMemsetD16Async"),   NX_ENTRY(MemsetD2D8Async, "cuMemsetD2D8Async"),
+    NX_ENTRY(MemsetD2D16Async, "cuMemsetD2D16Async"), NX_ENTRY(MemsetD2D32Async, "cuMemsetD2D32Async"),
+    NX_ENTRY(Memcpy2DAsync, "cuMemcpy2DAsync"),     NX_ENTRY(Memcpy3DAsync, "cuMemcpy3DAsync"),
+    NX_ENTRY(MemcpyPeerAsync, "cuMemcpyPeerAsync"), NX_ENTRY(Memcpy3DPeerAsync, "cuMemcpy3DPeerAsync"),
+    NX_ENTRY(MemcpyBatchAsync, "cuMemcpyBatchAsync"), NX_ENTRY(Memcpy3DBatchAsync, "cuMemcpy3DBatchAsync"),
+    NX_ENTRY(Memcpy, "cuMemcpy"),                   NX_ENTRY(MemcpyHtoD, "cuMemcpyHtoD"),
+    NX_ENTRY(MemcpyDtoH, "cuMemcpyDtoH"),           NX_ENTRY(MemcpyDtoD, "cuMemcpyDtoD"),
+    NX_ENTRY(Memcpy2D, "cuMemcpy2D"),               NX_ENTRY(Memcpy2DUnaligned, "cuMemcpy2DUnaligned"),
+    NX_ENTRY(Memcpy3D, "cuMemcpy3D"),               NX_ENTRY(MemcpyPeer, "cuMemcpyPeer"),
+    NX_ENTRY(Memcpy3DPeer, "cuMemcpy3DPeer"),       NX_ENTRY(MemsetD8, "cuMemsetD8"),
+    NX_ENTRY(MemsetD16, "cuMemsetD16"),             NX_ENTRY(MemsetD32, "cuMemsetD32"),
+    NX_ENTRY(MemsetD2D8, "cuMemsetD2D8"),           NX_ENTRY(MemsetD2D16, "cuMemsetD2D16"),
+    NX_ENTRY(MemsetD2D32, "cuMemsetD2D32"),
 };
+
+// dlsym names carry the ABI version and stream flavour (cuMemcpyHtoD_v2,
+// cuMemsetD8_v2_ptds, cuLaunchKernel_ptsz); cuGetProcAddress takes the base
+// name. The positional arguments are the same across versions.
+std::string base_symbol(const char* name) {
+  std::string n = name;
+  for (const char* suf : {"_ptds", "_ptsz"})
+    if (n.size() > 5 && n.compare(n.size() - 5, 5, suf) == 0) n.resize(n.size() - 5);
+  for (const char* suf : {"_v2", "_v3"})
+    if (n.size() > 3 && n.compare(n.size() - 3, 3, suf) == 0) n.resize(n.size() - 3);
+  return n;
+}
 
 std::mutex g_drv_mu;
 
@@ -857,7 +1040,7 @@ extern "C" void* dlsym(void* handle, const char* name) {
   if (!p || std::strncmp(name, "cu", 2) != 0) return p;
   if (std::strncmp(name, "cuGetProcAddress", 16) != 0) {
     // Direct lookups of the gated entry points (launchers that dlopen libcuda).
-    wrap_proc(name, &p, 0);
+    wrap_proc(base_symbol(name).c_str(), &p, 0);
     return p;
   }
   if (debug_on()) std::fprintf(stderr, "[nixie-shim] dlsym(%s)\n", name);
@@ -881,11 +1064,7 @@ cudaError_t cudaMalloc(void** devPtr, size_t size) {
   REAL(cudaMalloc);
   if (t_in_shim || !active() || size < g.min_bytes) {
     const cudaError_t e = real_cudaMalloc(devPtr, size);
-    if (e == cudaSuccess && g.active && !t_in_shim) {
-      std::lock_guard<std::mutex> lk(g.mu);
-      g.small[*devPtr] = size;
-      g.small_bytes += size;
-    }
+    if (e == cudaSuccess) small_add(*devPtr, size);
     return e;
   }
   return managed_alloc(devPtr, size) == 0 ? cudaSuccess : cudaErrorMemoryAllocation;
@@ -895,14 +1074,7 @@ cudaError_t cudaFree(void* devPtr) {
   REAL(cudaFree);
   if (t_in_shim || !devPtr || !active()) return real_cudaFree(devPtr);
   if (managed_free(devPtr)) return cudaSuccess;
-  {
-    std::lock_guard<std::mutex> lk(g.mu);
-    auto it = g.small.find(devPtr);
-    if (it != g.small.end()) {
-      g.small_bytes -= it->second;
-      g.small.erase(it);
-    }
-  }
+  small_remove(devPtr);
   return real_cudaFree(devPtr);
 }
 
@@ -934,11 +1106,123 @@ cudaError_t cudaFreeAsync(void* devPtr, cudaStream_t stream) {
   return cudaSuccess;
 }
 
+cudaError_t cudaMallocAsync_ptsz(void** devPtr, size_t size, cudaStream_t stream) {
+  REAL(cudaMallocAsync_ptsz);
+  if (t_in_shim || !active() || size < g.min_bytes) return real_cudaMallocAsync_ptsz(devPtr, size, stream);
+  return managed_alloc(devPtr, size) == 0 ? cudaSuccess : cudaErrorMemoryAllocation;
+}
+
+// Pitched allocations: managed ones get rows of pitch_of(width) bytes in the
+// shim's range (any pitch >= width with that alignment is a valid answer).
+cudaError_t cudaMallocPitch(void** devPtr, size_t* pitch, size_t width, size_t height) {
+  REAL(cudaMallocPitch);
+  const std::size_t pt = pitch_of(width);
+  if (t_in_shim || !active() || width == 0 || height == 0 || pt * height < g.min_bytes) {
+    const cudaError_t e = real_cudaMallocPitch(devPtr, pitch, width, height);
+    if (e == cudaSuccess && pitch) small_add(*devPtr, *pitch * height);
+    return e;
+  }
+  if (managed_alloc(devPtr, pt * height) != 0) return cudaErrorMemoryAllocation;
+  *pitch = pt;
+  return cudaSuccess;
+}
+
+cudaError_t cudaMalloc3D(cudaPitchedPtr* pp, cudaExtent ext) {
+  REAL(cudaMalloc3D);
+  const std::size_t pt = pitch_of(ext.width);
+  const std::size_t bytes = pt * ext.height * ext.depth;
+  if (t_in_shim || !active() || bytes == 0 || bytes < g.min_bytes) {
+    const cudaError_t e = real_cudaMalloc3D(pp, ext);
+    if (e == cudaSuccess) small_add(pp->ptr, pp->pitch * ext.height * ext.depth);
+    return e;
+  }
+  void* p = nullptr;
+  if (managed_alloc(&p, bytes) != 0) return cudaErrorMemoryAllocation;
+  pp->ptr = p;
+  pp->pitch = pt;
+  pp->xsize = ext.width;
+  pp->ysize = ext.height;
+  return cudaSuccess;
+}
+
+// ---- implicitly allocating runtime / library calls ---------------------------------------
+cudaError_t cudaStreamCreate(cudaStream_t* st) {
+  REAL(cudaStreamCreate);
+  return implicit_create(cudaSuccess, st, [&] { return real_cudaStreamCreate(st); });
+}
+cudaError_t cudaStreamCreateWithFlags(cudaStream_t* st, unsigned flags) {
+  REAL(cudaStreamCreateWithFlags);
+  return implicit_create(cudaSuccess, st, [&] { return real_cudaStreamCreateWithFlags(st, flags); });
+}
+cudaError_t cudaStreamCreateWithPriority(cudaStream_t* st, unsigned flags, int prio) {
+  REAL(cudaStreamCreateWithPriority);
+  return implicit_create(cudaSuccess, st, [&] { return real_cudaStreamCreateWithPriority(st, flags, prio); });
+}
+cudaError_t cudaStreamDestroy(cudaStream_t st) {
+  REAL(cudaStreamDestroy);
+  const cudaError_t e = real_cudaStreamDestroy(st);
+  implicit_release(st);
+  return e;
+}
+cudaError_t cudaGraphInstantiate(cudaGraphExec_t* ge, cudaGraph_t gr, unsigned long long flags) {
+  REAL(cudaGraphInstantiate);
+  return implicit_create(cudaSuccess, ge, [&] { return real_cudaGraphInstantiate(ge, gr, flags); });
+}
+cudaError_t cudaGraphInstantiateWithFlags(cudaGraphExec_t* ge, cudaGraph_t gr, unsigned long long flags) {
+  REAL(cudaGraphInstantiateWithFlags);
+  return implicit_create(cudaSuccess, ge, [&] { return real_cudaGraphInstantiateWithFlags(ge, gr, flags); });
+}
+cudaError_t cudaGraphExecDestroy(cudaGraphExec_t ge) {
+  REAL(cudaGraphExecDestroy);
+  const cudaError_t e = real_cudaGraphExecDestroy(ge);
+  implicit_release(ge);
+  return e;
+}
+// Stack / heap / printf-FIFO limits resize device reservations: the net
+// change is charged per limit.
+cudaError_t cudaDeviceSetLimit(cudaLimit limit, size_t value) {
+  REAL(cudaDeviceSetLimit);
+  ImplicitScope sc;
+  const cudaError_t e = real_cudaDeviceSetLimit(limit, value);
+  if (sc.on && e == cudaSuccess) implicit_adjust(reinterpret_cast<const void*>(static_cast<std::uintptr_t>(0x10 + limit)), sc.delta());
+  return e;
+}
+cublasStatus_t cublasCreate_v2(cublasHandle_t* h) {
+  static auto real = reinterpret_cast<cublasStatus_t (*)(cublasHandle_t*)>(real_sym("cublasCreate_v2"));
+  return implicit_create(CUBLAS_STATUS_SUCCESS, h, [&] { return real(h); });
+}
+cublasStatus_t cublasDestroy_v2(cublasHandle_t h) {
+  static auto real = reinterpret_cast<cublasStatus_t (*)(cublasHandle_t)>(real_sym("cublasDestroy_v2"));
+  const cublasStatus_t e = real(h);
+  implicit_release(h);
+  return e;
+}
+cublasStatus_t cublasLtCreate(cublasLtHandle_t* h) {
+  static auto real = reinterpret_cast<cublasStatus_t (*)(cublasLtHandle_t*)>(real_sym("cublasLtCreate"));
+  return implicit_create(CUBLAS_STATUS_SUCCESS, h, [&] { return real(h); });
+}
+cublasStatus_t cublasLtDestroy(cublasLtHandle_t h) {
+  static auto real = reinterpret_cast<cublasStatus_t (*)(cublasLtHandle_t)>(real_sym("cublasLtDestroy"));
+  const cublasStatus_t e = real(h);
+  implicit_release(h);
+  return e;
+}
+int cudnnCreate(void** h) {
+  static auto real = reinterpret_cast<int (*)(void**)>(real_sym("cudnnCreate"));
+  return implicit_create(0, h, [&] { return real(h); });
+}
+int cudnnDestroy(void* h) {
+  static auto real = reinterpret_cast<int (*)(void*)>(real_sym("cudnnDestroy"));
+  const int e = real(h);
+  implicit_release(h);
+  return e;
+}
+
 cudaError_t cudaMemGetInfo(size_t* free_b, size_t* total_b) {
   REAL(cudaMemGetInfo);
   if (t_in_shim || !active()) return real_cudaMemGetInfo(free_b, total_b);
   std::lock_guard<std::mutex> lk(g.mu);
-  const std::uint64_t used = g.managed_bytes + g.small_bytes;
+  const std::uint64_t used = g.managed_bytes + g.small_bytes + g.ctl->implicit_bytes.load(std::memory_order_relaxed);
   if (total_b) *total_b = g.budget;
   if (free_b) *free_b = used >= g.budget ? 0 : g.budget - used;
   return cudaSuccess;
@@ -965,7 +1249,49 @@ GATED(cudaError_t, cudaMemcpy2DAsync, (void* d, size_t dp, const void* s, size_t
 GATED(cudaError_t, cudaMemsetAsync, (void* d, int v, size_t n, cudaStream_t st), (d, v, n, st))
 GATED(cudaError_t, cudaMemsetAsync_ptsz, (void* d, int v, size_t n, cudaStream_t st), (d, v, n, st))
 GATED(cudaError_t, cudaMemset, (void* d, int v, size_t n), (d, v, n))
-GATED(cudaError_t, cudaMemcpy2D, (void* d, size_t dp, const void* s, size_t sp, size_t w, size_t h, cudaMemcpyKind k), (d, dp, s, sp, w, h, k))
+GATED(cudaError_t, cudaMemset_ptds, (void* d, int v, size_t n), (d, v, n))
+GATED(cudaError_t, cudaMemcpy2DAsync_ptsz, (void* d, size_t dp, const void* s, size_t sp, size_t w, size_t h, cudaMemcpyKind k, cudaStream_t st), (d, dp, s, sp, w, h, k, st))
+GATED(cudaError_t, cudaMemcpy3DAsync, (const cudaMemcpy3DParms* p, cudaStream_t st), (p, st))
+GATED(cudaError_t, cudaMemcpy3DAsync_ptsz, (const cudaMemcpy3DParms* p, cudaStream_t st), (p, st))
+GATED(cudaError_t, cudaMemcpyPeerAsync, (void* d, int dd, const void* s, int sd, size_t n, cudaStream_t st), (d, dd, s, sd, n, st))
+GATED(cudaError_t, cudaMemcpy3DPeerAsync, (const cudaMemcpy3DPeerParms* p, cudaStream_t st), (p, st))
+GATED(cudaError_t, cudaMemcpy3DPeerAsync_ptsz, (const cudaMemcpy3DPeerParms* p, cudaStream_t st), (p, st))
+GATED(cudaError_t, cudaMemset2D, (void* d, size_t p, int v, size_t w, size_t h), (d, p, v, w, h))
+GATED(cudaError_t, cudaMemset2D_ptds, (void* d, size_t p, int v, size_t w, size_t h), (d, p, v, w, h))
+GATED(cudaError_t, cudaMemset2DAsync, (void* d, size_t p, int v, size_t w, size_t h, cudaStream_t st), (d, p, v, w, h, st))
+GATED(cudaError_t, cudaMemset2DAsync_ptsz, (void* d, size_t p, int v, size_t w, size_t h, cudaStream_t st), (d, p, v, w, h, st))
+GATED(cudaError_t, cudaMemset3D, (cudaPitchedPtr p, int v, cudaExtent e), (p, v, e))
+GATED(cudaError_t, cudaMemset3D_ptds, (cudaPitchedPtr p, int v, cudaExtent e), (p, v, e))
+GATED(cudaError_t, cudaMemset3DAsync, (cudaPitchedPtr p, int v, cudaExtent e, cudaStream_t st), (p, v, e, st))
+GATED(cudaError_t, cudaMemset3DAsync_ptsz, (cudaPitchedPtr p, int v, cudaExtent e, cudaStream_t st), (p, v, e, st))
+GATED(cudaError_t, cudaMemcpyBatchAsync,
+      (void** d, void** s, size_t* sz, size_t n, cudaMemcpyAttributes* a, size_t* ai, size_t na, size_t* fi, cudaStream_t st),
+      (d, s, sz, n, a, ai, na, fi, st))
+GATED(cudaError_t, cudaMemcpyBatchAsync_ptsz,
+      (void** d, void** s, size_t* sz, size_t n, cudaMemcpyAttributes* a, size_t* ai, size_t na, size_t* fi, cudaStream_t st),
+      (d, s, sz, n, a, ai, na, fi, st))
+GATED(cudaError_t, cudaMemcpy3DBatchAsync, (size_t n, cudaMemcpy3DBatchOp* ops, size_t* fi, unsigned long long fl, cudaStream_t st),
+      (n, ops, fi, fl, st))
+GATED(cudaError_t, cudaMemcpy3DBatchAsync_ptsz, (size_t n, cudaMemcpy3DBatchOp* ops, size_t* fi, unsigned long long fl, cudaStream_t st),
+      (n, ops, fi, fl, st))
+
+// Synchronous copies: gated, and blocking calls for the MLFQ's idleness test.
+#define GATED_SYNC(ret, name, params, args) \
+  ret name params {                         \
+    REAL(name);                             \
+    Gate gate_;                             \
+    Blocking b_;                            \
+    return real_##name args;                \
+  }
+
+GATED_SYNC(cudaError_t, cudaMemcpy2D, (void* d, size_t dp, const void* s, size_t sp, size_t w, size_t h, cudaMemcpyKind k), (d, dp, s, sp, w, h, k))
+GATED_SYNC(cudaError_t, cudaMemcpy2D_ptds, (void* d, size_t dp, const void* s, size_t sp, size_t w, size_t h, cudaMemcpyKind k), (d, dp, s, sp, w, h, k))
+GATED_SYNC(cudaError_t, cudaMemcpy_ptds, (void* d, const void* s, size_t n, cudaMemcpyKind k), (d, s, n, k))
+GATED_SYNC(cudaError_t, cudaMemcpy3D, (const cudaMemcpy3DParms* p), (p))
+GATED_SYNC(cudaError_t, cudaMemcpy3D_ptds, (const cudaMemcpy3DParms* p), (p))
+GATED_SYNC(cudaError_t, cudaMemcpyPeer, (void* d, int dd, const void* s, int sd, size_t n), (d, dd, s, sd, n))
+GATED_SYNC(cudaError_t, cudaMemcpy3DPeer, (const cudaMemcpy3DPeerParms* p), (p))
+GATED_SYNC(cudaError_t, cudaMemcpy3DPeer_ptds, (const cudaMemcpy3DPeerParms* p), (p))
 
 // Like GATED, for names the C++ headers overload (the real symbol is the C one).
 #define GATED_C(ret, name, params, args)                                               \
@@ -1085,6 +1411,101 @@ CUresult cuLaunchKernel(CUfunction f, unsigned gx, unsigned gy, unsigned gz, uns
   Gate gate_;
   return real_cuLaunchKernel(f, gx, gy, gz, bx, by, bz, smem, st, params, extra);
 }
+
+CUresult cuMemAllocPitch_v2(CUdeviceptr* dptr, size_t* pitch, size_t width, size_t height, unsigned elem) {
+  REAL(cuMemAllocPitch_v2);
+  const std::size_t pt = pitch_of(width);
+  if (t_in_shim || !active() || width == 0 || height == 0 || pt * height < g.min_bytes)
+    return real_cuMemAllocPitch_v2(dptr, pitch, width, height, elem);
+  if (elem != 4 && elem != 8 && elem != 16) return CUDA_ERROR_INVALID_VALUE;
+  void* p = nullptr;
+  if (managed_alloc(&p, pt * height) != 0) return CUDA_ERROR_OUT_OF_MEMORY;
+  *dptr = reinterpret_cast<CUdeviceptr>(p);
+  *pitch = pt;
+  return CUDA_SUCCESS;
+}
+
+// Stream-ordered driver allocations: as cudaMallocAsync / cudaFreeAsync.
+CUresult cuMemAllocAsync(CUdeviceptr* dptr, size_t bytes, CUstream st) {
+  REAL(cuMemAllocAsync);
+  if (t_in_shim || !active() || bytes < g.min_bytes) return real_cuMemAllocAsync(dptr, bytes, st);
+  void* p = nullptr;
+  if (managed_alloc(&p, bytes) != 0) return CUDA_ERROR_OUT_OF_MEMORY;
+  *dptr = reinterpret_cast<CUdeviceptr>(p);
+  return CUDA_SUCCESS;
+}
+
+CUresult cuMemFreeAsync(CUdeviceptr dptr, CUstream st) {
+  REAL(cuMemFreeAsync);
+  if (t_in_shim || !dptr || !active()) return real_cuMemFreeAsync(dptr, st);
+  bool managed = false;
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    managed = g.regions.count(dptr) != 0;
+  }
+  if (!managed) return real_cuMemFreeAsync(dptr, st);
+  static auto sync = reinterpret_cast<CUresult (*)(CUstream)>(real_sym("cuStreamSynchronize"));
+  t_in_shim++;
+  const CUresult e = sync(st);
+  t_in_shim--;
+  if (e != CUDA_SUCCESS) return e;
+  managed_free(reinterpret_cast<void*>(dptr));
+  return CUDA_SUCCESS;
+}
+
+CUresult cuStreamCreate(CUstream* st, unsigned flags) {
+  REAL(cuStreamCreate);
+  return implicit_create(CUDA_SUCCESS, st, [&] { return real_cuStreamCreate(st, flags); });
+}
+CUresult cuStreamCreateWithPriority(CUstream* st, unsigned flags, int prio) {
+  REAL(cuStreamCreateWithPriority);
+  return implicit_create(CUDA_SUCCESS, st, [&] { return real_cuStreamCreateWithPriority(st, flags, prio); });
+}
+CUresult cuStreamDestroy_v2(CUstream st) {
+  REAL(cuStreamDestroy_v2);
+  const CUresult e = real_cuStreamDestroy_v2(st);
+  implicit_release(st);
+  return e;
+}
+
+// Driver launches, graph launches, copies and memsets called through the PLT
+// (applications linked against libcuda): the same gate as the table entries.
+#define GATED_DRV(name, params, args) \
+  CUresult name params {              \
+    REAL(name);                       \
+    Gate gate_;                       \
+    return real_##name args;          \
+  }
+
+GATED_DRV(cuLaunchKernelEx, (const CUlaunchConfig* c, CUfunction f, void** p, void** e), (c, f, p, e))
+GATED_DRV(cuLaunchCooperativeKernel,
+          (CUfunction f, unsigned gx, unsigned gy, unsigned gz, unsigned bx, unsigned by, unsigned bz, unsigned sm, CUstream st, void** p),
+          (f, gx, gy, gz, bx, by, bz, sm, st, p))
+GATED_DRV(cuGraphLaunch, (CUgraphExec e, CUstream st), (e, st))
+GATED_DRV(cuMemcpy, (CUdeviceptr d, CUdeviceptr s, size_t n), (d, s, n))
+GATED_DRV(cuMemcpyAsync, (CUdeviceptr d, CUdeviceptr s, size_t n, CUstream st), (d, s, n, st))
+GATED_DRV(cuMemcpyHtoD_v2, (CUdeviceptr d, const void* s, size_t n), (d, s, n))
+GATED_DRV(cuMemcpyDtoH_v2, (void* d, CUdeviceptr s, size_t n), (d, s, n))
+GATED_DRV(cuMemcpyDtoD_v2, (CUdeviceptr d, CUdeviceptr s, size_t n), (d, s, n))
+GATED_DRV(cuMemcpyHtoDAsync_v2, (CUdeviceptr d, const void* s, size_t n, CUstream st), (d, s, n, st))
+GATED_DRV(cuMemcpyDtoHAsync_v2, (void* d, CUdeviceptr s, size_t n, CUstream st), (d, s, n, st))
+GATED_DRV(cuMemcpyDtoDAsync_v2, (CUdeviceptr d, CUdeviceptr s, size_t n, CUstream st), (d, s, n, st))
+GATED_DRV(cuMemcpy2D_v2, (const CUDA_MEMCPY2D* c), (c))
+GATED_DRV(cuMemcpy2DUnaligned_v2, (const CUDA_MEMCPY2D* c), (c))
+GATED_DRV(cuMemcpy2DAsync_v2, (const CUDA_MEMCPY2D* c, CUstream st), (c, st))
+GATED_DRV(cuMemcpy3D_v2, (const CUDA_MEMCPY3D* c), (c))
+GATED_DRV(cuMemcpy3DAsync_v2, (const CUDA_MEMCPY3D* c, CUstream st), (c, st))
+GATED_DRV(cuMemcpyPeer, (CUdeviceptr d, CUcontext dc, CUdeviceptr s, CUcontext sc, size_t n), (d, dc, s, sc, n))
+GATED_DRV(cuMemcpyPeerAsync, (CUdeviceptr d, CUcontext dc, CUdeviceptr s, CUcontext sc, size_t n, CUstream st), (d, dc, s, sc, n, st))
+GATED_DRV(cuMemsetD8_v2, (CUdeviceptr d, unsigned char v, size_t n), (d, v, n))
+GATED_DRV(cuMemsetD16_v2, (CUdeviceptr d, unsigned short v, size_t n), (d, v, n))
+GATED_DRV(cuMemsetD32_v2, (CUdeviceptr d, unsigned v, size_t n), (d, v, n))
+GATED_DRV(cuMemsetD8Async, (CUdeviceptr d, unsigned char v, size_t n, CUstream st), (d, v, n, st))
+GATED_DRV(cuMemsetD16Async, (CUdeviceptr d, unsigned short v, size_t n, CUstream st), (d, v, n, st))
+GATED_DRV(cuMemsetD32Async, (CUdeviceptr d, unsigned v, size_t n, CUstream st), (d, v, n, st))
+GATED_DRV(cuMemsetD2D8_v2, (CUdeviceptr d, size_t p, unsigned char v, size_t w, size_t h), (d, p, v, w, h))
+GATED_DRV(cuMemsetD2D16_v2, (CUdeviceptr d, size_t p, unsigned short v, size_t w, size_t h), (d, p, v, w, h))
+GATED_DRV(cuMemsetD2D32_v2, (CUdeviceptr d, size_t p, unsigned v, size_t w, size_t h), (d, p, v, w, h))
 
 // Introspection for tests: 1 when the shim is connected to a daemon.
 int nixie_shim_active(void) { return active() ? 1 : 0; }

@@ -210,3 +210,58 @@ def test_app_killed_mid_run_does_not_stall_the_others():
     byes = [r for r in recs if r.get("event") == "bye"]
     assert len(byes) == 3
     assert all(r["mismatches"] == 0 for r in recs if r.get("event") == "switch")
+
+
+@pytest.mark.parametrize("combo", ["pitch_launchex", "drvpitch_async"])
+def test_interposer_api_breadth(combo):
+    """PAPER.md:137's breadth: working sets allocated with cudaMallocPitch /
+    cudaMalloc3D / cuMemAllocPitch / cuMemAllocAsync, kernels launched with
+    cuLaunchKernelEx (through the cuGetProcAddress table and through the
+    PLT), and every iteration opening with synchronous cudaMemcpy2D,
+    cudaMemcpy3D, cudaMemset2D and cuMemsetD32 calls right after a think gap
+    (when the app has likely been switched out). Two apps oversubscribe a
+    4 GiB budget with stale mappings kept (the default for two apps), so an
+    ungated synchronous call would read the other app's data (sync_mismatch)
+    or fault; all results must be byte-exact."""
+    a, b = {"pitch_launchex": (["--alloc", "pitch", "--driver", "2", "--streams", "8"], ["--alloc", "3d", "--driver", "3"]),
+            "drvpitch_async": (["--alloc", "drvpitch", "--driver", "2"], ["--alloc", "async", "--driver", "3", "--streams", "4"])}[combo]
+    with Daemon(gpu="4G", pinned="4G", paged="16G") as d:
+        res = run_apps(d, [_vec(3072, 5, 250, 91, "a") + a + ["--sync-ops", "1"],
+                           _vec(3072, 5, 250, 92, "b") + b + ["--sync-ops", "1"]], timeout=600)
+        _save("breadth_" + combo, d, res)
+        _check(res, d)
+        sw = d.switches()
+        recs = d.records()
+    for r in res:
+        o = r["out"]
+        assert o["device_errors"] == 0 and o["host_mismatch"] == 0 and o["sync_mismatch"] == 0, o
+        assert o["sync_calls"] == 7 * 5
+        assert o["bytes"] >= 3000 << 20
+    assert len(sw) >= 3 and all(s["mismatches"] == 0 for s in sw)
+    # the managed working sets crossed the link in both directions
+    assert sum(s["pcie_h2d"] for s in sw) >= 3 << 30 and sum(s["pcie_d2h"] for s in sw) >= 3 << 30
+    byes = [r for r in recs if r.get("event") == "bye"]
+    assert len(byes) == 2 and max(b_["table_launches"] for b_ in byes) >= 5 * 6
+
+
+def test_implicit_allocations_count_against_the_budget():
+    """cudaDeviceSetLimit(cudaLimitStackSize) grows the device's local-memory
+    reservation: the shim charges the drop in free memory to the app, its
+    cudaMemGetInfo reports it as used, and the daemon refuses a managed
+    allocation that would push managed + implicit bytes past the budget."""
+    with Daemon(gpu="4G", pinned="4G", paged="16G") as d:
+        res = run_apps(d, [_vec(1024, 1, 0, 7, "base")], timeout=300)
+        _check(res, d)
+        res2 = run_apps(d, [_vec(1024, 1, 0, 8, "stack") + ["--stack-kib", "4", "--streams", "4"]], timeout=300)
+        _check(res2, d)
+    used_base = res[0]["out"]["memgetinfo"][1] - res[0]["out"]["memgetinfo"][0]
+    used_stack = res2[0]["out"]["memgetinfo"][1] - res2[0]["out"]["memgetinfo"][0]
+    assert used_stack >= used_base + (64 << 20), (used_base, used_stack)
+    implicit = used_stack - used_base
+    # Now a working set that fits the budget alone but not with the stack
+    # reservation: the allocation that crosses the budget fails.
+    mib = (4096 - (implicit >> 20) // 2)  # > budget - implicit
+    with Daemon(gpu="4G", pinned="4G", paged="16G") as d:
+        p = d.spawn(_vec(mib, 1, 0, 9, "over") + ["--stack-kib", "4"])
+        out, err = p.communicate(timeout=300)
+    assert p.returncode != 0 and "out of memory" in err, (p.returncode, err[-400:])

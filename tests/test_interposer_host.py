@@ -22,6 +22,25 @@ INTERPOSED = {
     "cudaStreamBeginCapture", "cudaStreamEndCapture",
     "cublasLtMatmul", "cublasGemmEx", "cublasGemmStridedBatchedEx", "cublasSgemm_v2", "cublasSgemmStridedBatched",
     "cudnnBackendExecute",
+    # allocation breadth
+    "cudaMallocAsync_ptsz", "cudaMallocPitch", "cudaMalloc3D", "cuMemAllocPitch_v2", "cuMemAllocAsync", "cuMemFreeAsync",
+    # implicitly allocating APIs
+    "cudaStreamCreate", "cudaStreamCreateWithFlags", "cudaStreamCreateWithPriority", "cudaStreamDestroy",
+    "cudaGraphInstantiate", "cudaGraphInstantiateWithFlags", "cudaGraphExecDestroy", "cudaDeviceSetLimit",
+    "cuStreamCreate", "cuStreamCreateWithPriority", "cuStreamDestroy_v2", "cublasCreate_v2", "cublasDestroy_v2",
+    "cublasLtCreate", "cublasLtDestroy", "cudnnCreate", "cudnnDestroy",
+    # every copy / memset that can touch device memory
+    "cudaMemcpy_ptds", "cudaMemcpy2D_ptds", "cudaMemcpy2DAsync_ptsz", "cudaMemcpy3D", "cudaMemcpy3D_ptds",
+    "cudaMemcpy3DAsync", "cudaMemcpy3DAsync_ptsz", "cudaMemcpyPeer", "cudaMemcpyPeerAsync", "cudaMemcpy3DPeer",
+    "cudaMemcpy3DPeer_ptds", "cudaMemcpy3DPeerAsync", "cudaMemcpy3DPeerAsync_ptsz", "cudaMemcpyBatchAsync",
+    "cudaMemcpyBatchAsync_ptsz", "cudaMemcpy3DBatchAsync", "cudaMemcpy3DBatchAsync_ptsz", "cudaMemset_ptds",
+    "cudaMemset2D", "cudaMemset2D_ptds", "cudaMemset2DAsync", "cudaMemset2DAsync_ptsz", "cudaMemset3D",
+    "cudaMemset3D_ptds", "cudaMemset3DAsync", "cudaMemset3DAsync_ptsz",
+    "cuLaunchKernelEx", "cuLaunchCooperativeKernel", "cuGraphLaunch", "cuMemcpy", "cuMemcpyAsync", "cuMemcpyHtoD_v2",
+    "cuMemcpyDtoH_v2", "cuMemcpyDtoD_v2", "cuMemcpyHtoDAsync_v2", "cuMemcpyDtoHAsync_v2", "cuMemcpyDtoDAsync_v2",
+    "cuMemcpy2D_v2", "cuMemcpy2DUnaligned_v2", "cuMemcpy2DAsync_v2", "cuMemcpy3D_v2", "cuMemcpy3DAsync_v2",
+    "cuMemcpyPeer", "cuMemcpyPeerAsync", "cuMemsetD8_v2", "cuMemsetD16_v2", "cuMemsetD32_v2", "cuMemsetD8Async",
+    "cuMemsetD16Async", "cuMemsetD32Async", "cuMemsetD2D8_v2", "cuMemsetD2D16_v2", "cuMemsetD2D32_v2",
 }
 
 
@@ -36,7 +55,7 @@ def test_shim_exports_exactly_the_interposed_api():
     assert syms == want, sorted(syms ^ want)
     header = open(os.path.join(ROOT, "include", "nixie_shim.h")).read()
     for s in INTERPOSED:
-        base = s.replace("_ptsz", "")
+        base = s.replace("_ptsz", "").replace("_ptds", "")
         assert base in header, f"{s} not documented in include/nixie_shim.h"
 
 
@@ -54,6 +73,13 @@ def test_daemon_cli():
     assert r.returncode == 0 and "--socket" in r.stderr and "--phys-slack" in r.stderr
     r = subprocess.run([NIXIED, "--bogus"], capture_output=True, text=True, timeout=60)
     assert r.returncode == 1
+    # --slab-mib is validated as given: no truncation of 1 or 3 into a default or a neighbour
+    for bad in ("1", "3", "5", "2048", "x", "64m"):
+        r = subprocess.run([NIXIED, "--slab-mib", bad, "--help"], capture_output=True, text=True, timeout=60)
+        assert r.returncode == 1 and "power of two" in r.stderr, (bad, r.stderr)
+    r = subprocess.run([NIXIED, "--trace", "/tmp/x", "--prefetch", "--socket", "/nonexistent/dir/s"], capture_output=True,
+                       text=True, timeout=60)
+    assert r.returncode == 1 and "--trace" in r.stderr
 
 
 def test_test_app_links_the_shared_runtime():
