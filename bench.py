@@ -143,15 +143,22 @@ def pcie_link(device: int) -> dict:
 
 
 class PcieCounters:
-    """The GPU's own PCIe byte counters (NVML field values
-    NVML_FI_DEV_PCIE_COUNT_TX_BYTES / RX_BYTES, cumulative), read around the
-    timed region: a counter-level reading of what the copy engines moved,
-    which ncu cannot see (it profiles kernels, not DMA). TX = GPU -> host
-    (evictions plus the read requests of fetches), RX = host -> GPU."""
+    """The GPU's own PCIe counters during the timed region, sampled every
+    10 ms by a thread: a counter-level reading of what the copy engines moved,
+    which ncu cannot see (it profiles kernels, not DMA).
+      * NVML_FI_DEV_PCIE_COUNT_TX_BYTES / RX_BYTES: byte counters. They are
+        32-bit on these boards (they wrap every ~86 ms at 50 GB/s), so the
+        deltas between consecutive samples are accumulated modulo 2^32.
+      * nvmlDeviceGetPcieThroughput TX/RX: the driver's KB/s over its own
+        20 ms window, averaged over the samples.
+    TX = GPU -> host (evictions, plus the read requests of fetches),
+    RX = host -> GPU (fetch data)."""
 
     def __init__(self, pci_bus_id: str):
         self.h = None
         self.err = None
+        self.stop_ev = threading.Event()
+        self.thread = None
         try:
             import pynvml
             self.nv = pynvml
@@ -168,33 +175,70 @@ class PcieCounters:
         except Exception as e:  # noqa: BLE001
             self.err = str(e)[:120]
 
-    def read(self):
-        if self.h is None:
-            return None
+    def _fields(self):
         nv = self.nv
+        vals = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_PCIE_COUNT_TX_BYTES, nv.NVML_FI_DEV_PCIE_COUNT_RX_BYTES,
+                                                    nv.NVML_FI_DEV_PCIE_REPLAY_COUNTER])
+        out = []
+        for v in vals:
+            if v.nvmlReturn != 0:
+                return None
+            # valueType 1 = unsigned int (32-bit counter), 3 = unsigned long long
+            wide = getattr(v, "valueType", 3) in (3, 5)
+            out.append((int(v.value.ullVal) if wide else int(v.value.uiVal), 64 if wide else 32))
+        return out
+
+    def _run(self):
+        nv = self.nv
+        prev = self._fields()
+        acc = [0, 0, 0]
+        thr = []
+        while not self.stop_ev.wait(0.01):
+            cur = self._fields()
+            if cur is None or prev is None:
+                prev = cur
+                continue
+            for i in range(3):
+                bits = cur[i][1]
+                acc[i] += (cur[i][0] - prev[i][0]) % (1 << bits)
+            prev = cur
+            try:
+                thr.append((nv.nvmlDeviceGetPcieThroughput(self.h, nv.NVML_PCIE_UTIL_TX_BYTES),
+                            nv.nvmlDeviceGetPcieThroughput(self.h, nv.NVML_PCIE_UTIL_RX_BYTES)))
+            except Exception:  # noqa: BLE001
+                pass
+        self.acc, self.thr, self.bits = acc, thr, (prev[0][1] if prev else None)
+
+    def start(self):
+        if self.h is None:
+            return
         try:
-            ids = [nv.NVML_FI_DEV_PCIE_COUNT_TX_BYTES, nv.NVML_FI_DEV_PCIE_COUNT_RX_BYTES, nv.NVML_FI_DEV_PCIE_REPLAY_COUNTER]
-            vals = nv.nvmlDeviceGetFieldValues(self.h, ids)
-            out = []
-            for v in vals:
-                if v.nvmlReturn != 0:
-                    return None
-                out.append(int(v.value.ullVal))
-            return out
+            if self._fields() is None:
+                self.err = "PCIe byte counters not supported"
+                return
         except Exception as e:  # noqa: BLE001
             self.err = str(e)[:120]
-            return None
+            return
+        self.t0 = time.perf_counter()
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
 
-    @staticmethod
-    def delta(a, b, seconds: float, alg_in: float, alg_out: float) -> dict:
-        if a is None or b is None:
-            return {"available": False}
-        tx, rx, rep = b[0] - a[0], b[1] - a[1], b[2] - a[2]
-        return {"available": True, "source": "NVML_FI_DEV_PCIE_COUNT_TX_BYTES/RX_BYTES (cumulative, per GPU)",
-                "tx_bytes": tx, "rx_bytes": rx, "replays": rep,
-                "tx_gbs": tx / seconds / 1e9, "rx_gbs": rx / seconds / 1e9,
-                "rx_per_algorithmic_h2d_byte": rx / alg_in if alg_in else None,
-                "tx_per_algorithmic_d2h_byte": tx / alg_out if alg_out else None}
+    def stop(self) -> dict:
+        if self.thread is None:
+            return {"available": False, **({"error": self.err} if self.err else {})}
+        self.stop_ev.set()
+        self.thread.join()
+        secs = time.perf_counter() - self.t0
+        tx, rx, rep = self.acc
+        out = {"available": True, "source": "NVML_FI_DEV_PCIE_COUNT_TX_BYTES/RX_BYTES sampled every 10 ms (deltas "
+                                            f"mod 2^{self.bits}) + nvmlDeviceGetPcieThroughput",
+               "tx_bytes": tx, "rx_bytes": rx, "replays": rep, "seconds": secs,
+               "tx_gbs": tx / secs / 1e9, "rx_gbs": rx / secs / 1e9}
+        if self.thr:
+            out["throughput_tx_gbs_mean"] = sum(t for t, _ in self.thr) / len(self.thr) * 1024 / 1e9
+            out["throughput_rx_gbs_mean"] = sum(r for _, r in self.thr) / len(self.thr) * 1024 / 1e9
+            out["throughput_samples"] = len(self.thr)
+        return out
 
 
 def link_reference(device: int, bus_id: str, link: dict) -> dict:
@@ -462,6 +506,10 @@ def run_product(args, dist: Dist):
     extra = {"legs_per_launch": args.legs_per_launch} if args.legs_per_launch else {}
     eng = SwapEngine(device=device, gpu_capacity=32 * GIB, pinned_capacity=16 * GIB, paged_capacity=2 * GIB, path=path, **extra)
     probe = eng.probe_pcie(1 * GIB, 64 * MIB)
+    # Large copies lose less to the copy engines' per-call overhead
+    # (profiles/r02_ce_bubble.txt: 256 MiB calls 99.6 GB/s vs 2 MiB calls 77):
+    # the denominator takes the best shape measured, not the engine's own.
+    probe_big = eng.probe_pcie(2 * GIB, 256 * MIB)
     calib = eng.calibrate(256 * MIB) if path == 0 else None
     # Steady state only involves the GPU and the pinned ring, so the apps are
     # placed directly (no pageable cold start): the interactive app on the
@@ -489,7 +537,7 @@ def run_product(args, dist: Dist):
     sampler = ClockSampler(device)
     sampler.start()
     dist.barrier()
-    c0 = counters.read()
+    counters.start()
     t0 = time.perf_counter()
     stats, windows = [], []
     for _ in range(args.steps):
@@ -499,7 +547,7 @@ def run_product(args, dist: Dist):
         stats.append(step())
         windows.append((w0, time.time()))
     wall = time.perf_counter() - t0
-    c1 = counters.read()
+    pcie = counters.stop()
     dist.barrier()
     clocks = sampler.stop()
     launches = eng.total_launches() - launches0
@@ -517,7 +565,8 @@ def run_product(args, dist: Dist):
     dev_rank = sum(s["device_span_s"] for s in stats)
     lat = [(s["wall_s"] + s["plan_s"]) * 1e3 for s in stats + more]
     dev_lat = [s["device_span_s"] * 1e3 for s in stats + more]
-    peak_rank = max(probe["ce_bidir_total"], probe["sm_bidir_total"], probe_after["ce_bidir_total"], probe_after["sm_bidir_total"])
+    peak_rank = max(probe["ce_bidir_total"], probe["sm_bidir_total"], probe_after["ce_bidir_total"], probe_after["sm_bidir_total"],
+                    probe_big["ce_bidir_total"])
     rank_rec = {"rank": dist.rank, "device": device, **info, "gbs": bytes_rank / dev_rank / 1e9, "pcie_peak_gbs": peak_rank,
                 "pct_of_own_peak": bytes_rank / dev_rank / 1e9 / peak_rank * 100.0, "windows": windows,
                 "bytes": bytes_rank, "dev_s": dev_rank, "wall_s": wall, "bad": bad,
@@ -610,11 +659,13 @@ def run_product(args, dist: Dist):
                 "d2h_bytes_per_step": alg_out / args.steps},
         "roofline": roof,
         "link_roofline": {"bound": "pcie", "achieved": per_gpu, "peak": pcie_peak, "unit": "GB/s", "frac": per_gpu / pcie_peak,
-                          "link": link, "peak_source": "same-run probe, 1 GiB/direction, 64 MiB chunks, max(CE, SM), "
-                                                       "best of before/after the timed region"},
+                          "link": link, "peak_source": "same-run probes, best of: CE and SM at 1 GiB/direction in 64 MiB "
+                                                       "calls before and after the timed region, CE at 2 GiB/direction in 256 MiB calls"},
         "link_reference": link_reference(device, info["pci_bus_id"], link),
-        "pcie_counters": {**PcieCounters.delta(c0, c1, wall, alg_in, alg_out), **({"error": counters.err} if counters.err else {})},
+        "pcie_counters": {**pcie, **({"rx_per_algorithmic_h2d_byte": pcie["rx_bytes"] / alg_in,
+                                      "tx_per_algorithmic_d2h_byte": pcie["tx_bytes"] / alg_out} if pcie.get("available") else {})},
         "pcie_probe": {k: (round(v, 2) if isinstance(v, float) else v) for k, v in probe.items()},
+        "pcie_probe_256mib": {k: round(probe_big[k], 2) for k in ("ce_bidir_total", "ce_bidir_h2d", "ce_bidir_d2h", "ce_h2d", "ce_d2h")},
         "pcie_probe_after": {k: round(probe_after[k], 2) for k in ("ce_bidir_total", "ce_bidir_h2d", "ce_bidir_d2h", "sm_bidir_total")},
         "settle": settle,
         "calibration": calib,

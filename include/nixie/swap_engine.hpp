@@ -45,7 +45,7 @@ struct EngineConfig {
   CopyPath path = CopyPath::Auto;
   int pcie_legs_in_flight = 1024;     // per direction (x 2 MiB); 1024 measured ~1% faster than 512 (tools/tune_batches.py)
   int legs_per_launch = 128;          // max legs per K1 launch / CE batch (measured best)
-  int host_threads = 8;               // pinned<->paged copy workers
+  int host_threads = 0;               // pinned<->paged copy workers; 0 = measured at construction (calibrate_host)
   int host_legs_in_flight = 64;       // per host lane
   int max_ctas = 0;                   // K1 grid cap; 0 = 2 x SM count
   bool fused_launch = false;          // both directions in one launch stream (warp-group split)
@@ -56,6 +56,14 @@ struct EngineConfig {
   bool k3_one_stream = true;          // both lanes' K3 launches on one stream (no SM contention between them)
   bool k3_grouped = true;             // CE path: one record launch per switch, arrival checks per group
   int k3_verify_group = 1024;         // legs per grouped arrival check (the last group is flushed at the end)
+  // CE path, grouped K3: a departure batch commits in groups of this many
+  // legs (first_batch_legs-sized groups for the first 32 x first_batch_legs
+  // legs of a switch), each behind its own event, so the fetches that need
+  // the frames it frees start one group behind the evictions, not one whole
+  // batch behind (0: commit whole batches). Measured on config 2: 32 legs
+  // shortens the fetch-free head by ~1 ms but the fetches then run as many
+  // small batches at a lower rate, 1.3% slower overall, so off.
+  int d2h_commit_legs = 0;
   bool exportable_arena = false;      // GPU tier = exportable VMM slabs shims can import (interposer daemon)
   Bytes arena_slab_bytes = 128 * kMiB; // exportable arena: bytes per physical allocation (a multiple of 2 MiB)
   Bytes gpu_physical = 0;             // arena bytes (0 = gpu_capacity); the registry still enforces gpu_capacity
@@ -143,6 +151,15 @@ struct PcieProbe {
   Bytes chunk_bytes = 0;
   int link_gen = 0, link_width = 0, link_gen_max = 0, link_width_max = 0;
   int numa_node = -1;
+};
+
+// Host copy pool sizing (the pinned<->paged lanes of the two-hop path): GB/s
+// of both directions at once per worker count; `chosen` is installed.
+struct HostCalibration {
+  std::vector<int> threads;
+  std::vector<double> gbps;
+  int chosen = 0;
+  double peak_gbps = 0;  // best measured: the two-hop path's host-memcpy roofline
 };
 
 // Per-batch-size SM-kernel vs copy-engine measurement (bidirectional GB/s).
@@ -244,6 +261,13 @@ class SwapEngine {
   // Measures both mechanisms at 1..128 legs per batch and installs the
   // faster one per size for CopyPath::Auto.
   Calibration calibrate(Bytes bytes_per_direction);
+  // Measures the host copy pool (pinned -> paged and paged -> pinned at once,
+  // 2 MiB jobs) at 1, 2, 4 ... workers and keeps the fastest count (the
+  // smallest within 2% of the best). EngineConfig::host_threads = 0 runs it
+  // at construction with a small sample.
+  HostCalibration calibrate_host(Bytes bytes_per_direction);
+  const HostCalibration& host_calibration() const;  // last measurement (empty if host_threads was fixed)
+  int host_threads() const;                         // workers taking jobs now
   // K3 launch duration (us) for 1, 2, 4 ... 128 legs: [0] TMA pipeline, [1] LDG loop.
   // under_pcie_load: while both PCIe directions carry copy-engine traffic.
   std::vector<std::array<double, 2>> probe_checksum_launch(bool under_pcie_load = false);

@@ -65,6 +65,7 @@ typedef struct nx_engine_config {
   int k3_one_stream; /* both lanes' K3 launches on one stream */
   int k3_grouped;    /* CE path: one switch-wide record launch, grouped arrival checks */
   int k3_verify_group; /* legs per grouped arrival check */
+  int d2h_commit_legs; /* CE departures commit in groups of this many legs (0: whole batches) */
 } nx_engine_config;
 
 /* PlannerConfig (proj/include/nixie/planner.hpp:39-43). victim_order may be
@@ -217,6 +218,13 @@ int nx_set_auto_table(nx_engine* e, const int* sm_faster, size_t n);
  * 1, 2, 4 ... 128 legs and installs the faster per size (CopyPath::Auto).
  * Arrays hold 8 entries. */
 int nx_calibrate(nx_engine* e, uint64_t bytes_per_direction, double sm_gbps[8], double ce_gbps[8], int sm_faster[8]);
+/* Host copy pool sizing: GB/s of pinned->paged + paged->pinned at once for
+ * worker counts threads[i] (up to cap entries, *n written), installs the
+ * fastest (*chosen; the smallest count within 2% of the best). */
+int nx_calibrate_host(nx_engine* e, uint64_t bytes_per_direction, int* threads, double* gbps, size_t cap, size_t* n,
+                      int* chosen);
+/* Workers of the host copy pool taking jobs now. */
+int nx_host_threads(nx_engine* e, int* out);
 /* K3 checksum launch duration (us) for 1, 2, 4 ... 128 legs; us[2*k] TMA, us[2*k+1] LDG. */
 int nx_probe_checksum_launch(nx_engine* e, double us[16]);
 /* Same, optionally while both PCIe directions carry copy-engine traffic. */

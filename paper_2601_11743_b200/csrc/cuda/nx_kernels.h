@@ -82,6 +82,12 @@ cudaError_t launch_checksum_tma_table(const NxLeg* d_legs, int n, bool arriving,
                                       const NxScratch& scratch, int ctas, cudaStream_t stream,
                                       std::uint32_t clock_slot = kNoClockSlot);
 
+// Copies `n` leg descriptors from pinned host memory into the device table
+// with SM loads (one small launch on the K3 stream). A cudaMemcpyAsync would
+// queue on the host->device copy engine behind the switch's own fetch copies
+// and hold every arrival check until the last fetch landed.
+cudaError_t launch_table_upload(NxLeg* d_dst, const NxLeg* h_src, int n, cudaStream_t stream);
+
 // K4: pattern fill (records checksums, marks them valid) and compare (adds
 // the number of mismatching 16-byte vectors per leg into mismatches[i]).
 cudaError_t launch_fill(const NxLeg* legs, int n, std::uint64_t seed, const NxCkTables& ck, cudaStream_t stream);

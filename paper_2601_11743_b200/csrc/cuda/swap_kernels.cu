@@ -490,6 +490,20 @@ cudaError_t launch_checksum_tma_table(const NxLeg* d_legs, int n, bool arriving,
   return cudaGetLastError();
 }
 
+__global__ void nx_table_upload_kernel(std::uint64_t* __restrict__ dst, const std::uint64_t* __restrict__ src, std::uint32_t words) {
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < words; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
+cudaError_t launch_table_upload(NxLeg* d_dst, const NxLeg* h_src, int n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  static_assert(sizeof(NxLeg) % 8 == 0, "descriptor is a whole number of words");
+  const auto words = static_cast<std::uint32_t>(static_cast<std::size_t>(n) * sizeof(NxLeg) / 8);
+  const int ctas = static_cast<int>(std::min<std::uint32_t>(32u, (words + 255u) / 256u));
+  nx_table_upload_kernel<<<ctas, 256, 0, stream>>>(reinterpret_cast<std::uint64_t*>(d_dst),
+                                                     reinterpret_cast<const std::uint64_t*>(h_src), words);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill(const NxLeg* legs, int n, std::uint64_t seed, const NxCkTables& ck, cudaStream_t stream) {
   for (int done = 0; done < n; done += kMaxLegsPerLaunch) {
     FillParams p;

@@ -95,6 +95,7 @@ EngineConfig to_cpp(const nx_engine_config& c) {
   o.k3_one_stream = c.k3_one_stream != 0;
   o.k3_grouped = c.k3_grouped != 0;
   o.k3_verify_group = c.k3_verify_group;
+  o.d2h_commit_legs = c.d2h_commit_legs;
   return o;
 }
 
@@ -203,6 +204,7 @@ void nx_engine_config_default(nx_engine_config* c) {
   c->k3_one_stream = d.k3_one_stream;
   c->k3_grouped = d.k3_grouped;
   c->k3_verify_group = d.k3_verify_group;
+  c->d2h_commit_legs = d.d2h_commit_legs;
 }
 
 void nx_planner_config_default(nx_planner_config* c) {
@@ -485,6 +487,28 @@ int nx_calibrate(nx_engine* e, uint64_t bytes, double sm_gbps[8], double ce_gbps
       if (ce_gbps) ce_gbps[k] = c.ce_gbps[k];
       if (sm_faster) sm_faster[k] = c.sm_gbps[k] > c.ce_gbps[k] ? 1 : 0;
     }
+  });
+}
+
+int nx_calibrate_host(nx_engine* e, uint64_t bytes, int* threads, double* gbps, size_t cap, size_t* n, int* chosen) {
+  return guard([&] {
+    need(e, "engine");
+    const HostCalibration c = e->eng->calibrate_host(bytes);
+    std::size_t k = 0;
+    for (; k < c.threads.size() && k < cap; ++k) {
+      if (threads) threads[k] = c.threads[k];
+      if (gbps) gbps[k] = c.gbps[k];
+    }
+    if (n) *n = k;
+    if (chosen) *chosen = c.chosen;
+  });
+}
+
+int nx_host_threads(nx_engine* e, int* out) {
+  return guard([&] {
+    need(e, "engine");
+    need(out, "out");
+    *out = e->eng->host_threads();
   });
 }
 

@@ -107,11 +107,22 @@ struct SwapEngine::Impl final : detail::LaneSink {
     bool ce;
     bool end_on_side = false;                        // CE batch: ends on the checksum side stream
     cudaEvent_t dep_done = nullptr;                  // grouped K3: the record launch covering its departures
+    // CE departure batch (grouped K3): commit groups inside the batch, each
+    // ending at legs[end] (exclusive) behind its own copy event; the last
+    // group is the batch itself (ev_end / dep_done).
+    struct SubCommit {
+      std::uint32_t end;
+      cudaEvent_t copied;
+      cudaEvent_t dep_done;  // the record launch covering the group's departures
+    };
+    std::vector<SubCommit> subs;
+    std::size_t sub_next = 0, committed = 0;  // next group to poll; legs completed so far
     std::vector<std::array<cudaEvent_t, 2>> k3ev;    // CE batch: K3 launch start/end
     std::vector<std::uint32_t> k3slot;               // device-clock slot per K3 launch
     Bytes k3_bytes = 0;
   };
   std::array<int, 2> batches_sent{};  // per PCIe lane this execute (batch-size ramp)
+  std::size_t d2h_legs_sent = 0;      // departures submitted this execute (commit-group ramp)
 
   // Grouped K3 (CE path, one K3 stream): one table launch records every
   // departing block of the switch at its start; arrival checks run per group
@@ -148,7 +159,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
       const std::size_t cap = std::max<std::size_t>(n, 2 * ktab_cap);
       NX_CUDA(cudaMalloc(&d_ktab, sizeof(NxLeg) * cap));
       void* h = nullptr;
-      NX_CUDA(cudaHostAlloc(&h, sizeof(NxLeg) * cap, cudaHostAllocPortable));
+      NX_CUDA(cudaHostAlloc(&h, sizeof(NxLeg) * cap, cudaHostAllocPortable | cudaHostAllocMapped));  // read by launch_table_upload
       h_ktab = static_cast<NxLeg*>(h);
       ktab_cap = cap;
     }
@@ -173,7 +184,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
     if (ktab_used + n > ktab_cap) throw InvariantViolation("K3 descriptor table overflow");
     std::memcpy(h_ktab + ktab_used, l.data(), sizeof(NxLeg) * n);
     cudaStream_t cs = cks[0];
-    NX_CUDA(cudaMemcpyAsync(d_ktab + ktab_used, h_ktab + ktab_used, sizeof(NxLeg) * n, cudaMemcpyHostToDevice, cs));
+    NX_CUDA(launch_table_upload(d_ktab + ktab_used, h_ktab + ktab_used, static_cast<int>(n), cs));
+    ++launches_total;
     GroupK3 g{take_event(), take_event(), static_cast<int>(n), lane,
               k3_slots_used < kClockSlots ? k3_slots_used++ : kNoClockSlot};
     NX_CUDA(cudaEventRecord(g.a, cs));
@@ -256,7 +268,11 @@ struct SwapEngine::Impl final : detail::LaneSink {
                cfg.gpu_physical_max);
     pinned.init(cfg.pinned_capacity, numa.node);
     paged.init(cfg.paged_capacity);
-    pool.start(cfg.host_threads, numa.cpus);
+    {
+      const int ncpu = numa.cpus.empty() ? static_cast<int>(std::thread::hardware_concurrency()) : static_cast<int>(numa.cpus.size());
+      const int maxt = std::max(1, std::min(ncpu, 32));
+      pool.start(std::max(cfg.host_threads, maxt), numa.cpus, cfg.host_threads > 0 ? cfg.host_threads : maxt);
+    }
     for (auto& s : st) NX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     NX_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
     // K3 checksum launches of both lanes share one stream by default, so they
@@ -283,6 +299,58 @@ struct SwapEngine::Impl final : detail::LaneSink {
     bounce = static_cast<std::uint8_t*>(b);
     NX_CUDA(cudaEventCreate(&ev0));
     grow_tables(65536);
+    if (cfg.host_threads <= 0) calibrate_host(256 * kMiB);
+  }
+
+  HostCalibration host_cal;
+
+  HostCalibration calibrate_host(Bytes bytes) {
+    constexpr std::size_t kSpan = 64 * kMiB;  // per direction per round
+    const std::size_t rounds = std::max<std::size_t>(1, bytes / kSpan);
+    void* pin = nullptr;
+    NX_CUDA(cudaHostAlloc(&pin, 2 * kSpan, cudaHostAllocPortable));
+    auto* pg = static_cast<std::uint8_t*>(std::aligned_alloc(4096, 2 * kSpan));
+    if (!pg) {
+      cudaFreeHost(pin);
+      throw SimError(Err::IoError, "calibrate_host: out of host memory");
+    }
+    std::memset(pg, 0x5A, 2 * kSpan);
+    std::memset(pin, 0xA5, 2 * kSpan);
+    auto* pn = static_cast<std::uint8_t*>(pin);
+    std::vector<std::pair<void*, const void*>> pairs;
+    for (std::size_t r = 0; r < rounds; ++r)
+      for (std::size_t o = 0; o < kSpan; o += kBlockBytes) {
+        pairs.emplace_back(pg + o, pn + o);                  // demote: pinned -> paged
+        pairs.emplace_back(pn + kSpan + o, pg + kSpan + o);  // promote: paged -> pinned
+      }
+    HostCalibration c;
+    const int before = pool.active();
+    for (int t : {1, 2, 4, 6, 8, 12, 16, 24, 32}) {
+      if (t > pool.size()) break;
+      pool.set_active(t);
+      pool.copy_all(std::vector<std::pair<void*, const void*>>(pairs.begin(), pairs.begin() + std::min<std::size_t>(pairs.size(), 64)),
+                    kBlockBytes);  // warm the workers
+      const auto t0 = Clock::now();
+      pool.copy_all(pairs, kBlockBytes);
+      const double s = secs_since(t0);
+      c.threads.push_back(t);
+      c.gbps.push_back(static_cast<double>(pairs.size()) * kBlockBytes / s / 1e9);
+    }
+    std::free(pg);
+    cudaFreeHost(pin);
+    if (c.gbps.empty()) {
+      pool.set_active(before);
+      return c;
+    }
+    c.peak_gbps = *std::max_element(c.gbps.begin(), c.gbps.end());
+    for (std::size_t i = 0; i < c.gbps.size(); ++i)
+      if (c.gbps[i] >= 0.98 * c.peak_gbps) {
+        c.chosen = c.threads[i];
+        break;
+      }
+    pool.set_active(c.chosen);
+    host_cal = c;
+    return c;
   }
 
   // Synchronises only the engine's own streams: a device-wide sync could wait
@@ -591,23 +659,44 @@ struct SwapEngine::Impl final : detail::LaneSink {
       // batch ends (and may commit) only when both are done.
       cudaStream_t cs = cks[s];
       std::vector<NxLeg> ckl;
-      if (grouped && !d2h.empty()) {
+      auto dep_event = [&](std::size_t a, std::size_t z) {
         std::uint32_t last = 0;
-        for (auto i : d2h) last = std::max(last, dep_pos[legs[i].block]);
-        B.dep_done = last < dep_head ? rec_head : rec_all;
-      }
+        for (std::size_t k = a; k < z; ++k) last = std::max(last, dep_pos[legs[d2h[k]].block]);
+        return last < dep_head ? rec_head : rec_all;
+      };
+      if (grouped && !d2h.empty()) B.dep_done = dep_event(0, d2h.size());
       if (!grouped) {
         NX_CUDA(cudaStreamWaitEvent(cs, B.ev_start, 0));
         for (auto i : d2h) ckl.push_back(NxLeg{dev_addr(legs[i].from, legs[i].src_u), nullptr, static_cast<std::uint32_t>(legs[i].block), 0});
         if (!ckl.empty()) k3_launch(B, ckl, false, cs, flags);
       }  // grouped: the switch-wide record launch already covers these departures
-      copy_runs(d2h, s, cudaMemcpyDeviceToHost);
-      copy_runs(h2d, s, cudaMemcpyHostToDevice);
+      const bool record_covered = grouped && h2d.empty();  // departures only: ends on the copy stream
+      if (record_covered && cfg.d2h_commit_legs > 0) {
+        // Commit groups: small ones while the fetches ramp up, then
+        // d2h_commit_legs; each behind an event the poll loop checks.
+        const std::size_t small = static_cast<std::size_t>(std::max(1, cfg.first_batch_legs));
+        std::size_t i = 0;
+        while (i < d2h.size()) {
+          const std::size_t g = d2h_legs_sent < 32 * small ? small : static_cast<std::size_t>(cfg.d2h_commit_legs);
+          const std::size_t j = std::min(d2h.size(), i + g);
+          copy_runs(d2h.data() + i, j - i, s, cudaMemcpyDeviceToHost);
+          d2h_legs_sent += j - i;
+          if (j < d2h.size()) {
+            cudaEvent_t e = take_event();
+            NX_CUDA(cudaEventRecord(e, st[s]));
+            B.subs.push_back({static_cast<std::uint32_t>(j), e, dep_event(0, j)});
+          }
+          i = j;
+        }
+      } else {
+        copy_runs(d2h.data(), d2h.size(), s, cudaMemcpyDeviceToHost);
+        d2h_legs_sent += d2h.size();
+      }
+      copy_runs(h2d.data(), h2d.size(), s, cudaMemcpyHostToDevice);
       cudaEvent_t copied = take_event();
       NX_CUDA(cudaEventRecord(copied, st[s]));
       B.ev_copied = copied;
       const bool group_check = grouped && !h2d.empty() && d2h.empty();
-      const bool record_covered = grouped && h2d.empty();  // departures only: ends on the copy stream
       if (group_check) {
         for (auto i : h2d) vgroup.push_back(NxLeg{dev_addr(legs[i].to, legs[i].dst_u), nullptr, static_cast<std::uint32_t>(legs[i].block), 0});
         vgroup_copied = copied;  // the batch commits when its copy lands; a group launch checks it
@@ -638,14 +727,14 @@ struct SwapEngine::Impl final : detail::LaneSink {
   }
 
   // cudaMemcpyAsync over runs of legs whose source and destination are both contiguous.
-  void copy_runs(const std::vector<std::uint32_t>& idx, int s, cudaMemcpyKind kind) {
+  void copy_runs(const std::uint32_t* idx, std::size_t count, int s, cudaMemcpyKind kind) {
     std::size_t i = 0;
-    while (i < idx.size()) {
+    while (i < count) {
       const Leg& a = legs[idx[i]];
       auto* src = static_cast<std::uint8_t*>(dev_addr(a.from, a.src_u));
       auto* dst = static_cast<std::uint8_t*>(dev_addr(a.to, a.dst_u));
       std::size_t n = 1;
-      while (i + n < idx.size()) {
+      while (i + n < count) {
         const Leg& c = legs[idx[i + n]];
         if (dev_addr(c.from, c.src_u) != src + n * kBlockBytes || dev_addr(c.to, c.dst_u) != dst + n * kBlockBytes) break;
         ++n;
@@ -741,18 +830,34 @@ struct SwapEngine::Impl final : detail::LaneSink {
     bool progress = false;
     for (int s = 0; s < 2; ++s) {
       while (!inflight[s].empty()) {
-        if (inflight[s].front().dep_done != nullptr) {  // its departures must be recorded before its frames are reused
-          const cudaError_t r = cudaEventQuery(inflight[s].front().dep_done);
+        Batch& F = inflight[s].front();
+        // Commit groups of a departure batch that have landed (and whose
+        // departures are recorded): their frames are free for the fetches.
+        while (F.sub_next < F.subs.size()) {
+          const Batch::SubCommit& g = F.subs[F.sub_next];
+          const cudaError_t r = cudaEventQuery(g.dep_done);
+          if (r == cudaErrorNotReady) break;
+          NX_CUDA(r);
+          const cudaError_t c = cudaEventQuery(g.copied);
+          if (c == cudaErrorNotReady) break;
+          NX_CUDA(c);
+          for (; F.committed < g.end; ++F.committed) complete(F.legs[F.committed]);
+          ++F.sub_next;
+          progress = true;
+        }
+        if (F.sub_next < F.subs.size()) break;
+        if (F.dep_done != nullptr) {  // its departures must be recorded before its frames are reused
+          const cudaError_t r = cudaEventQuery(F.dep_done);
           if (r == cudaErrorNotReady) break;
           NX_CUDA(r);
         }
-        const cudaError_t e = cudaEventQuery(inflight[s].front().ev_end);
+        const cudaError_t e = cudaEventQuery(F.ev_end);
         if (e == cudaErrorNotReady) break;
         NX_CUDA(e);
         Batch B = std::move(inflight[s].front());
         inflight[s].pop_front();
         B.host_done = secs_since(t0);
-        for (auto i : B.legs) complete(i);
+        for (; B.committed < B.legs.size(); ++B.committed) complete(B.legs[B.committed]);
         landed.push_back(std::move(B));
         progress = true;
       }
@@ -857,6 +962,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
     landed.clear();
     events_used = 0;
     batches_sent = {0, 0};
+    d2h_legs_sent = 0;
     k3_slots_used = 0;
     NX_CUDA(cudaMemsetAsync(ck.kstart, 0xFF, sizeof(unsigned long long) * kClockSlots, aux));
     NX_CUDA(cudaMemsetAsync(ck.kend, 0, sizeof(unsigned long long) * kClockSlots, aux));
@@ -1438,6 +1544,10 @@ std::vector<std::array<double, 2>> SwapEngine::probe_checksum_launch(bool under_
   }
   return out;
 }
+
+HostCalibration SwapEngine::calibrate_host(Bytes bytes_per_direction) { return impl_->calibrate_host(bytes_per_direction); }
+const HostCalibration& SwapEngine::host_calibration() const { return impl_->host_cal; }
+int SwapEngine::host_threads() const { return impl_->pool.active(); }
 
 Calibration SwapEngine::calibrate(Bytes bytes_per_direction) {
   Calibration c;

@@ -215,9 +215,19 @@ PagedStore::~PagedStore() {
     if (p) munmap(p, static_cast<std::size_t>(kUnitsPerRegion) * kBlockBytes);
 }
 
-void HostCopyPool::start(int threads, const std::vector<int>& cpus) {
+void HostCopyPool::start(int threads, const std::vector<int>& cpus, int active) {
   if (threads < 1) threads = 1;
-  for (int i = 0; i < threads; ++i) threads_.emplace_back(&HostCopyPool::worker, this, cpus);
+  active_.store(active > 0 ? std::min(active, threads) : threads);
+  for (int i = 0; i < threads; ++i) threads_.emplace_back(&HostCopyPool::worker, this, i, cpus);
+}
+
+void HostCopyPool::set_active(int n) {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    active_.store(std::max(1, std::min(n, static_cast<int>(threads_.size()))));
+  }
+  idle_cv_.notify_all();
+  cv_.notify_all();
 }
 
 HostCopyPool::~HostCopyPool() {
@@ -226,17 +236,26 @@ HostCopyPool::~HostCopyPool() {
     stop_ = true;
   }
   cv_.notify_all();
+  idle_cv_.notify_all();
   for (auto& t : threads_) t.join();
 }
 
-void HostCopyPool::worker(std::vector<int> cpus) {
+void HostCopyPool::worker(int index, std::vector<int> cpus) {
   pin_thread_to(cpus);
   while (true) {
     Job j;
     {
       std::unique_lock<std::mutex> lk(mu_);
-      cv_.wait(lk, [&] { return stop_ || !jobs_.empty(); });
-      if (stop_ && jobs_.empty()) return;
+      for (;;) {
+        if (stop_ && jobs_.empty()) return;
+        if (!stop_ && index >= active_.load()) {  // parked: waits on its own condition
+          cv_.notify_one();                        // pass on a wake-up it may have taken
+          idle_cv_.wait(lk);
+          continue;
+        }
+        if (!jobs_.empty()) break;
+        cv_.wait(lk);
+      }
       j = jobs_.front();
       jobs_.pop_front();
     }

@@ -125,7 +125,13 @@ class PagedStore {
 // the engine thread.
 class HostCopyPool {
  public:
-  void start(int threads, const std::vector<int>& cpus);
+  // Starts `threads` workers; the first `active` of them take jobs (the rest
+  // wait until set_active raises the count: the engine sizes the pool from a
+  // measurement, SwapEngine::calibrate_host).
+  void start(int threads, const std::vector<int>& cpus, int active = 0);
+  void set_active(int n);
+  int active() const { return active_.load(); }
+  int size() const { return static_cast<int>(threads_.size()); }
   ~HostCopyPool();
   void submit(void* dst, const void* src, std::size_t bytes, std::uint64_t token);
   // Moves finished tokens into `out`; cheap when nothing finished.
@@ -140,16 +146,18 @@ class HostCopyPool {
     std::size_t bytes;
     std::uint64_t token;
   };
-  void worker(std::vector<int> cpus);
+  void worker(int index, std::vector<int> cpus);
   std::vector<std::thread> threads_;
   std::mutex mu_;
-  std::condition_variable cv_;
+  std::condition_variable cv_;       // active workers wait here for jobs
+  std::condition_variable idle_cv_;  // workers beyond the active count
   std::deque<Job> jobs_;
   std::mutex done_mu_;
   std::vector<std::uint64_t> done_;
   std::atomic<std::uint64_t> done_count_{0};
   std::uint64_t drained_ = 0;
   bool stop_ = false;
+  std::atomic<int> active_{0};
 };
 
 }  // namespace nixie::b200

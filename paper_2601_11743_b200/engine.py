@@ -30,7 +30,7 @@ class EngineConfig:
     path: int = L.PATH_AUTO
     pcie_legs_in_flight: int = 1024
     legs_per_launch: int = 128
-    host_threads: int = 8
+    host_threads: int = 0  # 0: measured at construction (calibrate_host)
     host_legs_in_flight: int = 64
     max_ctas: int = 0
     fused_launch: bool = False
@@ -41,6 +41,7 @@ class EngineConfig:
     k3_one_stream: bool = True
     k3_grouped: bool = True
     k3_verify_group: int = 1024
+    d2h_commit_legs: int = 0
 
     def to_c(self) -> L.EngineConfigC:
         c = L.EngineConfigC()
@@ -252,6 +253,19 @@ class SwapEngine:
         check(lib.nx_calibrate(self._h, bytes_per_direction, sm, ce, pick))
         return {"legs": [1 << k for k in range(8)], "sm_gbps": list(sm), "ce_gbps": list(ce),
                 "sm_faster": [bool(x) for x in pick]}
+
+    def calibrate_host(self, bytes_per_direction: int = 1024 * MIB) -> Dict:
+        """Size the host copy pool (two-hop pinned<->paged lanes) from a
+        measurement; returns GB/s per worker count and the installed count."""
+        th, gb, n, ch = (c_int * 16)(), (ctypes.c_double * 16)(), ctypes.c_size_t(), c_int()
+        check(lib.nx_calibrate_host(self._h, bytes_per_direction, th, gb, 16, ctypes.byref(n), ctypes.byref(ch)))
+        return {"threads": list(th)[:n.value], "gbps": list(gb)[:n.value], "chosen": ch.value,
+                "peak_gbps": max(list(gb)[:n.value], default=0.0)}
+
+    def host_threads(self) -> int:
+        v = c_int()
+        check(lib.nx_host_threads(self._h, ctypes.byref(v)))
+        return v.value
 
     def set_auto_table(self, sm_faster: Sequence[bool]) -> None:
         arr = (c_int * max(1, len(sm_faster)))(*[int(bool(x)) for x in sm_faster])

@@ -73,6 +73,22 @@ static long vm_hwm_kb() {
   return kb;
 }
 
+// Host memory in use system-wide (MemTotal - MemAvailable, bytes): sampled
+// around the round robin, its rise is what UVM's managed backing took on
+// the host (the driver's own pinned pages included).
+static long long host_used_bytes() {
+  FILE* f = std::fopen("/proc/meminfo", "r");
+  if (!f) return -1;
+  char line[256];
+  long long total = -1, avail = -1, v = 0;
+  while (std::fgets(line, sizeof(line), f)) {
+    if (std::sscanf(line, "MemTotal: %lld kB", &v) == 1) total = v;
+    if (std::sscanf(line, "MemAvailable: %lld kB", &v) == 1) avail = v;
+  }
+  std::fclose(f);
+  return total < 0 || avail < 0 ? -1 : (total - avail) * 1024;
+}
+
 static double ms_since(std::chrono::steady_clock::time_point t) {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
 }
@@ -94,6 +110,8 @@ int main(int argc, char** argv) {
   const std::size_t cap = static_cast<std::size_t>(cap_gib * (1ull << 30));
   void* balloon = nullptr;
   if (free_b > cap) CK(cudaMalloc(&balloon, free_b - cap));
+  const long long host0 = host_used_bytes();
+  long long host_peak = host0;
   const std::size_t ws = static_cast<std::size_t>(ws_gib * (1ull << 30));
   const std::uint64_t n = ws / 8;
   std::uint64_t* app[2];
@@ -116,7 +134,9 @@ int main(int argc, char** argv) {
     touch<<<148 * 8, 512, 0, s>>>(app[a], n, add, sum);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
-    return ms_since(t);
+    const double ms = ms_since(t);
+    host_peak = std::max(host_peak, host_used_bytes());
+    return ms;
   };
   // populate both (first touch on the GPU), then round-robin
   for (int a = 0; a < 2; ++a) {
@@ -145,7 +165,8 @@ int main(int argc, char** argv) {
               cap_gib, ws_gib);
   for (std::size_t i = 0; i < cost.size(); ++i) std::printf("%s%.2f", i ? ", " : "", cost[i]);
   std::printf("], \"median_ms\": %.2f, \"resident_kernel_ms\": %.2f, \"bidir_equiv_gbps\": %.2f, \"mismatches\": %llu"
-              ", \"host_peak_rss_bytes\": %lld}\n", med, res.back(), 2.0 * ws / (med * 1e-3) / 1e9, mismatches,
-              static_cast<long long>(vm_hwm_kb()) * 1024);
+              ", \"host_peak_rss_bytes\": %lld, \"host_mem_used_peak_bytes\": %lld}\n", med, res.back(),
+              2.0 * ws / (med * 1e-3) / 1e9, mismatches, static_cast<long long>(vm_hwm_kb()) * 1024,
+              host0 < 0 ? -1LL : host_peak - host0);
   return 0;
 }

@@ -17,7 +17,7 @@ def pytest_configure(config):
 # interposer test (real processes, wall-clock think times) must never stop
 # the run before the engine and full-size parity tests have run.
 _FILE_ORDER = ["test_oracle_pinned", "test_dropin", "test_parity_model", "test_parity_workload", "test_abi",
-               "test_gpu_engine", "test_gpu_scale", "test_gpu_workload", "test_gpu_uvm", "test_cli",
+               "test_gpu_engine", "test_gpu_scale", "test_gpu_budget", "test_gpu_workload", "test_gpu_uvm", "test_cli",
                "test_multirank", "test_interposer_host", "test_gpu_daemon_parity", "test_gpu_interposer"]
 
 

@@ -1,0 +1,64 @@
+"""BASELINE config 4 on the GPU: the pinned budget bounds the staging ring,
+small budgets go two-hop through pageable memory on the host copy pool, and
+the pool is sized from a same-run measurement (EngineConfig.host_threads = 0,
+SwapEngine.calibrate_host). Two budgets of a reduced config-4 exchange
+(2 x 8 GiB apps on an 8 GiB GPU cap): byte-exact, the budget held, the
+two-hop path near its host-memcpy roofline, latency falling with the budget.
+The full sweep with the UVM series is tools/budget_sweep.py
+(profiles/r02_budget_sweep.jsonl)."""
+import os
+import statistics
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+pytestmark = pytest.mark.gpu
+WS_GIB = 8
+
+
+def _point(budget_gib):
+    from paper_2601_11743_b200 import GIB, MIB, PlannerConfig, SwapEngine
+    from paper_2601_11743_b200._lib import TIER_PAGED
+    with SwapEngine(gpu_capacity=WS_GIB * GIB, pinned_capacity=budget_gib * GIB, paged_capacity=4 * WS_GIB * GIB) as e:
+        auto = e.host_threads()  # sized at construction (host_threads = 0)
+        hc = e.calibrate_host(512 * MIB)
+        e.allocate(0, WS_GIB * GIB, TIER_PAGED)
+        e.allocate(1, WS_GIB * GIB, TIER_PAGED)
+        e.fill_pattern(0, 3)
+        e.fill_pattern(1, 3)
+        pc = PlannerConfig(pinned_budget=budget_gib * GIB)
+        nxt, lat, host = 0, [], []
+        for _ in range(5):
+            pc.victim_order = [1 - nxt]
+            st = e.switch_to(nxt, pc)
+            assert st["mismatches"] == 0 and st["unverified"] == 0, st
+            nxt = 1 - nxt
+            lat.append(st["wall_s"] + st["plan_s"])
+            host.append(st["host_bytes"])
+        peak = e.pinned_physical()[1]
+        bad = e.verify_pattern(0, 3) + e.verify_pattern(1, 3)
+        threads = e.host_threads()
+    steady = statistics.median(lat[2:])
+    return {"auto_threads": auto, "calibration": hc, "threads": threads, "latency_s": steady, "peak": peak, "bad": bad,
+            "host_bytes": statistics.median(host[2:]), "host_gbs": statistics.median(host[2:]) / steady / 1e9}
+
+
+def test_two_budgets_two_hop_at_its_host_roofline():
+    from paper_2601_11743_b200 import GIB
+    small, large = _point(2), _point(8)
+    for p, b in ((small, 2), (large, 8)):
+        assert p["bad"] == 0
+        assert p["peak"] <= b * GIB, p  # the enforced budget
+        cal = p["calibration"]
+        assert cal["chosen"] in cal["threads"] and p["threads"] == cal["chosen"]
+        assert 1 <= p["auto_threads"] <= 32
+    # 2 GiB: most of each switch goes through pageable memory; the host copy
+    # pool is what bounds it
+    assert small["host_bytes"] >= 8 * GIB, small
+    assert small["host_gbs"] >= 0.5 * small["calibration"]["peak_gbs"], small
+    # a larger budget keeps more in pinned memory: fewer host bytes, faster
+    assert large["host_bytes"] < small["host_bytes"]
+    assert large["latency_s"] < small["latency_s"], (large["latency_s"], small["latency_s"])
