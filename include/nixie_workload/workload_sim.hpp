@@ -302,6 +302,10 @@ class Engine {
                   row.exec_at_level, row.idle_for, row.since_level_change, row.pending_for);
     for (const Request& r : res.requests)
       detail::put(res.trace, "Q %u %d %.17g %.17g %.17g\n", r.app, r.n, r.begin, r.first_done, r.end);
+    // Pinned bytes at their physical peak over the run: resident blocks plus
+    // transit, in-flight destination reservations and the streaming window
+    // (MemState::pinned_physical_peak, proj/include/nixie/mem_model.hpp:128).
+    detail::put(res.trace, "Z %" PRIu64 "\n", static_cast<std::uint64_t>(mem_.pinned_physical_peak()));
     return res;
   }
 

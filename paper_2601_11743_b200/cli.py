@@ -244,6 +244,7 @@ def metrics(trace: str, sc: Dict[str, Any]) -> Dict[str, Any]:
     req: Dict[int, List[Tuple[float, float, float]]] = {}
     switches, sizes = [], []
     pinned_after: Dict[str, int] = {}  # switch k -> pinned bytes resident over all apps after it
+    pinned_physical = None  # Z line: MemState::pinned_physical_peak (transit and reservations included)
     bad = {}
     for line in trace.splitlines():
         t = line.split()
@@ -257,6 +258,8 @@ def metrics(trace: str, sc: Dict[str, Any]) -> Dict[str, Any]:
             sizes.append((int(t[5]), int(t[7])))
         elif t[0] == "R":
             pinned_after[t[1]] = pinned_after.get(t[1], 0) + int(t[4])
+        elif t[0] == "Z":
+            pinned_physical = int(t[1])
         elif t[0] == "V" and (int(t[3]) != 0 or (len(t) >= 8 and int(t[7]) != 0)):
             bad[line] = True   # restore not byte-exact, or restored without a checksum check
         elif (t[0] == "F" and int(t[2]) != 0) or (t[0] == "M" and int(t[2]) != 0):
@@ -280,6 +283,9 @@ def metrics(trace: str, sc: Dict[str, Any]) -> Dict[str, Any]:
         "context_switches": {**_stats_ms(switches),
                              "bytes_in": sum(i for i, _ in sizes), "bytes_out": sum(o for _, o in sizes)},
         "pinned_resident_peak_bytes": max(pinned_after.values()) if pinned_after else 0,
+        # the figure comparable to UVM's pinned mirror: the registry's physical
+        # peak over the run (transient use during switches included)
+        "pinned_physical_peak_bytes": pinned_physical,
         "jain_fairness_interactive": None if jain(norm) is None else round(jain(norm), 6),
         "byte_check_failures": len(bad),  # --real only: V / F / M lines that are not clean
     }
@@ -388,7 +394,9 @@ def run_policy(sc: Dict[str, Any], policy: str, real: bool = False, log: Optiona
             raise ScenarioError(f"policies: '{policy}' needs a positive slice and runs on the model only")
         trace = simulate_uvm_rr(sc, w)
         u = [l.split() for l in trace.splitlines() if l.startswith("U ")][0]
-        return _with_log({"policy": policy, "mode": "model", **metrics(trace, sc),
+        m = metrics(trace, sc)
+        m["pinned_physical_peak_bytes"] = int(u[3])  # UVM: every GPU-resident page has a pinned mirror page
+        return _with_log({"policy": policy, "mode": "model", **m,
                           "uvm": {"faults": int(u[1]), "faulted_bytes": int(u[2]), "pinned_mirror_peak_bytes": int(u[3])}},
                          trace, log)
     if policy not in POLICIES:
@@ -410,6 +418,7 @@ def _rows(rep: Dict[str, Any]) -> List[List[Any]]:
         tag = r.get("label", r["policy"])
         for k in ("count", "mean_ms", "p50_ms", "p95_ms", "p99_ms", "max_ms", "bytes_in", "bytes_out"):
             rows.append([tag, "switch", k, r["context_switches"][k]])
+        rows.append([tag, "global", "pinned_physical_peak_bytes", r["pinned_physical_peak_bytes"]])
         rows.append([tag, "global", "pinned_resident_peak_bytes", r["pinned_resident_peak_bytes"]])
         rows.append([tag, "global", "jain_fairness_interactive", r["jain_fairness_interactive"]])
         for app, e in r["apps"].items():
@@ -433,7 +442,9 @@ def emit_report(rep: Dict[str, Any], fmt: str, path: Optional[str]) -> str:
             lines.append(f"== {r.get('label', r['policy'])} ({r['mode']})")
             lines.append(f"context switches {cs['count']:>5}  p50 {cs['p50_ms']} ms  p95 {cs['p95_ms']} ms  "
                          f"moved in {cs['bytes_in'] / 2**30:.2f} GiB out {cs['bytes_out'] / 2**30:.2f} GiB")
-            lines.append(f"pinned resident peak {r['pinned_resident_peak_bytes'] / 2**30:.2f} GiB   "
+            pp = r.get("pinned_physical_peak_bytes")
+            lines.append(f"pinned physical peak {'-' if pp is None else f'{pp / 2**30:.2f} GiB'}   "
+                         f"resident peak after switches {r['pinned_resident_peak_bytes'] / 2**30:.2f} GiB   "
                          f"Jain fairness (interactive) {r['jain_fairness_interactive']}")
             lines.append(f"{'app':>5} {'kind':>12} {'requests':>9} {'mean ms':>10} {'p50 ms':>10} {'p99 ms':>10}")
             for app, e in r["apps"].items():

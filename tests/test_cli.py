@@ -116,10 +116,11 @@ def test_csv_and_text_formats(tmp_path):
     path = _write(tmp_path, SMALL)
     p = _cli("run", "--scenario", path, "--format", "csv")
     rows = p.stdout.strip().splitlines()
-    # header + 8 switch metrics + 2 global + 5 per app
-    assert len(rows) == 1 + 8 + 2 + 5 * len(SMALL["apps"])
+    # header + 8 switch metrics + 3 global + 5 per app
+    assert len(rows) == 1 + 8 + 3 + 5 * len(SMALL["apps"])
+    assert any(r.split(",")[2] == "pinned_physical_peak_bytes" and int(r.split(",")[3]) > 0 for r in rows[1:])
     t = _cli("run", "--scenario", path, "--format", "text").stdout
-    assert "context switches" in t and "p95" in t and "pinned resident peak" in t
+    assert "context switches" in t and "p95" in t and "pinned physical peak" in t and "resident peak" in t
     assert _cli("run", "--scenario", path, "--format", "xml").returncode == 1
 
 
