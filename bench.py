@@ -143,22 +143,23 @@ def pcie_link(device: int) -> dict:
 
 
 class PcieCounters:
-    """The GPU's own PCIe counters during the timed region, sampled every
-    10 ms by a thread: a counter-level reading of what the copy engines moved,
-    which ncu cannot see (it profiles kernels, not DMA).
-      * NVML_FI_DEV_PCIE_COUNT_TX_BYTES / RX_BYTES: byte counters. They are
-        32-bit on these boards (they wrap every ~86 ms at 50 GB/s), so the
-        deltas between consecutive samples are accumulated modulo 2^32.
-      * nvmlDeviceGetPcieThroughput TX/RX: the driver's KB/s over its own
-        20 ms window, averaged over the samples.
-    TX = GPU -> host (evictions, plus the read requests of fetches),
-    RX = host -> GPU (fetch data)."""
+    """The GPU's own PCIe throughput during the timed region: the driver's
+    nvmlDeviceGetPcieThroughput TX/RX (KB/s over its 20 ms window), sampled
+    every 10 ms by a thread. A counter-level reading of what the copy engines
+    moved, which ncu cannot see (it profiles kernels, not DMA). The readings
+    include protocol overhead (TLP headers, the read requests of fetches on
+    TX, completions on RX), so they sit above the algorithmic rates.
+    TX = GPU -> host (evictions), RX = host -> GPU (fetches).
+    (The NVML_FI_DEV_PCIE_COUNT_{TX,RX}_BYTES byte counters are 32-bit on these
+    boards and, read every 10 ms, still under-count by ~15%: they update
+    less often than they wrap at 50 GB/s. Not used.)"""
 
     def __init__(self, pci_bus_id: str):
         self.h = None
         self.err = None
         self.stop_ev = threading.Event()
         self.thread = None
+        self.thr = []
         try:
             import pynvml
             self.nv = pynvml
@@ -175,70 +176,43 @@ class PcieCounters:
         except Exception as e:  # noqa: BLE001
             self.err = str(e)[:120]
 
-    def _fields(self):
+    def _sample(self):
         nv = self.nv
-        vals = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_PCIE_COUNT_TX_BYTES, nv.NVML_FI_DEV_PCIE_COUNT_RX_BYTES,
-                                                    nv.NVML_FI_DEV_PCIE_REPLAY_COUNTER])
-        out = []
-        for v in vals:
-            if v.nvmlReturn != 0:
-                return None
-            # valueType 1 = unsigned int (32-bit counter), 3 = unsigned long long
-            wide = getattr(v, "valueType", 3) in (3, 5)
-            out.append((int(v.value.ullVal) if wide else int(v.value.uiVal), 64 if wide else 32))
-        return out
+        return (nv.nvmlDeviceGetPcieThroughput(self.h, nv.NVML_PCIE_UTIL_TX_BYTES),
+                nv.nvmlDeviceGetPcieThroughput(self.h, nv.NVML_PCIE_UTIL_RX_BYTES))
 
     def _run(self):
-        nv = self.nv
-        prev = self._fields()
-        acc = [0, 0, 0]
-        thr = []
         while not self.stop_ev.wait(0.01):
-            cur = self._fields()
-            if cur is None or prev is None:
-                prev = cur
-                continue
-            for i in range(3):
-                bits = cur[i][1]
-                acc[i] += (cur[i][0] - prev[i][0]) % (1 << bits)
-            prev = cur
             try:
-                thr.append((nv.nvmlDeviceGetPcieThroughput(self.h, nv.NVML_PCIE_UTIL_TX_BYTES),
-                            nv.nvmlDeviceGetPcieThroughput(self.h, nv.NVML_PCIE_UTIL_RX_BYTES)))
-            except Exception:  # noqa: BLE001
-                pass
-        self.acc, self.thr, self.bits = acc, thr, (prev[0][1] if prev else None)
+                self.thr.append(self._sample())
+            except Exception as e:  # noqa: BLE001
+                self.err = str(e)[:120]
+                return
 
     def start(self):
         if self.h is None:
             return
         try:
-            if self._fields() is None:
-                self.err = "PCIe byte counters not supported"
-                return
+            self._sample()
         except Exception as e:  # noqa: BLE001
             self.err = str(e)[:120]
             return
-        self.t0 = time.perf_counter()
         self.thread = threading.Thread(target=self._run, daemon=True)
         self.thread.start()
 
     def stop(self) -> dict:
-        if self.thread is None:
+        if self.thread is None or not self.thr:
+            if self.thread is not None:
+                self.stop_ev.set()
+                self.thread.join()
             return {"available": False, **({"error": self.err} if self.err else {})}
         self.stop_ev.set()
         self.thread.join()
-        secs = time.perf_counter() - self.t0
-        tx, rx, rep = self.acc
-        out = {"available": True, "source": "NVML_FI_DEV_PCIE_COUNT_TX_BYTES/RX_BYTES sampled every 10 ms (deltas "
-                                            f"mod 2^{self.bits}) + nvmlDeviceGetPcieThroughput",
-               "tx_bytes": tx, "rx_bytes": rx, "replays": rep, "seconds": secs,
-               "tx_gbs": tx / secs / 1e9, "rx_gbs": rx / secs / 1e9}
-        if self.thr:
-            out["throughput_tx_gbs_mean"] = sum(t for t, _ in self.thr) / len(self.thr) * 1024 / 1e9
-            out["throughput_rx_gbs_mean"] = sum(r for _, r in self.thr) / len(self.thr) * 1024 / 1e9
-            out["throughput_samples"] = len(self.thr)
-        return out
+        tx = [t * 1024 / 1e9 for t, _ in self.thr]
+        rx = [r * 1024 / 1e9 for _, r in self.thr]
+        return {"available": True, "source": "nvmlDeviceGetPcieThroughput TX/RX (20 ms windows), sampled every 10 ms",
+                "samples": len(self.thr), "tx_gbs_mean": statistics.mean(tx), "rx_gbs_mean": statistics.mean(rx),
+                "tx_gbs_p50": statistics.median(tx), "rx_gbs_p50": statistics.median(rx)}
 
 
 def link_reference(device: int, bus_id: str, link: dict) -> dict:
@@ -662,8 +636,9 @@ def run_product(args, dist: Dist):
                           "link": link, "peak_source": "same-run probes, best of: CE and SM at 1 GiB/direction in 64 MiB "
                                                        "calls before and after the timed region, CE at 2 GiB/direction in 256 MiB calls"},
         "link_reference": link_reference(device, info["pci_bus_id"], link),
-        "pcie_counters": {**pcie, **({"rx_per_algorithmic_h2d_byte": pcie["rx_bytes"] / alg_in,
-                                      "tx_per_algorithmic_d2h_byte": pcie["tx_bytes"] / alg_out} if pcie.get("available") else {})},
+        "pcie_counters": {**pcie, **({"rx_over_algorithmic_h2d_rate": pcie["rx_gbs_mean"] / (alg_in / wall / 1e9),
+                                      "tx_over_algorithmic_d2h_rate": pcie["tx_gbs_mean"] / (alg_out / wall / 1e9)}
+                                     if pcie.get("available") else {})},
         "pcie_probe": {k: (round(v, 2) if isinstance(v, float) else v) for k, v in probe.items()},
         "pcie_probe_256mib": {k: round(probe_big[k], 2) for k in ("ce_bidir_total", "ce_bidir_h2d", "ce_bidir_d2h", "ce_h2d", "ce_d2h")},
         "pcie_probe_after": {k: round(probe_after[k], 2) for k in ("ce_bidir_total", "ce_bidir_h2d", "ce_bidir_d2h", "sm_bidir_total")},
@@ -685,7 +660,7 @@ def run_product(args, dist: Dist):
                       "concurrent_window_gbs": agg["window_gbs"],
                       "concurrent_window_what": "sum of bytes over ranks / sum over steps of (last rank's end - first "
                                                 "rank's start), host clock, steps barrier-aligned at N > 1",
-                      "topo": topo_matrix() if args.gpus > 1 else None},
+                      "topo": topo_matrix()},
         "shared_device": shared_device,
     }
     print(json.dumps(line), flush=True)

@@ -56,14 +56,20 @@ struct EngineConfig {
   bool k3_one_stream = true;          // both lanes' K3 launches on one stream (no SM contention between them)
   bool k3_grouped = true;             // CE path: one record launch per switch, arrival checks per group
   int k3_verify_group = 1024;         // legs per grouped arrival check (the last group is flushed at the end)
-  // CE path, grouped K3: a departure batch commits in groups of this many
+  // CE path, grouped K3: departure batches are cut into groups of this many
   // legs (first_batch_legs-sized groups for the first 32 x first_batch_legs
-  // legs of a switch), each behind its own event, so the fetches that need
-  // the frames it frees start one group behind the evictions, not one whole
-  // batch behind (0: commit whole batches). Measured on config 2: 32 legs
-  // shortens the fetch-free head by ~1 ms but the fetches then run as many
-  // small batches at a lower rate, 1.3% slower overall, so off.
-  int d2h_commit_legs = 0;
+  // legs of a switch), each ending at its own event (0: whole batches).
+  //  * early_frame_release (default): a departure commits when its copy is
+  //    queued; a fetch landing in the frame it vacated waits on the device
+  //    for that group's event (and the departure record), so the fetch stream
+  //    trails the evictions by one group without a host round trip, in
+  //    batches as large as the lanes allow. A second hop out of the pinned
+  //    slot (pinned -> paged) waits for the landing on the host.
+  //  * otherwise each group commits when the host sees its event (measured
+  //    on config 2: fetches then run as many small batches, 1.3% slower than
+  //    whole-batch commits).
+  int d2h_commit_legs = 32;
+  bool early_frame_release = true;
   bool exportable_arena = false;      // GPU tier = exportable VMM slabs shims can import (interposer daemon)
   Bytes arena_slab_bytes = 128 * kMiB; // exportable arena: bytes per physical allocation (a multiple of 2 MiB)
   Bytes gpu_physical = 0;             // arena bytes (0 = gpu_capacity); the registry still enforces gpu_capacity
@@ -258,6 +264,11 @@ class SwapEngine {
   // Per-batch-size choice for CopyPath::Auto: index k covers launches of
   // 2^k legs; true = SM kernel, false = copy engines.
   void set_auto_table(const std::vector<bool>& sm_faster);
+  // Per-switch tunables, changeable between executes (paired A/B runs on
+  // one engine, tools/ab_switch.py): legs_per_launch, first_batch_legs,
+  // d2h_commit_legs, early_frame_release, k3_verify_group. Throws
+  // ValidationError for other names or bad values.
+  void set_option(const std::string& name, int value);
   // Measures both mechanisms at 1..128 legs per batch and installs the
   // faster one per size for CopyPath::Auto.
   Calibration calibrate(Bytes bytes_per_direction);

@@ -65,7 +65,8 @@ typedef struct nx_engine_config {
   int k3_one_stream; /* both lanes' K3 launches on one stream */
   int k3_grouped;    /* CE path: one switch-wide record launch, grouped arrival checks */
   int k3_verify_group; /* legs per grouped arrival check */
-  int d2h_commit_legs; /* CE departures commit in groups of this many legs (0: whole batches) */
+  int d2h_commit_legs; /* CE departures are cut into event groups of this many legs (0: whole batches) */
+  int early_frame_release; /* departures commit when queued; fetches wait on the device for their frames */
 } nx_engine_config;
 
 /* PlannerConfig (proj/include/nixie/planner.hpp:39-43). victim_order may be
@@ -223,6 +224,9 @@ int nx_calibrate(nx_engine* e, uint64_t bytes_per_direction, double sm_gbps[8], 
  * fastest (*chosen; the smallest count within 2% of the best). */
 int nx_calibrate_host(nx_engine* e, uint64_t bytes_per_direction, int* threads, double* gbps, size_t cap, size_t* n,
                       int* chosen);
+/* Per-switch tunables between executes: legs_per_launch, first_batch_legs,
+ * d2h_commit_legs, early_frame_release, k3_verify_group. */
+int nx_engine_set_option(nx_engine* e, const char* name, int value);
 /* Workers of the host copy pool taking jobs now. */
 int nx_host_threads(nx_engine* e, int* out);
 /* K3 checksum launch duration (us) for 1, 2, 4 ... 128 legs; us[2*k] TMA, us[2*k+1] LDG. */

@@ -54,7 +54,7 @@ class EngineConfigC(Structure):
         ("path", c_int), ("pcie_legs_in_flight", c_int), ("legs_per_launch", c_int), ("host_threads", c_int),
         ("host_legs_in_flight", c_int), ("max_ctas", c_int), ("fused_launch", c_int), ("verify", c_int),
         ("numa_bind", c_int), ("first_batch_legs", c_int), ("k3_tma", c_int), ("k3_one_stream", c_int),
-        ("k3_grouped", c_int), ("k3_verify_group", c_int), ("d2h_commit_legs", c_int),
+        ("k3_grouped", c_int), ("k3_verify_group", c_int), ("d2h_commit_legs", c_int), ("early_frame_release", c_int),
     ]
 
 
@@ -143,6 +143,7 @@ _SIGNATURES = [
     ("nx_calibrate_host", c_int, [c_void_p, c_uint64, POINTER(c_int), POINTER(c_double), c_size_t, POINTER(c_size_t),
                                   POINTER(c_int)]),
     ("nx_host_threads", c_int, [c_void_p, POINTER(c_int)]),
+    ("nx_engine_set_option", c_int, [c_void_p, c_char_p, c_int]),
     ("nx_probe_checksum_launch", c_int, [c_void_p, POINTER(c_double)]),
     ("nx_probe_checksum_launch_ex", c_int, [c_void_p, c_int, POINTER(c_double)]),
     ("nx_mlfq_config_default", None, [POINTER(MlfqConfigC)]),

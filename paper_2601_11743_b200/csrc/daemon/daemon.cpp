@@ -642,6 +642,8 @@ class Daemon {
           deferred_acquires_.push_back(a.id);
         } else {
           ++rpcs_in_switch_;
+          note("{\"t\": %.6f, \"event\": \"rpc_in_switch\", \"app\": %u, \"type\": \"%s\"}", now(), a.id,
+               type == ipc::Msg::Alloc ? "alloc" : type == ipc::Msg::Free ? "free" : "other");
           serve(a, type, req);
         }
       }

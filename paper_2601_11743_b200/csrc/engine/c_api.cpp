@@ -96,6 +96,7 @@ EngineConfig to_cpp(const nx_engine_config& c) {
   o.k3_grouped = c.k3_grouped != 0;
   o.k3_verify_group = c.k3_verify_group;
   o.d2h_commit_legs = c.d2h_commit_legs;
+  o.early_frame_release = c.early_frame_release != 0;
   return o;
 }
 
@@ -205,6 +206,7 @@ void nx_engine_config_default(nx_engine_config* c) {
   c->k3_grouped = d.k3_grouped;
   c->k3_verify_group = d.k3_verify_group;
   c->d2h_commit_legs = d.d2h_commit_legs;
+  c->early_frame_release = d.early_frame_release;
 }
 
 void nx_planner_config_default(nx_planner_config* c) {
@@ -501,6 +503,14 @@ int nx_calibrate_host(nx_engine* e, uint64_t bytes, int* threads, double* gbps, 
     }
     if (n) *n = k;
     if (chosen) *chosen = c.chosen;
+  });
+}
+
+int nx_engine_set_option(nx_engine* e, const char* name, int value) {
+  return guard([&] {
+    need(e, "engine");
+    need(name, "name");
+    e->eng->set_option(name, value);
   });
 }
 

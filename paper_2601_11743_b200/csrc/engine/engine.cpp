@@ -116,6 +116,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
       cudaEvent_t dep_done;  // the record launch covering the group's departures
     };
     std::vector<SubCommit> subs;
+    bool early = false;  // departures committed at submission (early_frame_release)
     std::size_t sub_next = 0, committed = 0;  // next group to poll; legs completed so far
     std::vector<std::array<cudaEvent_t, 2>> k3ev;    // CE batch: K3 launch start/end
     std::vector<std::uint32_t> k3slot;               // device-clock slot per K3 launch
@@ -123,6 +124,27 @@ struct SwapEngine::Impl final : detail::LaneSink {
   };
   std::array<int, 2> batches_sent{};  // per PCIe lane this execute (batch-size ramp)
   std::size_t d2h_legs_sent = 0;      // departures submitted this execute (commit-group ramp)
+
+  // early_frame_release: a departure commits when its copy is queued. Its
+  // GPU frame is free "as of" the event ending its group (seq, 1-based, in
+  // D2H stream order) and of the record launch covering it; a fetch into the
+  // frame waits for both on the H2D stream. Its pinned slot holds data in
+  // flight until the batch lands (a second hop out of it waits).
+  bool early_mode = false;
+  std::vector<std::uint32_t> frame_seq;   // arena frame -> group seq freeing it (0: free)
+  std::vector<cudaEvent_t> frame_dep;     // arena frame -> record launch covering its departure
+  std::vector<cudaEvent_t> seq_events;    // seq - 1 -> event
+  std::vector<std::uint8_t> slot_inflight;  // pinned slot -> early-committed copy still landing
+  std::uint32_t h2d_seq_waited = 0;
+  bool h2d_waited_head = false, h2d_waited_all = false;
+  std::vector<std::uint32_t> early_done;  // departures to commit once the current flush pass ends
+  std::vector<std::uint32_t> host_wait;   // host legs waiting for their pinned source to land
+
+  template <typename T>
+  static T& at_grow(std::vector<T>& v, std::size_t i) {
+    if (i >= v.size()) v.resize(i + 1, T{});
+    return v[i];
+  }
 
   // Grouped K3 (CE path, one K3 stream): one table launch records every
   // departing block of the switch at its start; arrival checks run per group
@@ -595,9 +617,10 @@ struct SwapEngine::Impl final : detail::LaneSink {
       pending[lane].push_back(idx);
     } else {
       host_fifo[lane].push_back(idx);
-      pool.submit(host_addr(to, L.dst_u), host_addr(from, L.src_u), kBlockBytes, idx);
       stats.host_bytes += kBlockBytes;
       ++stats.host_legs;
+      if (from == TierId::PinnedHost && at_grow(slot_inflight, L.src_u)) host_wait.push_back(idx);  // still landing
+      else pool.submit(host_addr(to, L.dst_u), host_addr(from, L.src_u), kBlockBytes, idx);
     }
   }
 
@@ -671,7 +694,33 @@ struct SwapEngine::Impl final : detail::LaneSink {
         if (!ckl.empty()) k3_launch(B, ckl, false, cs, flags);
       }  // grouped: the switch-wide record launch already covers these departures
       const bool record_covered = grouped && h2d.empty();  // departures only: ends on the copy stream
-      if (record_covered && cfg.d2h_commit_legs > 0) {
+      if (record_covered && early_mode) {
+        // Early frame release: event groups; every departure commits after
+        // this flush pass, its frame tagged with its group's event.
+        const std::size_t small = static_cast<std::size_t>(std::max(1, cfg.first_batch_legs));
+        std::size_t i = 0;
+        while (i < d2h.size()) {
+          std::size_t g = d2h_legs_sent < 32 * small ? small : static_cast<std::size_t>(cfg.d2h_commit_legs);
+          if (g == 0) g = d2h.size();
+          const std::size_t j = std::min(d2h.size(), i + g);
+          copy_runs(d2h.data() + i, j - i, s, cudaMemcpyDeviceToHost);
+          d2h_legs_sent += j - i;
+          cudaEvent_t e = take_event();
+          NX_CUDA(cudaEventRecord(e, st[s]));
+          seq_events.push_back(e);
+          const auto seq = static_cast<std::uint32_t>(seq_events.size());
+          for (std::size_t k = i; k < j; ++k) {
+            const Leg& L = legs[d2h[k]];
+            at_grow(frame_seq, L.src_u) = seq;
+            at_grow(frame_dep, L.src_u) = dep_event(k, k + 1);
+            at_grow(slot_inflight, L.dst_u) = 1;
+            early_done.push_back(d2h[k]);
+          }
+          i = j;
+        }
+        B.early = true;
+        B.committed = B.legs.size();
+      } else if (record_covered && cfg.d2h_commit_legs > 0 && !cfg.early_frame_release) {
         // Commit groups: small ones while the fetches ramp up, then
         // d2h_commit_legs; each behind an event the poll loop checks.
         const std::size_t small = static_cast<std::size_t>(std::max(1, cfg.first_batch_legs));
@@ -692,7 +741,8 @@ struct SwapEngine::Impl final : detail::LaneSink {
         copy_runs(d2h.data(), d2h.size(), s, cudaMemcpyDeviceToHost);
         d2h_legs_sent += d2h.size();
       }
-      copy_runs(h2d.data(), h2d.size(), s, cudaMemcpyHostToDevice);
+      if (early_mode && !h2d.empty()) copy_runs_after_frames(h2d.data(), h2d.size(), s);
+      else copy_runs(h2d.data(), h2d.size(), s, cudaMemcpyHostToDevice);
       cudaEvent_t copied = take_event();
       NX_CUDA(cudaEventRecord(copied, st[s]));
       B.ev_copied = copied;
@@ -724,6 +774,40 @@ struct SwapEngine::Impl final : detail::LaneSink {
                             fetches_total - fetches_submitted < static_cast<std::size_t>(cfg.k3_verify_group)))
       flush_verify();
     maybe_release_gate();
+  }
+
+  // Fetches under early frame release: each leg's frame may still be being
+  // vacated; the H2D stream waits for the newest group event (and departure
+  // record) its legs need before the copies that need it. Waits are monotone
+  // (D2H groups end in stream order), so a batch adds only the waits it
+  // needs beyond the ones already queued.
+  void copy_runs_after_frames(const std::uint32_t* idx, std::size_t count, int s) {
+    std::size_t i = 0;
+    while (i < count) {
+      std::size_t j = i;
+      // extend the segment while no new wait is needed
+      while (j < count) {
+        const std::uint32_t f = legs[idx[j]].dst_u;
+        const std::uint32_t need = f < frame_seq.size() ? frame_seq[f] : 0;
+        const cudaEvent_t dep = f < frame_dep.size() ? frame_dep[f] : nullptr;
+        const bool dep_needed = dep != nullptr && !h2d_waited_all && !(dep == rec_head && h2d_waited_head);
+        if (need > h2d_seq_waited || dep_needed) {
+          if (j > i) break;  // copy what needs nothing new first
+          if (need > h2d_seq_waited) {
+            NX_CUDA(cudaStreamWaitEvent(st[s], seq_events[need - 1], 0));
+            h2d_seq_waited = need;
+          }
+          if (dep_needed) {
+            NX_CUDA(cudaStreamWaitEvent(st[s], dep, 0));
+            if (dep == rec_all) h2d_waited_all = true;
+            h2d_waited_head = true;
+          }
+        }
+        ++j;
+      }
+      copy_runs(idx + i, j - i, s, cudaMemcpyHostToDevice);
+      i = j;
+    }
   }
 
   // cudaMemcpyAsync over runs of legs whose source and destination are both contiguous.
@@ -771,7 +855,19 @@ struct SwapEngine::Impl final : detail::LaneSink {
     if (opts->gate_callback != nullptr) opts->gate_callback(opts->gate_ctx);
   }
 
+  // Submits pending legs; departures committed early (at submission) are
+  // committed between passes, which may admit more fetches.
   void flush() {
+    flush_pass();
+    while (!early_done.empty()) {
+      std::vector<std::uint32_t> v;
+      v.swap(early_done);
+      for (auto i : v) complete(i);
+      flush_pass();
+    }
+  }
+
+  void flush_pass() {
     const int L = cfg.legs_per_launch;
     if (cfg.fused_launch) {
       while (!pending[kD2H].empty() || !pending[kH2D].empty()) {
@@ -846,7 +942,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
           progress = true;
         }
         if (F.sub_next < F.subs.size()) break;
-        if (F.dep_done != nullptr) {  // its departures must be recorded before its frames are reused
+        if (F.dep_done != nullptr && !F.early) {  // its departures must be recorded before its frames are reused
           const cudaError_t r = cudaEventQuery(F.dep_done);
           if (r == cudaErrorNotReady) break;
           NX_CUDA(r);
@@ -858,6 +954,18 @@ struct SwapEngine::Impl final : detail::LaneSink {
         inflight[s].pop_front();
         B.host_done = secs_since(t0);
         for (; B.committed < B.legs.size(); ++B.committed) complete(B.legs[B.committed]);
+        if (B.early) {  // landed: second hops out of these pinned slots may start
+          for (auto i : B.legs) slot_inflight[legs[i].dst_u] = 0;
+          for (std::size_t k = 0; k < host_wait.size();) {
+            const Leg& L = legs[host_wait[k]];
+            if (!slot_inflight[L.src_u]) {
+              pool.submit(host_addr(L.to, L.dst_u), host_addr(L.from, L.src_u), kBlockBytes, host_wait[k]);
+              host_wait.erase(host_wait.begin() + static_cast<std::ptrdiff_t>(k));
+            } else {
+              ++k;
+            }
+          }
+        }
         landed.push_back(std::move(B));
         progress = true;
       }
@@ -963,6 +1071,14 @@ struct SwapEngine::Impl final : detail::LaneSink {
     events_used = 0;
     batches_sent = {0, 0};
     d2h_legs_sent = 0;
+    std::fill(frame_seq.begin(), frame_seq.end(), 0u);
+    std::fill(frame_dep.begin(), frame_dep.end(), nullptr);
+    std::fill(slot_inflight.begin(), slot_inflight.end(), std::uint8_t{0});
+    seq_events.clear();
+    h2d_seq_waited = 0;
+    h2d_waited_head = h2d_waited_all = false;
+    early_done.clear();
+    host_wait.clear();
     k3_slots_used = 0;
     NX_CUDA(cudaMemsetAsync(ck.kstart, 0xFF, sizeof(unsigned long long) * kClockSlots, aux));
     NX_CUDA(cudaMemsetAsync(ck.kend, 0, sizeof(unsigned long long) * kClockSlots, aux));
@@ -976,6 +1092,10 @@ struct SwapEngine::Impl final : detail::LaneSink {
     for (const Move& m : plan.moves)
       if (m.dst == TierId::Gpu) ++fetches_total;
     grouped = cfg.k3_grouped && cfg.k3_tma && cks[0] == cks[1] && cfg.path != CopyPath::SmKernel;
+    // Early frame release needs every departure batch on the copy engines
+    // (an SM-kernel batch records and moves in one launch).
+    early_mode = cfg.early_frame_release && grouped && !cfg.fused_launch &&
+                 (cfg.path == CopyPath::CopyEngine || (cfg.path == CopyPath::Auto && std::none_of(auto_sm.begin(), auto_sm.end(), [](bool b) { return b; })));
     gk3.clear();
     vgroup.clear();
     ktab_used = 0;
@@ -1059,6 +1179,10 @@ struct SwapEngine::Impl final : detail::LaneSink {
       cudaStreamSynchronize(cks[1]);
       throw;
     }
+    // Early-committed departures nothing waited on may still be landing.
+    while (!inflight[kD2H].empty() || !inflight[kH2D].empty())
+      if (!poll()) std::this_thread::yield();
+    if (!host_wait.empty()) throw InvariantViolation("swap engine finished with host legs still waiting");
     lanes = nullptr;
     if (grouped) NX_CUDA(cudaStreamSynchronize(cks[0]));  // the last arrival check (the switch is verified)
     stats.wall_s = secs_since(t0);
@@ -1543,6 +1667,16 @@ std::vector<std::array<double, 2>> SwapEngine::probe_checksum_launch(bool under_
     cudaFreeHost(hload);
   }
   return out;
+}
+
+void SwapEngine::set_option(const std::string& name, int value) {
+  EngineConfig& c = impl_->cfg;
+  if (name == "legs_per_launch" && value >= 1) c.legs_per_launch = value;
+  else if (name == "first_batch_legs" && value >= 1) c.first_batch_legs = value;
+  else if (name == "d2h_commit_legs" && value >= 0) c.d2h_commit_legs = value;
+  else if (name == "early_frame_release" && (value == 0 || value == 1)) c.early_frame_release = value != 0;
+  else if (name == "k3_verify_group" && value >= 1) c.k3_verify_group = value;
+  else throw SimError(Err::ValidationError, "set_option: unknown option or bad value: " + name + "=" + std::to_string(value));
 }
 
 HostCalibration SwapEngine::calibrate_host(Bytes bytes_per_direction) { return impl_->calibrate_host(bytes_per_direction); }

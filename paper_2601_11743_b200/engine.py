@@ -41,7 +41,8 @@ class EngineConfig:
     k3_one_stream: bool = True
     k3_grouped: bool = True
     k3_verify_group: int = 1024
-    d2h_commit_legs: int = 0
+    d2h_commit_legs: int = 32
+    early_frame_release: bool = True
 
     def to_c(self) -> L.EngineConfigC:
         c = L.EngineConfigC()
@@ -260,7 +261,11 @@ class SwapEngine:
         th, gb, n, ch = (c_int * 16)(), (ctypes.c_double * 16)(), ctypes.c_size_t(), c_int()
         check(lib.nx_calibrate_host(self._h, bytes_per_direction, th, gb, 16, ctypes.byref(n), ctypes.byref(ch)))
         return {"threads": list(th)[:n.value], "gbps": list(gb)[:n.value], "chosen": ch.value,
-                "peak_gbps": max(list(gb)[:n.value], default=0.0)}
+                "peak_gbs": max(list(gb)[:n.value], default=0.0)}
+
+    def set_option(self, name: str, value: int) -> None:
+        """Per-switch tunable between switches (SwapEngine::set_option)."""
+        check(lib.nx_engine_set_option(self._h, name.encode(), int(value)))
 
     def host_threads(self) -> int:
         v = c_int()

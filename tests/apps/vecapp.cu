@@ -6,8 +6,12 @@
 //
 //   nx_vecapp --mib N --buffers K --iters I --think-ms T --seed S [--name X] [--host-check 0|1] [--driver 0|1]
 //             [--passes P]   (P step kernels over the working set per iteration)
-//             [--graph 0|1|2] (iterations as launches of one captured CUDA graph;
-//                              2: captured in global mode)
+//             [--graph 0|1|2|3] (iterations as launches of one captured CUDA graph;
+//                              1: thread-local capture, 2: global, 3: relaxed)
+//             [--capture-alloc-ms T] (--graph: while capturing, sleep T ms, cudaMalloc
+//                              a 4 MiB buffer (a managed allocation: a daemon round
+//                              trip), sleep T ms again: a pause arriving meanwhile
+//                              must wait for the capture without deadlocking)
 //             [--driver 2|3]  (2: cuLaunchKernelEx from cudaGetDriverEntryPoint;
 //                              3: cuLaunchKernelEx called through the PLT, -lcuda)
 //             [--alloc rt|pitch|3d|drvpitch|async]  (how the working set is allocated:
@@ -102,6 +106,7 @@ int main(int argc, char** argv) {
   int graph = 0;   // 1: each iteration is one cudaGraphLaunch of a graph captured once (per pass offset)
   std::string alloc = "rt";
   int streams = 0, sync_ops = 0, stack_kib = 0;
+  double capture_alloc_ms = 0;
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string a = argv[i];
     if (a == "--mib") mib = std::atof(argv[i + 1]);
@@ -118,6 +123,7 @@ int main(int argc, char** argv) {
     else if (a == "--streams") streams = std::atoi(argv[i + 1]);
     else if (a == "--sync-ops") sync_ops = std::atoi(argv[i + 1]);
     else if (a == "--stack-kib") stack_kib = std::atoi(argv[i + 1]);
+    else if (a == "--capture-alloc-ms") capture_alloc_ms = std::atof(argv[i + 1]);
   }
   const auto t_start = std::chrono::steady_clock::now();
   // Pitched allocations: rows of kRow bytes (a multiple of 512, so the pitch
@@ -209,12 +215,21 @@ int main(int argc, char** argv) {
     CK(cudaMemset(d_k, 0, sizeof(std::uint32_t)));
     CK(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
     cudaGraph_t g = nullptr;
-    CK(cudaStreamBeginCapture(gs, graph == 2 ? cudaStreamCaptureModeGlobal : cudaStreamCaptureModeThreadLocal));
+    CK(cudaStreamBeginCapture(gs, graph == 2   ? cudaStreamCaptureModeGlobal
+                                  : graph == 3 ? cudaStreamCaptureModeRelaxed
+                                               : cudaStreamCaptureModeThreadLocal));
+    void* in_capture = nullptr;
+    if (capture_alloc_ms > 0) {
+      std::this_thread::sleep_for(std::chrono::duration<double, std::milli>(capture_alloc_ms));
+      CK(cudaMalloc(&in_capture, 4 << 20));
+      std::this_thread::sleep_for(std::chrono::duration<double, std::milli>(capture_alloc_ms));
+    }
     for (int pass = 0; pass < passes; ++pass) {
       for (int b = 0; b < buffers; ++b) step_dev<<<1184, 256, 0, gs>>>(buf[b], n, seed, b, d_k, d_err);
       bump<<<1, 1, 0, gs>>>(d_k);
     }
     CK(cudaStreamEndCapture(gs, &g));
+    if (in_capture) CK(cudaFree(in_capture));
     CK(cudaGraphInstantiate(&gexec, g, 0));
     CK(cudaGraphDestroy(g));
   }

@@ -265,3 +265,30 @@ def test_implicit_allocations_count_against_the_budget():
         p = d.spawn(_vec(mib, 1, 0, 9, "over") + ["--stack-kib", "4"])
         out, err = p.communicate(timeout=300)
     assert p.returncode != 0 and "out of memory" in err, (p.returncode, err[-400:])
+
+
+def test_pause_during_a_capture_with_an_allocation_does_not_deadlock():
+    """an app holding the GPU begins a stream capture, the daemon
+    switches to another app (Pause), and the capturing thread then calls
+    cudaMalloc (a managed allocation: an Alloc RPC) before ending the capture.
+    The shim's pause waits for the capture to end, so the daemon must serve
+    that RPC while it awaits the Drained ack instead of deadlocking until its
+    60 s ack timeout (which used to drop the app)."""
+    import time
+    with Daemon(gpu="4G", pinned="4G", paged="16G", idle_ms=20) as d:
+        t0 = time.time()
+        a = d.spawn(_vec(3072, 3, 100, 101, "cap") + ["--graph", "3", "--capture-alloc-ms", "4000"])
+        time.sleep(2.0)  # the capture begins about now: app b's first launch asks for the GPU
+        b = d.spawn(_vec(3072, 3, 100, 102, "other"))
+        outs = [p.communicate(timeout=300) for p in (a, b)]
+        elapsed = time.time() - t0
+    recs = d.records()  # after stop: the summary line is written at exit
+    _save("capture_pause", d, [])
+    for p, (out, err) in zip((a, b), outs):
+        assert p.returncode == 0, err[-2000:]
+    assert elapsed < 50, elapsed  # no ack timeout (60 s) on the way
+    summ = [r for r in recs if r.get("event") == "summary"]
+    sw = [r for r in recs if r.get("event") == "switch"]
+    assert sw and all(s["mismatches"] == 0 for s in sw)
+    assert summ and summ[-1]["rpcs_in_switch"] >= 1, summ  # the Alloc was served inside a switch
+    assert any(r.get("event") == "rpc_in_switch" and r.get("type") == "alloc" for r in recs)
