@@ -68,7 +68,8 @@ def main() -> int:
             for _ in range(2):
                 st = switch()
                 samples[name].append({"round": r, "span_ms": st["device_span_s"] * 1e3,
-                                      "wall_ms": (st["wall_s"] + st["plan_s"]) * 1e3})
+                                      "wall_ms": (st["wall_s"] + st["plan_s"]) * 1e3, "ce_calls": st["ce_calls"],
+                                      "ce_batches": [st["ce_batches_h2d"], st["ce_batches_d2h"]]})
     exact = e.verify_pattern(0, 7) == 0 and e.verify_pattern(1, 7) == 0
     e.close()
     base = variants[0][0]
@@ -89,6 +90,7 @@ def main() -> int:
                           "span_ms_min": round(min(sp), 2), "wall_ms_p50": round(statistics.median(wl), 2),
                           "paired_delta_ms_p50_vs_" + base: round(statistics.median(deltas), 2) if deltas else None,
                           "gbs_p50": round(16 * GIB / (statistics.median(sp) * 1e-3) / 1e9, 2),
+                          "ce_calls_p50": statistics.median(s["ce_calls"] for s in samples[name]),
                           "probe_ce_bidir_total": round(probe["ce_bidir_total"], 2), "byte_exact": exact}), flush=True)
     if a.out:
         with open(a.out, "w") as f:
