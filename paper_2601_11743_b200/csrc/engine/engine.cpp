@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <limits>
 #include <array>
 #include <chrono>
 #include <cstring>
@@ -124,6 +125,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   };
   std::array<int, 2> batches_sent{};  // per PCIe lane this execute (batch-size ramp)
   std::size_t d2h_legs_sent = 0;      // departures submitted this execute (commit-group ramp)
+  std::size_t batches_submitted = 0;  // PCIe batches submitted since construction
 
   // early_frame_release: a departure commits when its copy is queued. Its
   // GPU frame is free "as of" the event ending its group (seq, 1-based, in
@@ -656,6 +658,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
 
   // Submits `d2h` and `h2d` legs as one batch on stream `s`.
   void submit(int s, const std::vector<std::uint32_t>& d2h, const std::vector<std::uint32_t>& h2d) {
+    ++batches_submitted;
     Batch B;
     B.stream = s;
     B.legs = d2h;
@@ -857,17 +860,24 @@ struct SwapEngine::Impl final : detail::LaneSink {
 
   // Submits pending legs; departures committed early (at submission) are
   // committed between passes, which may admit more fetches.
+  // Under early frame release a pass submits one departure batch at most, so
+  // the fetches its commits admit go out right behind it instead of after
+  // every departure batch of the switch has been queued (~0.5 ms of host time).
   void flush() {
-    flush_pass();
-    while (!early_done.empty()) {
-      std::vector<std::uint32_t> v;
-      v.swap(early_done);
-      for (auto i : v) complete(i);
-      flush_pass();
+    for (;;) {
+      const std::size_t before = batches_submitted;
+      flush_pass(early_mode ? 1 : std::numeric_limits<int>::max());
+      if (!early_done.empty()) {
+        std::vector<std::uint32_t> v;
+        v.swap(early_done);
+        for (auto i : v) complete(i);
+        continue;
+      }
+      if (batches_submitted == before) break;
     }
   }
 
-  void flush_pass() {
+  void flush_pass(int max_d2h_batches) {
     const int L = cfg.legs_per_launch;
     if (cfg.fused_launch) {
       while (!pending[kD2H].empty() || !pending[kH2D].empty()) {
@@ -882,9 +892,11 @@ struct SwapEngine::Impl final : detail::LaneSink {
       }
       return;
     }
+    int d2h_batches = 0;
     for (int lane : {kD2H, kH2D}) {
       auto& p = pending[lane];
       while (!p.empty()) {
+        if (lane == kD2H && d2h_batches >= max_d2h_batches) break;
         // Batches ramp up from first_batch_legs so the first fetches can start
         // (into frames the first evictions free) after a short first batch.
         int cap = std::min<int>(L, std::max(1, cfg.first_batch_legs) << std::min(batches_sent[lane], 12));
@@ -901,10 +913,12 @@ struct SwapEngine::Impl final : detail::LaneSink {
         ++batches_sent[lane];
         std::vector<std::uint32_t> part(p.begin(), p.begin() + take);
         p.erase(p.begin(), p.begin() + take);
-        if (lane == kD2H)
+        if (lane == kD2H) {
           submit(kD2H, part, {});
-        else
+          ++d2h_batches;
+        } else {
           submit(kH2D, {}, part);
+        }
       }
     }
   }
