@@ -216,6 +216,9 @@ class SwapEngine {
   void prefetch_wait();  // runs every queued leg to completion
   bool prefetch_active() const;
   Bytes prefetched_bytes() const;  // committed since construction
+  // Blocks whose prefetch leg committed (paged -> pinned), in commit order,
+  // since the last call (the daemon's --trace replays them on the reference).
+  std::vector<BlockId> take_prefetch_commits();
 
   const SwitchStats& last_stats() const;
   const std::array<std::vector<LegTrace>, 6>& lane_trace() const;  // per lane, start order, last execute

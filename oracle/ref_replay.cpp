@@ -7,6 +7,12 @@
 //   alloc APP BYTES TIER CHUNKS...  MemState::allocate (proj/src/mem_model.cpp:48-86);
 //                                   the chunk ids must be the daemon's
 //   free APP CHUNK                  MemState::free_chunk (mem_model.cpp:88-116)
+//   prefetch K APP moves N           + its Q (dump) lines: the reference's
+//                                    plan_prefetch(APP) on the same state
+//                                    (planner.cpp:218-242) is printed as F lines
+//   pcommit BLOCK                    a prefetch leg (paged -> pinned) that
+//                                    committed: begin_move + commit_move
+//                                    (mem_model.cpp:118-172)
 //   plan K KIND APP in I out O victims V...   + its P (dump) and L (lane) lines
 //       -> the reference's plan_switch(APP) on the same state with the same
 //          victim order (proj/src/planner.cpp:111-216): printed as S/P/A lines;
@@ -19,6 +25,7 @@
 //   P K <dump line>         the reference plan (MigrationPlan::dump, planner.cpp:18-25)
 //   A K ref|daemon APPS...  victim apps in order of their first eviction
 //   L K LANE BLOCK SRC DST  reference execution of the daemon's plan
+//   F K <dump line>         the reference's prefetch plan K
 // With `victims reference` the daemon runs the planner unmodified, so its P
 // and L lines must equal these; with `victims slab` (slab-aligned victim
 // blocks) totals and victim app order must match while blocks may differ.
@@ -83,6 +90,7 @@ class Replay {
     std::istringstream ls(raw);
     std::string op;
     if (!(ls >> op)) return;
+    if (op == "Q") return;  // the daemon's prefetch plan: compared by the test
     if (op == "P" || op == "L") {
       if (!cur_.open) throw std::runtime_error("P/L line outside a plan");
       if (op == "P") {
@@ -124,6 +132,18 @@ class Replay {
       unsigned app, chunk;
       ls >> app >> chunk;
       mem_.free_chunk(static_cast<AppId>(app), static_cast<ChunkId>(chunk));
+    } else if (op == "prefetch") {
+      std::uint64_t k;
+      unsigned app;
+      ls >> k >> app;
+      const MigrationPlan ref = plan_prefetch(static_cast<AppId>(app), mem_, pc_);
+      std::istringstream dump(ref.dump());
+      for (std::string l; std::getline(dump, l);) std::printf("F %" PRIu64 " %s\n", k, l.c_str());
+    } else if (op == "pcommit") {
+      std::uint64_t b;
+      ls >> b;
+      mem_.begin_move(static_cast<BlockId>(b), TierId::PinnedHost, false);
+      mem_.commit_move(static_cast<BlockId>(b), TierId::PinnedHost);
     } else if (op == "plan") {
       std::string kind, tok;
       unsigned app;

@@ -158,8 +158,6 @@ bool parse_args(int argc, char** argv, Options& o) {
     }
   }
   o.mlfq.validate();
-  if (!o.trace_path.empty() && o.prefetch)
-    throw SimError(Err::ValidationError, "--trace replays whole plans; it cannot be combined with --prefetch");
   // Larger slabs mean fewer driver mappings per switch (each costs ~1 ms
   // whatever its size); smaller ones waste less physical memory on partly
   // resident slabs, which matters on small budgets.
@@ -604,6 +602,7 @@ class Daemon {
       if (cand && cand != holder) {
         const MigrationPlan pf = plan_prefetch(*cand, eng_.mem(), opt_.planner);
         if (!pf.moves.empty()) {
+          trace_prefetch(*cand, pf);
           eng_.prefetch_begin(pf);
           note("{\"t\": %.6f, \"event\": \"prefetch\", \"app\": %u, \"moves\": %zu}", t, *cand, pf.moves.size());
         }
@@ -911,8 +910,29 @@ class Daemon {
                  opt_.planner.pinned_budget, opt_.reference_victims ? "reference" : "slab");
     std::fflush(trace_);
   }
+  // Prefetch legs commit inside the engine (its pump runs wherever the
+  // registry must be quiescent): their commits are written ahead of the next
+  // trace line, which is where they happened relative to it.
+  void trace_pcommits() {
+    if (!trace_) return;
+    for (BlockId b : eng_.take_prefetch_commits()) std::fprintf(trace_, "pcommit %" PRIu64 "\n", static_cast<std::uint64_t>(b));
+  }
+  void trace_prefetch(AppId app, const MigrationPlan& plan) {
+    if (!trace_) return;
+    trace_pcommits();
+    const std::uint64_t k = prefetches_++;
+    std::fprintf(trace_, "prefetch %" PRIu64 " %u moves %zu\n", k, app, plan.moves.size());
+    std::string dump = plan.dump();
+    for (std::size_t i = 0; i < dump.size();) {
+      const std::size_t j = dump.find('\n', i);
+      std::fprintf(trace_, "Q %" PRIu64 " %s\n", k, dump.substr(i, j - i).c_str());
+      i = j == std::string::npos ? dump.size() : j + 1;
+    }
+    std::fflush(trace_);
+  }
   void trace_alloc(AppId app, Bytes bytes, TierId tier, const std::vector<ChunkId>& chunks) {
     if (!trace_) return;
+    trace_pcommits();
     std::fprintf(trace_, "alloc %u %" PRIu64 " %s", app, bytes, tier_name(tier));
     for (ChunkId c : chunks) std::fprintf(trace_, " %u", static_cast<unsigned>(c));
     std::fputc('\n', trace_);
@@ -920,11 +940,13 @@ class Daemon {
   }
   void trace_free(AppId app, ChunkId c) {
     if (!trace_) return;
+    trace_pcommits();
     std::fprintf(trace_, "free %u %u\n", app, static_cast<unsigned>(c));
     std::fflush(trace_);
   }
   void trace_plan(const char* kind, AppId app, const PlannerConfig& cfg, const MigrationPlan& plan) {
     if (!trace_) return;
+    trace_pcommits();
     const std::uint64_t k = plans_++;
     std::fprintf(trace_, "plan %" PRIu64 " %s %u in %" PRIu64 " out %" PRIu64 " victims", k, kind, app, plan.bytes_in, plan.bytes_out);
     for (AppId v : cfg.eviction_policy.victim_order) std::fprintf(trace_, " %u", v);
@@ -977,6 +999,7 @@ class Daemon {
   std::FILE* log_ = nullptr;
   std::FILE* trace_ = nullptr;
   std::uint64_t plans_ = 0;             // plans written to the trace
+  std::uint64_t prefetches_ = 0;        // prefetch plans written to the trace
   std::vector<AppId> deferred_acquires_;
   std::uint64_t rpcs_in_switch_ = 0;    // requests served while awaiting an ack
 };

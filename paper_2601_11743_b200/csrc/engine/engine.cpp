@@ -1015,6 +1015,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   std::deque<BlockId> pf_queue;   // not started
   std::deque<PfLeg> pf_inflight;  // started, FIFO
   Bytes pf_committed = 0;
+  std::vector<BlockId> pf_log;    // committed prefetch legs not yet taken (take_prefetch_commits)
 
   void prefetch_begin(const MigrationPlan& plan) {
     if (!pf_queue.empty() || !pf_inflight.empty()) throw SimError(Err::InvalidState, "a prefetch is already running");
@@ -1041,6 +1042,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
       give_unit(TierId::PagedHost, L.block, L.src_u);
       unit[L.block] = L.dst_u;
       pf_committed += kBlockBytes;
+      pf_log.push_back(L.block);
     }
     while (!pf_queue.empty() && static_cast<int>(pf_inflight.size()) < cfg.host_legs_in_flight) {
       const BlockId b = pf_queue.front();
@@ -1366,6 +1368,11 @@ void SwapEngine::prefetch_quiesce() { impl_->prefetch_quiesce(); }
 void SwapEngine::prefetch_wait() { impl_->prefetch_wait(); }
 bool SwapEngine::prefetch_active() const { return !impl_->pf_queue.empty() || !impl_->pf_inflight.empty(); }
 Bytes SwapEngine::prefetched_bytes() const { return impl_->pf_committed; }
+std::vector<BlockId> SwapEngine::take_prefetch_commits() {
+  std::vector<BlockId> out;
+  out.swap(impl_->pf_log);
+  return out;
+}
 void SwapEngine::set_progress_hook(std::function<void()> hook) { impl_->progress = std::move(hook); }
 
 int SwapEngine::arena_export_fd(std::uint32_t slab) const {

@@ -60,10 +60,14 @@ def compare(trace_path, expect_identical):
     with open(trace_path) as f:
         tl = f.read().splitlines()
     ref = _replay(trace_path)
-    mine = _by_plan(tl, ("P", "L"))
-    theirs = _by_plan(ref, ("S", "P", "A", "L"))
+    mine = _by_plan(tl, ("P", "L", "Q"))
+    theirs = _by_plan(ref, ("S", "P", "A", "L", "F"))
     plans = _daemon_plans(tl)
-    assert plans and set(plans) == set(theirs), (sorted(plans), sorted(theirs))
+    assert plans and set(plans) <= set(theirs), (sorted(plans), sorted(theirs))
+    # prefetch plans (plan_prefetch, planner.cpp:218-242) on the same registry
+    prefetches = sorted(int(ln.split()[1]) for ln in tl if ln.startswith("prefetch "))
+    for k in prefetches:
+        assert mine[k]["Q"] == theirs[k]["F"], f"prefetch plan {k} differs from the reference's"
     differing = 0
     for k, p in sorted(plans.items()):
         s = theirs[k]["S"][0].split()
@@ -77,7 +81,7 @@ def compare(trace_path, expect_identical):
         # per lane, in start order: the real engine vs the reference executor on the same plan
         lanes = lambda rows: {ln: [r for r in rows if r.split()[0] == ln] for ln in {r.split()[0] for r in rows}}
         assert lanes(mine[k]["L"]) == lanes(theirs[k]["L"]), f"plan {k}: per-lane leg order differs"
-    return {"plans": len(plans), "differing_plans": differing,
+    return {"plans": len(plans), "differing_plans": differing, "prefetches": len(prefetches),
             "moved": sum(p["in"] + p["out"] for p in plans.values())}
 
 
@@ -121,7 +125,16 @@ def _vec(mib, iters, think_ms, seed, name):
 def _run(mode, tmp_path):
     from paper_2601_11743_b200.interpose import Daemon, run_apps
     trace = str(tmp_path / f"daemon_{mode}.trace")
-    extra = ["--trace", trace] + (["--reference-victims"] if mode == "reference" else [])
+    extra = ["--trace", trace] + (["--reference-victims"] if mode in ("reference", "prefetch") else [])
+    if mode == "prefetch":  # three apps on a small pinned budget: pageable blocks get prefetched
+        with Daemon(gpu="4G", pinned="2G", paged="16G", prefetch=True, extra=extra) as d:
+            res = run_apps(d, [_vec(2048, 5, 300, 41 + i, "abc"[i]) for i in range(3)], timeout=600)
+            for r in res:
+                assert r["rc"] == 0, (r["stderr"], d.stderr())
+                assert r["out"]["device_errors"] == 0 and r["out"]["host_mismatch"] == 0
+            sw = d.switches()
+        assert len(sw) >= 3 and all(s["mismatches"] == 0 for s in sw)
+        return trace
     with Daemon(gpu="4G", pinned="4G", paged="16G", extra=extra) as d:
         res = run_apps(d, [_vec(3072, 5, 250, 81, "a"), _vec(3072, 5, 250, 82, "b")], timeout=600)
         for r in res:
@@ -153,3 +166,13 @@ def test_daemon_slab_victims_documented_delta(tmp_path):
     differ."""
     st = compare(_run("slab", tmp_path), expect_identical=False)
     assert st["plans"] >= 3 and st["moved"] > 4 * 1024 * MIB, st
+
+
+@pytest.mark.gpu
+def test_daemon_prefetch_plans_equal_reference(tmp_path):
+    """`nixied --prefetch --reference-victims`: three apps on a 2 GiB pinned
+    budget. Every prefetch plan the daemon started equals the reference's
+    plan_prefetch on the replayed registry (prefetch commits are replayed as
+    begin_move + commit_move), and every switch plan equals plan_switch."""
+    st = compare(_run("prefetch", tmp_path), expect_identical=True)
+    assert st["plans"] >= 3 and st["prefetches"] >= 1, st
