@@ -329,6 +329,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   HostCalibration host_cal;
 
   HostCalibration calibrate_host(Bytes bytes) {
+    if (!pf_queue.empty() || !pf_inflight.empty()) prefetch_quiesce();  // the pool's completions must all be ours
     constexpr std::size_t kSpan = 64 * kMiB;  // per direction per round
     const std::size_t rounds = std::max<std::size_t>(1, bytes / kSpan);
     void* pin = nullptr;
