@@ -25,8 +25,7 @@
  *                cudaGraphLaunch, cuLaunchKernel, cuLaunchKernelEx, cuLaunchCooperativeKernel,
  *                cuGraphLaunch, cudaMemcpy, cudaMemcpyAsync, cudaMemcpy2D, cudaMemcpy2DAsync,
  *                cudaMemcpy3D, cudaMemcpy3DAsync, cudaMemcpyPeer, cudaMemcpyPeerAsync,
- *                cudaMemcpy3DPeer, cudaMemcpy3DPeerAsync, cudaMemcpyBatchAsync,
- *                cudaMemcpy3DBatchAsync, cudaMemset, cudaMemsetAsync, cudaMemset2D,
+ *                cudaMemcpy3DPeer, cudaMemcpy3DPeerAsync, cudaMemset, cudaMemsetAsync, cudaMemset2D,
  *                cudaMemset2DAsync, cudaMemset3D, cudaMemset3DAsync
  *                (and the _ptds / _ptsz per-thread-stream variants of each runtime call)
  *                cuMemcpy, cuMemcpyAsync, cuMemcpyHtoD_v2, cuMemcpyDtoH_v2, cuMemcpyDtoD_v2,
@@ -35,7 +34,7 @@
  *                cuMemcpyPeer, cuMemcpyPeerAsync, cuMemsetD8_v2, cuMemsetD16_v2, cuMemsetD32_v2,
  *                cuMemsetD8Async, cuMemsetD16Async, cuMemsetD32Async, cuMemsetD2D8_v2,
  *                cuMemsetD2D16_v2, cuMemsetD2D32_v2 (driver entry points; the same set, plus the
- *                2D/3D/peer/batch async copies and 2D memsets, is wrapped in the table
+ *                2D/3D/peer async copies and 2D memsets, is wrapped in the table
  *                cuGetProcAddress hands to cudart and libraries)
  *                cublasLtMatmul, cublasGemmEx, cublasGemmStridedBatchedEx, cublasSgemm_v2,
  *                cublasSgemmStridedBatched, cudnnBackendExecute (cuBLAS and cuDNN launch

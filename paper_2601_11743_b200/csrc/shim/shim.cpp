@@ -20,7 +20,7 @@
 //   cuLaunchKernelEx, cuLaunchCooperativeKernel, cuGraphLaunch, and every
 //   copy/memset that can touch device memory: cudaMemcpy{,2D,3D,Peer,3DPeer}
 //   [Async] and cudaMemset{,2D,3D}[Async] (with their _ptds/_ptsz
-//   per-thread-stream twins), cudaMemcpy[3D]BatchAsync; the driver's
+//   per-thread-stream twins); the driver's
 //   cuMemcpy*/cuMemset* (synchronous and async) through the PLT and through
 //   the cuGetProcAddress table
 //       the launch gate (PAPER.md:116 steps 1-2 and 6): pass while the
@@ -100,9 +100,6 @@ cudaError_t cudaMemset2D_ptds(void*, size_t, int, size_t, size_t);
 cudaError_t cudaMemset2DAsync_ptsz(void*, size_t, int, size_t, size_t, cudaStream_t);
 cudaError_t cudaMemset3D_ptds(cudaPitchedPtr, int, cudaExtent);
 cudaError_t cudaMemset3DAsync_ptsz(cudaPitchedPtr, int, cudaExtent, cudaStream_t);
-cudaError_t cudaMemcpyBatchAsync_ptsz(void**, void**, size_t*, size_t, cudaMemcpyAttributes*, size_t*, size_t, size_t*,
-                                      cudaStream_t);
-cudaError_t cudaMemcpy3DBatchAsync_ptsz(size_t, cudaMemcpy3DBatchOp*, size_t*, unsigned long long, cudaStream_t);
 }
 
 namespace ipc = nixie::ipc;
@@ -890,12 +887,6 @@ NX_DRV(Memcpy3DAsync, CUresult, (const CUDA_MEMCPY3D* c, CUstream st), (c, st))
 NX_DRV(MemcpyPeerAsync, CUresult, (CUdeviceptr d, CUcontext dc, CUdeviceptr s, CUcontext sc, size_t n, CUstream st),
        (d, dc, s, sc, n, st))
 NX_DRV(Memcpy3DPeerAsync, CUresult, (const CUDA_MEMCPY3D_PEER* c, CUstream st), (c, st))
-NX_DRV(MemcpyBatchAsync, CUresult,
-       (CUdeviceptr* d, CUdeviceptr* s, size_t* sz, size_t n, CUmemcpyAttributes* at, size_t* ai, size_t na, size_t* fi,
-        CUstream st),
-       (d, s, sz, n, at, ai, na, fi, st))
-NX_DRV(Memcpy3DBatchAsync, CUresult, (size_t n, CUDA_MEMCPY3D_BATCH_OP* ops, size_t* fi, unsigned long long fl, CUstream st),
-       (n, ops, fi, fl, st))
 // Synchronous copies and memsets: a paused app's thread must not touch device
 // memory either (its mappings may be gone or, kept stale, another app's).
 NX_DRV(Memcpy, CUresult, (CUdeviceptr d, CUdeviceptr s, size_t n), (d, s, n))
@@ -933,7 +924,6 @@ const DrvWrap kDrvWraps[] = {
     NX_ENTRY(MemsetD2D16Async, "cuMemsetD2D16Async"), NX_ENTRY(MemsetD2D32Async, "cuMemsetD2D32Async"),
     NX_ENTRY(Memcpy2DAsync, "cuMemcpy2DAsync"),     NX_ENTRY(Memcpy3DAsync, "cuMemcpy3DAsync"),
     NX_ENTRY(MemcpyPeerAsync, "cuMemcpyPeerAsync"), NX_ENTRY(Memcpy3DPeerAsync, "cuMemcpy3DPeerAsync"),
-    NX_ENTRY(MemcpyBatchAsync, "cuMemcpyBatchAsync"), NX_ENTRY(Memcpy3DBatchAsync, "cuMemcpy3DBatchAsync"),
     NX_ENTRY(Memcpy, "cuMemcpy"),                   NX_ENTRY(MemcpyHtoD, "cuMemcpyHtoD"),
     NX_ENTRY(MemcpyDtoH, "cuMemcpyDtoH"),           NX_ENTRY(MemcpyDtoD, "cuMemcpyDtoD"),
     NX_ENTRY(Memcpy2D, "cuMemcpy2D"),               NX_ENTRY(Memcpy2DUnaligned, "cuMemcpy2DUnaligned"),
@@ -1264,16 +1254,6 @@ GATED(cudaError_t, cudaMemset3D, (cudaPitchedPtr p, int v, cudaExtent e), (p, v,
 GATED(cudaError_t, cudaMemset3D_ptds, (cudaPitchedPtr p, int v, cudaExtent e), (p, v, e))
 GATED(cudaError_t, cudaMemset3DAsync, (cudaPitchedPtr p, int v, cudaExtent e, cudaStream_t st), (p, v, e, st))
 GATED(cudaError_t, cudaMemset3DAsync_ptsz, (cudaPitchedPtr p, int v, cudaExtent e, cudaStream_t st), (p, v, e, st))
-GATED(cudaError_t, cudaMemcpyBatchAsync,
-      (void** d, void** s, size_t* sz, size_t n, cudaMemcpyAttributes* a, size_t* ai, size_t na, size_t* fi, cudaStream_t st),
-      (d, s, sz, n, a, ai, na, fi, st))
-GATED(cudaError_t, cudaMemcpyBatchAsync_ptsz,
-      (void** d, void** s, size_t* sz, size_t n, cudaMemcpyAttributes* a, size_t* ai, size_t na, size_t* fi, cudaStream_t st),
-      (d, s, sz, n, a, ai, na, fi, st))
-GATED(cudaError_t, cudaMemcpy3DBatchAsync, (size_t n, cudaMemcpy3DBatchOp* ops, size_t* fi, unsigned long long fl, cudaStream_t st),
-      (n, ops, fi, fl, st))
-GATED(cudaError_t, cudaMemcpy3DBatchAsync_ptsz, (size_t n, cudaMemcpy3DBatchOp* ops, size_t* fi, unsigned long long fl, cudaStream_t st),
-      (n, ops, fi, fl, st))
 
 // Synchronous copies: gated, and blocking calls for the MLFQ's idleness test.
 #define GATED_SYNC(ret, name, params, args) \

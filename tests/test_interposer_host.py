@@ -32,8 +32,8 @@ INTERPOSED = {
     # every copy / memset that can touch device memory
     "cudaMemcpy_ptds", "cudaMemcpy2D_ptds", "cudaMemcpy2DAsync_ptsz", "cudaMemcpy3D", "cudaMemcpy3D_ptds",
     "cudaMemcpy3DAsync", "cudaMemcpy3DAsync_ptsz", "cudaMemcpyPeer", "cudaMemcpyPeerAsync", "cudaMemcpy3DPeer",
-    "cudaMemcpy3DPeer_ptds", "cudaMemcpy3DPeerAsync", "cudaMemcpy3DPeerAsync_ptsz", "cudaMemcpyBatchAsync",
-    "cudaMemcpyBatchAsync_ptsz", "cudaMemcpy3DBatchAsync", "cudaMemcpy3DBatchAsync_ptsz", "cudaMemset_ptds",
+    "cudaMemcpy3DPeer_ptds", "cudaMemcpy3DPeerAsync", "cudaMemcpy3DPeerAsync_ptsz", 
+    "cudaMemset_ptds",
     "cudaMemset2D", "cudaMemset2D_ptds", "cudaMemset2DAsync", "cudaMemset2DAsync_ptsz", "cudaMemset3D",
     "cudaMemset3D_ptds", "cudaMemset3DAsync", "cudaMemset3DAsync_ptsz",
     "cuLaunchKernelEx", "cuLaunchCooperativeKernel", "cuGraphLaunch", "cuMemcpy", "cuMemcpyAsync", "cuMemcpyHtoD_v2",
