@@ -120,7 +120,10 @@ def main():
         tr = eng.batch_trace()
         raw.append({"stats": {k: st[k] for k in ("bytes_in", "bytes_out", "device_span_s", "wall_s", "plan_s")}, "batches": tr,
                     "k3": eng.k3_trace()})
-        rows.append(analyse(tr, st))
+        row = analyse(tr, st)
+        row["ce_calls"] = st["ce_calls"]
+        row["mib_per_ce_call"] = (st["pcie_h2d_bytes"] + st["pcie_d2h_bytes"]) / MIB / max(1, st["ce_calls"])
+        rows.append(row)
     bad = eng.verify_pattern(0, 7) + eng.verify_pattern(1, 7)
     eng.close()
     summary = {"probe": {k: probe[k] for k in ("ce_bidir_h2d", "ce_bidir_d2h", "ce_bidir_total", "ce_h2d", "ce_d2h")},
