@@ -376,10 +376,11 @@ def run_reference(args, dist: Dist):
 # ---------------------------------------------------------------------------------------------
 # Product arm
 # ---------------------------------------------------------------------------------------------
-def x16_exchange(path: int, probe: dict, switches: int = 20) -> dict:
+def x16_exchange(path: int, probes: list, switches: int = 20) -> dict:
     """North-star latency case: 16 GiB <-> 16 GiB exchange at a 16 GiB cap,
     `switches` times. Ideal = max(bytes / H2D-while-bidirectional, bytes /
-    D2H-while-bidirectional) from the same-run probe."""
+    D2H-while-bidirectional) from the same-run probes, the
+    most demanding of the probed shapes."""
     from paper_2601_11743_b200 import PlannerConfig, SwapEngine
     from paper_2601_11743_b200._lib import TIER_GPU, TIER_PINNED
     e = SwapEngine(gpu_capacity=16 * GIB, pinned_capacity=34 * GIB, paged_capacity=2 * GIB, path=path)
@@ -399,7 +400,7 @@ def x16_exchange(path: int, probe: dict, switches: int = 20) -> dict:
         bad = e.verify_pattern(0, 1) + e.verify_pattern(1, 1)
     finally:
         e.close()
-    ideal = max(16 * GIB / (probe["ce_bidir_h2d"] * 1e9), 16 * GIB / (probe["ce_bidir_d2h"] * 1e9))
+    ideal = min(max(16 * GIB / (p["ce_bidir_h2d"] * 1e9), 16 * GIB / (p["ce_bidir_d2h"] * 1e9)) for p in probes)
     return {"bytes_each_way": 16 * GIB, "n": len(lat), "ideal_s": ideal,
             "p50_s": pct(lat, 0.5), "p99_s": pct(lat, 0.99), "max_s": max(lat),
             "p50_over_ideal": pct(lat, 0.5) / ideal, "p99_over_ideal": pct(lat, 0.99) / ideal, "target_over_ideal": 1.2,
@@ -493,6 +494,12 @@ def run_product(args, dist: Dist):
     # (profiles/r02_ce_bubble.txt: 256 MiB calls 99.6 GB/s vs 2 MiB calls 77):
     # the denominator takes the best shape measured, not the engine's own.
     probe_big = eng.probe_pcie(2 * GIB, 256 * MIB)
+    # The engine's own paced shape (D2H held behind landed H2D,
+    # EngineConfig::pace_lag_legs) moves more bytes per second than either
+    # free-running shape on these links (profiles/r02_pcie_pace.txt), so it
+    # is in the denominator too.
+    probe_paced = max((eng.probe_pcie_paced(2 * GIB, c * MIB, k) for c, k in ((64, 2), (32, 3))),
+                      key=lambda p: p["ce_bidir_total"])
     calib = eng.calibrate(256 * MIB) if path == 0 else None
     # Steady state only involves the GPU and the pinned ring, so the apps are
     # placed directly (no pageable cold start): the interactive app on the
@@ -549,13 +556,13 @@ def run_product(args, dist: Dist):
     lat = [(s["wall_s"] + s["plan_s"]) * 1e3 for s in stats + more]
     dev_lat = [s["device_span_s"] * 1e3 for s in stats + more]
     peak_rank = max(probe["ce_bidir_total"], probe["sm_bidir_total"], probe_after["ce_bidir_total"], probe_after["sm_bidir_total"],
-                    probe_big["ce_bidir_total"])
+                    probe_big["ce_bidir_total"], probe_paced["ce_bidir_total"])
     rank_rec = {"rank": dist.rank, "device": device, **info, "gbs": bytes_rank / dev_rank / 1e9, "pcie_peak_gbs": peak_rank,
                 "pct_of_own_peak": bytes_rank / dev_rank / 1e9 / peak_rank * 100.0, "windows": windows,
                 "bytes": bytes_rank, "dev_s": dev_rank, "wall_s": wall, "bad": bad,
                 "spans": [s["device_span_s"] for s in stats]}
     ranks = dist.gather(rank_rec)
-    x16 = x16_exchange(path, probe, args.x16_switches) if (args.x16 and dist.rank == 0) else None
+    x16 = x16_exchange(path, [probe, probe_big, probe_paced], args.x16_switches) if (args.x16 and dist.rank == 0) else None
     ip = None
     if args.interposer and args.gpus == 1 and dist.rank == 0:
         try:
@@ -618,7 +625,10 @@ def run_product(args, dist: Dist):
     roof["frac"] = roof["achieved"] / roof["peak"] if roof["peak"] else None
     base = cpu_baseline(2)
     st0 = stats[0]
-    ideal_ms = max(st0["bytes_in"] / (probe["ce_bidir_h2d"] * 1e9), st0["bytes_out"] / (probe["ce_bidir_d2h"] * 1e9)) * 1e3
+    # Ideal switch: bytes / per-direction rate with the other direction
+    # saturated, for each probed shape; the most demanding (smallest) one.
+    ideal_ms = min(max(st0["bytes_in"] / (p["ce_bidir_h2d"] * 1e9), st0["bytes_out"] / (p["ce_bidir_d2h"] * 1e9)) * 1e3
+                   for p in (probe, probe_big, probe_paced))
     link = pcie_link(device)
     alg_in = sum(s["bytes_in"] for s in stats)
     alg_out = sum(s["bytes_out"] for s in stats)
@@ -643,13 +653,16 @@ def run_product(args, dist: Dist):
         "roofline": roof,
         "link_roofline": {"bound": "pcie", "achieved": per_gpu, "peak": pcie_peak, "unit": "GB/s", "frac": per_gpu / pcie_peak,
                           "link": link, "peak_source": "same-run probes, best of: CE and SM at 1 GiB/direction in 64 MiB "
-                                                       "calls before and after the timed region, CE at 2 GiB/direction in 256 MiB calls"},
+                                                       "calls before and after the timed region, CE at 2 GiB/direction in 256 MiB calls, "
+                                                       "CE paced (D2H chunk i after H2D chunk i-k landed) at 2 GiB/direction in "
+                                                       "64 MiB (k=2) and 32 MiB (k=3) calls"},
         "link_reference": link_reference(device, info["pci_bus_id"], link),
         "pcie_counters": {**pcie, **({"rx_over_algorithmic_h2d_rate": pcie["rx_gbs_mean"] / (alg_in / wall / 1e9),
                                       "tx_over_algorithmic_d2h_rate": pcie["tx_gbs_mean"] / (alg_out / wall / 1e9)}
                                      if pcie.get("available") else {})},
         "pcie_probe": {k: (round(v, 2) if isinstance(v, float) else v) for k, v in probe.items()},
         "pcie_probe_256mib": {k: round(probe_big[k], 2) for k in ("ce_bidir_total", "ce_bidir_h2d", "ce_bidir_d2h", "ce_h2d", "ce_d2h")},
+        "pcie_probe_paced": {k: (round(v, 2) if isinstance(v, float) else v) for k, v in probe_paced.items()},
         "pcie_probe_after": {k: round(probe_after[k], 2) for k in ("ce_bidir_total", "ce_bidir_h2d", "ce_bidir_d2h", "sm_bidir_total")},
         "settle": settle,
         "calibration": calib,

@@ -70,6 +70,17 @@ struct EngineConfig {
   //    whole-batch commits).
   int d2h_commit_legs = 32;
   bool early_frame_release = true;
+  // Early frame release only: a departure group may start once the fetches
+  // of the switch have landed up to (its first leg - pace_lag_legs), while
+  // fetches remain (-1: no pacing). With both PCIe directions saturated the
+  // upstream link carries the D2H data AND the fetches' read requests, so an
+  // unpaced D2H runs ahead, H2D slows down and finishes alone; holding D2H a
+  // few groups behind the fetches moves more bytes per second in total
+  // (tools/pcie_pace.cu: 4+4 GiB in 64 MiB calls, 89 GB/s free vs 97 paced).
+  // Config 2, paired A/B (profiles/r02_ab_pace*.txt): lag 64 legs 3.1% faster
+  // per switch than none; 48-96 within 0.5%; 0 serialises the two directions
+  // (the fetches need the frames the departures vacate) and 128 gains nothing.
+  int pace_lag_legs = 64;
   bool exportable_arena = false;      // GPU tier = exportable VMM slabs shims can import (interposer daemon)
   Bytes arena_slab_bytes = 128 * kMiB; // exportable arena: bytes per physical allocation (a multiple of 2 MiB)
   Bytes gpu_physical = 0;             // arena bytes (0 = gpu_capacity); the registry still enforces gpu_capacity
@@ -99,6 +110,7 @@ struct SwitchStats {
   int ce_batches[2] = {0, 0};               // copy-engine batches per stream
   int host_legs = 0;
   int ce_calls = 0;                         // cudaMemcpyAsync calls (contiguous runs) of the CE batches
+  int pace_waits = 0;                       // D2H groups held behind landed fetches (pace_lag_legs)
   std::uint64_t verified = 0, unverified = 0, mismatches = 0;
   // Per kernel kind (CUDA events on the launching stream):
   double k1_s = 0;      // K1 swap launches (SM path): summed durations
@@ -262,6 +274,10 @@ class SwapEngine {
 
   // Measures the host link: CE and SM, H2D / D2H alone and both at once.
   PcieProbe probe_pcie(Bytes bytes_per_direction, Bytes chunk_bytes);
+  // Both directions at once on the copy engines, D2H chunk i held (on the
+  // device) until H2D chunk i - lag_chunks has landed: the paced shape the
+  // engine uses (EngineConfig::pace_lag_legs). {H2D, D2H, both} GB/s, best of 3.
+  std::array<double, 3> probe_pcie_paced(Bytes bytes_per_direction, Bytes chunk_bytes, int lag_chunks);
   // Raw SM copy variants (csrc/cuda/copy_variants.cu): {H2D, D2H, both} GB/s.
   std::array<double, 3> probe_copy_variant(int variant, Bytes bytes_per_direction, int ctas);
   // Per-batch-size choice for CopyPath::Auto: index k covers launches of

@@ -67,6 +67,7 @@ typedef struct nx_engine_config {
   int k3_verify_group; /* legs per grouped arrival check */
   int d2h_commit_legs; /* CE departures are cut into event groups of this many legs (0: whole batches) */
   int early_frame_release; /* departures commit when queued; fetches wait on the device for their frames */
+  int pace_lag_legs; /* departure groups wait for fetches landed up to (first leg - lag); -1: off */
 } nx_engine_config;
 
 /* PlannerConfig (proj/include/nixie/planner.hpp:39-43). victim_order may be
@@ -95,6 +96,7 @@ typedef struct nx_switch_stats {
   double k3_busy_s;   /* union of the K3 launch intervals (CUDA events) */
   double k3_kernel_s; /* summed in-kernel K3 spans (%globaltimer) */
   int ce_calls;       /* cudaMemcpyAsync calls of the CE batches */
+  int pace_waits;     /* departure groups held behind landed fetches (pace_lag_legs) */
 } nx_switch_stats;
 
 typedef struct nx_pcie_probe {
@@ -198,6 +200,10 @@ void* nx_lane_stream(nx_engine* e, int lane);
 /* ---- host link ------------------------------------------------------------ */
 /* CE and SM bandwidth, H2D / D2H alone and simultaneously. */
 int nx_probe_pcie(nx_engine* e, uint64_t bytes_per_direction, uint64_t chunk_bytes, nx_pcie_probe* out);
+/* Both directions at once on the copy engines, D2H chunk i held on the device
+ * until H2D chunk i - lag_chunks has landed (the engine's paced shape,
+ * pace_lag_legs): gbs = {H2D, D2H, both}, best of 3. */
+int nx_probe_pcie_paced(nx_engine* e, uint64_t bytes_per_direction, uint64_t chunk_bytes, int lag_chunks, double gbs[3]);
 /* Where a device sits on the host: PCI bus id, NUMA node
  * (sysfs numa_node; when that reads -1, the node holding most of the
  * device's local_cpulist, node_from_cpus = 1) and the local CPUs this process
@@ -225,7 +231,7 @@ int nx_calibrate(nx_engine* e, uint64_t bytes_per_direction, double sm_gbps[8], 
 int nx_calibrate_host(nx_engine* e, uint64_t bytes_per_direction, int* threads, double* gbps, size_t cap, size_t* n,
                       int* chosen);
 /* Per-switch tunables between executes: legs_per_launch, first_batch_legs,
- * d2h_commit_legs, early_frame_release, k3_verify_group. */
+ * d2h_commit_legs, early_frame_release, k3_verify_group, pace_lag_legs. */
 int nx_engine_set_option(nx_engine* e, const char* name, int value);
 /* Workers of the host copy pool taking jobs now. */
 int nx_host_threads(nx_engine* e, int* out);

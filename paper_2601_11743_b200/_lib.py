@@ -55,6 +55,7 @@ class EngineConfigC(Structure):
         ("host_legs_in_flight", c_int), ("max_ctas", c_int), ("fused_launch", c_int), ("verify", c_int),
         ("numa_bind", c_int), ("first_batch_legs", c_int), ("k3_tma", c_int), ("k3_one_stream", c_int),
         ("k3_grouped", c_int), ("k3_verify_group", c_int), ("d2h_commit_legs", c_int), ("early_frame_release", c_int),
+        ("pace_lag_legs", c_int),
     ]
 
 
@@ -72,7 +73,7 @@ class SwitchStatsC(Structure):
         ("unverified", c_uint64), ("mismatches", c_uint64), ("tp_to_gpu", c_double), ("tp_from_gpu", c_double),
         ("tp_bidir", c_double), ("k1_s", c_double), ("k3_s", c_double), ("k1_bytes", c_uint64), ("k3_bytes", c_uint64),
         ("k1_launches", c_int), ("k3_launches", c_int), ("k3_busy_s", c_double), ("k3_kernel_s", c_double),
-        ("ce_calls", c_int),
+        ("ce_calls", c_int), ("pace_waits", c_int),
     ]
 
     def as_dict(self) -> dict:
@@ -137,6 +138,7 @@ _SIGNATURES = [
     ("nx_batch_trace", c_int, [c_void_p, POINTER(BatchRecordC), c_size_t, POINTER(c_size_t)]),
     ("nx_lane_stream", c_void_p, [c_void_p, c_int]),
     ("nx_probe_pcie", c_int, [c_void_p, c_uint64, c_uint64, POINTER(PcieProbeC)]),
+    ("nx_probe_pcie_paced", c_int, [c_void_p, c_uint64, c_uint64, c_int, POINTER(c_double)]),
     ("nx_probe_copy_variant", c_int, [c_void_p, c_int, c_uint64, c_int, POINTER(c_double)]),
     ("nx_set_auto_table", c_int, [c_void_p, POINTER(c_int), c_size_t]),
     ("nx_calibrate", c_int, [c_void_p, c_uint64, POINTER(c_double), POINTER(c_double), POINTER(c_int)]),

@@ -97,6 +97,7 @@ EngineConfig to_cpp(const nx_engine_config& c) {
   o.k3_verify_group = c.k3_verify_group;
   o.d2h_commit_legs = c.d2h_commit_legs;
   o.early_frame_release = c.early_frame_release != 0;
+  o.pace_lag_legs = c.pace_lag_legs;
   return o;
 }
 
@@ -140,6 +141,7 @@ void fill_stats(const SwapEngine& eng, const ExecResult& r, nx_switch_stats* out
   out->k3_busy_s = s.k3_busy_s;
   out->k3_kernel_s = s.k3_kernel_s;
   out->ce_calls = s.ce_calls;
+  out->pace_waits = s.pace_waits;
   if (s.device_span_s > 0) {
     double lo = 1e30, hi = 0;
     for (const TransferRecord& t : r.events)
@@ -207,6 +209,7 @@ void nx_engine_config_default(nx_engine_config* c) {
   c->k3_verify_group = d.k3_verify_group;
   c->d2h_commit_legs = d.d2h_commit_legs;
   c->early_frame_release = d.early_frame_release;
+  c->pace_lag_legs = d.pace_lag_legs;
 }
 
 void nx_planner_config_default(nx_planner_config* c) {
@@ -430,6 +433,16 @@ int nx_batch_trace(nx_engine* e, nx_batch_record* out, size_t cap, size_t* n) {
   });
 }
 void* nx_lane_stream(nx_engine* e, int lane) { return e ? static_cast<void*>(e->eng->stream(lane)) : nullptr; }
+
+int nx_probe_pcie_paced(nx_engine* e, uint64_t bytes, uint64_t chunk, int lag_chunks, double gbs[3]) {
+  return guard([&] {
+    need(e, "engine");
+    need(gbs, "gbs");
+    if (lag_chunks < 1) throw SimError(Err::ValidationError, "lag_chunks must be >= 1");
+    const auto r = e->eng->probe_pcie_paced(bytes, chunk, lag_chunks);
+    for (int k = 0; k < 3; ++k) gbs[k] = r[k];
+  });
+}
 
 int nx_probe_pcie(nx_engine* e, uint64_t bytes, uint64_t chunk, nx_pcie_probe* out) {
   return guard([&] {

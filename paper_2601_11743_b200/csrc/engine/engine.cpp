@@ -142,6 +142,39 @@ struct SwapEngine::Impl final : detail::LaneSink {
   std::vector<std::uint32_t> early_done;  // departures to commit once the current flush pass ends
   std::vector<std::uint32_t> host_wait;   // host legs waiting for their pinned source to land
 
+  // Pacing (EngineConfig::pace_lag_legs, early frame release only): the D2H
+  // group starting at departure x waits on the device for the fetches to have
+  // landed up to x - lag. Fetch copies leave marks (fetch legs copied so far,
+  // event after them) on the H2D stream; a departure group is submitted only
+  // once the mark it needs exists (device waits are enqueued after the work
+  // that satisfies them), unless nothing on the H2D side can move without it.
+  bool pacing = false;
+  std::vector<std::pair<std::size_t, cudaEvent_t>> h2d_marks;
+  std::size_t h2d_marked = 0;     // fetch legs covered by marks this execute
+  std::size_t d2h_mark_next = 0;  // marks before this one are already waited on by the D2H stream
+
+  // Fetch legs that must have landed before the departure group starting at x.
+  std::size_t pace_need(std::size_t x) const {
+    const auto lag = static_cast<std::size_t>(cfg.pace_lag_legs);
+    if (!pacing || x <= lag || x - lag > fetches_total) return 0;  // nothing (left) to pace against
+    return x - lag;
+  }
+  std::size_t d2h_group_legs(std::size_t sent) const {
+    const std::size_t small = static_cast<std::size_t>(std::max(1, cfg.first_batch_legs));
+    return sent < 32 * small ? small : static_cast<std::size_t>(std::max(1, cfg.d2h_commit_legs));
+  }
+  void pace_wait(std::size_t x) {
+    const std::size_t need = pace_need(x);
+    if (need == 0) return;
+    if (d2h_mark_next > 0 && h2d_marks[d2h_mark_next - 1].first >= need) return;  // already waited on
+    std::size_t m = d2h_mark_next;
+    while (m < h2d_marks.size() && h2d_marks[m].first < need) ++m;
+    if (m == h2d_marks.size()) return;  // not queued yet (flush_pass let it go unpaced)
+    NX_CUDA(cudaStreamWaitEvent(st[kD2H], h2d_marks[m].second, 0));
+    ++stats.pace_waits;
+    d2h_mark_next = m + 1;
+  }
+
   template <typename T>
   static T& at_grow(std::vector<T>& v, std::size_t i) {
     if (i >= v.size()) v.resize(i + 1, T{});
@@ -707,6 +740,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
           std::size_t g = d2h_legs_sent < 32 * small ? small : static_cast<std::size_t>(cfg.d2h_commit_legs);
           if (g == 0) g = d2h.size();
           const std::size_t j = std::min(d2h.size(), i + g);
+          pace_wait(d2h_legs_sent);
           copy_runs(d2h.data() + i, j - i, s, cudaMemcpyDeviceToHost);
           d2h_legs_sent += j - i;
           cudaEvent_t e = take_event();
@@ -772,10 +806,13 @@ struct SwapEngine::Impl final : detail::LaneSink {
       if (lanes->move(L.mi).dst == TierId::Gpu) ++fetches_submitted;
     }
     inflight[s].push_back(std::move(B));
-    // Group arrival checks; in the tail (fewer fetches left than a group) check
-    // each batch as it is submitted so the last check after the last copy is short.
+    // Group arrival checks; in the tail (fewer fetches left than a group) a
+    // check covers at least as many legs as remain to be submitted, so group
+    // sizes halve towards the end: the last check after the last copy is
+    // short and the tail takes a few launches, not one per batch.
+    const std::size_t remaining = fetches_total - fetches_submitted;
     if (!vgroup.empty() && (static_cast<int>(vgroup.size()) >= cfg.k3_verify_group ||
-                            fetches_total - fetches_submitted < static_cast<std::size_t>(cfg.k3_verify_group)))
+                            (remaining < static_cast<std::size_t>(cfg.k3_verify_group) && vgroup.size() >= remaining)))
       flush_verify();
     maybe_release_gate();
   }
@@ -810,6 +847,12 @@ struct SwapEngine::Impl final : detail::LaneSink {
         ++j;
       }
       copy_runs(idx + i, j - i, s, cudaMemcpyHostToDevice);
+      if (pacing) {
+        h2d_marked += j - i;
+        cudaEvent_t e = take_event();
+        NX_CUDA(cudaEventRecord(e, st[s]));
+        h2d_marks.emplace_back(h2d_marked, e);
+      }
       i = j;
     }
   }
@@ -908,8 +951,29 @@ struct SwapEngine::Impl final : detail::LaneSink {
           const int left = static_cast<int>(p.size() + lanes->queued(kD2H));
           cap = std::min(cap, std::max(std::max(1, cfg.first_batch_legs), left / 4));
         }
-        // Enough queued on the stream to hide the host: wait for a full batch.
-        if (inflight[lane].size() >= 2 && static_cast<int>(p.size()) < cap) break;
+        if (lane == kD2H && pacing) {
+          // Only groups whose pacing mark exists (or needs none).
+          std::size_t allow = 0;
+          while (allow < static_cast<std::size_t>(cap) && allow < p.size()) {
+            const std::size_t x = d2h_legs_sent + allow;
+            const std::size_t need = pace_need(x);
+            if (need > h2d_marked) break;
+            allow += d2h_group_legs(x);
+          }
+          if (allow == 0) {
+            // The fetches in flight or pending will land and leave marks; with
+            // none, nothing moves without more departures: go unpaced.
+            if (!pending[kH2D].empty() || !inflight[kH2D].empty()) break;
+          } else {
+            cap = std::min<int>(cap, static_cast<int>(allow));
+          }
+        }
+        // Enough queued on the stream to hide the host: wait for a full batch
+        // (paced: the fetch backlog stays within the lag, so a smaller one).
+        int hold = cap;
+        if (lane == kH2D && pacing)
+          hold = std::min(cap, std::max(std::max(1, cfg.d2h_commit_legs), cfg.pace_lag_legs));
+        if (inflight[lane].size() >= 2 && static_cast<int>(p.size()) < hold) break;
         const int take = std::min<int>(static_cast<int>(p.size()), cap);
         ++batches_sent[lane];
         std::vector<std::uint32_t> part(p.begin(), p.begin() + take);
@@ -1113,6 +1177,10 @@ struct SwapEngine::Impl final : detail::LaneSink {
     // (an SM-kernel batch records and moves in one launch).
     early_mode = cfg.early_frame_release && grouped && !cfg.fused_launch &&
                  (cfg.path == CopyPath::CopyEngine || (cfg.path == CopyPath::Auto && std::none_of(auto_sm.begin(), auto_sm.end(), [](bool b) { return b; })));
+    pacing = early_mode && cfg.pace_lag_legs >= 0 && fetches_total > 0;
+    h2d_marks.clear();
+    h2d_marked = 0;
+    d2h_mark_next = 0;
     gk3.clear();
     vgroup.clear();
     ktab_used = 0;
@@ -1533,6 +1601,58 @@ PcieProbe SwapEngine::probe_pcie(Bytes bytes, Bytes chunk) {
   return out;
 }
 
+std::array<double, 3> SwapEngine::probe_pcie_paced(Bytes bytes, Bytes chunk, int lag) {
+  Impl& m = *impl_;
+  if (chunk < kBlockBytes || chunk % kBlockBytes) chunk = kBlockBytes;
+  bytes = std::max<Bytes>(chunk, bytes - bytes % chunk);
+  lag = std::max(1, lag);
+  ProbeBufs b;
+  for (int i = 0; i < 2; ++i) {
+    NX_CUDA(cudaMalloc(&b.dev[i], bytes));
+    NX_CUDA(cudaMemset(b.dev[i], i, bytes));
+    prefer_numa_node(m.numa.node);
+    void* h = nullptr;
+    const cudaError_t e = cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+    prefer_numa_node(-1);
+    NX_CUDA(e);
+    b.host[i] = static_cast<std::uint8_t*>(h);
+    std::memset(h, 1 + i, bytes);
+  }
+  const std::size_t n = bytes / chunk;
+  std::vector<cudaEvent_t> landed(n);
+  for (auto& e : landed) NX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t ev[4];
+  for (auto& e : ev) NX_CUDA(cudaEventCreate(&e));
+  std::array<double, 3> best{0, 0, 0};
+  for (int rep = 0; rep < 4; ++rep) {
+    m.sync_own();
+    NX_CUDA(cudaEventRecord(ev[0], m.st[0]));
+    NX_CUDA(cudaEventRecord(ev[2], m.st[1]));
+    for (std::size_t i = 0; i < n; ++i) {
+      const Bytes off = i * chunk;
+      NX_CUDA(cudaMemcpyAsync(b.dev[1] + off, b.host[1] + off, chunk, cudaMemcpyHostToDevice, m.st[0]));
+      NX_CUDA(cudaEventRecord(landed[i], m.st[0]));
+      if (i >= static_cast<std::size_t>(lag)) NX_CUDA(cudaStreamWaitEvent(m.st[1], landed[i - lag], 0));
+      NX_CUDA(cudaMemcpyAsync(b.host[0] + off, b.dev[0] + off, chunk, cudaMemcpyDeviceToHost, m.st[1]));
+    }
+    NX_CUDA(cudaEventRecord(ev[1], m.st[0]));
+    NX_CUDA(cudaEventRecord(ev[3], m.st[1]));
+    m.sync_own();
+    if (rep == 0) continue;  // warm-up
+    float th = 0, td = 0, a = 0, z = 0;
+    NX_CUDA(cudaEventElapsedTime(&th, ev[0], ev[1]));
+    NX_CUDA(cudaEventElapsedTime(&td, ev[2], ev[3]));
+    NX_CUDA(cudaEventElapsedTime(&a, ev[0], ev[2]));
+    NX_CUDA(cudaEventElapsedTime(&z, ev[0], ev[3]));
+    const double span = std::max<double>(th, z) - std::min<double>(0.0, a);
+    const double total = 2.0 * static_cast<double>(bytes) / (span * 1e-3) / 1e9;
+    if (total > best[2]) best = {static_cast<double>(bytes) / (th * 1e-3) / 1e9, static_cast<double>(bytes) / (td * 1e-3) / 1e9, total};
+  }
+  for (auto& e : landed) cudaEventDestroy(e);
+  for (auto& e : ev) cudaEventDestroy(e);
+  return best;
+}
+
 }  // namespace nixie::b200
 
 namespace nixie::b200 {
@@ -1698,6 +1818,7 @@ void SwapEngine::set_option(const std::string& name, int value) {
   else if (name == "d2h_commit_legs" && value >= 0) c.d2h_commit_legs = value;
   else if (name == "early_frame_release" && (value == 0 || value == 1)) c.early_frame_release = value != 0;
   else if (name == "k3_verify_group" && value >= 1) c.k3_verify_group = value;
+  else if (name == "pace_lag_legs" && value >= -1) c.pace_lag_legs = value;
   else throw SimError(Err::ValidationError, "set_option: unknown option or bad value: " + name + "=" + std::to_string(value));
 }
 

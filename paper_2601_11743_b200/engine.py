@@ -43,6 +43,7 @@ class EngineConfig:
     k3_verify_group: int = 1024
     d2h_commit_legs: int = 32
     early_frame_release: bool = True
+    pace_lag_legs: int = 64
 
     def to_c(self) -> L.EngineConfigC:
         c = L.EngineConfigC()
@@ -246,6 +247,14 @@ class SwapEngine:
             out[f"sm_{key}"] = arr[1]
         out.update(bytes_per_direction=p.bytes_per_direction, chunk_bytes=p.chunk_bytes, numa_node=p.numa_node)
         return out
+
+    def probe_pcie_paced(self, bytes_per_direction: int = 2 * GIB, chunk_bytes: int = 64 * MIB, lag_chunks: int = 2) -> Dict:
+        """Both directions on the copy engines, D2H chunk i held until H2D chunk
+        i - lag_chunks landed (the engine's paced shape)."""
+        g = (ctypes.c_double * 3)()
+        check(lib.nx_probe_pcie_paced(self._h, bytes_per_direction, chunk_bytes, lag_chunks, g))
+        return {"ce_bidir_h2d": g[0], "ce_bidir_d2h": g[1], "ce_bidir_total": g[2], "bytes_per_direction": bytes_per_direction,
+                "chunk_bytes": chunk_bytes, "lag_chunks": lag_chunks}
 
     def calibrate(self, bytes_per_direction: int = 256 * MIB) -> Dict:
         """Measure SM kernel vs copy engines per batch size (1..128 legs) with
