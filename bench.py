@@ -302,9 +302,10 @@ def ncu_traffic() -> dict:
     """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            return json.load(f)
+            d = json.load(f)
     except OSError:
         return {}
+    return d.get("current", d)  # the capture of the current build (older rounds keyed by round)
 
 
 # ---------------------------------------------------------------------------------------------
