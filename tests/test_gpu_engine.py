@@ -195,3 +195,44 @@ def test_prefetch_then_switch_is_byte_exact(gpu):
         e.audit()
         for a in (0, 1, 2):
             assert e.verify_pattern(a, SEED) == 0
+
+
+@pytest.mark.parametrize("lag", [-1, 0, 8, 64])
+@pytest.mark.parametrize("name", ["small_three_apps", "c1_two_apps_2g"])
+def test_pacing_keeps_reference_trace(gpu, golden, name, lag):
+    """D2H pacing (pace_lag_legs) only delays departure groups on the device:
+    plans, per-lane orders and placements still equal the reference's, every
+    restore is byte-exact, and lag 0 (the direction lockstep) still finishes."""
+    real = run_scenario_real(load_scenario(name), seed=SEED, path=PATH_CE, pace_lag_legs=lag)
+    assert det_sha(real) == golden["scenarios"][name]["det_sha256"]
+    v = [ln.split() for ln in real.splitlines() if ln.startswith("V ")]
+    assert v and all(x[3] == "0" for x in v), v
+
+
+@pytest.mark.parametrize("lag", [0, 16, 64])
+def test_paced_full_gpu_exchange(gpu, oracle_lib, lag):
+    """A full GPU exchanging 1 GiB each way: with pacing on, departure groups
+    wait for landed fetches (pace_waits > 0), the lanes keep the plan's order
+    and both apps stay byte-exact over several switches."""
+    with SwapEngine(gpu_capacity=1 * GIB, pinned_capacity=2 * GIB, paged_capacity=64 * MIB, path=PATH_CE,
+                    pace_lag_legs=lag) as e:
+        e.allocate(0, 1 * GIB, TIER_GPU)
+        e.allocate(1, 1 * GIB, TIER_PINNED)
+        e.fill_pattern(0, SEED)
+        e.fill_pattern(1, SEED)
+        nxt = 1
+        for _ in range(4):
+            pc = PlannerConfig(streaming_window=64 * MIB, victim_order=[1 - nxt])
+            plan, bi, bo = e.plan_switch(nxt, pc)
+            st = e.switch_to(nxt, pc)
+            assert (st["bytes_in"], st["bytes_out"]) == (bi, bo) == (1 * GIB, 1 * GIB)
+            assert st["mismatches"] == 0 and st["verified"] == 512 and st["unverified"] == 0
+            assert st["pace_waits"] > 0, st
+            moves = [ln.split() for ln in plan.splitlines()]
+            assert [b for b, *_ in e.lane_trace(0)] == [int(m[0]) for m in moves if m[4] == "fetch"]
+            assert [b for b, *_ in e.lane_trace(1)] == [int(m[0]) for m in moves if m[4] == "evict"]
+            e.audit()
+            nxt = 1 - nxt
+        assert e.verify_pattern(0, SEED) == 0 and e.verify_pattern(1, SEED) == 0
+        for b in e.app_blocks(1)[::61]:
+            assert oracle_block_ok(e, oracle_lib, 1, b) == oracle_lib.so_pattern_block_checksum(SEED, 1, b)
