@@ -194,6 +194,17 @@ typedef struct {
   double host_submit_s, host_done_s;
 } nx_batch_record;
 int nx_batch_trace(nx_engine* e, nx_batch_record* out, size_t cap, size_t* n);
+/* Every leg of the last nx_switch (the reference's TransferRecord log,
+ * transfer.hpp:40-47), in commit order: PCIe legs carry their batch's device
+ * start/end, host legs (pinned<->paged) the host times of submission and
+ * commit (s, from the switch start). */
+typedef struct {
+  uint64_t block;
+  uint8_t src, dst; /* TierId */
+  uint8_t pad[6];
+  double start_s, end_s;
+} nx_leg_record;
+int nx_leg_records(nx_engine* e, nx_leg_record* out, size_t cap, size_t* n);
 /* cudaStream_t of a PCIe lane: 0 = H2D, 1 = D2H. */
 void* nx_lane_stream(nx_engine* e, int lane);
 

@@ -91,6 +91,11 @@ class BatchRecordC(Structure):
                 ("copied_s", c_double), ("end_s", c_double), ("host_submit_s", c_double), ("host_done_s", c_double)]
 
 
+class LegRecordC(Structure):
+    _fields_ = [("block", c_uint64), ("src", c_uint8), ("dst", c_uint8), ("pad", c_uint8 * 6), ("start_s", c_double),
+                ("end_s", c_double)]
+
+
 class DeviceInfoC(Structure):
     _fields_ = [("pci_bus_id", c_char * 32), ("numa_node", c_int), ("node_from_cpus", c_int), ("n_cpus", c_int),
                 ("cpulist", c_char * 256)]
@@ -136,6 +141,7 @@ _SIGNATURES = [
     ("nx_k3_trace", c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_int), POINTER(c_int), c_size_t,
                             POINTER(c_size_t)]),
     ("nx_batch_trace", c_int, [c_void_p, POINTER(BatchRecordC), c_size_t, POINTER(c_size_t)]),
+    ("nx_leg_records", c_int, [c_void_p, POINTER(LegRecordC), c_size_t, POINTER(c_size_t)]),
     ("nx_lane_stream", c_void_p, [c_void_p, c_int]),
     ("nx_probe_pcie", c_int, [c_void_p, c_uint64, c_uint64, POINTER(PcieProbeC)]),
     ("nx_probe_pcie_paced", c_int, [c_void_p, c_uint64, c_uint64, c_int, POINTER(c_double)]),

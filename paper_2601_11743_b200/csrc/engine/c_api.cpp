@@ -25,6 +25,7 @@ using namespace nixie::b200;
 
 struct nx_engine {
   std::unique_ptr<SwapEngine> eng;
+  std::vector<TransferRecord> last_legs;  // the last nx_switch's per-leg log
 };
 
 struct nx_gate {
@@ -365,6 +366,18 @@ int nx_switch(nx_engine* e, uint32_t incoming, const nx_planner_config* cfg, voi
     need(e, "engine");
     const ExecResult r = e->eng->switch_to(incoming, to_cpp(cfg), static_cast<cudaStream_t>(drain));
     fill_stats(*e->eng, r, out);
+    e->last_legs = r.events;
+  });
+}
+
+int nx_leg_records(nx_engine* e, nx_leg_record* out, size_t cap, size_t* n) {
+  return guard([&] {
+    need(e, "engine");
+    const auto& t = e->last_legs;
+    for (size_t i = 0; i < t.size() && i < cap && out; ++i)
+      out[i] = nx_leg_record{t[i].block, static_cast<uint8_t>(t[i].src), static_cast<uint8_t>(t[i].dst), {0}, t[i].start,
+                             t[i].end};
+    if (n) *n = t.size();
   });
 }
 

@@ -233,6 +233,17 @@ class SwapEngine:
         keys = ("stream", "legs", "ce", "start_s", "copied_s", "end_s", "host_submit_s", "host_done_s")
         return [{k: getattr(arr[i], k) for k in keys} for i in range(n.value)]
 
+    def leg_records(self) -> List[Dict]:
+        """Every leg of the last switch (TransferRecord log): block, src/dst tier,
+        start/end (s from the switch start; device times for PCIe legs, host
+        submit/commit times for pinned<->paged legs)."""
+        n = c_size_t()
+        check(lib.nx_leg_records(self._h, None, 0, byref(n)))
+        arr = (L.LegRecordC * max(1, n.value))()
+        check(lib.nx_leg_records(self._h, arr, n.value, byref(n)))
+        return [{"block": arr[i].block, "src": arr[i].src, "dst": arr[i].dst, "start_s": arr[i].start_s, "end_s": arr[i].end_s}
+                for i in range(n.value)]
+
     def lane_stream(self, lane: int) -> int:
         return lib.nx_lane_stream(self._h, lane) or 0
 
