@@ -277,8 +277,12 @@ def test_pause_during_a_capture_with_an_allocation_does_not_deadlock():
     import time
     with Daemon(gpu="4G", pinned="4G", paged="16G", idle_ms=20) as d:
         t0 = time.time()
-        a = d.spawn(_vec(3072, 3, 100, 101, "cap") + ["--graph", "3", "--capture-alloc-ms", "4000"])
-        time.sleep(2.0)  # the capture begins about now: app b's first launch asks for the GPU
+        a = d.spawn(_vec(3072, 3, 100, 101, "cap") + ["--graph", "3", "--capture-alloc-ms", "8000"])
+        # The capture begins about now; app b's first launch then asks for the
+        # GPU. The in-capture cudaMalloc comes 8 s into the capture, well after
+        # b's request even where b's CUDA start-up takes seconds (one box: 2.5 s
+        # with a 4 s delay let the Alloc land before the switch began).
+        time.sleep(2.0)
         b = d.spawn(_vec(3072, 3, 100, 102, "other"))
         outs = [p.communicate(timeout=300) for p in (a, b)]
         elapsed = time.time() - t0
