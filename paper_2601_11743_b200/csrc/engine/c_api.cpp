@@ -364,9 +364,9 @@ int nx_plan(nx_engine* e, uint32_t incoming, const nx_planner_config* cfg, char*
 int nx_switch(nx_engine* e, uint32_t incoming, const nx_planner_config* cfg, void* drain, nx_switch_stats* out) {
   return guard([&] {
     need(e, "engine");
-    const ExecResult r = e->eng->switch_to(incoming, to_cpp(cfg), static_cast<cudaStream_t>(drain));
+    ExecResult r = e->eng->switch_to(incoming, to_cpp(cfg), static_cast<cudaStream_t>(drain));
     fill_stats(*e->eng, r, out);
-    e->last_legs = r.events;
+    e->last_legs = std::move(r.events);
   });
 }
 
