@@ -807,12 +807,14 @@ struct SwapEngine::Impl final : detail::LaneSink {
     }
     inflight[s].push_back(std::move(B));
     // Group arrival checks; in the tail (fewer fetches left than a group) a
-    // check covers at least as many legs as remain to be submitted, so group
-    // sizes halve towards the end: the last check after the last copy is
-    // short and the tail takes a few launches, not one per batch.
+    // check covers at least three times the legs that remain to be
+    // submitted, so group sizes shrink geometrically towards the end: the
+    // last check after the last copy is one small batch and the tail takes
+    // ~3 launches (each pays ~30 us of launch cost under PCIe load, §3),
+    // not one per batch.
     const std::size_t remaining = fetches_total - fetches_submitted;
     if (!vgroup.empty() && (static_cast<int>(vgroup.size()) >= cfg.k3_verify_group ||
-                            (remaining < static_cast<std::size_t>(cfg.k3_verify_group) && vgroup.size() >= remaining)))
+                            (remaining < static_cast<std::size_t>(cfg.k3_verify_group) && vgroup.size() >= 3 * remaining)))
       flush_verify();
     maybe_release_gate();
   }
