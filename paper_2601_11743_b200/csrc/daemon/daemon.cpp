@@ -100,7 +100,7 @@ void usage() {
                "usage: nixied [--socket PATH] [--device N] [--gpu SIZE] [--pinned SIZE] [--paged SIZE]\n"
                "              [--window SIZE] [--min-bytes SIZE] [--path auto|ce|sm] [--host-threads N]\n"
                "              [--tick-ms X] [--idle-ms X] [--allot-s X] [--preempt-s X] [--log FILE] [--trace FILE]\n"
-               "              [--phys-slack SLABS] [--slab-mib 2..1024, power of 2] [--prefetch] [--exit-after-apps N]\n              [--reference-victims] [--keep-stale-maps | --isolate-victims]\n"
+               "              [--phys-slack SLABS] [--slab-mib 2..1024, power of 2] [--prefetch] [--exit-after-apps N]\n              [--reference-victims] [--keep-stale-maps | --isolate-victims] [--pace-lag LEGS (-1: off)]\n"
                "sizes take a K/M/G suffix (GiB when bare). The daemon serves LD_PRELOAD=libnixie_shim.so apps\n"
                "that set NIXIE_SOCKET=PATH.\n");
 }
@@ -143,6 +143,13 @@ bool parse_args(int argc, char** argv, Options& o) {
       o.slab_blocks = static_cast<std::uint32_t>(mib / 2);
     }
     else if (a == "--prefetch") o.prefetch = true;
+    else if (a == "--pace-lag") {
+      char* end = nullptr;
+      const char* v = val();
+      const long lag = std::strtol(v, &end, 10);
+      if (!end || *end != 0 || lag < -1) throw SimError(Err::ValidationError, std::string("--pace-lag must be >= -1, got ") + v);
+      o.eng.pace_lag_legs = static_cast<int>(lag);
+    }
     else if (a == "--reference-victims") o.reference_victims = true;
     else if (a == "--keep-stale-maps") o.keep_stale_maps = 1;
     else if (a == "--isolate-victims") o.keep_stale_maps = 0;

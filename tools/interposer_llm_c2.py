@@ -16,14 +16,15 @@ from paper_2601_11743_b200.interpose import Daemon, run_apps  # noqa: E402
 
 LLM = os.path.join(ROOT, "tests", "apps", "llm_app.py")
 reqs = int(sys.argv[1]) if len(sys.argv) > 1 else 12
-out = sys.argv[2] if len(sys.argv) > 2 else None
+out = (sys.argv[2] or None) if len(sys.argv) > 2 else None
 slab = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3] != "0" else None
 flags = sys.argv[4].split(",") if len(sys.argv) > 4 else []
 ref_victims = "ref" in flags  # the planner's own victim blocks
 isolate = "isolate" in flags  # --isolate-victims
+nopace = "nopace" in flags  # --pace-lag -1
 slack = int(sys.argv[5]) if len(sys.argv) > 5 else None  # physical slack slabs
 with Daemon(gpu="32G", pinned="16G", paged="96G", log=out, slab_mib=slab,
-            extra=(["--reference-victims"] if ref_victims else []) + (["--isolate-victims"] if isolate else []) + (["--phys-slack", str(slack)] if slack is not None else [])) as d:
+            extra=(["--reference-victims"] if ref_victims else []) + (["--isolate-victims"] if isolate else []) + (["--phys-slack", str(slack)] if slack is not None else []) + (["--pace-lag", "-1"] if nopace else [])) as d:
     res = run_apps(d, [[sys.executable, LLM, str(reqs), "1.0", "1", "qwen3-8b", "1", "512"],
                        [sys.executable, LLM, str(reqs), "1.5", "2", "flux-12b", "1", "1024"]], timeout=1800, stagger_s=1.0)
     sw = d.switches()
