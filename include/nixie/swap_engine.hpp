@@ -111,6 +111,10 @@ struct SwitchStats {
   int host_legs = 0;
   int ce_calls = 0;                         // cudaMemcpyAsync calls (contiguous runs) of the CE batches
   int pace_waits = 0;                       // D2H groups held behind landed fetches (pace_lag_legs)
+  // CE runs per direction ([0] H2D, [1] D2H) and why each run ended early:
+  // source not contiguous, destination not contiguous (the rest end at a
+  // group or batch boundary).
+  int ce_calls_dir[2] = {0, 0}, run_breaks_src[2] = {0, 0}, run_breaks_dst[2] = {0, 0};
   std::uint64_t verified = 0, unverified = 0, mismatches = 0;
   // Per kernel kind (CUDA events on the launching stream):
   double k1_s = 0;      // K1 swap launches (SM path): summed durations

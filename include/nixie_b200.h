@@ -97,6 +97,8 @@ typedef struct nx_switch_stats {
   double k3_kernel_s; /* summed in-kernel K3 spans (%globaltimer) */
   int ce_calls;       /* cudaMemcpyAsync calls of the CE batches */
   int pace_waits;     /* departure groups held behind landed fetches (pace_lag_legs) */
+  int ce_calls_dir[2]; /* CE calls per direction: [0] H2D, [1] D2H */
+  int run_breaks_src[2], run_breaks_dst[2]; /* runs ended by a non-contiguous source / destination */
 } nx_switch_stats;
 
 typedef struct nx_pcie_probe {

@@ -73,11 +73,14 @@ class SwitchStatsC(Structure):
         ("unverified", c_uint64), ("mismatches", c_uint64), ("tp_to_gpu", c_double), ("tp_from_gpu", c_double),
         ("tp_bidir", c_double), ("k1_s", c_double), ("k3_s", c_double), ("k1_bytes", c_uint64), ("k3_bytes", c_uint64),
         ("k1_launches", c_int), ("k3_launches", c_int), ("k3_busy_s", c_double), ("k3_kernel_s", c_double),
-        ("ce_calls", c_int), ("pace_waits", c_int),
+        ("ce_calls", c_int), ("pace_waits", c_int), ("ce_calls_dir", c_int * 2), ("run_breaks_src", c_int * 2),
+        ("run_breaks_dst", c_int * 2),
     ]
 
     def as_dict(self) -> dict:
-        return {name: getattr(self, name) for name, _ in self._fields_}
+        return {name: (list(getattr(self, name)) if name in ("ce_calls_dir", "run_breaks_src", "run_breaks_dst")
+                       else getattr(self, name)) for name, _ in self._fields_}
+
 
 
 class PcieProbeC(Structure):

@@ -892,14 +892,16 @@ class Daemon {
          ", \"premap_ms\": %.3f, \"premap_calls\": %" PRIu64 ", \"premap_unmap_ms\": %.3f, \"total_ms\": %.3f"
          ", \"device_span_ms\": %.3f"
          ", \"verified\": %" PRIu64 ", \"unverified\": %" PRIu64 ", \"mismatches\": %" PRIu64
-         ", \"partial_slabs\": %" PRIu64 ", \"free_slabs\": %zu, \"live_slabs\": %zu}",
+         ", \"partial_slabs\": %" PRIu64 ", \"free_slabs\": %zu, \"live_slabs\": %zu, \"ce_calls\": %d, \"pace_waits\": %d"
+         ", \"ce_calls_dir\": [%d, %d], \"run_breaks_src\": [%d, %d], \"run_breaks_dst\": [%d, %d]}",
          t, holder ? static_cast<int>(*holder) : -1, to, plan.bytes_in, plan.bytes_out, s.pcie_h2d_bytes, s.pcie_d2h_bytes,
          s.host_bytes, ms(t_start, t_drained), ms(t_drained, t_planned), ms(t_planned, t_copied), ms(t_copied, t_unmapped),
          ms(t_unmapped, t_end), static_cast<double>(gm.map_ns) * 1e-6, gm.map_calls, gm.unmap_calls,
          gm.recv_ns > t_grant_sent ? ms(t_grant_sent, gm.recv_ns) : 0.0, static_cast<double>(gm.premap_ns) * 1e-6, gm.premap_calls,
          static_cast<double>(gm.premap_unmap_ns) * 1e-6, ms(t_start, t_end),
          s.device_span_s * 1e3, s.verified, s.unverified, s.mismatches, placer_.partial(), placer_.free_slabs(),
-         placer_.live_slabs());
+         placer_.live_slabs(), s.ce_calls, s.pace_waits, s.ce_calls_dir[0], s.ce_calls_dir[1], s.run_breaks_src[0],
+         s.run_breaks_src[1], s.run_breaks_dst[0], s.run_breaks_dst[1]);
   }
 
   // ---- reference replay trace (--trace) ---------------------------------------

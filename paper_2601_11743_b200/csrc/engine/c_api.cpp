@@ -143,6 +143,11 @@ void fill_stats(const SwapEngine& eng, const ExecResult& r, nx_switch_stats* out
   out->k3_kernel_s = s.k3_kernel_s;
   out->ce_calls = s.ce_calls;
   out->pace_waits = s.pace_waits;
+  for (int k = 0; k < 2; ++k) {
+    out->ce_calls_dir[k] = s.ce_calls_dir[k];
+    out->run_breaks_src[k] = s.run_breaks_src[k];
+    out->run_breaks_dst[k] = s.run_breaks_dst[k];
+  }
   if (s.device_span_s > 0) {
     double lo = 1e30, hi = 0;
     for (const TransferRecord& t : r.events)

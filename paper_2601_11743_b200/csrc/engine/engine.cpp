@@ -303,6 +303,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   bool gate_done = false;
 
   explicit Impl(const EngineConfig& c) : cfg(c) {
+    pinned_prev.fill(UnitRing::kNone);
     if (cfg.gpu_capacity % kBlockBytes || cfg.pinned_capacity % kBlockBytes ||
         (cfg.paged_capacity != kUnbounded && cfg.paged_capacity % kBlockBytes))
       throw SimError(Err::ValidationError, "tier budgets must be multiples of 2 MiB");
@@ -494,8 +495,17 @@ struct SwapEngine::Impl final : detail::LaneSink {
     }
   }
 
-  std::uint32_t take_unit(TierId t, BlockId b) {
+  // Pinned slots of one lane's legs are taken contiguously when they can be
+  // (UnitRing::acquire_after), so departures and the later fetches of the
+  // same blocks copy in long runs even after the ring's free order fragments.
+  std::array<std::uint32_t, detail::kLaneCount> pinned_prev;
+  std::uint32_t take_unit(TierId t, BlockId b, int lane = -1) {
     if (t == TierId::Gpu && placer) return placer->acquire(b);
+    if (t == TierId::PinnedHost && lane >= 0) {
+      const std::uint32_t u = pinned.ring.acquire_after(pinned_prev[lane], tier_name(t));
+      pinned_prev[lane] = u;
+      return u;
+    }
     return ring_of(t).acquire(tier_name(t));
   }
   void give_unit(TierId t, BlockId b, std::uint32_t u) {
@@ -645,7 +655,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
   // ---- lane sink ----------------------------------------------------------
   void leg_started(int lane, std::size_t mi, TierId from, TierId to, bool) override {
     const BlockId b = lanes->move(mi).block;
-    Leg L{mi, b, from, to, unit[b], take_unit(to, b), lane, false, secs_since(t0), 0};
+    Leg L{mi, b, from, to, unit[b], take_unit(to, b, lane), lane, false, secs_since(t0), 0};
     const auto idx = static_cast<std::uint32_t>(legs.size());
     legs.push_back(L);
     trace[lane].push_back(LegTrace{b, from, to});
@@ -869,11 +879,19 @@ struct SwapEngine::Impl final : detail::LaneSink {
       std::size_t n = 1;
       while (i + n < count) {
         const Leg& c = legs[idx[i + n]];
-        if (dev_addr(c.from, c.src_u) != src + n * kBlockBytes || dev_addr(c.to, c.dst_u) != dst + n * kBlockBytes) break;
+        const bool src_ok = dev_addr(c.from, c.src_u) == src + n * kBlockBytes;
+        const bool dst_ok = dev_addr(c.to, c.dst_u) == dst + n * kBlockBytes;
+        if (!src_ok || !dst_ok) {
+          const int d = kind == cudaMemcpyHostToDevice ? 0 : 1;
+          stats.run_breaks_src[d] += !src_ok;
+          stats.run_breaks_dst[d] += !dst_ok;
+          break;
+        }
         ++n;
       }
       NX_CUDA(cudaMemcpyAsync(dst, src, n * kBlockBytes, kind, st[s]));
       ++stats.ce_calls;
+      ++stats.ce_calls_dir[kind == cudaMemcpyHostToDevice ? 0 : 1];
       i += n;
     }
   }

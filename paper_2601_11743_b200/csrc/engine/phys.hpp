@@ -34,26 +34,65 @@ class CudaFailure : public SimError {
 
 // A fixed set of 2 MiB units handed out FIFO (a ring: freed units go to the
 // back). acquire() failing means the registry let a tier overcommit.
+// acquire_after(prev) hands out the unit right after `prev` when it is free:
+// consecutive acquisitions of one stream of legs (a lane's departures into
+// the pinned ring) then stay contiguous, so their copies merge into long
+// copy-engine calls even after the ring's free order has fragmented. A unit
+// taken that way stays in the FIFO as a stale entry, skipped when reached.
 class UnitRing {
  public:
+  static constexpr std::uint32_t kNone = ~0u;
   void reset(std::uint32_t units) {
     free_.clear();
+    is_free_.assign(units, 1);
     for (std::uint32_t u = 0; u < units; ++u) free_.push_back(u);
     units_ = units;
+    n_free_ = units;
   }
   std::uint32_t acquire(const char* tier) {
+    while (!free_.empty() && !is_free_[free_.front()]) free_.pop_front();  // stale entries
     if (free_.empty()) throw InvariantViolation(std::string(tier) + " has no free 2 MiB unit (budget overcommitted)");
     const std::uint32_t u = free_.front();
     free_.pop_front();
+    take(u);
     return u;
   }
-  void release(std::uint32_t u) { free_.push_back(u); }
+  std::uint32_t acquire_after(std::uint32_t prev, const char* tier) {
+    if (prev != kNone && prev + 1 < units_ && is_free_[prev + 1]) {
+      take(prev + 1);
+      return prev + 1;
+    }
+    return acquire(tier);
+  }
+  void release(std::uint32_t u) {
+    is_free_[u] = 1;
+    ++n_free_;
+    free_.push_back(u);
+    if (free_.size() > 2 * static_cast<std::size_t>(units_) + 64) compact();
+  }
   std::uint32_t units() const { return units_; }
-  std::size_t free_units() const { return free_.size(); }
+  std::size_t free_units() const { return n_free_; }
 
  private:
+  void take(std::uint32_t u) {
+    is_free_[u] = 0;
+    --n_free_;
+  }
+  // Drops stale and duplicate entries, keeping the FIFO order of the rest.
+  void compact() {
+    std::vector<std::uint8_t> seen(units_, 0);
+    std::deque<std::uint32_t> keep;
+    for (std::uint32_t u : free_)
+      if (is_free_[u] && !seen[u]) {
+        seen[u] = 1;
+        keep.push_back(u);
+      }
+    free_.swap(keep);
+  }
   std::deque<std::uint32_t> free_;
+  std::vector<std::uint8_t> is_free_;
   std::uint32_t units_ = 0;
+  std::size_t n_free_ = 0;
 };
 
 // NUMA placement of the GPU's host-side resources.

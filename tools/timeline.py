@@ -123,6 +123,8 @@ def main():
         row = analyse(tr, st)
         row["ce_calls"] = st["ce_calls"]
         row["mib_per_ce_call"] = (st["pcie_h2d_bytes"] + st["pcie_d2h_bytes"]) / MIB / max(1, st["ce_calls"])
+        for k in ("ce_calls_dir", "run_breaks_src", "run_breaks_dst"):
+            row[k] = st[k]
         rows.append(row)
     bad = eng.verify_pattern(0, 7) + eng.verify_pattern(1, 7)
     eng.close()
