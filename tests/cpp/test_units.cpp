@@ -3,7 +3,9 @@
 //     slab by the blocks of one vslab, release, affinity, exhaustion,
 //     mapping bookkeeping;
 //   RangeAlloc (csrc/shim/range_alloc.hpp): first fit, slab alignment,
-//     coalescing on free.
+//     coalescing on free;
+//   UnitRing (csrc/engine/phys.hpp): FIFO order, contiguity-preferring
+//     acquire_after, stale entries, never handing out a unit twice.
 // Built by paper_2601_11743_b200/Makefile (lib/nx_unit_tests); run by
 // tests/test_interposer_host.py.
 #include <cstdio>
@@ -13,6 +15,7 @@
 #include <algorithm>
 
 #include "nixie/planner.hpp"
+#include "phys.hpp"
 #include "range_alloc.hpp"
 #include "slab_placer.hpp"
 
@@ -166,7 +169,49 @@ static void range_alloc() {
   CHECK(!r.take(1, 64, d));
 }
 
+static void unit_ring() {
+  UnitRing r;
+  r.reset(8);
+  CHECK(r.acquire("t") == 0 && r.acquire("t") == 1 && r.free_units() == 6);  // FIFO
+  r.release(0);                                                          // free order: 2..7, 0
+  CHECK(r.acquire_after(1, "t") == 2);                                   // contiguous after 1
+  CHECK(r.acquire_after(2, "t") == 3);
+  r.release(1);                                                          // 4..7, 0, 1
+  CHECK(r.acquire_after(7, "t") == 4);                                   // 8 is out of range: FIFO head
+  CHECK(r.acquire_after(UnitRing::kNone, "t") == 5);
+  CHECK(r.acquire_after(5, "t") == 6);
+  CHECK(r.acquire("t") == 7);                                           // 2, 3 and 6 were stale entries
+  CHECK(r.acquire("t") == 0 && r.acquire("t") == 1 && r.free_units() == 0);
+  bool threw = false;
+  try {
+    r.acquire("t");
+  } catch (const InvariantViolation&) {
+    threw = true;
+  }
+  CHECK(threw);
+  // Random churn: every acquired unit is free before and never handed out twice.
+  r.reset(64);
+  std::set<std::uint32_t> held;
+  std::uint32_t prev = UnitRing::kNone;
+  unsigned x = 12345;
+  for (int i = 0; i < 20000; ++i) {
+    x = x * 1103515245u + 12345u;
+    if ((x >> 16) % 3 != 0 && held.size() < 64) {
+      const std::uint32_t u = ((x >> 8) & 1) ? r.acquire_after(prev, "t") : r.acquire("t");
+      CHECK(held.insert(u).second);
+      prev = u;
+    } else if (!held.empty()) {
+      auto it = held.begin();
+      std::advance(it, (x >> 4) % held.size());
+      r.release(*it);
+      held.erase(it);
+    }
+    CHECK(r.free_units() == 64 - held.size());
+  }
+}
+
 int main() {
+  unit_ring();
   slab_placer();
   slab_growth();
   range_alloc();
