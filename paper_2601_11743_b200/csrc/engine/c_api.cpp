@@ -798,14 +798,22 @@ int nx_scenario_real(const char* spec, const nx_engine_config* cfg, uint64_t see
     SwitchRunner runner;
     runner.mem = [&]() -> MemState& { return eng.mem(); };
     runner.virtual_clock = false;
+    // The scenario's schedule runs on the virtual clock, as in the reference:
+    // a switch completes when the model (on a copy of the registry) says so,
+    // not when the real copies end. Otherwise a scenario whose switch times
+    // are close together would schedule differently on real hardware (which
+    // request arrives before which switch ends feeds the MLFQ's decisions),
+    // and the plans of later switches would follow another schedule.
     runner.run = [&](const MigrationPlan& plan, const PlannerConfig& pc, Seconds now,
                      std::array<std::vector<std::array<std::uint64_t, 3>>, 6>& lanes) {
-      const ExecResult r = eng.execute(plan, pc);
+      MemState shadow = eng.mem();
+      const ExecResult model = execute(plan, shadow, sc.hw, pc, now);
+      eng.execute(plan, pc);
       const auto& t = eng.lane_trace();
       for (int l = 0; l < 6; ++l)
         for (const LegTrace& x : t[l])
           lanes[l].push_back({x.block, static_cast<std::uint64_t>(x.src), static_cast<std::uint64_t>(x.dst)});
-      return now + r.completion;
+      return model.completion;
     };
     runner.after_switch = [&](std::size_t k, AppId incoming, std::string& out) {
       const SwitchStats& s = eng.last_stats();
