@@ -81,6 +81,7 @@ struct EngineConfig {
   // per switch than none; 48-96 within 0.5%; 0 serialises the two directions
   // (the fetches need the frames the departures vacate) and 128 gains nothing.
   int pace_lag_legs = 64;
+  bool fetch_first_pump = true;  // lanes toward the GPU pumped first after a commit (LaneSet::set_fetch_first)
   bool exportable_arena = false;      // GPU tier = exportable VMM slabs shims can import (interposer daemon)
   Bytes arena_slab_bytes = 128 * kMiB; // exportable arena: bytes per physical allocation (a multiple of 2 MiB)
   Bytes gpu_physical = 0;             // arena bytes (0 = gpu_capacity); the registry still enforces gpu_capacity

@@ -99,6 +99,7 @@ EngineConfig to_cpp(const nx_engine_config& c) {
   o.d2h_commit_legs = c.d2h_commit_legs;
   o.early_frame_release = c.early_frame_release != 0;
   o.pace_lag_legs = c.pace_lag_legs;
+  o.fetch_first_pump = c.fetch_first_pump != 0;
   return o;
 }
 
@@ -216,6 +217,7 @@ void nx_engine_config_default(nx_engine_config* c) {
   c->d2h_commit_legs = d.d2h_commit_legs;
   c->early_frame_release = d.early_frame_release;
   c->pace_lag_legs = d.pace_lag_legs;
+  c->fetch_first_pump = d.fetch_first_pump;
 }
 
 void nx_planner_config_default(nx_planner_config* c) {

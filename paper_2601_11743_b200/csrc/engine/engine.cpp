@@ -1219,6 +1219,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
     ls.set_limit(kD2H, cfg.pcie_legs_in_flight);
     ls.set_limit(2, cfg.host_legs_in_flight);
     ls.set_limit(3, cfg.host_legs_in_flight);
+    ls.set_fetch_first(cfg.fetch_first_pump);
     lanes = &ls;
     finished = false;
 
@@ -1839,6 +1840,7 @@ void SwapEngine::set_option(const std::string& name, int value) {
   else if (name == "early_frame_release" && (value == 0 || value == 1)) c.early_frame_release = value != 0;
   else if (name == "k3_verify_group" && value >= 1) c.k3_verify_group = value;
   else if (name == "pace_lag_legs" && value >= -1) c.pace_lag_legs = value;
+  else if (name == "fetch_first_pump" && (value == 0 || value == 1)) c.fetch_first_pump = value != 0;
   else throw SimError(Err::ValidationError, "set_option: unknown option or bad value: " + name + "=" + std::to_string(value));
 }
 

@@ -106,9 +106,9 @@ bool LaneSet::extra_leaves_room(int lane, TierId hop, bool use_window) const {
 }
 
 // Head-of-direction pump; see lanes.hpp for why it equals ref :145-171.
-void LaneSet::pump(int lane) {
+void LaneSet::pump(int lane, int cap) {
   Lane& L = lanes_[lane];
-  while (L.inflight < L.limit && !(loading_ && L.inflight > 0)) {
+  while (L.inflight < std::min(L.limit, cap) && !(loading_ && L.inflight > 0)) {
     int first = 0;
     if (L.q[0].empty() || (!L.q[1].empty() && L.q[1].front().seq < L.q[0].front().seq)) first = 1;
     int pick = -1;
@@ -133,6 +133,14 @@ void LaneSet::pump(int lane) {
 }
 
 void LaneSet::pump_all() {
+  if (fetch_first_) {
+    // Every lane's first leg in the reference's lane order (the one-leg
+    // decisions), then the extra legs: toward the GPU first.
+    for (int lane = 0; lane < kLaneCount; ++lane) pump(lane, 1);
+    for (int dir = 0; dir < 2; ++dir)
+      for (int lane = dir; lane < kLaneCount; lane += 2) pump(lane);
+    return;
+  }
   for (int lane = 0; lane < kLaneCount; ++lane) pump(lane);
 }
 

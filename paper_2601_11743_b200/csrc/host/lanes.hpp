@@ -50,6 +50,15 @@ class LaneSet {
   LaneSet(MemState& mem, const HardwareConfig& hw);
 
   void set_limit(int lane, int legs);
+  // Concurrent lanes only: after a commit, start every lane's first leg in
+  // lane order (as the reference would, transfer.cpp:217-221), then the
+  // extra legs of the lanes toward the GPU (0, 2, 4) before the others. In
+  // plain lane order, with many legs per lane, the evictions into the pinned
+  // tier (lane 1) take every slot that frees, and the fetches' first hop into
+  // it (lane 2) starves until they are done: the two halves of a two-hop
+  // switch run one after the other. Per-lane FIFO order, and so the
+  // decisions, are the same either way.
+  void set_fetch_first(bool on) { fetch_first_ = on; }
   int limit(int lane) const { return lanes_[lane].limit; }
 
   void begin(const MigrationPlan& plan, const PlannerConfig& cfg, bool gate_evictions, AppId window_owner,
@@ -97,7 +106,7 @@ class LaneSet {
 
   static TierId next_hop(const MoveState& ms);
   void enqueue(std::size_t mi);
-  void pump(int lane);
+  void pump(int lane, int cap = 1 << 30);  // starts legs while fewer than min(limit, cap) are in flight
   void pump_all();
   bool gated(const MoveState& ms) const;
   bool startable(const MoveState& ms, TierId hop, bool* use_window) const;
@@ -116,6 +125,7 @@ class LaneSet {
   std::uint64_t seq_ = 0;
   bool gate_open_ = true;
   bool loading_ = false;  // begin(): first legs only
+  bool fetch_first_ = false;
   bool window_wanted_ = false;
   bool window_held_ = false;
   Bytes window_size_ = 0;

@@ -92,6 +92,7 @@ bool Orchestrator::quiesced() const { return lanes_->quiesced(); }
 
 void Orchestrator::set_lane_concurrency(int legs_per_lane) {
   for (int lane = 0; lane < detail::kLaneCount; ++lane) lanes_->set_limit(lane, legs_per_lane);
+  lanes_->set_fetch_first(legs_per_lane > 1);
 }
 
 // reference transfer.cpp:250-271

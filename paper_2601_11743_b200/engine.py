@@ -44,6 +44,7 @@ class EngineConfig:
     d2h_commit_legs: int = 32
     early_frame_release: bool = True
     pace_lag_legs: int = 64
+    fetch_first_pump: bool = True
 
     def to_c(self) -> L.EngineConfigC:
         c = L.EngineConfigC()
