@@ -163,6 +163,33 @@ def test_calibration_and_probe(gpu):
             assert p[k] > 5.0, p
         c = e.calibrate(64 * MIB)
         assert len(c["legs"]) == 8 and all(x > 1.0 for x in c["ce_gbps"] + c["sm_gbps"])
+        q = e.probe_pcie_paced(256 * MIB, 32 * MIB, 2)  # the engine's paced shape
+        assert q["ce_bidir_h2d"] > 5.0 and q["ce_bidir_d2h"] > 5.0, q
+        assert q["ce_bidir_total"] <= q["ce_bidir_h2d"] + q["ce_bidir_d2h"] + 1e-6, q
+
+
+def test_leg_records_log_every_hop(gpu):
+    """nx_leg_records: one record per hop of the last switch (the reference's
+    TransferRecord log), PCIe hops with device times inside the switch, host
+    hops (two-hop through a 16 MiB pinned budget) with host times."""
+    with SwapEngine(gpu_capacity=64 * MIB, pinned_capacity=16 * MIB, paged_capacity=256 * MIB, path=PATH_CE,
+                    host_threads=2) as e:
+        e.allocate(0, 64 * MIB, TIER_GPU)
+        e.allocate(1, 64 * MIB, TIER_PAGED)
+        e.fill_pattern(0, SEED)
+        e.fill_pattern(1, SEED)
+        pc = PlannerConfig(streaming_window=4 * MIB, pinned_budget=16 * MIB, victim_order=[0])
+        plan, bi, bo = e.plan_switch(1, pc)
+        st = e.switch_to(1, pc)
+        recs = e.leg_records()
+        hops = sum(int(m[3]) for m in (ln.split() for ln in plan.splitlines()))  # "block src dst distance kind"
+        assert len(recs) == hops > (bi + bo) // (2 * MIB), (len(recs), hops)  # some moves are two-hop
+        pcie = [r for r in recs if 0 in (r["src"], r["dst"])]
+        host = [r for r in recs if 0 not in (r["src"], r["dst"])]
+        assert len(pcie) == (st["pcie_h2d_bytes"] + st["pcie_d2h_bytes"]) // (2 * MIB) and host, (len(pcie), len(host))
+        span = st["wall_s"] + 1e-3
+        assert all(0 <= r["start_s"] <= r["end_s"] <= span for r in recs), recs[:4]
+        assert e.verify_pattern(1, SEED) == 0 and e.verify_pattern(0, SEED) == 0
 
 
 def test_prefetch_then_switch_is_byte_exact(gpu):
