@@ -7,7 +7,8 @@ sys.path.insert(0, ".")
 from paper_2601_11743_b200 import MIB, PlannerConfig, SwapEngine
 from paper_2601_11743_b200._lib import PATH_CE, PATH_SM, TIER_GPU, TIER_PAGED, TIER_PINNED
 
-for opts in (dict(path=PATH_SM), dict(path=PATH_CE, k3_grouped=False), dict(path=PATH_CE, k3_grouped=True)):
+for opts in (dict(path=PATH_SM), dict(path=PATH_CE, k3_grouped=False), dict(path=PATH_CE, k3_grouped=True),
+             dict(path=PATH_CE, pace_lag_legs=2, first_batch_legs=1, d2h_commit_legs=1)):  # paced, tiny groups
     with SwapEngine(gpu_capacity=32 * MIB, pinned_capacity=48 * MIB, paged_capacity=64 * MIB, **opts) as e:
         e.allocate(0, 32 * MIB, TIER_GPU)
         e.allocate(1, 24 * MIB, TIER_PINNED)
