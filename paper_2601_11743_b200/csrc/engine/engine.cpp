@@ -1169,6 +1169,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
     for (auto& t : trace) t.clear();
     legs.clear();
     landed.clear();
+    detail_pending = false;
     events_used = 0;
     batches_sent = {0, 0};
     d2h_legs_sent = 0;
@@ -1298,55 +1299,66 @@ struct SwapEngine::Impl final : detail::LaneSink {
     return res;
   }
 
-  // Device timestamps for the PCIe records and the per-stream kernel time.
+  // Device timing of the last execute. The switch span and the K3 figures
+  // are computed before execute() returns. The per-batch detail (the batch
+  // timeline, per-stream launch time, K1 figures, device times on the PCIe
+  // records) costs one cudaEventElapsedTime per event, ~300 per config-2
+  // switch and ~1.4 ms in all. On the copy-engine path with grouped checks it
+  // is computed only when asked for (batch_trace(); the events stay valid
+  // until the next execute), and the records keep their host times (leg
+  // start, commit).
+  bool detail_pending = false;
+  float since_ev0(cudaEvent_t e) {
+    float ms = 0;
+    NX_CUDA(cudaEventElapsedTime(&ms, ev0, e));
+    return ms;
+  }
   void finalize_timing(ExecResult& res) {
-    double first = 1e30, last = 0;
     std::vector<std::pair<double, double>> k3_spans;
     k3_trace.clear();
     batch_tr.clear();
-    for (const Batch& B : landed) {
-      float a = 0, b = 0, c = 0;
-      NX_CUDA(cudaEventElapsedTime(&a, ev0, B.ev_start));
-      NX_CUDA(cudaEventElapsedTime(&b, ev0, B.ev_end));
-      if (B.ev_copied != nullptr) NX_CUDA(cudaEventElapsedTime(&c, ev0, B.ev_copied));
-      const double s0 = a * 1e-3, s1 = b * 1e-3;
-      batch_tr.push_back(BatchTrace{B.stream, static_cast<int>(B.legs.size()), B.ce, s0,
-                                    B.ev_copied != nullptr ? c * 1e-3 : s1, s1, B.host_submit, B.host_done});
-      first = std::min(first, s0);
-      last = std::max(last, s1);
-      stats.kernel_s[B.stream] += s1 - s0;
-      if (!B.ce) {
-        stats.k1_s += s1 - s0;
-        stats.k1_bytes += B.legs.size() * kBlockBytes;
-        ++stats.k1_launches;
+    const bool fast = grouped && std::all_of(landed.begin(), landed.end(), [](const Batch& B) {
+      return B.ce && !B.end_on_side && B.k3ev.empty();
+    });
+    if (fast) {
+      // Batches of a stream start and end in submission order: the span is
+      // the first start and the last end of each stream.
+      double first = 1e30, last = 0;
+      for (int s = 0; s < 2; ++s) {
+        const Batch* a = nullptr;
+        const Batch* z = nullptr;
+        for (const Batch& B : landed)
+          if (B.stream == s) {
+            if (!a) a = &B;
+            z = &B;
+          }
+        if (!a) continue;
+        first = std::min(first, since_ev0(a->ev_start) * 1e-3);
+        last = std::max(last, since_ev0(z->ev_end) * 1e-3);
       }
-      for (const auto& ke : B.k3ev) {
-        float a0 = 0, a1 = 0;
-        NX_CUDA(cudaEventElapsedTime(&a0, ev0, ke[0]));
-        NX_CUDA(cudaEventElapsedTime(&a1, ev0, ke[1]));
-        stats.k3_s += (a1 - a0) * 1e-3;
-        k3_spans.emplace_back(a0 * 1e-3, a1 * 1e-3);
-        k3_trace.push_back(K3Launch{a0 * 1e-3, a1 * 1e-3, static_cast<int>(B.k3_bytes / kBlockBytes / B.k3ev.size()), B.stream});
-        ++stats.k3_launches;
-      }
-      stats.k3_bytes += B.k3_bytes;
-      for (auto i : B.legs) {
-        TransferRecord& r = res.events[legs[i].rec];
-        r.start = s0;
-        r.end = s1;
-      }
+      stats.device_span_s = landed.empty() ? 0.0 : last - first;
+      detail_pending = !landed.empty();
+    } else {
+      batch_detail(&res);
     }
     for (const GroupK3& g : gk3) {
-      float a0 = 0, a1 = 0;
-      NX_CUDA(cudaEventElapsedTime(&a0, ev0, g.a));
-      NX_CUDA(cudaEventElapsedTime(&a1, ev0, g.z));
-      stats.k3_s += (a1 - a0) * 1e-3;
-      k3_spans.emplace_back(a0 * 1e-3, a1 * 1e-3);
-      k3_trace.push_back(K3Launch{a0 * 1e-3, a1 * 1e-3, g.legs, g.lane});
+      const double a0 = since_ev0(g.a) * 1e-3, a1 = since_ev0(g.z) * 1e-3;
+      stats.k3_s += a1 - a0;
+      k3_spans.emplace_back(a0, a1);
+      k3_trace.push_back(K3Launch{a0, a1, g.legs, g.lane});
       stats.k3_bytes += static_cast<Bytes>(g.legs) * kBlockBytes;
       ++stats.k3_launches;
     }
-    stats.device_span_s = landed.empty() ? 0.0 : last - first;
+    for (const Batch& B : landed) {  // per-batch K3 launches (ungrouped CE path)
+      stats.k3_bytes += B.k3_bytes;
+      for (const auto& ke : B.k3ev) {
+        const double a0 = since_ev0(ke[0]) * 1e-3, a1 = since_ev0(ke[1]) * 1e-3;
+        stats.k3_s += a1 - a0;
+        k3_spans.emplace_back(a0, a1);
+        k3_trace.push_back(K3Launch{a0, a1, static_cast<int>(B.k3_bytes / kBlockBytes / B.k3ev.size()), B.stream});
+        ++stats.k3_launches;
+      }
+    }
     // K3 launches of the two lanes overlap on the device; their busy time is
     // the union of their intervals (bytes / busy = achieved HBM bandwidth).
     std::sort(k3_spans.begin(), k3_spans.end());
@@ -1373,6 +1385,38 @@ struct SwapEngine::Impl final : detail::LaneSink {
       for (std::uint32_t i = 0; i < k3_slots_used; ++i)
         if (ke[i] > ks[i] && ks[i] != ~0ull) stats.k3_kernel_s += (ke[i] - ks[i]) * 1e-9;
     }
+  }
+
+  // Per-batch device timing: the batch timeline, per-stream launch time, K1
+  // figures, and (when `res` is given) device times on the PCIe records.
+  void batch_detail(ExecResult* res) {
+    detail_pending = false;
+    batch_tr.clear();
+    stats.kernel_s[0] = stats.kernel_s[1] = 0;
+    stats.k1_s = 0;
+    stats.k1_bytes = 0;
+    stats.k1_launches = 0;
+    double first = 1e30, last = 0;
+    for (const Batch& B : landed) {
+      const double s0 = since_ev0(B.ev_start) * 1e-3, s1 = since_ev0(B.ev_end) * 1e-3;
+      const double c = B.ev_copied != nullptr ? since_ev0(B.ev_copied) * 1e-3 : s1;
+      batch_tr.push_back(BatchTrace{B.stream, static_cast<int>(B.legs.size()), B.ce, s0, c, s1, B.host_submit, B.host_done});
+      first = std::min(first, s0);
+      last = std::max(last, s1);
+      stats.kernel_s[B.stream] += s1 - s0;
+      if (!B.ce) {
+        stats.k1_s += s1 - s0;
+        stats.k1_bytes += B.legs.size() * kBlockBytes;
+        ++stats.k1_launches;
+      }
+      if (res)
+        for (auto i : B.legs) {
+          TransferRecord& r = res->events[legs[i].rec];
+          r.start = s0;
+          r.end = s1;
+        }
+    }
+    if (res) stats.device_span_s = landed.empty() ? 0.0 : last - first;
   }
 
   void check_status() {
@@ -1430,7 +1474,10 @@ const SwitchStats& SwapEngine::last_stats() const { return impl_->stats; }
 const std::array<std::vector<LegTrace>, 6>& SwapEngine::lane_trace() const { return impl_->trace; }
 std::uint64_t SwapEngine::total_launches() const { return impl_->launches_total; }
 const std::vector<K3Launch>& SwapEngine::k3_launches() const { return impl_->k3_trace; }
-const std::vector<BatchTrace>& SwapEngine::batch_trace() const { return impl_->batch_tr; }
+const std::vector<BatchTrace>& SwapEngine::batch_trace() const {
+  if (impl_->detail_pending) impl_->batch_detail(nullptr);  // events of the last execute are still valid
+  return impl_->batch_tr;
+}
 Bytes SwapEngine::pinned_overhead() const {
   return static_cast<Bytes>(kBounceUnits) * kBlockBytes + impl_->ktab_cap * sizeof(NxLeg) + 2 * impl_->ck_cap * sizeof(std::uint64_t);
 }
