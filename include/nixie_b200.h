@@ -198,9 +198,9 @@ typedef struct {
 } nx_batch_record;
 int nx_batch_trace(nx_engine* e, nx_batch_record* out, size_t cap, size_t* n);
 /* Every leg of the last nx_switch (the reference's TransferRecord log,
- * transfer.hpp:40-47), in commit order: PCIe legs carry their batch's device
- * start/end, host legs (pinned<->paged) the host times of submission and
- * commit (s, from the switch start). */
+ * transfer.hpp:40-47), in commit order, times in s from the switch start:
+ * host times of the leg's start and commit; on the SM path and with per-batch
+ * checks, PCIe legs carry their batch's device start/end instead. */
 typedef struct {
   uint64_t block;
   uint8_t src, dst; /* TierId */

@@ -236,8 +236,8 @@ class SwapEngine:
 
     def leg_records(self) -> List[Dict]:
         """Every leg of the last switch (TransferRecord log): block, src/dst tier,
-        start/end (s from the switch start; device times for PCIe legs, host
-        submit/commit times for pinned<->paged legs)."""
+        start/end (s from the switch start: host times of the leg's start and
+        commit; device batch times for PCIe legs on the SM path)."""
         n = c_size_t()
         check(lib.nx_leg_records(self._h, None, 0, byref(n)))
         arr = (L.LegRecordC * max(1, n.value))()
