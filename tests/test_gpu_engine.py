@@ -170,8 +170,8 @@ def test_calibration_and_probe(gpu):
 
 def test_leg_records_log_every_hop(gpu):
     """nx_leg_records: one record per hop of the last switch (the reference's
-    TransferRecord log), PCIe hops with device times inside the switch, host
-    hops (two-hop through a 16 MiB pinned budget) with host times."""
+    TransferRecord log) with times inside the switch, PCIe and host hops
+    (two-hop through a 16 MiB pinned budget) alike."""
     with SwapEngine(gpu_capacity=64 * MIB, pinned_capacity=16 * MIB, paged_capacity=256 * MIB, path=PATH_CE,
                     host_threads=2) as e:
         e.allocate(0, 64 * MIB, TIER_GPU)
