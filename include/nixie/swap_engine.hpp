@@ -81,7 +81,12 @@ struct EngineConfig {
   // per switch than none; 48-96 within 0.5%; 0 serialises the two directions
   // (the fetches need the frames the departures vacate) and 128 gains nothing.
   int pace_lag_legs = 64;
-  bool fetch_first_pump = true;  // lanes toward the GPU pumped first after a commit (LaneSet::set_fetch_first)
+  bool fetch_first_pump = true;
+  // Host copy pool (pinned <-> paged legs): AVX2 streaming stores. A plain
+  // memcpy of a 2 MiB leg reads the destination before writing it; with the
+  // two-hop switch host-DRAM-bound that third transfer per byte costs 15-17%
+  // of a config-4 switch at 2-4 GiB budgets (profiles/r02_ab_streaming_copy_c4.txt).
+  bool host_streaming_copy = true;  // lanes toward the GPU pumped first after a commit (LaneSet::set_fetch_first)
   bool exportable_arena = false;      // GPU tier = exportable VMM slabs shims can import (interposer daemon)
   Bytes arena_slab_bytes = 128 * kMiB; // exportable arena: bytes per physical allocation (a multiple of 2 MiB)
   Bytes gpu_physical = 0;             // arena bytes (0 = gpu_capacity); the registry still enforces gpu_capacity

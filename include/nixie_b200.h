@@ -69,6 +69,7 @@ typedef struct nx_engine_config {
   int early_frame_release; /* departures commit when queued; fetches wait on the device for their frames */
   int pace_lag_legs; /* departure groups wait for fetches landed up to (first leg - lag); -1: off */
   int fetch_first_pump; /* after a commit, lanes toward the GPU are pumped first (concurrent lanes) */
+  int host_streaming_copy; /* host copy pool copies with AVX2 streaming stores */
 } nx_engine_config;
 
 /* PlannerConfig (proj/include/nixie/planner.hpp:39-43). victim_order may be

@@ -55,7 +55,7 @@ class EngineConfigC(Structure):
         ("host_legs_in_flight", c_int), ("max_ctas", c_int), ("fused_launch", c_int), ("verify", c_int),
         ("numa_bind", c_int), ("first_batch_legs", c_int), ("k3_tma", c_int), ("k3_one_stream", c_int),
         ("k3_grouped", c_int), ("k3_verify_group", c_int), ("d2h_commit_legs", c_int), ("early_frame_release", c_int),
-        ("pace_lag_legs", c_int), ("fetch_first_pump", c_int),
+        ("pace_lag_legs", c_int), ("fetch_first_pump", c_int), ("host_streaming_copy", c_int),
     ]
 
 

@@ -100,6 +100,7 @@ EngineConfig to_cpp(const nx_engine_config& c) {
   o.early_frame_release = c.early_frame_release != 0;
   o.pace_lag_legs = c.pace_lag_legs;
   o.fetch_first_pump = c.fetch_first_pump != 0;
+  o.host_streaming_copy = c.host_streaming_copy != 0;
   return o;
 }
 
@@ -218,6 +219,7 @@ void nx_engine_config_default(nx_engine_config* c) {
   c->early_frame_release = d.early_frame_release;
   c->pace_lag_legs = d.pace_lag_legs;
   c->fetch_first_pump = d.fetch_first_pump;
+  c->host_streaming_copy = d.host_streaming_copy;
 }
 
 void nx_planner_config_default(nx_planner_config* c) {

@@ -330,6 +330,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
       const int ncpu = numa.cpus.empty() ? static_cast<int>(std::thread::hardware_concurrency()) : static_cast<int>(numa.cpus.size());
       const int maxt = std::max(1, std::min(ncpu, 32));
       pool.start(std::max(cfg.host_threads, maxt), numa.cpus, cfg.host_threads > 0 ? cfg.host_threads : maxt);
+      pool.set_streaming(cfg.host_streaming_copy);
     }
     for (auto& s : st) NX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     NX_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
@@ -1888,6 +1889,10 @@ void SwapEngine::set_option(const std::string& name, int value) {
   else if (name == "k3_verify_group" && value >= 1) c.k3_verify_group = value;
   else if (name == "pace_lag_legs" && value >= -1) c.pace_lag_legs = value;
   else if (name == "fetch_first_pump" && (value == 0 || value == 1)) c.fetch_first_pump = value != 0;
+  else if (name == "host_streaming_copy" && (value == 0 || value == 1)) {
+    c.host_streaming_copy = value != 0;
+    impl_->pool.set_streaming(value != 0);
+  }
   else throw SimError(Err::ValidationError, "set_option: unknown option or bad value: " + name + "=" + std::to_string(value));
 }
 

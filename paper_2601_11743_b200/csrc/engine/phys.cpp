@@ -8,6 +8,8 @@
 #include <sys/syscall.h>
 #include <unistd.h>
 
+#include <immintrin.h>
+
 #include <cctype>
 #include <cstring>
 #include <fstream>
@@ -240,6 +242,37 @@ HostCopyPool::~HostCopyPool() {
   for (auto& t : threads_) t.join();
 }
 
+namespace {
+// 256 bytes per iteration: eight 32-byte loads, eight streaming stores. The
+// sfence makes the stores visible before the completion is published.
+__attribute__((target("avx2"))) void stream_copy(void* dst, const void* src, std::size_t bytes) {
+  auto* d = static_cast<__m256i*>(dst);
+  const auto* s = static_cast<const __m256i*>(src);
+  const std::size_t n = bytes / 32;
+  std::size_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    const __m256i a0 = _mm256_load_si256(s + i), a1 = _mm256_load_si256(s + i + 1), a2 = _mm256_load_si256(s + i + 2),
+                  a3 = _mm256_load_si256(s + i + 3), a4 = _mm256_load_si256(s + i + 4), a5 = _mm256_load_si256(s + i + 5),
+                  a6 = _mm256_load_si256(s + i + 6), a7 = _mm256_load_si256(s + i + 7);
+    _mm256_stream_si256(d + i, a0);
+    _mm256_stream_si256(d + i + 1, a1);
+    _mm256_stream_si256(d + i + 2, a2);
+    _mm256_stream_si256(d + i + 3, a3);
+    _mm256_stream_si256(d + i + 4, a4);
+    _mm256_stream_si256(d + i + 5, a5);
+    _mm256_stream_si256(d + i + 6, a6);
+    _mm256_stream_si256(d + i + 7, a7);
+  }
+  for (; i < n; ++i) _mm256_stream_si256(d + i, _mm256_load_si256(s + i));
+  _mm_sfence();
+  std::memcpy(static_cast<char*>(dst) + n * 32, static_cast<const char*>(src) + n * 32, bytes - n * 32);
+}
+bool have_avx2() {
+  static const bool ok = __builtin_cpu_supports("avx2");
+  return ok;
+}
+}  // namespace
+
 void HostCopyPool::worker(int index, std::vector<int> cpus) {
   pin_thread_to(cpus);
   while (true) {
@@ -259,9 +292,11 @@ void HostCopyPool::worker(int index, std::vector<int> cpus) {
       j = jobs_.front();
       jobs_.pop_front();
     }
-    // Plain memcpy: measured equal to 32-byte streaming stores on the B200
-    // hosts (the pinned<->paged lanes are host-DRAM-bound either way).
-    std::memcpy(j.dst, j.src, j.bytes);
+    if (streaming_.load(std::memory_order_relaxed) && have_avx2() &&
+        ((reinterpret_cast<std::uintptr_t>(j.dst) | reinterpret_cast<std::uintptr_t>(j.src)) & 31) == 0)
+      stream_copy(j.dst, j.src, j.bytes);
+    else
+      std::memcpy(j.dst, j.src, j.bytes);
     {
       std::lock_guard<std::mutex> lk(done_mu_);
       done_.push_back(j.token);

@@ -169,6 +169,10 @@ class HostCopyPool {
   // measurement, SwapEngine::calibrate_host).
   void start(int threads, const std::vector<int>& cpus, int active = 0);
   void set_active(int n);
+  // Copy with non-temporal (streaming) stores when the CPU has AVX2 and the
+  // buffers are 32-byte aligned: no read-for-ownership of the destination, so
+  // a copied byte costs two DRAM transfers instead of three.
+  void set_streaming(bool on) { streaming_.store(on); }
   int active() const { return active_.load(); }
   int size() const { return static_cast<int>(threads_.size()); }
   ~HostCopyPool();
@@ -197,6 +201,7 @@ class HostCopyPool {
   std::uint64_t drained_ = 0;
   bool stop_ = false;
   std::atomic<int> active_{0};
+  std::atomic<bool> streaming_{false};
 };
 
 }  // namespace nixie::b200

@@ -45,6 +45,7 @@ class EngineConfig:
     early_frame_release: bool = True
     pace_lag_legs: int = 64
     fetch_first_pump: bool = True
+    host_streaming_copy: bool = True
 
     def to_c(self) -> L.EngineConfigC:
         c = L.EngineConfigC()
