@@ -55,7 +55,7 @@ struct EngineConfig {
   bool k3_tma = true;                 // CE-path checksum pass on the TMA pipeline (else the LDG loop)
   bool k3_one_stream = true;          // both lanes' K3 launches on one stream (no SM contention between them)
   bool k3_grouped = true;             // CE path: one record launch per switch, arrival checks per group
-  int k3_verify_group = 1024;         // legs per grouped arrival check (the last group is flushed at the end)
+  int k3_verify_group = 4096;         // legs per grouped arrival check (the last group is flushed at the end)
   // CE path, grouped K3: departure batches are cut into groups of this many
   // legs (first_batch_legs-sized groups for the first 32 x first_batch_legs
   // legs of a switch), each ending at its own event (0: whole batches).

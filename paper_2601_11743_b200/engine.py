@@ -40,7 +40,7 @@ class EngineConfig:
     k3_tma: bool = True
     k3_one_stream: bool = True
     k3_grouped: bool = True
-    k3_verify_group: int = 1024
+    k3_verify_group: int = 4096
     d2h_commit_legs: int = 32
     early_frame_release: bool = True
     pace_lag_legs: int = 64

@@ -21,7 +21,7 @@ from paper_2601_11743_b200 import GIB, PlannerConfig, SwapEngine  # noqa: E402
 from paper_2601_11743_b200._lib import TIER_PAGED  # noqa: E402
 
 DEFAULTS = {"legs_per_launch": 128, "first_batch_legs": 8, "d2h_commit_legs": 32, "early_frame_release": 1,
-            "k3_verify_group": 1024, "pace_lag_legs": 64, "fetch_first_pump": 1, "host_streaming_copy": 1}
+            "k3_verify_group": 4096, "pace_lag_legs": 64, "fetch_first_pump": 1, "host_streaming_copy": 1}
 
 
 def parse(v: str) -> dict:

@@ -23,7 +23,7 @@ from paper_2601_11743_b200 import GIB, MIB, PlannerConfig, SwapEngine  # noqa: E
 from paper_2601_11743_b200._lib import TIER_GPU, TIER_PINNED  # noqa: E402
 
 DEFAULTS = {"legs_per_launch": 128, "first_batch_legs": 8, "d2h_commit_legs": 32, "early_frame_release": 1,
-            "k3_verify_group": 1024, "pace_lag_legs": 64, "fetch_first_pump": 1}
+            "k3_verify_group": 4096, "pace_lag_legs": 64, "fetch_first_pump": 1}
 
 
 def parse(v: str) -> dict:
@@ -69,7 +69,9 @@ def main() -> int:
                 st = switch()
                 samples[name].append({"round": r, "span_ms": st["device_span_s"] * 1e3,
                                       "wall_ms": (st["wall_s"] + st["plan_s"]) * 1e3, "ce_calls": st["ce_calls"], "pace_waits": st["pace_waits"],
-                                      "ce_batches": [st["ce_batches_h2d"], st["ce_batches_d2h"]]})
+                                      "ce_batches": [st["ce_batches_h2d"], st["ce_batches_d2h"]],
+                                      "k3_s": st["k3_s"], "k3_kernel_s": st["k3_kernel_s"], "k3_bytes": st["k3_bytes"],
+                                      "k3_launches": st["k3_launches"]})
     exact = e.verify_pattern(0, 7) == 0 and e.verify_pattern(1, 7) == 0
     e.close()
     base = variants[0][0]
@@ -92,6 +94,9 @@ def main() -> int:
                           "gbs_p50": round(16 * GIB / (statistics.median(sp) * 1e-3) / 1e9, 2),
                           "ce_calls_p50": statistics.median(s["ce_calls"] for s in samples[name]),
                           "pace_waits_p50": statistics.median(s["pace_waits"] for s in samples[name]),
+                          "k3_launches_p50": statistics.median(s["k3_launches"] for s in samples[name]),
+                          "k3_event_gbs": round(sum(s["k3_bytes"] for s in samples[name]) / max(1e-12, sum(s["k3_s"] for s in samples[name])) / 1e9, 1),
+                          "k3_kernel_gbs": round(sum(s["k3_bytes"] for s in samples[name]) / max(1e-12, sum(s["k3_kernel_s"] for s in samples[name])) / 1e9, 1),
                           "probe_ce_bidir_total": round(probe["ce_bidir_total"], 2), "byte_exact": exact}), flush=True)
     if a.out:
         with open(a.out, "w") as f:
