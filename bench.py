@@ -200,7 +200,11 @@ class PcieCounters:
         self.thread = threading.Thread(target=self._run, daemon=True)
         self.thread.start()
 
-    def stop(self) -> dict:
+    def stop(self, raw_gbs_per_direction: float = 0.0) -> dict:
+        """Readings above the link's raw per-direction rate (Gen5 x16: 63.0
+        GB/s) cannot be real traffic: on some boxes the NVML window is shorter
+        than 20 ms under load and the KB/s figure over-reads. They stay in the
+        sample list but not in the statistics."""
         if self.thread is None or not self.thr:
             if self.thread is not None:
                 self.stop_ev.set()
@@ -208,20 +212,33 @@ class PcieCounters:
             return {"available": False, **({"error": self.err} if self.err else {})}
         self.stop_ev.set()
         self.thread.join()
-        tx = [t * 1024 / 1e9 for t, _ in self.thr]
-        rx = [r * 1024 / 1e9 for _, r in self.thr]
-        return {"available": True, "source": "nvmlDeviceGetPcieThroughput TX/RX (20 ms windows), sampled every 10 ms",
-                "samples": len(self.thr), "tx_gbs_mean": statistics.mean(tx), "rx_gbs_mean": statistics.mean(rx),
+        tx_all = [t * 1024 / 1e9 for t, _ in self.thr]
+        rx_all = [r * 1024 / 1e9 for _, r in self.thr]
+        ok = [i for i in range(len(self.thr))
+              if raw_gbs_per_direction <= 0 or max(tx_all[i], rx_all[i]) <= raw_gbs_per_direction]
+        out = {"available": True, "source": "nvmlDeviceGetPcieThroughput TX/RX (20 ms windows), sampled every 10 ms",
+               "samples": len(self.thr), "samples_above_raw_link_rate": len(self.thr) - len(ok),
+               "raw_gbs_per_direction": raw_gbs_per_direction,
+               "tx_gbs_samples": [round(v, 1) for v in tx_all], "rx_gbs_samples": [round(v, 1) for v in rx_all]}
+        if not ok:
+            return {**out, "available": False, "error": "every reading exceeds the link's raw rate"}
+        tx, rx = [tx_all[i] for i in ok], [rx_all[i] for i in ok]
+        return {**out, "tx_gbs_mean": statistics.mean(tx), "rx_gbs_mean": statistics.mean(rx),
                 "tx_gbs_p50": statistics.median(tx), "rx_gbs_p50": statistics.median(rx)}
+
+
+def raw_link_gbs(link: dict) -> float:
+    """The link's raw per-direction rate in GB/s from its generation and width (after line encoding)."""
+    gt = {1: 2.5, 2: 5.0, 3: 8.0, 4: 16.0, 5: 32.0, 6: 64.0}.get(link.get("gen", 0), 0.0)
+    enc = 0.8 if link.get("gen", 0) <= 2 else (242 / 256 if link.get("gen", 0) >= 6 else 128 / 130)
+    return gt * link.get("width", 0) * enc / 8.0
 
 
 def link_reference(device: int, bus_id: str, link: dict) -> dict:
     """An independent ceiling beside the same-run probe: the link's raw rate
     from its generation and width, and the TLP-payload bound from the max
     payload size (lspci); nvbandwidth when installed."""
-    gt = {1: 2.5, 2: 5.0, 3: 8.0, 4: 16.0, 5: 32.0, 6: 64.0}.get(link.get("gen", 0), 0.0)
-    enc = 0.8 if link.get("gen", 0) <= 2 else (242 / 256 if link.get("gen", 0) >= 6 else 128 / 130)
-    raw = gt * link.get("width", 0) * enc / 8.0
+    raw = raw_link_gbs(link)
     out = {"raw_gbs_per_direction": raw, "gen": link.get("gen"), "width": link.get("width")}
     try:
         txt = subprocess.run(["lspci", "-vvv", "-s", bus_id], capture_output=True, text=True, timeout=10).stdout
@@ -546,7 +563,8 @@ def run_product(args, dist: Dist):
         stats.append(step())
         windows.append((w0, time.time()))
     wall = time.perf_counter() - t0
-    pcie = counters.stop()
+    lk = pcie_link(device)  # the idle link may have trained down already: bound by its maximum
+    pcie = counters.stop(raw_link_gbs({"gen": lk.get("gen_max", 0), "width": lk.get("width_max", 0)}))
     dist.barrier()
     clocks = sampler.stop()
     launches = eng.total_launches() - launches0
