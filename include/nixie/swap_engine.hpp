@@ -48,6 +48,11 @@ struct EngineConfig {
   int host_threads = 0;               // pinned<->paged copy workers; 0 = measured at construction (calibrate_host)
   int host_legs_in_flight = 64;       // per host lane
   int max_ctas = 0;                   // K1 grid cap; 0 = 2 x SM count
+  // SM copy path kernel: > 0 runs K1T (TMA bulk copies) on this many CTAs per
+  // launch, -1 the same on half the SMs (the two directions' launches stay
+  // co-resident, one CTA per SM), 0 K1 (LDG/STG). Config 2 on the SM path,
+  // paired A/B (profiles/r02_k1t_ab.txt): K1 60.4 GB/s, K1T on 74 CTAs 78.9.
+  int sm_tma_ctas = -1;
   bool fused_launch = false;          // both directions in one launch stream (warp-group split)
   bool verify = true;                 // checksum every restore
   bool numa_bind = true;              // pinned ring + workers on the GPU's NUMA node

@@ -65,6 +65,13 @@ enum NxSwapFlags : std::uint32_t {
 cudaError_t launch_swap(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t flags, const NxCkTables& ck,
                         const NxScratch& scratch, int max_ctas, cudaStream_t stream);
 
+// K1T: the same swap (same legs, checksum record/verify, every dst non-null)
+// on the TMA pipeline: `ctas` CTAs each stream a balanced range of 32 KiB
+// chunks through a 4-stage shared-memory ring with cp.async.bulk loads and
+// stores; 16 consumer warps checksum each stage. kNxNoChecksum: copy only.
+cudaError_t launch_swap_tma(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t flags, const NxCkTables& ck,
+                            const NxScratch& scratch, int ctas, cudaStream_t stream);
+
 // K3 on the TMA pipeline: checksum-only pass over `n` legs of HBM frames
 // (legs[i].src), recorded (arriving = false) or verified (arriving = true).
 // One CTA per SM: a producer thread streams 32 KiB cp.async.bulk chunks into

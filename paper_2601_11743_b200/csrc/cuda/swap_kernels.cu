@@ -372,6 +372,105 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) nx_checksum_tma_kernel(
   if (threadIdx.x == 0 && p.clock_slot != kNoClockSlot) atomicMax(&p.ck.kend[p.clock_slot], global_ns());
 }
 
+// K1T: the swap copy on the TMA pipeline (round 2). Same chunk sequence and
+// balanced CTA ranges as K3, over the legs' sources (pinned host memory for
+// fetches, HBM frames for departures). The producer thread bulk-loads a chunk
+// into a 4-stage ring, bulk-stores it to the leg's destination as soon as it
+// landed, and refills a stage once its store has read shared memory and the
+// consumer warps have checksummed it (record on departure, verify on arrival,
+// as K1). Few CTAs suffice: one CTA keeps 128 KiB in flight per direction,
+// and a sweep of grid sizes (tools/sm_inflight_sweep.py) put the best
+// bidirectional rate at 8-74 CTAs per direction, not at a full grid.
+constexpr int kSwapTmaStages = 4;
+
+template <class P>
+__global__ void __launch_bounds__(kTmaConsumers + 32, 1) nx_swap_tma_kernel(const __grid_constant__ P p) {
+  extern __shared__ __align__(1024) std::uint8_t ring[];
+  __shared__ __align__(8) std::uint64_t full[kSwapTmaStages];
+  __shared__ __align__(8) std::uint64_t empty[kSwapTmaStages];
+  __shared__ unsigned long long red[kTmaConsumers / 32];
+  const std::uint64_t total = static_cast<std::uint64_t>(p.n_d2h + p.n_h2d) * kTmaChunksPerLeg;
+  const std::uint64_t c0 = total * blockIdx.x / gridDim.x;
+  const std::uint64_t c1 = total * (blockIdx.x + 1) / gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSwapTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaConsumers / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (c0 >= c1) return;
+  const std::uint64_t n = c1 - c0;
+  const int warp = threadIdx.x / 32;
+  const bool checksum = (p.flags & kNxNoChecksum) == 0u;
+  auto chunk_ptr = [&](std::uint64_t c, bool dst) {
+    const NxLeg& l = p.legs[c / kTmaChunksPerLeg];
+    return static_cast<std::uint8_t*>(dst ? l.dst : const_cast<void*>(l.src)) +
+           (c % kTmaChunksPerLeg) * static_cast<std::uint64_t>(kTmaChunk);
+  };
+
+  if (warp == kTmaConsumers / 32) {  // producer warp: loads and stores
+    if ((threadIdx.x & 31) == 0) {
+      const std::uint64_t pre = n < kSwapTmaStages ? n : kSwapTmaStages;
+      for (std::uint64_t i = 0; i < pre; ++i) {
+        mbar_expect_tx(&full[i], kTmaChunk);
+        bulk_load(ring + i * kTmaChunk, chunk_ptr(c0 + i, false), kTmaChunk, &full[i]);
+      }
+      for (std::uint64_t j = 0; j < n; ++j) {
+        const int s = static_cast<int>(j % kSwapTmaStages);
+        mbar_wait(&full[s], static_cast<unsigned>((j / kSwapTmaStages) & 1));
+        bulk_store(chunk_ptr(c0 + j, true), ring + s * kTmaChunk, kTmaChunk);
+        // Refill the stage of chunk j-1 (store j stays in flight meanwhile).
+        if (j >= 1 && j - 1 + kSwapTmaStages < n) {
+          bulk_wait_read<1>();
+          const int r = static_cast<int>((j - 1) % kSwapTmaStages);
+          mbar_wait(&empty[r], static_cast<unsigned>(((j - 1) / kSwapTmaStages) & 1));
+          mbar_expect_tx(&full[r], kTmaChunk);
+          bulk_load(ring + r * kTmaChunk, chunk_ptr(c0 + j - 1 + kSwapTmaStages, false), kTmaChunk, &full[r]);
+        }
+      }
+      bulk_wait_all();  // every store written before the kernel (and its completion event) ends
+    }
+    return;
+  }
+
+  constexpr int kVecsPerThread = kTmaChunk / 16 / kTmaConsumers;
+  constexpr std::uint64_t kKeyStep = 2ull * kTmaConsumers * kGolden;
+  std::uint32_t leg = static_cast<std::uint32_t>(c0 / kTmaChunksPerLeg);
+  std::uint32_t seg_chunks = 0;
+  unsigned long long acc = 0;
+  for (std::uint64_t i = 0; i < n; ++i) {
+    const std::uint64_t c = c0 + i;
+    const auto li = static_cast<std::uint32_t>(c / kTmaChunksPerLeg);
+    if (li != leg) {
+      if (checksum) tma_flush(p, 0u, leg, seg_chunks, acc, leg >= p.n_d2h, red);
+      leg = li;
+      seg_chunks = 0;
+      acc = 0;
+    }
+    const int s = static_cast<int>(i % kSwapTmaStages);
+    mbar_wait(&full[s], static_cast<unsigned>((i / kSwapTmaStages) & 1));
+    if (checksum) {
+      const uint4* v = reinterpret_cast<const uint4*>(ring + s * kTmaChunk);
+      const std::uint64_t vbase = (c % kTmaChunksPerLeg) * static_cast<std::uint64_t>(kTmaChunk / 16);
+      std::uint64_t key = 2ull * (vbase + threadIdx.x) * kGolden;
+#pragma unroll
+      for (int k = 0; k < kVecsPerThread; ++k) {
+        const uint4 x = v[threadIdx.x + k * kTmaConsumers];
+        const std::uint64_t w0 = static_cast<std::uint64_t>(x.x) | (static_cast<std::uint64_t>(x.y) << 32);
+        const std::uint64_t w1 = static_cast<std::uint64_t>(x.z) | (static_cast<std::uint64_t>(x.w) << 32);
+        acc += ck_term_keyed(w0, key) + ck_term_keyed(w1, key + kGolden);
+        key += kKeyStep;
+      }
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+    ++seg_chunks;
+  }
+  if (checksum) tma_flush(p, 0u, leg, seg_chunks, acc, leg >= p.n_d2h, red);
+}
+
 int parts_log2_for(int n_legs, int groups_wanted) {
   int k = 0;
   while (k < kMaxPartsLog2 && (n_legs << k) < groups_wanted) ++k;
@@ -452,6 +551,43 @@ cudaError_t launch_swap(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t f
   if (n <= 32) return launch_swap_n<32>(legs, n_d2h, n_h2d, flags, ck, scratch, max_ctas, stream);
   if (n <= 128) return launch_swap_n<128>(legs, n_d2h, n_h2d, flags, ck, scratch, max_ctas, stream);
   return launch_swap_n<kMaxLegsPerLaunch>(legs, n_d2h, n_h2d, flags, ck, scratch, max_ctas, stream);
+}
+
+template <int N>
+cudaError_t launch_swap_tma_n(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t flags, const NxCkTables& ck,
+                              const NxScratch& scratch, int ctas, cudaStream_t stream) {
+  static bool configured = false;
+  constexpr int kSmem = kSwapTmaStages * kTmaChunk;
+  if (!configured) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(nx_swap_tma_kernel<SwapParamsT<N>>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  SwapParamsT<N> p;
+  for (int i = 0; i < n_d2h + n_h2d; ++i) p.legs[i] = legs[i];
+  p.ck = ck;
+  p.scratch = scratch;
+  p.n_d2h = static_cast<std::uint32_t>(n_d2h);
+  p.n_h2d = static_cast<std::uint32_t>(n_h2d);
+  p.parts_log2 = 0;
+  p.flags = flags;
+  p.clock_slot = kNoClockSlot;
+  // no more CTAs than chunks: every CTA gets at least one
+  const int chunks = (n_d2h + n_h2d) * static_cast<int>(kTmaChunksPerLeg);
+  nx_swap_tma_kernel<SwapParamsT<N>><<<ctas < chunks ? ctas : chunks, kTmaConsumers + 32, kSmem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_swap_tma(const NxLeg* legs, int n_d2h, int n_h2d, std::uint32_t flags, const NxCkTables& ck,
+                            const NxScratch& scratch, int ctas, cudaStream_t stream) {
+  if (n_d2h < 0 || n_h2d < 0 || n_d2h + n_h2d > kMaxLegsPerLaunch || ctas < 1) return cudaErrorInvalidValue;
+  const int n = n_d2h + n_h2d;
+  if (n == 0) return cudaSuccess;
+  if (n <= 8) return launch_swap_tma_n<8>(legs, n_d2h, n_h2d, flags, ck, scratch, ctas, stream);
+  if (n <= 32) return launch_swap_tma_n<32>(legs, n_d2h, n_h2d, flags, ck, scratch, ctas, stream);
+  if (n <= 128) return launch_swap_tma_n<128>(legs, n_d2h, n_h2d, flags, ck, scratch, ctas, stream);
+  return launch_swap_tma_n<kMaxLegsPerLaunch>(legs, n_d2h, n_h2d, flags, ck, scratch, ctas, stream);
 }
 
 cudaError_t launch_checksum_tma(const NxLeg* legs, int n, bool arriving, std::uint32_t flags, const NxCkTables& ck,

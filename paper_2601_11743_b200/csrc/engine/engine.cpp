@@ -697,6 +697,12 @@ struct SwapEngine::Impl final : detail::LaneSink {
     return true;
   }
 
+  // The SM copy path: K1T (TMA bulk copies) when cfg.sm_tma_ctas > 0, else K1.
+  cudaError_t sm_copy_launch(const NxLeg* l, int n_d2h, int n_h2d, std::uint32_t flags, const NxScratch& sc, cudaStream_t s) {
+    const int tma = cfg.sm_tma_ctas < 0 ? std::max(1, sm_count / 2) : cfg.sm_tma_ctas;
+    return tma > 0 ? launch_swap_tma(l, n_d2h, n_h2d, flags, ck, sc, tma, s) : launch_swap(l, n_d2h, n_h2d, flags, ck, sc, max_ctas, s);
+  }
+
   NxLeg kernel_leg(const Leg& L) {
     return NxLeg{dev_addr(L.from, L.src_u), dev_addr(L.to, L.dst_u), static_cast<std::uint32_t>(L.block), 0};
   }
@@ -718,8 +724,7 @@ struct SwapEngine::Impl final : detail::LaneSink {
       std::vector<NxLeg> kl;
       kl.reserve(B.legs.size());
       for (auto i : B.legs) kl.push_back(kernel_leg(legs[i]));
-      NX_CUDA(launch_swap(kl.data(), static_cast<int>(d2h.size()), static_cast<int>(h2d.size()), flags, ck, scratch[s],
-                          max_ctas, st[s]));
+      NX_CUDA(sm_copy_launch(kl.data(), static_cast<int>(d2h.size()), static_cast<int>(h2d.size()), flags, scratch[s], st[s]));
       ++stats.launches[s];
       ++launches_total;
     } else {
@@ -1613,8 +1618,8 @@ PcieProbe SwapEngine::probe_pcie(Bytes bytes, Bytes chunk) {
       for (int k = 0; k < legs_per_chunk; ++k) {
         const Bytes o = off + static_cast<Bytes>(k) * kBlockBytes;
         if (legs.size() == static_cast<std::size_t>(kMaxLegsPerLaunch)) {
-          NX_CUDA(launch_swap(legs.data(), dir == 1 ? static_cast<int>(legs.size()) : 0, dir == 0 ? static_cast<int>(legs.size()) : 0,
-                              kNxNoChecksum, m.ck, m.scratch[dir], m.max_ctas, s));
+          NX_CUDA(m.sm_copy_launch(legs.data(), dir == 1 ? static_cast<int>(legs.size()) : 0, dir == 0 ? static_cast<int>(legs.size()) : 0,
+                                   kNxNoChecksum, m.scratch[dir], s));
           legs.clear();
         }
         if (dir == 0)
@@ -1622,8 +1627,8 @@ PcieProbe SwapEngine::probe_pcie(Bytes bytes, Bytes chunk) {
         else
           legs.push_back(NxLeg{b.dev[0] + o, b.host[0] + o, 0, 0});
       }
-      NX_CUDA(launch_swap(legs.data(), dir == 1 ? static_cast<int>(legs.size()) : 0, dir == 0 ? static_cast<int>(legs.size()) : 0,
-                          kNxNoChecksum, m.ck, m.scratch[dir], m.max_ctas, s));
+      NX_CUDA(m.sm_copy_launch(legs.data(), dir == 1 ? static_cast<int>(legs.size()) : 0, dir == 0 ? static_cast<int>(legs.size()) : 0,
+                               kNxNoChecksum, m.scratch[dir], s));
       ++m.launches_total;
     }
   };
@@ -1889,6 +1894,7 @@ void SwapEngine::set_option(const std::string& name, int value) {
   else if (name == "k3_verify_group" && value >= 1) c.k3_verify_group = value;
   else if (name == "pace_lag_legs" && value >= -1) c.pace_lag_legs = value;
   else if (name == "fetch_first_pump" && (value == 0 || value == 1)) c.fetch_first_pump = value != 0;
+  else if (name == "sm_tma_ctas" && value >= -1) c.sm_tma_ctas = value;
   else if (name == "host_streaming_copy" && (value == 0 || value == 1)) {
     c.host_streaming_copy = value != 0;
     impl_->pool.set_streaming(value != 0);

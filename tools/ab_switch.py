@@ -19,11 +19,12 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from paper_2601_11743_b200 import GIB, MIB, PlannerConfig, SwapEngine  # noqa: E402
+from paper_2601_11743_b200 import GIB, MIB, PlannerConfig, SwapEngine, parse_path  # noqa: E402
 from paper_2601_11743_b200._lib import TIER_GPU, TIER_PINNED  # noqa: E402
 
 DEFAULTS = {"legs_per_launch": 128, "first_batch_legs": 8, "d2h_commit_legs": 32, "early_frame_release": 1,
-            "k3_verify_group": 4096, "pace_lag_legs": 64, "fetch_first_pump": 1}
+            "k3_verify_group": 4096, "pace_lag_legs": 64, "fetch_first_pump": 1,
+            "sm_tma_ctas": -1}
 
 
 def parse(v: str) -> dict:
@@ -36,10 +37,11 @@ def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--rounds", type=int, default=12)
     ap.add_argument("--out")
+    ap.add_argument("--path", default="auto", help="copy path: auto, sm or ce (sm: K1 / K1T variants via sm_tma_ctas)")
     ap.add_argument("variants", nargs="+")
     a = ap.parse_args()
     variants = [(v, {**DEFAULTS, **parse(v)}) for v in a.variants]
-    e = SwapEngine(gpu_capacity=32 * GIB, pinned_capacity=16 * GIB, paged_capacity=2 * GIB)
+    e = SwapEngine(gpu_capacity=32 * GIB, pinned_capacity=16 * GIB, paged_capacity=2 * GIB, path=parse_path(a.path))
     probe = e.probe_pcie(1 * GIB, 64 * MIB)
     e.allocate(0, 16 * GIB, TIER_GPU)
     e.allocate(1, 16 * GIB, TIER_GPU)
