@@ -38,11 +38,12 @@ def load(path):
 
 
 def kind(name, m):
-    if "nx_swap_kernel" in name:
-        # what the launch moved: one direction or both (fused warp groups)
-        rd, wr = m.get("pcie__read_bytes.sum", 0.0), m.get("pcie__write_bytes.sum", 0.0)
-        d = "H2D" if wr < 0.25 * rd else ("D2H" if rd < 0.25 * wr else "H2D+D2H (fused)")
-        return "K1 nx_swap_kernel, " + d
+    for k, label in (("nx_swap_tma_kernel", "K1T nx_swap_tma_kernel, "), ("nx_swap_kernel", "K1 nx_swap_kernel, ")):
+        if k in name:
+            # what the launch moved: one direction or both (fused warp groups)
+            rd, wr = m.get("pcie__read_bytes.sum", 0.0), m.get("pcie__write_bytes.sum", 0.0)
+            d = "H2D" if wr < 0.25 * rd else ("D2H" if rd < 0.25 * wr else "H2D+D2H (fused)")
+            return label + d
     for k in ("nx_checksum_tma_kernel", "nx_pattern_kernel<0>", "nx_pattern_kernel<1>", "nx_table_upload_kernel"):
         if k in name:
             return {"nx_checksum_tma_kernel": "K3 nx_checksum_tma_kernel", "nx_pattern_kernel<0>": "K4 fill nx_pattern_kernel<0>",

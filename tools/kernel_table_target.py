@@ -2,7 +2,8 @@
 and write bytes/s and DRAM GB/s per launch; tools/kernel_table.py builds the
 table against the same box's per-direction link peak):
   K4 nx_pattern_kernel        fill (record) and compare of a GPU-resident app
-  K1 nx_swap_kernel           SM-path switches (split and fused-launch engines;
+  K1T nx_swap_tma_kernel      SM-path switches with the default kernel
+  K1 nx_swap_kernel           SM-path switches with sm_tma_ctas = 0 (split and fused-launch engines;
                               on this full-GPU shape the departures all go out
                               before any fetch, so the launches move one direction)
   K3 nx_checksum_tma_kernel   CE-path switch: grouped record + arrival checks
@@ -18,8 +19,9 @@ from paper_2601_11743_b200 import GIB, MIB, PlannerConfig, SwapEngine  # noqa: E
 from paper_2601_11743_b200._lib import PATH_CE, PATH_SM, TIER_GPU, TIER_PINNED  # noqa: E402
 
 
-def exchange(**opts):
+def exchange(sm_tma_ctas=-1, **opts):
     with SwapEngine(gpu_capacity=1 * GIB, pinned_capacity=2 * GIB, paged_capacity=64 * MIB, **opts) as e:
+        e.set_option("sm_tma_ctas", sm_tma_ctas)  # -1: K1T on half the SMs (default), 0: K1
         e.allocate(0, 1 * GIB, TIER_GPU)
         e.allocate(1, 1 * GIB, TIER_PINNED)
         e.fill_pattern(0, 5)  # K4 fill (GPU tier: record on the device)
@@ -38,7 +40,8 @@ if __name__ == "__main__":
         with SwapEngine(gpu_capacity=64 * MIB, pinned_capacity=64 * MIB, paged_capacity=64 * MIB) as e:
             print(json.dumps(e.probe_pcie(1 * GIB, 64 * MIB)))
         sys.exit(0)
-    exchange(path=PATH_SM)                      # K1 split launches
-    exchange(path=PATH_SM, fused_launch=True)   # K1 fused launches
+    exchange(path=PATH_SM)                      # K1T split launches (the SM path's default kernel)
+    exchange(path=PATH_SM, sm_tma_ctas=0)       # K1 split launches
+    exchange(path=PATH_SM, sm_tma_ctas=0, fused_launch=True)   # K1 fused launches
     exchange(path=PATH_CE)                      # K3 + table upload
     print("done")
