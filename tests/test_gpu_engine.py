@@ -51,13 +51,25 @@ def test_fill_verify_every_tier(gpu, oracle_lib):
         assert e.verify_pattern(1, SEED) == 1
 
 
-PATHS = [dict(path=PATH_SM), dict(path=PATH_SM, fused_launch=True), dict(path=PATH_CE), dict(path=PATH_AUTO),
-         dict(path=PATH_SM, legs_per_launch=3, pcie_legs_in_flight=5), dict(path=PATH_CE, legs_per_launch=1)]
+# sm_tma_ctas (an engine option, set after construction): the SM path's
+# default kernel is K1T (TMA bulk copies, -1 = half the SMs); 0 selects K1 (LDG/STG).
+PATHS = [dict(path=PATH_SM), dict(path=PATH_SM, sm_tma_ctas=0), dict(path=PATH_SM, sm_tma_ctas=3),
+         dict(path=PATH_SM, fused_launch=True), dict(path=PATH_SM, fused_launch=True, sm_tma_ctas=0), dict(path=PATH_CE),
+         dict(path=PATH_AUTO), dict(path=PATH_SM, legs_per_launch=3, pcie_legs_in_flight=5), dict(path=PATH_CE, legs_per_launch=1)]
+
+
+def engine(opts, **kw):
+    opts = dict(opts)
+    tma = opts.pop("sm_tma_ctas", None)
+    e = SwapEngine(**kw, **opts)
+    if tma is not None:
+        e.set_option("sm_tma_ctas", tma)
+    return e
 
 
 @pytest.mark.parametrize("opts", PATHS, ids=lambda o: "-".join(f"{k}{v}" for k, v in o.items()))
 def test_full_gpu_switch_is_byte_exact(gpu, oracle_lib, opts):
-    with SwapEngine(gpu_capacity=64 * MIB, pinned_capacity=112 * MIB, paged_capacity=64 * MIB, **opts) as e:
+    with engine(opts, gpu_capacity=64 * MIB, pinned_capacity=112 * MIB, paged_capacity=64 * MIB) as e:
         e.allocate(0, 64 * MIB, TIER_GPU)  # the incumbent fills the GPU
         e.allocate(1, 48 * MIB, TIER_PINNED)
         e.fill_pattern(0, SEED)
@@ -94,9 +106,10 @@ def test_real_engine_trace_equals_reference(gpu, golden, name, path):
     assert f and all(x[2] == "0" for x in f), f
 
 
-@pytest.mark.parametrize("path", [PATH_SM, PATH_CE])
-def test_corrupted_restore_is_detected(gpu, path):
-    with SwapEngine(gpu_capacity=32 * MIB, pinned_capacity=64 * MIB, paged_capacity=64 * MIB, path=path) as e:
+@pytest.mark.parametrize("opts", [dict(path=PATH_SM), dict(path=PATH_SM, sm_tma_ctas=0), dict(path=PATH_CE)],
+                         ids=["sm-k1t", "sm-k1", "ce"])
+def test_corrupted_restore_is_detected(gpu, opts):
+    with engine(opts, gpu_capacity=32 * MIB, pinned_capacity=64 * MIB, paged_capacity=64 * MIB) as e:
         e.allocate(0, 32 * MIB, TIER_GPU)
         e.allocate(1, 16 * MIB, TIER_PINNED)
         e.fill_pattern(0, SEED)
