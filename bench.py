@@ -399,6 +399,26 @@ def run_reference(args, dist: Dist):
 # ---------------------------------------------------------------------------------------------
 # Product arm
 # ---------------------------------------------------------------------------------------------
+def sm_path_switches(eng, step, n: int, path: int) -> dict:
+    """The hand-written SM copy path on the same steady config-2 switches,
+    after the timed region (not part of `value`): the engine's copy path is
+    set to the SM kernel (K1T, the TMA pipeline on half the SMs) for `n`
+    switches, every restore checksum-verified, then set back. DESIGN.md §3:
+    the copy engines win on this link, which is why `calibrate()` keeps them."""
+    eng.set_option("path", 1)
+    try:
+        sts = [step() for _ in range(n)]
+    finally:
+        eng.set_option("path", int(path))
+    spans = [s["device_span_s"] for s in sts]
+    gbs = [(s["bytes_in"] + s["bytes_out"]) / s["device_span_s"] / 1e9 for s in sts]
+    return {"kernel": "K1T nx_swap_tma_kernel (cp.async.bulk ring, checksum fused; half the SMs per launch)",
+            "switches": n, "gbs_p50": statistics.median(gbs), "device_span_ms_p50": statistics.median(spans) * 1e3,
+            "mismatches": sum(s["mismatches"] for s in sts), "verified": sum(s["verified"] for s in sts),
+            "k1_launches": sum(s["k1_launches"] for s in sts),
+            "what": "same engine and workload as `value`, copy path forced to the SM kernel after the timed region"}
+
+
 def x16_exchange(path: int, probes: list, switches: int = 20) -> dict:
     """North-star latency case: 16 GiB <-> 16 GiB exchange at a 16 GiB cap,
     `switches` times. Ideal = max(bytes / H2D-while-bidirectional, bytes /
@@ -571,6 +591,7 @@ def run_product(args, dist: Dist):
     # Latency distribution: >= --latency-switches steady switches (the timed
     # ones included), independent of --steps (p50/p99 over >= 100).
     more = [step() for _ in range(max(0, args.latency_switches - args.steps))]
+    sm_path = sm_path_switches(eng, step, args.sm_switches, path) if args.sm_switches > 0 else None
     probe_after = eng.probe_pcie(1 * GIB, 64 * MIB)
     pinned_now, pinned_peak = eng.pinned_physical()
     pinned_extra = eng.pinned_overhead()
@@ -694,6 +715,7 @@ def run_product(args, dist: Dist):
         "pcie_probe_after": {k: round(probe_after[k], 2) for k in ("ce_bidir_total", "ce_bidir_h2d", "ce_bidir_d2h", "sm_bidir_total")},
         "settle": settle,
         "calibration": calib,
+        "sm_path": sm_path,
         # The paper's own data mechanism restated on the box (SURVEY.md §8d CPU-baseline item 2):
         # one cudaMemcpyAsync per 2 MiB block on two streams, both directions at once.
         "paper_mechanism_2mib_ce": ({"gbs": round(calib["ce_gbps"][0], 2), "what": "per-2 MiB cudaMemcpyAsync, one D2H and one "
@@ -731,6 +753,8 @@ def main():
     ap.add_argument("--path", choices=["auto", "sm", "ce"], default="auto")
     ap.add_argument("--no-x16", dest="x16", action="store_false")
     ap.add_argument("--x16-switches", type=int, default=20)
+    ap.add_argument("--sm-switches", type=int, default=4,
+                    help="steady switches on the SM copy kernel (K1T) after the timed region, reported as sm_path (0: skip)")
     ap.add_argument("--latency-switches", type=int, default=100,
                     help="steady switches sampled for p50/p99 (the timed ones included)")
     ap.add_argument("--no-uvm", dest="uvm", action="store_false", help="skip the cudaMallocManaged comparator")

@@ -1895,6 +1895,7 @@ void SwapEngine::set_option(const std::string& name, int value) {
   else if (name == "pace_lag_legs" && value >= -1) c.pace_lag_legs = value;
   else if (name == "fetch_first_pump" && (value == 0 || value == 1)) c.fetch_first_pump = value != 0;
   else if (name == "sm_tma_ctas" && value >= -1) c.sm_tma_ctas = value;
+  else if (name == "path" && value >= 0 && value <= 2) c.path = static_cast<CopyPath>(value);  // read per execute
   else if (name == "host_streaming_copy" && (value == 0 || value == 1)) {
     c.host_streaming_copy = value != 0;
     impl_->pool.set_streaming(value != 0);
