@@ -248,7 +248,8 @@ int nx_calibrate_host(nx_engine* e, uint64_t bytes_per_direction, int* threads, 
 /* Per-switch tunables between executes: legs_per_launch, first_batch_legs,
  * d2h_commit_legs, early_frame_release, k3_verify_group, pace_lag_legs,
  * fetch_first_pump, host_streaming_copy, sm_tma_ctas (SM copy kernel: -1 K1T
- * on half the SMs, the default; > 0 K1T on that many CTAs; 0 K1). */
+ * on half the SMs, the default; > 0 K1T on that many CTAs; 0 K1), path (the
+ * copy path, 0 Auto / 1 SmKernel / 2 CopyEngine, read at each execute). */
 int nx_engine_set_option(nx_engine* e, const char* name, int value);
 /* Workers of the host copy pool taking jobs now. */
 int nx_host_threads(nx_engine* e, int* out);

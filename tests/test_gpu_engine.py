@@ -122,6 +122,25 @@ def test_corrupted_restore_is_detected(gpu, opts):
         assert "checksum mismatch" in str(err.value) and str(victim) in str(err.value)
 
 
+def test_copy_path_option_between_switches(gpu):
+    """set_option("path") changes the copy path between executes (bench.py's
+    sm_path key): SM-kernel switches launch K1T, copy-engine ones do not."""
+    with SwapEngine(gpu_capacity=64 * MIB, pinned_capacity=112 * MIB, paged_capacity=64 * MIB, path=PATH_CE) as e:
+        e.allocate(0, 64 * MIB, TIER_GPU)
+        e.allocate(1, 48 * MIB, TIER_PINNED)
+        e.fill_pattern(0, SEED)
+        e.fill_pattern(1, SEED)
+        nxt = 1
+        for p in (PATH_CE, PATH_SM, PATH_CE, PATH_SM):
+            e.set_option("path", p)
+            st = e.switch_to(nxt, PlannerConfig(streaming_window=8 * MIB, victim_order=[1 - nxt]))
+            assert st["mismatches"] == 0 and st["verified"] == st["pcie_h2d_bytes"] // (2 * MIB)
+            assert (st["k1_launches"] > 0) == (p == PATH_SM), (p, st["k1_launches"])
+            nxt = 1 - nxt
+        assert e.verify_pattern(0, SEED) == 0 and e.verify_pattern(1, SEED) == 0
+        e.audit()
+
+
 def test_launch_gate_holds_kernels_until_swap_in(gpu, oracle_lib):
     e = SwapEngine(gpu_capacity=64 * MIB, pinned_capacity=112 * MIB, paged_capacity=64 * MIB)
     s0, s1 = nxe.stream_create(), nxe.stream_create()
