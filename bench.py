@@ -591,7 +591,12 @@ def run_product(args, dist: Dist):
     # Latency distribution: >= --latency-switches steady switches (the timed
     # ones included), independent of --steps (p50/p99 over >= 100).
     more = [step() for _ in range(max(0, args.latency_switches - args.steps))]
-    sm_path = sm_path_switches(eng, step, args.sm_switches, path) if args.sm_switches > 0 else None
+    sm_path = None
+    if args.sm_switches > 0:
+        try:
+            sm_path = sm_path_switches(eng, step, args.sm_switches, path)
+        except Exception as e:  # noqa: BLE001  (reported, never fatal to the bench line)
+            sm_path = {"error": str(e)[-300:]}
     probe_after = eng.probe_pcie(1 * GIB, 64 * MIB)
     pinned_now, pinned_peak = eng.pinned_physical()
     pinned_extra = eng.pinned_overhead()
